@@ -1,0 +1,855 @@
+"""Reference restatement of the hpeel H1 path (see oracle/__init__.py).
+
+TEST INFRASTRUCTURE ONLY: never imported by the product package.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+
+__all__ = [
+    "GAMMA", "scramble", "mix_seed", "SplitMix64", "gaussian_matrix", "gaussian_matrix_libm",
+    "random_cloud", "equispaced_1d", "uniform_grid_points", "PointCloud", "Box", "BoxTree",
+    "Adjacency", "adjacency", "admissible_pairs", "dense_pairs", "ConstraintSet",
+    "build_constraints", "incompatible", "build_graph", "dsatur_color", "plan_coloring",
+    "BlockTestMatrix", "payload_gaussian", "assemble_test_matrices", "make_plan",
+    "qr_orthonormal", "pinv_apply", "DenseOperator", "KernelOperator", "H1Rep", "run_h1",
+    "extract_leaf", "compress", "rel_error_power_method", "synth_rank_structured",
+    "kernel_matrix", "H1", "LEAF", "UNIF1",
+]
+
+M64 = (1 << 64) - 1
+GAMMA = 0x9E3779B97F4A7C15
+H1, UNIF1, UNIF2, LEAF = 0, 1, 2, 3
+GAUSSIAN, IDENTITY = 0, 1
+
+
+# --------------------------------------------------------------------------- RNG
+# proj/src/rng.cpp:8-59, proj/include/hpeel/rng.hpp:12-48
+
+def scramble(z: int) -> int:
+    """proj/src/rng.cpp:11-15."""
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def mix_seed(seed: int, *tags: int) -> int:
+    """proj/src/rng.cpp:31-33 and the variadic form rng.hpp:39-42."""
+    for t in tags:
+        seed = scramble((seed * GAMMA + t + 1) & M64)
+    return seed
+
+
+class SplitMix64:
+    """proj/src/rng.cpp:18-29."""
+
+    def __init__(self, seed: int):
+        self.state = seed & M64
+
+    def next(self) -> int:
+        self.state = (self.state + GAMMA) & M64
+        return scramble(self.state)
+
+    def next_open_closed(self) -> float:
+        return float((self.next() >> 11) + 1) * 2.0 ** -53
+
+    def next_closed_open(self) -> float:
+        return float(self.next() >> 11) * 2.0 ** -53
+
+
+def _scramble_np(z: np.ndarray) -> np.ndarray:
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def _uniform_pairs(seed: int, npairs: int):
+    q = np.arange(npairs, dtype=np.uint64)
+    s = np.uint64(seed & M64)
+    g = np.uint64(GAMMA)
+    with np.errstate(over="ignore"):
+        z1 = _scramble_np(s + (np.uint64(2) * q + np.uint64(1)) * g)
+        z2 = _scramble_np(s + (np.uint64(2) * q + np.uint64(2)) * g)
+    u1 = ((z1 >> np.uint64(11)) + np.uint64(1)).astype(np.float64) * 2.0 ** -53
+    u2 = (z2 >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return u1, u2
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """proj/src/rng.cpp:35-59: row-major Box-Muller stream, the sine variate
+    of each (u1, u2) pair is the next entry. Vectorized; log/cos/sin from
+    numpy (within an ulp of glibc, see gaussian_matrix_libm)."""
+    if rows < 0 or cols < 0:
+        raise ValueError("negative shape")
+    total = rows * cols
+    npairs = (total + 1) // 2
+    u1, u2 = _uniform_pairs(seed, npairs)
+    radius = np.sqrt(-2.0 * np.log(u1))
+    angle = 2.0 * math.pi * u2
+    out = np.empty(2 * npairs)
+    out[0::2] = radius * np.cos(angle)
+    out[1::2] = radius * np.sin(angle)
+    return out[:total].reshape(rows, cols)
+
+
+def gaussian_matrix_libm(rows: int, cols: int, seed: int) -> np.ndarray:
+    """Same stream, scalar loop with the C library's log/cos/sin (the
+    reference's std::log/std::cos/std::sin), for bit-exact pinning."""
+    st = SplitMix64(seed)
+    out = np.empty((rows, cols))
+    spare, have = 0.0, False
+    for i in range(rows):
+        for j in range(cols):
+            if have:
+                out[i, j] = spare
+                have = False
+                continue
+            u1 = st.next_open_closed()
+            u2 = st.next_closed_open()
+            radius = math.sqrt(-2.0 * math.log(u1))
+            angle = 2.0 * math.pi * u2
+            out[i, j] = radius * math.cos(angle)
+            spare = radius * math.sin(angle)
+            have = True
+    return out
+
+
+def random_cloud(n: int, dim: int, seed: int) -> np.ndarray:
+    """proj/src/operators.cpp:88-95 (row by row, next_closed_open)."""
+    u1, _ = None, None
+    total = n * dim
+    q = np.arange(1, total + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = _scramble_np(np.uint64(seed & M64) + q * np.uint64(GAMMA))
+    vals = (z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+    return vals.reshape(n, dim)
+
+
+def equispaced_1d(n: int) -> np.ndarray:
+    """proj/src/operators.cpp:97-103."""
+    return ((np.arange(n, dtype=np.float64) + 0.5) / float(n))[:, None]
+
+
+def uniform_grid_points(per_dim: int, dim: int) -> np.ndarray:
+    """proj/src/operators.cpp:74-86."""
+    total = per_dim ** dim
+    out = np.empty((total, dim))
+    rem = np.arange(total)
+    for j in range(dim):
+        out[:, j] = ((rem % per_dim).astype(np.float64) + 0.5) / float(per_dim)
+        rem = rem // per_dim
+    return out
+
+
+# --------------------------------------------------------------------------- tree
+# proj/src/box_tree.cpp
+
+class PointCloud:
+    """proj/src/box_tree.cpp:55-70."""
+
+    def __init__(self, raw):
+        raw = np.asarray(raw, dtype=np.float64)
+        if raw.ndim == 1:
+            raw = raw[:, None]
+        if raw.shape[0] < 1:
+            raise ValueError("empty point cloud")
+        if not np.all(np.isfinite(raw)):
+            raise ValueError("non-finite coordinates")
+        c = raw.copy()
+        for j in range(raw.shape[1]):
+            lo, hi = raw[:, j].min(), raw[:, j].max()
+            c[:, j] = (raw[:, j] - lo) / (hi - lo) if hi > lo else 0.5
+        self.coords = c
+
+    @property
+    def dim(self):
+        return self.coords.shape[1]
+
+    def __len__(self):
+        return self.coords.shape[0]
+
+
+@dataclass
+class Box:
+    id: int
+    level: int
+    coord: tuple
+    parent: int
+    children: list = field(default_factory=list)
+    points: np.ndarray = None
+
+    @property
+    def is_leaf(self):
+        return not self.children
+
+
+class BoxTree:
+    """BoxTree::build, proj/src/box_tree.cpp:99-180 (BFS ids; split boxes with
+    more than m points; children in corner-mask order; a point on a bisection
+    plane goes to the lower child)."""
+
+    MAX_DEPTH = 62
+
+    def __init__(self, cloud: PointCloud, leaf_capacity: int):
+        if leaf_capacity < 1:
+            raise ValueError("leaf capacity >= 1")
+        d = cloud.dim
+        self.dim = d
+        self.leaf_capacity = leaf_capacity
+        self.num_points = len(cloud)
+        self.boxes = [Box(0, 0, tuple([0] * d), -1, [], np.arange(len(cloud)))]
+        self.levels = [[0]]
+        frontier = [0]
+        level = 0
+        while True:
+            if not any(len(self.boxes[i].points) > leaf_capacity for i in frontier):
+                break
+            if level >= self.MAX_DEPTH:
+                raise RuntimeError("degenerate geometry: leaf capacity unreachable at depth cap")
+            nxt = []
+            for bid in frontier:
+                parent = self.boxes[bid]
+                if len(parent.points) <= leaf_capacity:
+                    continue
+                pts = parent.points
+                mask = np.zeros(len(pts), dtype=np.int64)
+                for j in range(d):
+                    lo = math.ldexp(float(parent.coord[j]), -parent.level)
+                    hi = math.ldexp(float(parent.coord[j] + 1), -parent.level)
+                    mid = 0.5 * (lo + hi)
+                    mask |= (cloud.coords[pts, j] > mid).astype(np.int64) << j
+                for m in range(1 << d):
+                    sel = pts[mask == m]
+                    if len(sel) == 0:
+                        continue
+                    cid = len(self.boxes)
+                    coord = tuple(2 * parent.coord[j] + ((m >> j) & 1) for j in range(d))
+                    self.boxes.append(Box(cid, level + 1, coord, bid, [], sel))
+                    parent.children.append(cid)
+                    nxt.append(cid)
+            self.levels.append(nxt)
+            frontier = nxt
+            level += 1
+        self.depth = level
+
+    def level_boxes(self, level):
+        return self.levels[level]
+
+    def box(self, i):
+        return self.boxes[i]
+
+    @property
+    def num_boxes(self):
+        return len(self.boxes)
+
+    def max_leaf_size(self):
+        return max(len(b.points) for b in self.boxes if b.is_leaf)
+
+    def is_fully_populated(self):
+        want = 1 << self.dim
+        return all(len(b.children) == want for b in self.boxes if b.level < self.depth)
+
+
+@dataclass
+class Adjacency:
+    neighbors: list
+    interaction: list
+    coarse_leaf_neighbors: list
+    dense_partners: list
+    cross_level_adjacencies: int
+
+
+def adjacency(tree: BoxTree) -> Adjacency:
+    """proj/src/box_tree.cpp:214-300."""
+    nb = tree.num_boxes
+    d = tree.dim
+    index = [dict() for _ in range(tree.depth + 1)]
+    for b in tree.boxes:
+        index[b.level][b.coord] = b.id
+    neighbors = [None] * nb
+    offsets = [()]
+    for _ in range(d):
+        offsets = [o + (s,) for o in offsets for s in (-1, 0, 1)]
+    for b in tree.boxes:
+        lim = (1 << b.level) - 1
+        ns = []
+        for off in offsets:
+            probe = tuple(b.coord[j] + off[j] for j in range(d))
+            if all(0 <= p <= lim for p in probe) and probe in index[b.level]:
+                ns.append(index[b.level][probe])
+        neighbors[b.id] = sorted(ns)
+    interaction = [[] for _ in range(nb)]
+    for b in tree.boxes:
+        if b.parent < 0:
+            continue
+        il = []
+        for pn in neighbors[b.parent]:
+            for c in tree.boxes[pn].children:
+                cc = tree.boxes[c].coord
+                if any(abs(cc[j] - b.coord[j]) > 1 for j in range(d)):
+                    il.append(c)
+        interaction[b.id] = sorted(il)
+    cl = [[] for _ in range(nb)]
+    cross = 0
+    for b in tree.boxes:
+        if b.parent < 0:
+            continue
+        s = set(cl[b.parent])
+        s.update(pn for pn in neighbors[b.parent] if tree.boxes[pn].is_leaf)
+        cl[b.id] = sorted(s)
+        cross += len(cl[b.id])
+    dp = [set() for _ in range(nb)]
+    for b in tree.boxes:
+        if not b.is_leaf:
+            continue
+        dp[b.id].update(n for n in neighbors[b.id] if tree.boxes[n].is_leaf)
+        for c in cl[b.id]:
+            dp[b.id].add(c)
+            dp[c].add(b.id)
+    return Adjacency(neighbors, interaction, cl, [sorted(s) for s in dp], cross)
+
+
+def admissible_pairs(tree, adj, level):
+    """proj/src/box_tree.cpp:302-313."""
+    if level < 2 or level > tree.depth:
+        raise ValueError("admissible pairs exist for levels 2..depth")
+    return [(a, b) for a in tree.level_boxes(level) for b in adj.interaction[a]]
+
+
+def dense_pairs(tree, adj):
+    """proj/src/box_tree.cpp:315-323."""
+    return [(b.id, m) for b in tree.boxes if b.is_leaf for m in adj.dense_partners[b.id]]
+
+
+# --------------------------------------------------------------------------- coloring
+# proj/src/coloring.cpp
+
+@dataclass
+class ConstraintSet:
+    payload: tuple   # ((box, tag), ...) sorted
+    zero: tuple      # sorted
+    owners: list
+
+
+def build_constraints(tree, adj, level, mode):
+    """proj/src/coloring.cpp:55-113 (kH1, kUnifStage1, kLeaf)."""
+    index = {}
+    sets = []
+
+    def add(payload, zero, owner):
+        key = (payload, zero)
+        if key in index:
+            sets[index[key]].owners.append(owner)
+        else:
+            index[key] = len(sets)
+            sets.append(ConstraintSet(payload, zero, [owner]))
+
+    if mode == H1:
+        for a, b in admissible_pairs(tree, adj, level):
+            z = set(adj.neighbors[a]) | set(adj.interaction[a]) | set(adj.coarse_leaf_neighbors[a])
+            z.discard(b)
+            add(((b, GAUSSIAN),), tuple(sorted(z)), (a, b))
+    elif mode == UNIF1:
+        if level < 2 or level > tree.depth:
+            raise ValueError("sampling level out of range")
+        for a in tree.level_boxes(level):
+            if not adj.interaction[a]:
+                continue
+            payload = tuple((b, GAUSSIAN) for b in adj.interaction[a])
+            z = sorted(set(adj.neighbors[a]) | set(adj.coarse_leaf_neighbors[a]))
+            add(payload, tuple(z), (a, -1))
+    elif mode == LEAF:
+        for lam, mu in dense_pairs(tree, adj):
+            z = [x for x in adj.dense_partners[lam] if x != mu]
+            add(((mu, IDENTITY),), tuple(z), (lam, mu))
+    else:
+        raise ValueError("unsupported mode")
+    return sets
+
+
+def incompatible(a: ConstraintSet, b: ConstraintSet) -> bool:
+    """proj/src/coloring.cpp:115-146."""
+    za, zb = set(a.zero), set(b.zero)
+    if any(p in zb for p, _ in a.payload) or any(p in za for p, _ in b.payload):
+        return True
+    tb = dict(b.payload)
+    return any(p in tb and tb[p] != t for p, t in a.payload)
+
+
+def build_graph(sets):
+    """proj/src/coloring.cpp:154-167, the literal pairwise scan (vectorized
+    over j through Python sets; same edge set)."""
+    n = len(sets)
+    zeros = [set(s.zero) for s in sets]
+    pays = [dict(s.payload) for s in sets]
+    edges = [[] for _ in range(n)]
+    for i in range(n):
+        pi, zi = pays[i], zeros[i]
+        for j in range(i + 1, n):
+            pj, zj = pays[j], zeros[j]
+            hit = False
+            for p in pi:
+                if p in zj or (p in pj and pj[p] != pi[p]):
+                    hit = True
+                    break
+            if not hit:
+                for p in pj:
+                    if p in zi:
+                        hit = True
+                        break
+            if hit:
+                edges[i].append(j)
+                edges[j].append(i)
+    return [sorted(e) for e in edges]
+
+
+def dsatur_color(edges):
+    """proj/src/coloring.cpp:169-216: max (saturation, uncolored degree, -v);
+    smallest free color. Returns (colors, num_colors)."""
+    import heapq
+    n = len(edges)
+    color = [-1] * n
+    if n == 0:
+        return color, 0
+    seen = [set() for _ in range(n)]
+    udeg = [len(e) for e in edges]
+    stamp = [0] * n
+    heap = [(0, -udeg[v], v, 0) for v in range(n)]  # min-heap on (-sat, -udeg, v)
+    heapq.heapify(heap)
+    ncol = 0
+    done = 0
+    while done < n:
+        negsat, negud, v, st = heapq.heappop(heap)
+        if color[v] != -1 or st != stamp[v]:
+            continue
+        c = 0
+        while c in seen[v]:
+            c += 1
+        color[v] = c
+        ncol = max(ncol, c + 1)
+        done += 1
+        for w in edges[v]:
+            if color[w] != -1:
+                continue
+            udeg[w] -= 1
+            seen[w].add(c)
+            stamp[w] += 1
+            heapq.heappush(heap, (-len(seen[w]), -udeg[w], w, stamp[w]))
+    return color, ncol
+
+
+def plan_coloring(tree, sets, edges, mode):
+    """proj/src/coloring.cpp:218-250."""
+    color, ncol = dsatur_color(edges)
+    if not tree.is_fully_populated():
+        return color, ncol
+    mod = {H1: 6, UNIF1: 5, LEAF: 3}[mode]
+    relabel = {}
+    tile = []
+    for s in sets:
+        box = s.owners[0][0] if mode == UNIF1 else s.payload[0][0]
+        idx, mul = 0, 1
+        for c in tree.box(box).coord:
+            idx += (c % mod) * mul
+            mul *= mod
+        if idx not in relabel:
+            relabel[idx] = len(relabel)
+        tile.append(relabel[idx])
+    if len(relabel) < ncol:
+        return tile, len(relabel)
+    return color, ncol
+
+
+def payload_gaussian(tree, box, width, seed, level, phase):
+    """proj/src/coloring.cpp:252-259."""
+    return gaussian_matrix(len(tree.box(box).points), width, mix_seed(seed, level, box, phase))
+
+
+@dataclass
+class BlockTestMatrix:
+    rows: int
+    width: int
+    seed: int
+    level: int
+    phase: int
+    payload: list
+    zero: list
+    serves: list
+
+    def realize(self, tree):
+        """proj/src/coloring.cpp:261-291."""
+        out = np.zeros((self.rows, self.width))
+        for box, tag in self.payload:
+            pts = tree.box(box).points
+            if tag == GAUSSIAN:
+                blk = payload_gaussian(tree, box, self.width, self.seed, self.level, self.phase)
+            else:
+                blk = np.zeros((len(pts), self.width))
+                k = min(len(pts), self.width)
+                blk[np.arange(k), np.arange(k)] = 1.0
+            out[pts, :] = blk
+        return out
+
+
+def assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase):
+    """proj/src/coloring.cpp:293-332."""
+    mats = [BlockTestMatrix(tree.num_points, width, seed, level, phase, [], [], []) for _ in range(ncol)]
+    merged = [dict() for _ in range(ncol)]
+    zeros = [set() for _ in range(ncol)]
+    for i, s in enumerate(sets):
+        c = color[i]
+        mats[c].serves.append(i)
+        for box, tag in s.payload:
+            if box in merged[c] and merged[c][box] != tag:
+                raise AssertionError("conflicting payload tags within a color")
+            merged[c][box] = tag
+        zeros[c].update(s.zero)
+    for c in range(ncol):
+        mats[c].payload = sorted(merged[c].items())
+        mats[c].zero = sorted(zeros[c])
+    return mats
+
+
+@dataclass
+class Plan:
+    sets: list
+    edges: list
+    color: list
+    matrices: list
+    block_to_matrix: dict
+
+
+def make_plan(tree, adj, level, mode, width, seed, phase):
+    """proj/src/peeling.cpp:98-154 (graph strategy)."""
+    sets = build_constraints(tree, adj, level, mode)
+    if not sets:
+        return Plan([], [], [], [], {})
+    edges = build_graph(sets)
+    color, ncol = plan_coloring(tree, sets, edges, mode)
+    mats = assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase)
+    b2m = {}
+    for i, s in enumerate(sets):
+        for o in s.owners:
+            b2m[o] = color[i]
+    return Plan(sets, edges, color, mats, b2m)
+
+
+# --------------------------------------------------------------------------- linalg
+# proj/src/linalg.cpp
+
+QR_RANK_DROP_TOL = 1e-14   # proj/include/hpeel/linalg.hpp:33
+PINV_CUTOFF = 1e-12        # proj/include/hpeel/linalg.hpp:35
+
+
+def qr_orthonormal(m, max_rank=-1):
+    """proj/src/linalg.cpp:53-78: column-pivoted Householder QR (LAPACK
+    dgeqp3 standing in for Eigen::ColPivHouseholderQR), keep the leading
+    columns with |R_jj| > 1e-14 |R_00|, capped at max_rank."""
+    m = np.asarray(m, dtype=np.float64)
+    if m.shape[0] == 0 or m.shape[1] == 0:
+        return np.zeros((m.shape[0], 0))
+    if not np.all(np.isfinite(m)):
+        raise ValueError("non-finite matrix in qr")
+    q, r, _ = scipy.linalg.qr(m, mode="economic", pivoting=True)
+    kmax = min(m.shape)
+    p0 = abs(r[0, 0])
+    keep = 0
+    while keep < kmax and abs(r[keep, keep]) > QR_RANK_DROP_TOL * p0:
+        keep += 1
+    if max_rank >= 0:
+        keep = min(keep, max_rank)
+    return q[:, :keep]
+
+
+def pinv_apply(c, rhs):
+    """proj/src/linalg.cpp:110-127 (SVD cutoff 1e-12 sigma_1)."""
+    c = np.asarray(c, dtype=np.float64)
+    if c.shape[0] != rhs.shape[0]:
+        raise ValueError("pinv_apply: row mismatch")
+    if c.shape[0] == 0 or c.shape[1] == 0:
+        return np.zeros((c.shape[1], rhs.shape[1]))
+    u, s, vt = np.linalg.svd(c, full_matrices=False)
+    inv = np.where(s > PINV_CUTOFF * s[0], 1.0 / np.where(s > 0, s, 1.0), 0.0)
+    return vt.T @ (inv[:, None] * (u.T @ rhs))
+
+
+# --------------------------------------------------------------------------- operators
+
+def kernel_matrix(kind, xi, xj, same=None, param=0.1):
+    """Kernel blocks of the BASELINE.json on-the-fly operators, evaluated on
+    raw coordinates: log|x-y| (A_ii = 0), 1/(4 pi |x-y|) (A_ii = 0),
+    exp(-|x-y|/param)."""
+    diff = xi[:, None, :] - xj[None, :, :]
+    r = np.sqrt(np.sum(diff * diff, axis=2))
+    with np.errstate(divide="ignore"):
+        if kind == "log":
+            k = np.log(r)
+        elif kind == "invdist4pi":
+            k = 1.0 / (4.0 * math.pi * r)
+        elif kind == "exp":
+            return np.exp(-r / param)
+        else:
+            raise ValueError(kind)
+    if same is not None:
+        k[same] = 0.0
+    return k
+
+
+class DenseOperator:
+    """proj/include/hpeel/operators.hpp:56-69."""
+
+    def __init__(self, a):
+        self.a = np.asarray(a, dtype=np.float64)
+        self.shape = self.a.shape
+
+    def apply(self, x):
+        return self.a @ x
+
+    def apply_adjoint(self, x):
+        return self.a.T @ x
+
+
+class KernelOperator:
+    """On-the-fly kernel black box (row-chunked K(X, X) @ x), for sizes where
+    a dense A does not fit."""
+
+    def __init__(self, kind, points, param=0.1, chunk=2048):
+        self.kind = kind
+        self.x = np.asarray(points, dtype=np.float64)
+        if self.x.ndim == 1:
+            self.x = self.x[:, None]
+        self.param = param
+        self.chunk = chunk
+        n = self.x.shape[0]
+        self.shape = (n, n)
+
+    def block(self, i0, i1):
+        n = self.shape[0]
+        same = None
+        if self.kind != "exp":
+            same = (np.arange(i0, i1)[:, None] == np.arange(n)[None, :])
+        return kernel_matrix(self.kind, self.x[i0:i1], self.x, same, self.param)
+
+    def apply(self, x):
+        n = self.shape[0]
+        y = np.empty((n, x.shape[1]))
+        for i0 in range(0, n, self.chunk):
+            i1 = min(n, i0 + self.chunk)
+            y[i0:i1] = self.block(i0, i1) @ x
+        return y
+
+    apply_adjoint = apply  # symmetric kernels
+
+
+# --------------------------------------------------------------------------- H1 rep
+# proj/src/hmatrix.cpp:21-150
+
+class H1Rep:
+    def __init__(self, tree, adj):
+        self.tree = tree
+        self.adj = adj
+        self.built_level = 1
+        self.dense_ready = False
+        self.levels = [dict() for _ in range(tree.depth + 1)]
+        self.dense = {}
+
+    def _check(self, level):
+        if level > self.built_level:
+            raise RuntimeError(f"h1 apply: representation incomplete for level {level}")
+
+    def apply_truncated(self, level, x):
+        """proj/src/hmatrix.cpp:86-100."""
+        self._check(level)
+        y = np.zeros_like(x)
+        for l in range(2, min(level, self.tree.depth) + 1):
+            for (a, b), (u, bb, v) in sorted(self.levels[l].items()):
+                y[self.tree.box(a).points] += u @ (bb @ (v.T @ x[self.tree.box(b).points]))
+        return y
+
+    def apply_truncated_adjoint(self, level, x):
+        """proj/src/hmatrix.cpp:102-116."""
+        self._check(level)
+        y = np.zeros_like(x)
+        for l in range(2, min(level, self.tree.depth) + 1):
+            for (a, b), (u, bb, v) in sorted(self.levels[l].items()):
+                y[self.tree.box(b).points] += v @ (bb.T @ (u.T @ x[self.tree.box(a).points]))
+        return y
+
+    def _dense(self, x, y, adjoint):
+        """proj/src/hmatrix.cpp:59-73."""
+        for (lam, mu), d in sorted(self.dense.items()):
+            rows = self.tree.box(mu if adjoint else lam).points
+            cols = self.tree.box(lam if adjoint else mu).points
+            y[rows] += (d.T if adjoint else d) @ x[cols]
+
+    def apply(self, x):
+        if not self.dense_ready:
+            raise RuntimeError("h1 apply: dense blocks missing")
+        y = self.apply_truncated(self.tree.depth, x)
+        self._dense(x, y, False)
+        return y
+
+    def apply_adjoint(self, x):
+        if not self.dense_ready:
+            raise RuntimeError("h1 apply: dense blocks missing")
+        y = self.apply_truncated_adjoint(self.tree.depth, x)
+        self._dense(x, y, True)
+        return y
+
+    def storage(self):
+        """proj/src/hmatrix.cpp:132-150 (total scalars)."""
+        t = 0
+        for lv in self.levels:
+            for u, b, v in lv.values():
+                t += u.size + b.size + v.size
+        t += sum(d.size for d in self.dense.values())
+        return t
+
+
+# --------------------------------------------------------------------------- driver
+# proj/src/peeling.cpp
+
+def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None):
+    """proj/src/peeling.cpp:158-178. Returns (samples, cols)."""
+    samples, cols = [], 0
+    for m in plan.matrices:
+        if not m.payload:
+            samples.append(None)
+            continue
+        if phase is not None:
+            m = BlockTestMatrix(m.rows, m.width, m.seed, m.level, phase, m.payload, m.zero, m.serves)
+        omega = m.realize(rep.tree)
+        y = op.apply_adjoint(omega) if adjoint else op.apply(omega)
+        cols += omega.shape[1]
+        if prev_level >= 2:
+            y = y - (rep.apply_truncated_adjoint(prev_level, omega) if adjoint
+                     else rep.apply_truncated(prev_level, omega))
+        samples.append(y)
+    return samples, cols
+
+
+def run_h1(op, tree, adj, k, p, seed, report, capture=None):
+    """proj/src/peeling.cpp:211-275 (Alg. 4.1)."""
+    rep = H1Rep(tree, adj)
+    r = k + p
+    for l in range(2, tree.depth + 1):
+        pairs = admissible_pairs(tree, adj, l)
+        if not pairs:
+            continue
+        ps = set(pairs)
+        if any((b, a) not in ps for a, b in pairs):
+            raise AssertionError("asymmetric admissibility structure")
+        plan = make_plan(tree, adj, l, H1, r, seed, 0)
+        ys, fcols = _residual_samples(op, rep, l - 1, plan, False)
+        u_bases = {}
+        for a, b in pairs:
+            y = ys[plan.block_to_matrix[(a, b)]]
+            u_bases[(a, b)] = qr_orthonormal(y[tree.box(a).points], k)
+        zs, acols = _residual_samples(op, rep, l - 1, plan, True, phase=1)
+        if capture is not None:
+            capture[l] = {(a, b): (ys[plan.block_to_matrix[(a, b)]][tree.box(a).points],
+                                   zs[plan.block_to_matrix[(a, b)]][tree.box(a).points])
+                          for a, b in pairs}
+        for a, b in pairs:
+            z = zs[plan.block_to_matrix[(b, a)]]
+            u = u_bases[(a, b)]
+            v = qr_orthonormal(z[tree.box(b).points], k)
+            g = payload_gaussian(tree, b, r, seed, l, 0)
+            gp = payload_gaussian(tree, a, r, seed, l, 1)
+            yb = ys[plan.block_to_matrix[(a, b)]][tree.box(a).points]
+            middle = gp.T @ yb
+            left = pinv_apply(gp.T @ u, middle)
+            bmat = pinv_apply((v.T @ g).T, left.T).T
+            rep.levels[l][(a, b)] = (u, bmat, v)
+        rep.built_level = l
+        report.append({"phase": "h1", "level": l, "colors": len(plan.matrices),
+                       "forward_cols": fcols, "adjoint_cols": acols})
+    rep.built_level = tree.depth
+    return rep
+
+
+def extract_leaf(op, rep, seed, report, capture=None):
+    """proj/src/peeling.cpp:490-524."""
+    tree, adj = rep.tree, rep.adj
+    if rep.built_level < tree.depth:
+        raise RuntimeError("leaf extraction needs all admissible levels built")
+    width = tree.max_leaf_size()
+    plan = make_plan(tree, adj, tree.depth, LEAF, width, seed, 0)
+    ys, fcols = _residual_samples(op, rep, tree.depth, plan, False)
+    for lam, mu in dense_pairs(tree, adj):
+        y = ys[plan.block_to_matrix[(lam, mu)]]
+        blk = y[tree.box(lam).points]
+        if capture is not None:
+            capture[(lam, mu)] = blk
+        rep.dense[(lam, mu)] = blk[:, :len(tree.box(mu).points)]
+    rep.dense_ready = True
+    report.append({"phase": "leaf", "level": tree.depth, "colors": len(plan.matrices),
+                   "forward_cols": fcols, "adjoint_cols": 0})
+
+
+def compress(op, tree, k, p, seed, capture=None, leaf_capture=None):
+    """proj/src/peeling.cpp:576-639 for format h1. Returns (rep, report)."""
+    if op.shape[0] != tree.num_points or op.shape[1] != tree.num_points:
+        raise ValueError("operator and tree dimensions differ")
+    if k < 1:
+        raise ValueError("fixed rank must be >= 1")
+    if p < 0:
+        raise ValueError("negative oversampling")
+    adj = adjacency(tree)
+    report = []
+    rep = run_h1(op, tree, adj, k, p, seed, report, capture)
+    extract_leaf(op, rep, seed, report, leaf_capture)
+    return rep, report
+
+
+def _power_norm_diff(a, b, iters, seed, n):
+    """proj/src/linalg.cpp:179-196."""
+    x = gaussian_matrix(n, 1, seed)
+    x = x / np.linalg.norm(x)
+    est = 0.0
+    for _ in range(iters):
+        y = a.apply(x)
+        if b is not None:
+            y = y - b.apply(x)
+        z = a.apply_adjoint(y)
+        if b is not None:
+            z = z - b.apply_adjoint(y)
+        nz = np.linalg.norm(z)
+        if nz == 0.0:
+            return 0.0
+        est = math.sqrt(nz)
+        x = z / nz
+    return est
+
+
+def rel_error_power_method(approx, ref, iters, seed):
+    """proj/src/linalg.cpp:206-218."""
+    n = ref.shape[0]
+    err = _power_norm_diff(approx, ref, iters, mix_seed(seed, 11), n)
+    base = _power_norm_diff(ref, None, iters, mix_seed(seed, 12), n)
+    if base == 0.0:
+        return 0.0 if err == 0.0 else math.inf
+    return err / base
+
+
+def synth_rank_structured(tree, adj, k, seed):
+    """proj/src/operators.cpp:375-448, H1 format: per-pair rank-k blocks and
+    Gaussian dense leaf blocks."""
+    n = tree.num_points
+    if n > 4096:
+        raise ValueError("synthetic dense capped at 4096")
+    a = np.zeros((n, n))
+    for l in range(2, tree.depth + 1):
+        for al, be in admissible_pairs(tree, adj, l):
+            rows, cols = tree.box(al).points, tree.box(be).points
+            gu = gaussian_matrix(len(rows), k, mix_seed(seed, 201, al, be))
+            gv = gaussian_matrix(k, len(cols), mix_seed(seed, 202, al, be))
+            a[np.ix_(rows, cols)] = gu @ gv / math.sqrt(k)
+    for lam, mu in dense_pairs(tree, adj):
+        rows, cols = tree.box(lam).points, tree.box(mu).points
+        a[np.ix_(rows, cols)] = gaussian_matrix(len(rows), len(cols), mix_seed(seed, 204, lam, mu))
+    return a

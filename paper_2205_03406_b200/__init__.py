@@ -1,0 +1,446 @@
+"""B200-native H1 graph-colored peeling core (arxiv 2205.03406).
+
+Python surface mirroring the reference binding ``hpeel``
+(proj/bindings/module.cpp:97-230): ``gaussian_matrix``, ``build_tree``,
+``level_coloring``, ``dense_operator``, ``compress``, ``rel_error_power_method``
+and the point generators, plus the on-the-fly kernel operators of
+BASELINE.json. Every call goes through the C ABI of ``libhpeel_b200.so``; the
+compression itself runs in hand-written sm_100a kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, fmat, iptr, lptr, lib
+
+__all__ = [
+    "gaussian_matrix", "mix_seed", "random_cloud", "equispaced_1d", "uniform_grid_points",
+    "BoxTree", "build_tree", "Plan", "plan", "level_coloring", "dsatur",
+    "Operator", "dense_operator", "kernel_operator", "CompressedRep", "compress",
+    "rel_error_power_method", "device_count", "debug_payload",
+]
+
+MODES = {"h1": 0, "unif-stage1": 1, "unif-stage2": 2, "leaf": 3}
+FORMATS = {"h1": 0, "unif-h1": 1, "h1-plus-unif": 2, "h2": 3}
+STRATEGIES = {"graph": 0, "fallback-pattern": 1}
+KERNELS = {"log": 1, "invdist4pi": 2, "exp": 3}
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(lib().hp_device_count(C.byref(n)))
+    return n.value
+
+
+def mix_seed(seed: int, *tags: int) -> int:
+    for t in tags:
+        seed = lib().hp_mix_seed(seed, t)
+    return int(seed)
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """proj/src/rng.cpp:35-59 (row-major Box-Muller stream)."""
+    out = np.zeros((rows, cols), dtype=np.float64, order="F")
+    check(lib().hp_gaussian_matrix(rows, cols, seed, dptr(out)))
+    return out
+
+
+def random_cloud(n: int, dim: int, seed: int) -> np.ndarray:
+    """proj/src/operators.cpp:88-95."""
+    out = np.zeros((n, dim), dtype=np.float64, order="F")
+    check(lib().hp_random_cloud(n, dim, seed, dptr(out)))
+    return out
+
+
+def equispaced_1d(n: int) -> np.ndarray:
+    """proj/src/operators.cpp:97-103: (i + 0.5) / n."""
+    return ((np.arange(n, dtype=np.float64) + 0.5) / float(n))[:, None]
+
+
+def uniform_grid_points(per_dim: int, dim: int) -> np.ndarray:
+    """proj/src/operators.cpp:74-86 (cell centers, dimension 0 fastest)."""
+    total = per_dim ** dim
+    idx = np.arange(total)
+    out = np.empty((total, dim))
+    for j in range(dim):
+        out[:, j] = ((idx % per_dim).astype(np.float64) + 0.5) / float(per_dim)
+        idx = idx // per_dim
+    return out
+
+
+class BoxTree:
+    """BoxTree + AdjacencyInfo handle (binding PyTree, module.cpp:12-26)."""
+
+    def __init__(self, handle, points: np.ndarray):
+        self._h = C.c_void_p(handle)
+        self.raw_points = points
+        info = np.zeros(8, dtype=np.int64)
+        check(lib().hp_tree_info(self._h, lptr(info)))
+        (self.num_points, self.dim, self.depth, self.num_boxes, self.max_leaf_size,
+         fp, self.leaf_capacity, self._npts) = (int(v) for v in info)
+        self.fully_populated = bool(fp)
+        self._boxes = None
+        self._lists = {}
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().hp_tree_free(self._h)
+        except Exception:
+            pass
+
+    def _box_arrays(self):
+        if self._boxes is None:
+            nb = self.num_boxes
+            level = np.zeros(nb, dtype=np.int32)
+            parent = np.zeros(nb, dtype=np.int32)
+            coord = np.zeros((nb, self.dim), dtype=np.int64)
+            off = np.zeros(nb + 1, dtype=np.int64)
+            pts = np.zeros(max(self._npts, 1), dtype=np.int32)
+            check(lib().hp_tree_boxes(self._h, iptr(level), iptr(parent), lptr(coord), lptr(off), iptr(pts)))
+            self._boxes = (level, parent, coord, off, pts)
+        return self._boxes
+
+    def _list(self, which):
+        if which not in self._lists:
+            off = np.zeros(self.num_boxes + 1, dtype=np.int64)
+            check(lib().hp_tree_lists(self._h, which, lptr(off), None))
+            items = np.zeros(max(int(off[-1]), 1), dtype=np.int32)
+            check(lib().hp_tree_lists(self._h, which, lptr(off), iptr(items)))
+            self._lists[which] = (off, items)
+        return self._lists[which]
+
+    def _get(self, which, box):
+        off, items = self._list(which)
+        return [int(v) for v in items[off[box]:off[box + 1]]]
+
+    def level_boxes(self, level: int):
+        lv = self._box_arrays()[0]
+        return [int(i) for i in np.nonzero(lv == level)[0]]
+
+    def box_level(self, box: int) -> int:
+        return int(self._box_arrays()[0][box])
+
+    def box_parent(self, box: int) -> int:
+        return int(self._box_arrays()[1][box])
+
+    def box_coord(self, box: int):
+        return [int(v) for v in self._box_arrays()[2][box]]
+
+    def box_points(self, box: int):
+        off, pts = self._box_arrays()[3:]
+        return [int(v) for v in pts[off[box]:off[box + 1]]]
+
+    def children(self, box: int):
+        return self._get(4, box)
+
+    def neighbors(self, box: int):
+        return self._get(0, box)
+
+    def interaction(self, box: int):
+        return self._get(1, box)
+
+    def coarse_leaf_neighbors(self, box: int):
+        return self._get(2, box)
+
+    def dense_partners(self, box: int):
+        return self._get(3, box)
+
+    @property
+    def cross_level_adjacencies(self) -> int:
+        return int(lib().hp_tree_cross_level_adjacencies(self._h))
+
+    def _pairs(self, level):
+        cnt = C.c_int64(0)
+        check(lib().hp_tree_pairs(self._h, level, C.byref(cnt), None))
+        arr = np.zeros(max(2 * cnt.value, 2), dtype=np.int32)
+        check(lib().hp_tree_pairs(self._h, level, C.byref(cnt), iptr(arr)))
+        return [(int(arr[2 * i]), int(arr[2 * i + 1])) for i in range(cnt.value)]
+
+    def admissible_pairs(self, level: int):
+        return self._pairs(level)
+
+    def dense_pairs(self):
+        return self._pairs(-1)
+
+    def layout(self):
+        """Device tree order: (perm, start, count)."""
+        perm = np.zeros(self.num_points, dtype=np.int32)
+        start = np.zeros(self.num_boxes, dtype=np.int64)
+        count = np.zeros(self.num_boxes, dtype=np.int64)
+        check(lib().hp_tree_layout(self._h, iptr(perm), lptr(start), lptr(count)))
+        return perm, start, count
+
+
+def build_tree(points, leaf_capacity: int) -> BoxTree:
+    """PointCloud::from_raw + BoxTree::build + adjacency (module.cpp:19-26)."""
+    pts = fmat(points)
+    h = C.c_void_p()
+    check(lib().hp_tree_build(dptr(pts), pts.shape[0], pts.shape[1], int(leaf_capacity), C.byref(h)))
+    return BoxTree(h.value, pts)
+
+
+class Plan:
+    """make_plan output for one level (proj/src/peeling.cpp:98-154)."""
+
+    def __init__(self, tree: BoxTree, level: int, mode: str, width: int, seed: int, phase: int,
+                 pairwise: bool = False):
+        self.tree = tree
+        self.width = width
+        h = C.c_void_p()
+        check(lib().hp_plan_build(tree._h, level, MODES[mode], width, seed, phase, int(pairwise), C.byref(h)))
+        self._h = h
+        info = np.zeros(8, dtype=np.int64)
+        check(lib().hp_plan_info(h, lptr(info)))
+        self.n_vertices, self.n_edges, self.n_colors, self.queue_ops = (int(v) for v in info[:4])
+        npay, nzero, nown, nmp = (int(v) for v in info[4:])
+        nv = self.n_vertices
+        pay_off = np.zeros(nv + 1, dtype=np.int64)
+        zero_off = np.zeros(nv + 1, dtype=np.int64)
+        own_off = np.zeros(nv + 1, dtype=np.int64)
+        pay_box = np.zeros(max(npay, 1), dtype=np.int32)
+        pay_tag = np.zeros(max(npay, 1), dtype=np.int32)
+        zero = np.zeros(max(nzero, 1), dtype=np.int32)
+        owners = np.zeros(max(2 * nown, 2), dtype=np.int32)
+        check(lib().hp_plan_sets(h, lptr(pay_off), iptr(pay_box), iptr(pay_tag), lptr(zero_off),
+                                 iptr(zero), lptr(own_off), iptr(owners)))
+        self.sets = []
+        for i in range(nv):
+            self.sets.append({
+                "payload": [(int(pay_box[j]), int(pay_tag[j])) for j in range(pay_off[i], pay_off[i + 1])],
+                "zero": [int(z) for z in zero[zero_off[i]:zero_off[i + 1]]],
+                "owners": [(int(owners[2 * j]), int(owners[2 * j + 1])) for j in range(own_off[i], own_off[i + 1])],
+            })
+        goff = np.zeros(nv + 1, dtype=np.int64)
+        check(lib().hp_plan_graph(h, lptr(goff), None))
+        gadj = np.zeros(max(int(goff[-1]), 1), dtype=np.int32)
+        check(lib().hp_plan_graph(h, lptr(goff), iptr(gadj)))
+        self.edges = [[int(w) for w in gadj[goff[v]:goff[v + 1]]] for v in range(nv)]
+        color = np.zeros(max(nv, 1), dtype=np.int32)
+        dcolor = np.zeros(max(nv, 1), dtype=np.int32)
+        dn = C.c_int(0)
+        check(lib().hp_plan_coloring(h, iptr(color), iptr(dcolor), C.byref(dn)))
+        self.color = [int(c) for c in color[:nv]]
+        self.dsatur_color = [int(c) for c in dcolor[:nv]]
+        self.dsatur_colors = dn.value
+        moff = np.zeros(self.n_colors + 1, dtype=np.int64)
+        mbox = np.zeros(max(nmp, 1), dtype=np.int32)
+        if nv:
+            check(lib().hp_plan_matrices(h, lptr(moff), iptr(mbox)))
+        self.color_payload = [[int(b) for b in mbox[moff[c]:moff[c + 1]]] for c in range(self.n_colors)]
+
+    def __del__(self):
+        try:
+            lib().hp_plan_free(self._h)
+        except Exception:
+            pass
+
+    def block_to_matrix(self):
+        out = {}
+        for i, s in enumerate(self.sets):
+            for o in s["owners"]:
+                out[o] = self.color[i]
+        return out
+
+    def realize(self, color: int) -> np.ndarray:
+        out = np.zeros((self.tree.num_points, self.width), order="F")
+        check(lib().hp_plan_realize(self._h, color, dptr(out)))
+        return out
+
+
+def plan(tree, level, mode="h1", width=10, seed=0, phase=0, pairwise=False) -> Plan:
+    return Plan(tree, level, mode, width, seed, phase, pairwise)
+
+
+def level_coloring(tree: BoxTree, level: int, mode: str) -> dict:
+    """module.cpp:190-205."""
+    p = Plan(tree, level, mode, 1, 0, 0)
+    return {"n_vertices": p.n_vertices, "n_edges": p.n_edges, "n_colors": p.n_colors}
+
+
+def dsatur(edges):
+    """DSatur (proj/src/coloring.cpp:169-216) on an explicit adjacency list."""
+    nv = len(edges)
+    off = np.zeros(nv + 1, dtype=np.int64)
+    for v, e in enumerate(edges):
+        off[v + 1] = off[v] + len(e)
+    adj = np.array([w for e in edges for w in sorted(e)] or [0], dtype=np.int32)
+    color = np.zeros(max(nv, 1), dtype=np.int32)
+    nc = C.c_int(0)
+    qops = C.c_int64(0)
+    check(lib().hp_dsatur(nv, lptr(off), iptr(adj), iptr(color), C.byref(nc), C.byref(qops)))
+    return {"color": [int(c) for c in color[:nv]], "num_colors": nc.value, "queue_ops": qops.value}
+
+
+class Operator:
+    """Device-resident black box (LinearOperator, linear_operator.hpp:12-24)."""
+
+    def __init__(self, handle, n):
+        self._h = C.c_void_p(handle)
+        self.shape = (n, n)
+
+    def __del__(self):
+        try:
+            lib().hp_op_free(self._h)
+        except Exception:
+            pass
+
+    def _apply(self, x, adjoint):
+        x = fmat(x)
+        y = np.zeros_like(x, order="F")
+        check(lib().hp_op_apply(self._h, int(adjoint), dptr(x), x.shape[1], dptr(y)))
+        return y
+
+    def apply(self, x):
+        return self._apply(x, False)
+
+    def apply_adjoint(self, x):
+        return self._apply(x, True)
+
+
+def dense_operator(a, device: int = 0) -> Operator:
+    a = fmat(a)
+    h = C.c_void_p()
+    check(lib().hp_op_dense(dptr(a), a.shape[0], device, C.byref(h)))
+    return Operator(h.value, a.shape[0])
+
+
+def kernel_operator(kind: str, points, param: float = 1.0, device: int = 0) -> Operator:
+    """On-the-fly kernel black box over raw coordinates (BASELINE.json configs)."""
+    pts = fmat(points)
+    h = C.c_void_p()
+    check(lib().hp_op_kernel(KERNELS[kind], dptr(pts), pts.shape[0], pts.shape[1], float(param), device, C.byref(h)))
+    return Operator(h.value, pts.shape[0])
+
+
+class CompressedRep:
+    """Device-resident H1Rep (hmatrix.hpp:52-70) + RunReport."""
+
+    def __init__(self, handle, tree: BoxTree, rank: int, oversample: int):
+        self._h = C.c_void_p(handle)
+        self.tree = tree
+        self.rank = rank
+        self.width = rank + oversample
+        self.format = "h1"
+        totals = np.zeros(6)
+        nph = C.c_int64(0)
+        check(lib().hp_rep_report(self._h, dptr(totals), C.byref(nph)))
+        ln = C.c_int64(0)
+        check(lib().hp_rep_csv(self._h, None, 0, C.byref(ln)))
+        buf = C.create_string_buffer(ln.value + 1)
+        check(lib().hp_rep_csv(self._h, buf, ln.value + 1, C.byref(ln)))
+        phases = []
+        for i in range(nph.value):
+            ints = np.zeros(6, dtype=np.int64)
+            times = np.zeros(8)
+            check(lib().hp_rep_phase(self._h, i, lptr(ints), dptr(times)))
+            phases.append({
+                "phase": "leaf" if ints[0] else "h1", "level": int(ints[1]), "colors": int(ints[2]),
+                "forward_cols": int(ints[3]), "adjoint_cols": int(ints[4]), "net_flops": int(ints[5]),
+                "wall_ms_total": times[0], "wall_ms_net": times[1], "apply_ms": times[2],
+                "peel_ms": times[3], "qr_ms": times[4], "bsolve_ms": times[5],
+                "apply_flops": times[6], "kernel_evals": times[7],
+            })
+        self.report = {
+            "forward_cols": int(totals[0]), "adjoint_cols": int(totals[1]),
+            "max_sampling_colors": int(totals[2]), "wall_s_total": totals[3],
+            "wall_s_net": totals[4], "net_flops": int(totals[5]), "csv": buf.value.decode(),
+            "phases": phases,
+        }
+
+    def __del__(self):
+        try:
+            lib().hp_rep_free(self._h)
+        except Exception:
+            pass
+
+    def _apply(self, x, adjoint):
+        x = fmat(x)
+        y = np.zeros_like(x, order="F")
+        check(lib().hp_rep_apply(self._h, int(adjoint), dptr(x), x.shape[1], dptr(y)))
+        return y
+
+    def apply(self, x):
+        return self._apply(x, False)
+
+    def apply_adjoint(self, x):
+        return self._apply(x, True)
+
+    def num_pairs(self, level: int) -> int:
+        c = C.c_int64(0)
+        check(lib().hp_rep_num_pairs(self._h, level, C.byref(c)))
+        return c.value
+
+    def block(self, level: int, pair: int):
+        """(U, B, V) of admissible_pairs(level)[pair], rows in box.points order."""
+        ku, kv = C.c_int(0), C.c_int(0)
+        check(lib().hp_rep_block(self._h, level, pair, C.byref(ku), C.byref(kv), None, None, None))
+        a, b = self.tree.admissible_pairs(level)[pair]
+        ma, mb = len(self.tree.box_points(a)), len(self.tree.box_points(b))
+        u = np.zeros((ma, ku.value), order="F")
+        bb = np.zeros((ku.value, kv.value), order="F")
+        v = np.zeros((mb, kv.value), order="F")
+        check(lib().hp_rep_block(self._h, level, pair, C.byref(ku), C.byref(kv), dptr(u), dptr(bb), dptr(v)))
+        return u, bb, v
+
+    def dense_block(self, pair: int) -> np.ndarray:
+        lam, mu = self.tree.dense_pairs()[pair]
+        d = np.zeros((len(self.tree.box_points(lam)), len(self.tree.box_points(mu))), order="F")
+        check(lib().hp_rep_dense_block(self._h, pair, dptr(d)))
+        return d
+
+    def captured(self, level: int, pair: int) -> np.ndarray:
+        """Post-peel samples [Y | Z] of a pair (level < 0: leaf probe block)."""
+        rows, cols = C.c_int64(0), C.c_int64(0)
+        check(lib().hp_rep_captured(self._h, level, pair, C.byref(rows), C.byref(cols), None))
+        out = np.zeros((rows.value, cols.value), order="F")
+        check(lib().hp_rep_captured(self._h, level, pair, C.byref(rows), C.byref(cols), dptr(out)))
+        return out
+
+    def storage(self) -> dict:
+        t = C.c_int64(0)
+        check(lib().hp_rep_storage(self._h, C.byref(t)))
+        return {"total": t.value, "per_dof": t.value / float(self.tree.num_points)}
+
+    def sizes(self):
+        f, d = C.c_int64(0), C.c_int64(0)
+        check(lib().hp_rep_sizes(self._h, C.byref(f), C.byref(d)))
+        return f.value, d.value
+
+    def export(self, host_factors: np.ndarray, host_dense: np.ndarray) -> int:
+        """Bulk device->host copy of the whole representation; returns bytes."""
+        b = C.c_int64(0)
+        check(lib().hp_rep_export(self._h, dptr(host_factors), dptr(host_dense), C.byref(b)))
+        return b.value
+
+
+def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, oversample: int = 10,
+             tol: float = 0.0, seed: int = 0, strategy: str = "graph", capture: bool = False) -> CompressedRep:
+    """compress_py (module.cpp:65-93) on the device; fixed-rank H1 only."""
+    if format not in FORMATS:
+        raise ValueError("unknown format: " + format)
+    if strategy not in STRATEGIES:
+        raise ValueError("unknown strategy: " + strategy)
+    if tol > 0.0:
+        raise ValueError("relative-tolerance truncation is outside the H1 fixed-rank hot path")
+    h = C.c_void_p()
+    check(lib().hp_compress(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
+                            STRATEGIES[strategy], int(capture), C.byref(h)))
+    return CompressedRep(h.value, tree, rank, oversample)
+
+
+def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, seed: int = 0) -> float:
+    """proj/src/linalg.cpp:206-218 (module.cpp:219-229)."""
+    out = C.c_double(0.0)
+    check(lib().hp_rel_error_power_method(rep._h, ref._h, int(iters), int(seed), C.byref(out)))
+    return out.value
+
+
+def debug_payload(tree: BoxTree, level: int, r: int, seed: int, device: int = 0) -> np.ndarray:
+    """K1 probe: n x 2r payload rows (input order) generated on the device."""
+    out = np.zeros((tree.num_points, 2 * r), order="F")
+    check(lib().hp_debug_payload(tree._h, level, r, seed, device, dptr(out)))
+    return out

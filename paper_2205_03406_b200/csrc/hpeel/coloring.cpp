@@ -1,0 +1,372 @@
+// Sampling plan; see coloring.hpp for the reference mapping.
+#include "coloring.hpp"
+
+#include <algorithm>
+#include <queue>
+#include <stdexcept>
+#include <tuple>
+
+#include "rng.hpp"
+
+namespace hpeel {
+
+namespace {
+
+std::vector<int> merge_sorted(const std::vector<int>& a, const std::vector<int>& b) {
+  std::vector<int> out;
+  out.reserve(a.size() + b.size());
+  std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
+  return out;
+}
+
+void drop(std::vector<int>& v, int value) {
+  v.erase(std::remove(v.begin(), v.end(), value), v.end());
+}
+
+// Dedup keyed by the literal (payload, zero) requirement
+// (proj/src/coloring.cpp:26-51); first occurrence fixes the vertex id.
+class Dedup {
+ public:
+  void add(std::vector<std::pair<int, PayloadTag>> payload, std::vector<int> zero,
+           std::pair<int, int> owner) {
+    auto key = std::make_pair(std::move(payload), std::move(zero));
+    auto it = index_.find(key);
+    if (it != index_.end()) {
+      sets_[size_t(it->second)].owners.push_back(owner);
+      return;
+    }
+    ConstraintSet s;
+    s.payload = key.first;
+    s.zero = key.second;
+    s.owners.push_back(owner);
+    index_.emplace(std::move(key), int(sets_.size()));
+    sets_.push_back(std::move(s));
+  }
+  std::vector<ConstraintSet> take() { return std::move(sets_); }
+
+ private:
+  std::map<std::pair<std::vector<std::pair<int, PayloadTag>>, std::vector<int>>, int> index_;
+  std::vector<ConstraintSet> sets_;
+};
+
+}  // namespace
+
+std::vector<ConstraintSet> build_constraints(const BoxTree& tree, const AdjacencyInfo& adj,
+                                             int level, SampleMode mode) {
+  Dedup dd;
+  switch (mode) {
+    case SampleMode::kH1: {
+      int last_alpha = -1;
+      std::vector<int> reach;
+      for (auto [alpha, beta] : admissible_pairs(tree, adj, level)) {
+        if (alpha != last_alpha) {
+          reach = merge_sorted(adj.neighbors[size_t(alpha)],
+                               merge_sorted(adj.interaction[size_t(alpha)],
+                                            adj.coarse_leaf_neighbors[size_t(alpha)]));
+          last_alpha = alpha;
+        }
+        std::vector<int> zero = reach;
+        drop(zero, beta);
+        dd.add({{beta, PayloadTag::kGaussian}}, std::move(zero), {alpha, beta});
+      }
+      break;
+    }
+    case SampleMode::kUnifStage1: {
+      if (level < 2 || level > tree.depth()) throw std::invalid_argument("sampling level out of range");
+      for (int alpha : tree.level_boxes(level)) {
+        if (adj.interaction[size_t(alpha)].empty()) continue;
+        std::vector<std::pair<int, PayloadTag>> payload;
+        for (int beta : adj.interaction[size_t(alpha)]) payload.emplace_back(beta, PayloadTag::kGaussian);
+        dd.add(std::move(payload),
+               merge_sorted(adj.neighbors[size_t(alpha)], adj.coarse_leaf_neighbors[size_t(alpha)]),
+               {alpha, -1});
+      }
+      break;
+    }
+    case SampleMode::kLeaf: {
+      for (auto [lambda, mu] : dense_pairs(tree, adj)) {
+        std::vector<int> zero = adj.dense_partners[size_t(lambda)];
+        drop(zero, mu);
+        dd.add({{mu, PayloadTag::kIdentity}}, std::move(zero), {lambda, mu});
+      }
+      break;
+    }
+    case SampleMode::kUnifStage2:
+      throw std::invalid_argument("unif-stage2 constraints need the uniform driver (out of scope)");
+  }
+  return dd.take();
+}
+
+bool incompatible(const ConstraintSet& a, const ConstraintSet& b) {
+  auto hits = [](const ConstraintSet& s, const ConstraintSet& t) {
+    auto p = s.payload.begin();
+    auto z = t.zero.begin();
+    while (p != s.payload.end() && z != t.zero.end()) {
+      if (p->first < *z) ++p;
+      else if (*z < p->first) ++z;
+      else return true;
+    }
+    return false;
+  };
+  if (hits(a, b) || hits(b, a)) return true;
+  auto x = a.payload.begin();
+  auto y = b.payload.begin();
+  while (x != a.payload.end() && y != b.payload.end()) {
+    if (x->first < y->first) ++x;
+    else if (y->first < x->first) ++y;
+    else {
+      if (x->second != y->second) return true;
+      ++x;
+      ++y;
+    }
+  }
+  return false;
+}
+
+std::size_t IncompatibilityGraph::num_edges() const {
+  std::size_t e = 0;
+  for (const auto& a : edges) e += a.size();
+  return e / 2;
+}
+
+int IncompatibilityGraph::max_degree() const {
+  std::size_t d = 0;
+  for (const auto& a : edges) d = std::max(d, a.size());
+  return int(d);
+}
+
+IncompatibilityGraph build_graph(const std::vector<ConstraintSet>& sets) {
+  IncompatibilityGraph g;
+  g.num_vertices = int(sets.size());
+  g.edges.resize(sets.size());
+  int max_box = -1;
+  for (const auto& s : sets) {
+    for (auto& p : s.payload) max_box = std::max(max_box, p.first);
+    for (int z : s.zero) max_box = std::max(max_box, z);
+  }
+  // CSR inverted indexes: which sets zero a box, which sets carry it.
+  const size_t nb = size_t(max_box + 1);
+  std::vector<int> zoff(nb + 1, 0), poff(nb + 1, 0);
+  for (const auto& s : sets) {
+    for (int z : s.zero) ++zoff[size_t(z) + 1];
+    for (auto& p : s.payload) ++poff[size_t(p.first) + 1];
+  }
+  for (size_t b = 0; b < nb; ++b) {
+    zoff[b + 1] += zoff[b];
+    poff[b + 1] += poff[b];
+  }
+  std::vector<int> zsets(size_t(zoff[nb])), psets(size_t(poff[nb]));
+  std::vector<PayloadTag> ptags(size_t(poff[nb]));
+  {
+    std::vector<int> zc(zoff.begin(), zoff.end() - 1), pc(poff.begin(), poff.end() - 1);
+    for (size_t i = 0; i < sets.size(); ++i) {
+      for (int z : sets[i].zero) zsets[size_t(zc[size_t(z)]++)] = int(i);
+      for (auto& p : sets[i].payload) {
+        ptags[size_t(pc[size_t(p.first)])] = p.second;
+        psets[size_t(pc[size_t(p.first)]++)] = int(i);
+      }
+    }
+  }
+  for (size_t i = 0; i < sets.size(); ++i) {
+    for (auto& [box, tag] : sets[i].payload) {
+      for (int k = zoff[size_t(box)]; k < zoff[size_t(box) + 1]; ++k) {
+        const int j = zsets[size_t(k)];
+        if (j == int(i)) continue;
+        g.edges[i].push_back(j);
+        g.edges[size_t(j)].push_back(int(i));
+      }
+      for (int k = poff[size_t(box)]; k < poff[size_t(box) + 1]; ++k) {
+        const int j = psets[size_t(k)];
+        if (j != int(i) && ptags[size_t(k)] != tag) g.edges[i].push_back(j);
+      }
+    }
+  }
+  for (auto& e : g.edges) {
+    std::sort(e.begin(), e.end());
+    e.erase(std::unique(e.begin(), e.end()), e.end());
+  }
+  return g;
+}
+
+IncompatibilityGraph build_graph_pairwise(const std::vector<ConstraintSet>& sets) {
+  IncompatibilityGraph g;
+  g.num_vertices = int(sets.size());
+  g.edges.resize(sets.size());
+  for (size_t i = 0; i < sets.size(); ++i)
+    for (size_t j = i + 1; j < sets.size(); ++j)
+      if (incompatible(sets[i], sets[j])) {
+        g.edges[i].push_back(int(j));
+        g.edges[j].push_back(int(i));
+      }
+  return g;
+}
+
+Coloring dsatur_color(const IncompatibilityGraph& graph) {
+  const int n = graph.num_vertices;
+  Coloring out;
+  out.color.assign(size_t(n), -1);
+  if (n == 0) return out;
+  std::vector<std::vector<int>> seen(static_cast<size_t>(n));  // sorted distinct neighbor colors
+  std::vector<int> udeg(static_cast<size_t>(n));
+  std::vector<std::uint64_t> stamp(size_t(n), 0);
+  using Entry = std::tuple<int, int, int, std::uint64_t>;
+  std::priority_queue<Entry> heap;
+  for (int v = 0; v < n; ++v) {
+    udeg[size_t(v)] = int(graph.edges[size_t(v)].size());
+    heap.emplace(0, udeg[size_t(v)], -v, 0);
+    ++out.queue_ops;
+  }
+  int done = 0;
+  while (done < n) {
+    auto [sat, ud, negv, st] = heap.top();
+    heap.pop();
+    ++out.queue_ops;
+    const int v = -negv;
+    if (out.color[size_t(v)] != -1 || st != stamp[size_t(v)]) continue;
+    int c = 0;
+    for (int used : seen[size_t(v)]) {
+      if (used == c) ++c;
+      else if (used > c) break;
+    }
+    out.color[size_t(v)] = c;
+    out.num_colors = std::max(out.num_colors, c + 1);
+    ++done;
+    for (int w : graph.edges[size_t(v)]) {
+      if (out.color[size_t(w)] != -1) continue;
+      --udeg[size_t(w)];
+      auto& sw = seen[size_t(w)];
+      auto pos = std::lower_bound(sw.begin(), sw.end(), c);
+      if (pos == sw.end() || *pos != c) sw.insert(pos, c);
+      ++stamp[size_t(w)];
+      heap.emplace(int(sw.size()), udeg[size_t(w)], -w, stamp[size_t(w)]);
+      ++out.queue_ops;
+    }
+  }
+  return out;
+}
+
+Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets,
+                       const IncompatibilityGraph& graph, SampleMode mode) {
+  Coloring best = dsatur_color(graph);
+  if (mode == SampleMode::kUnifStage2 || !tree.is_fully_populated()) return best;
+  const int mod = mode == SampleMode::kH1 ? 6 : mode == SampleMode::kUnifStage1 ? 5 : 3;
+  std::vector<int> tile(sets.size());
+  std::map<int, int> relabel;
+  for (size_t i = 0; i < sets.size(); ++i) {
+    const int box = mode == SampleMode::kUnifStage1 ? sets[i].owners.front().first
+                                                    : sets[i].payload.front().first;
+    int idx = 0, mul = 1;
+    for (std::int64_t c : tree.box(box).coord) {
+      idx += int(c % mod) * mul;
+      mul *= mod;
+    }
+    auto ins = relabel.emplace(idx, int(relabel.size()));
+    tile[i] = ins.first->second;
+  }
+  if (int(relabel.size()) < best.num_colors) {
+    best.color = std::move(tile);
+    best.num_colors = int(relabel.size());
+  }
+  return best;
+}
+
+Matrix gaussian_matrix(Index rows, Index cols, std::uint64_t seed) {
+  if (rows < 0 || cols < 0) throw std::invalid_argument("negative shape");
+  Matrix out(rows, cols);
+  SplitMix64 stream(seed);
+  bool have_spare = false;
+  double spare = 0.0;
+  for (Index i = 0; i < rows; ++i) {
+    for (Index j = 0; j < cols; ++j) {
+      if (have_spare) {
+        out(i, j) = spare;
+        have_spare = false;
+        continue;
+      }
+      const double u1 = stream.next_open_closed();
+      const double u2 = stream.next_closed_open();
+      const double radius = std::sqrt(-2.0 * std::log(u1));
+      const double angle = 2.0 * M_PI * u2;
+      out(i, j) = radius * std::cos(angle);
+      spare = radius * std::sin(angle);
+      have_spare = true;
+    }
+  }
+  return out;
+}
+
+Matrix payload_gaussian(const BoxTree& tree, int box, int width, std::uint64_t seed, int level,
+                        int phase) {
+  return gaussian_matrix(Index(tree.box(box).points.size()), width,
+                         payload_seed(seed, level, box, phase));
+}
+
+Matrix BlockTestMatrix::realize(const BoxTree& tree) const {
+  Matrix out(rows, width);
+  for (auto [box, tag] : payload) {
+    const auto& pts = tree.box(box).points;
+    if (tag == PayloadTag::kGaussian) {
+      const Matrix g = payload_gaussian(tree, box, width, seed, level, phase);
+      for (size_t r = 0; r < pts.size(); ++r)
+        for (int c = 0; c < width; ++c) out(pts[r], c) = g(Index(r), c);
+    } else if (tag == PayloadTag::kIdentity) {
+      for (size_t r = 0; r < pts.size(); ++r)
+        for (int c = 0; c < width; ++c) out(pts[r], c) = (Index(r) == c) ? 1.0 : 0.0;
+    } else {
+      throw std::runtime_error("missing basis for payload box");
+    }
+  }
+  return out;
+}
+
+std::vector<BlockTestMatrix> assemble_test_matrices(const std::vector<ConstraintSet>& sets,
+                                                    const Coloring& coloring, const BoxTree& tree,
+                                                    int level, int width, std::uint64_t seed,
+                                                    int phase) {
+  std::vector<BlockTestMatrix> mats(size_t(coloring.num_colors));
+  std::vector<std::map<int, PayloadTag>> merged(size_t(coloring.num_colors));
+  std::vector<std::vector<int>> zeros(size_t(coloring.num_colors));
+  for (size_t i = 0; i < sets.size(); ++i) {
+    const int c = coloring.color[i];
+    mats[size_t(c)].serves.push_back(int(i));
+    for (auto [box, tag] : sets[i].payload) {
+      auto ins = merged[size_t(c)].emplace(box, tag);
+      if (!ins.second && ins.first->second != tag) {
+        throw std::logic_error("conflicting payload tags within a color");
+      }
+      if (tag == PayloadTag::kBasis) throw std::runtime_error("missing basis for payload box");
+    }
+    zeros[size_t(c)].insert(zeros[size_t(c)].end(), sets[i].zero.begin(), sets[i].zero.end());
+  }
+  for (int c = 0; c < coloring.num_colors; ++c) {
+    auto& m = mats[size_t(c)];
+    m.payload.assign(merged[size_t(c)].begin(), merged[size_t(c)].end());
+    auto& z = zeros[size_t(c)];
+    std::sort(z.begin(), z.end());
+    z.erase(std::unique(z.begin(), z.end()), z.end());
+    m.zero = std::move(z);
+    m.rows = tree.num_points();
+    m.level = level;
+    m.seed = seed;
+    m.phase = phase;
+    m.width = width;
+  }
+  return mats;
+}
+
+SamplingPlan make_plan(const BoxTree& tree, const AdjacencyInfo& adj, int level, SampleMode mode,
+                       int width, std::uint64_t seed, int phase) {
+  SamplingPlan plan;
+  const auto sets = build_constraints(tree, adj, level, mode);
+  if (sets.empty()) return plan;
+  const auto graph = build_graph(sets);
+  const auto coloring = plan_coloring(tree, sets, graph, mode);
+  plan.n_vertices = sets.size();
+  plan.n_edges = graph.num_edges();
+  plan.matrices = assemble_test_matrices(sets, coloring, tree, level, width, seed, phase);
+  for (size_t i = 0; i < sets.size(); ++i)
+    for (const auto& owner : sets[i].owners) plan.block_to_matrix[owner] = coloring.color[i];
+  return plan;
+}
+
+}  // namespace hpeel

@@ -1,0 +1,103 @@
+// Sampling plan: constraint sets, incompatibility graph, DSatur, tile
+// coloring and per-color block test matrices.
+//
+// Restates proj/include/hpeel/coloring.hpp:14-113 and
+// proj/src/coloring.cpp:14-332 for the H1 (kH1) and leaf (kLeaf) modes on the
+// hot path. `build_graph` produces the reference's edge set through an
+// inverted box index instead of the O(V^2) pairwise scan of
+// proj/src/coloring.cpp:154-167; DSatur depends only on the edge set and the
+// vertex numbering (proj/src/coloring.cpp:169-216), so colorings are
+// bit-identical. `build_graph_pairwise` keeps the literal scan for tests.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <utility>
+#include <vector>
+
+#include "box_tree.hpp"
+
+namespace hpeel {
+
+enum class PayloadTag : std::uint8_t { kGaussian = 0, kIdentity = 1, kBasis = 2 };
+enum class SampleMode : std::uint8_t { kH1 = 0, kUnifStage1 = 1, kUnifStage2 = 2, kLeaf = 3 };
+
+struct ConstraintSet {
+  std::vector<std::pair<int, PayloadTag>> payload;  // sorted by box id
+  std::vector<int> zero;                            // sorted
+  std::vector<std::pair<int, int>> owners;
+  bool same_requirements(const ConstraintSet& o) const {
+    return payload == o.payload && zero == o.zero;
+  }
+};
+
+/// proj/src/coloring.cpp:55-113. Modes kH1 and kLeaf (the hot path) and
+/// kUnifStage1 (used by the known-answer tests); kUnifStage2 needs per-box
+/// bases of the uniform driver and throws std::invalid_argument here.
+std::vector<ConstraintSet> build_constraints(const BoxTree& tree, const AdjacencyInfo& adj,
+                                             int level, SampleMode mode);
+
+struct IncompatibilityGraph {
+  int num_vertices = 0;
+  std::vector<std::vector<int>> edges;  // sorted adjacency
+  std::size_t num_edges() const;
+  int max_degree() const;
+};
+
+/// proj/src/coloring.cpp:115-146.
+bool incompatible(const ConstraintSet& a, const ConstraintSet& b);
+
+/// Same edge set as the reference's pairwise scan, via an inverted index.
+IncompatibilityGraph build_graph(const std::vector<ConstraintSet>& sets);
+/// Literal O(V^2) scan of proj/src/coloring.cpp:154-167 (tests only).
+IncompatibilityGraph build_graph_pairwise(const std::vector<ConstraintSet>& sets);
+
+struct Coloring {
+  std::vector<int> color;
+  int num_colors = 0;
+  std::size_t queue_ops = 0;
+};
+
+/// proj/src/coloring.cpp:169-216: max (saturation, uncolored degree, -v),
+/// smallest free color; same lazy max-heap, so queue_ops match.
+Coloring dsatur_color(const IncompatibilityGraph& graph);
+
+/// proj/src/coloring.cpp:218-250.
+Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets,
+                       const IncompatibilityGraph& graph, SampleMode mode);
+
+struct BlockTestMatrix {
+  Index rows = 0;
+  int width = 0;
+  std::uint64_t seed = 0;
+  int level = 0;
+  int phase = 0;
+  std::vector<std::pair<int, PayloadTag>> payload;
+  std::vector<int> zero;
+  std::vector<int> serves;
+  /// Dense N x width realization (proj/src/coloring.cpp:261-291), host
+  /// reference used by tests; the device path never forms dense Omega.
+  Matrix realize(const BoxTree& tree) const;
+};
+
+Matrix payload_gaussian(const BoxTree& tree, int box, int width, std::uint64_t seed, int level,
+                        int phase);
+
+/// proj/src/coloring.cpp:293-332 (Gaussian and identity payloads).
+std::vector<BlockTestMatrix> assemble_test_matrices(const std::vector<ConstraintSet>& sets,
+                                                    const Coloring& coloring, const BoxTree& tree,
+                                                    int level, int width, std::uint64_t seed,
+                                                    int phase);
+
+/// Output of make_plan (proj/src/peeling.cpp:98-154), graph strategy.
+struct SamplingPlan {
+  std::vector<BlockTestMatrix> matrices;
+  std::map<std::pair<int, int>, int> block_to_matrix;
+  std::size_t n_vertices = 0;
+  std::size_t n_edges = 0;
+  int colors() const { return int(matrices.size()); }
+};
+SamplingPlan make_plan(const BoxTree& tree, const AdjacencyInfo& adj, int level, SampleMode mode,
+                       int width, std::uint64_t seed, int phase);
+
+}  // namespace hpeel

@@ -1,0 +1,273 @@
+// K5 coupling-matrix solve (sm_100a): the per-pair B of run_h1
+// (proj/src/peeling.cpp:252-269)
+//   middle = G'^T Y(I_a)            (r x r)
+//   left   = pinv(G'^T U) middle    (k x r)
+//   B      = (pinv((V^T G)^T) left^T)^T
+// with pinv_apply's SVD cutoff 1e-12 * sigma_1 (proj/src/linalg.cpp:110-127).
+// The row reductions (G'^T Y, G'^T U, V^T G) run as chunked Gram tasks with a
+// fixed-order partial sum; the pseudo-inverses use one-sided Jacobi SVD in
+// shared memory, one CTA per pair.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace hpeel {
+
+namespace {
+
+constexpr int kGramThreads = 256;
+constexpr int kGramRows = 32;
+
+template <int E>
+__global__ void __launch_bounds__(kGramThreads)
+gram_kernel(const GramTask* __restrict__ tasks, const double* __restrict__ xb,
+            const double* __restrict__ yb, int nx, int ny, double* __restrict__ out) {
+  extern __shared__ double sm[];
+  double* xs = sm;                    // kGramRows x nx (row-major)
+  double* ys = sm + kGramRows * nx;   // kGramRows x ny (row-major)
+  const GramTask t = tasks[blockIdx.x];
+  const int tid = threadIdx.x;
+  double acc[E];
+#pragma unroll
+  for (int u = 0; u < E; ++u) acc[u] = 0.0;
+  for (int r0 = 0; r0 < t.rows; r0 += kGramRows) {
+    const int cnt = t.rows - r0 < kGramRows ? t.rows - r0 : kGramRows;
+    __syncthreads();
+    for (int e = tid; e < kGramRows * nx; e += kGramThreads) {
+      const int i = e / nx, a = e - i * nx;
+      double v = 0.0;
+      if (i < cnt) {
+        const std::int64_t row = r0 + i;
+        v = t.x_rowmajor ? xb[t.x + row * t.lx + a] : xb[t.x + row + std::int64_t(a) * t.lx];
+      }
+      xs[e] = v;
+    }
+    for (int e = tid; e < kGramRows * ny; e += kGramThreads) {
+      const int i = e / ny, b = e - i * ny;
+      double v = 0.0;
+      if (i < cnt) {
+        const std::int64_t row = r0 + i;
+        v = t.y_rowmajor ? yb[t.y + row * t.ly + b] : yb[t.y + row + std::int64_t(b) * t.ly];
+      }
+      ys[e] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < E; ++u) {
+      const int e = tid + u * kGramThreads;
+      if (e < nx * ny) {
+        const int a = e % nx, b = e / nx;
+        double s = acc[u];
+        for (int i = 0; i < cnt; ++i) s = fma(xs[i * nx + a], ys[i * ny + b], s);
+        acc[u] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const int e = tid + u * kGramThreads;
+    if (e < nx * ny) out[t.out + e] = acc[u];
+  }
+}
+
+__global__ void sum_partials_kernel(const std::int64_t* __restrict__ off, const double* src,
+                                    int len, double* dst) {
+  const int d = blockIdx.x;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    double s = 0.0;
+    for (std::int64_t p = off[d]; p < off[d + 1]; ++p) s += src[p * len + i];
+    dst[std::int64_t(d) * len + i] = s;
+  }
+}
+
+constexpr int kSvdThreads = 256;
+constexpr int kSvdWarps = kSvdThreads / 32;
+
+__device__ __forceinline__ double wsum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One-sided Jacobi on the n columns of c (m x n, ld m) with v (n x n) = I
+// accumulated: afterwards c = W (orthogonal columns), sigma_j = |W_j|.
+// Round-robin pair schedule; warps take disjoint pairs.
+__device__ void jacobi(double* c, double* v, int m, int n, int* done) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < n * n; e += kSvdThreads) v[e] = (e % n == e / n) ? 1.0 : 0.0;
+  const int np = n + (n & 1);  // even player count (one dummy when n is odd)
+  const double conv = 4.0e-16 * sqrt(double(m));
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) *done = 1;
+    __syncthreads();
+    for (int round = 0; round < np - 1; ++round) {
+      for (int pr = warp; pr < np / 2; pr += kSvdWarps) {
+        // circle method: player np-1 fixed, others rotate
+        int p = pr == 0 ? np - 1 : (round + pr) % (np - 1);
+        int q = pr == 0 ? round : (round + np - 1 - pr) % (np - 1);
+        if (p >= n || q >= n) continue;
+        if (p > q) { const int t = p; p = q; q = t; }
+        double* cp = c + p * m;
+        double* cq = c + q * m;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int i = lane; i < m; i += 32) {
+          a = fma(cp[i], cp[i], a);
+          b = fma(cq[i], cq[i], b);
+          g = fma(cp[i], cq[i], g);
+        }
+        a = wsum(a);
+        b = wsum(b);
+        g = wsum(g);
+        if (g == 0.0 || fabs(g) <= conv * sqrt(a * b)) continue;
+        if (lane == 0) *done = 0;
+        const double zeta = (b - a) / (2.0 * g);
+        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int i = lane; i < m; i += 32) {
+          const double x = cp[i], y = cq[i];
+          cp[i] = cs * x - sn * y;
+          cq[i] = sn * x + cs * y;
+        }
+        double* vp = v + p * n;
+        double* vq = v + q * n;
+        for (int i = lane; i < n; i += 32) {
+          const double x = vp[i], y = vq[i];
+          vp[i] = cs * x - sn * y;
+          vq[i] = sn * x + cs * y;
+        }
+      }
+      __syncthreads();
+    }
+    if (*done) break;
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
+// inv2[j] = 1 / sigma_j^2 for sigma_j > tol * sigma_max else 0.
+__device__ void pinv_weights(const double* c, int m, int n, double tol, double* inv2) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < n; j += kSvdWarps) {
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s = fma(c[j * m + i], c[j * m + i], s);
+    s = wsum(s);
+    if (lane == 0) inv2[j] = sqrt(s);
+  }
+  __syncthreads();
+  __shared__ double smax;
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < n; ++j) mx = fmax(mx, inv2[j]);
+    smax = mx;
+  }
+  __syncthreads();
+  const double cut = tol * smax;
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += kSvdThreads) {
+    const double sg = inv2[j];
+    inv2[j] = sg > cut && sg > 0.0 ? 1.0 / (sg * sg) : 0.0;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSvdThreads)
+bsolve_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle,
+              const double* __restrict__ vg, int r, int k, double tol,
+              const std::int64_t* __restrict__ boff, double* __restrict__ bout) {
+  extern __shared__ double sm[];
+  double* c = sm;              // r x k
+  double* v = c + r * k;       // k x k
+  double* mid = v + k * k;     // r x r
+  double* left = mid + r * r;  // k x r
+  double* tmp = left + k * r;  // k x r (scratch)
+  double* inv2 = tmp + k * r;  // k
+  __shared__ int done;
+  const std::int64_t p = blockIdx.x;
+  const int tid = threadIdx.x;
+
+  // 1) pinv(G'^T U) middle
+  for (int e = tid; e < r * k; e += kSvdThreads) c[e] = gpu_[p * r * k + e];
+  for (int e = tid; e < r * r; e += kSvdThreads) mid[e] = middle[p * r * r + e];
+  __syncthreads();
+  jacobi(c, v, r, k, &done);
+  pinv_weights(c, r, k, tol, inv2);
+  // tmp = diag(inv2) W^T mid  (k x r)
+  for (int e = tid; e < k * r; e += kSvdThreads) {
+    const int i = e % k, j = e / k;
+    double s = 0.0;
+    if (inv2[i] != 0.0)
+      for (int l = 0; l < r; ++l) s = fma(c[i * r + l], mid[l + j * r], s);
+    tmp[e] = s * inv2[i];
+  }
+  __syncthreads();
+  // left = V tmp  (k x r)
+  for (int e = tid; e < k * r; e += kSvdThreads) {
+    const int i = e % k, j = e / k;
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) s = fma(v[i + l * k], tmp[l + j * k], s);
+    left[e] = s;
+  }
+  __syncthreads();
+  // 2) D = (V^T G)^T = vg^T (r x k)
+  for (int e = tid; e < r * k; e += kSvdThreads) {
+    const int i = e % r, j = e / r;  // D(i, j) = vg(j, i), vg is k x r col-major
+    c[e] = vg[p * k * r + j + std::int64_t(i) * k];
+  }
+  __syncthreads();
+  jacobi(c, v, r, k, &done);
+  pinv_weights(c, r, k, tol, inv2);
+  // B = left W2 diag(inv2) V2^T : tmp = left W2 (k x k) scaled, then * V2^T
+  for (int e = tid; e < k * k; e += kSvdThreads) {
+    const int i = e % k, j = e / k;
+    double s = 0.0;
+    if (inv2[j] != 0.0)
+      for (int l = 0; l < r; ++l) s = fma(left[i + l * k], c[j * r + l], s);
+    tmp[e] = s * inv2[j];
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += kSvdThreads) {
+    const int i = e % k, j = e / k;
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) s = fma(tmp[i + l * k], v[j + l * k], s);
+    bout[boff[p] + e] = s;
+  }
+}
+
+}  // namespace
+
+void launch_gram(const GramTask* tasks, int ntasks, const double* xbase, const double* ybase,
+                 int nx, int ny, double* out, cudaStream_t s) {
+  if (ntasks == 0) return;
+  const int e = (nx * ny + kGramThreads - 1) / kGramThreads;
+  const size_t smem = size_t(kGramRows) * size_t(nx + ny) * sizeof(double);
+#define HP_G(EE)                                                                            \
+  if (e <= EE) {                                                                            \
+    HP_CUDA(cudaFuncSetAttribute(gram_kernel<EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                 int(smem)));                                               \
+    gram_kernel<EE><<<ntasks, kGramThreads, smem, s>>>(tasks, xbase, ybase, nx, ny, out);   \
+    HP_CUDA(cudaGetLastError());                                                            \
+    return;                                                                                 \
+  }
+  HP_G(2) HP_G(4) HP_G(8) HP_G(12) HP_G(16) HP_G(20) HP_G(25) HP_G(32)
+#undef HP_G
+  throw std::invalid_argument("gram block too large (nx * ny > 8192)");
+}
+
+void launch_sum_partials(const std::int64_t* off, int ndst, const double* src, int len,
+                         double* dst, cudaStream_t s) {
+  if (ndst == 0) return;
+  sum_partials_kernel<<<ndst, 128, 0, s>>>(off, src, len, dst);
+  HP_CUDA(cudaGetLastError());
+}
+
+void launch_bsolve(int npairs, const double* gpu_, const double* middle, const double* vg, int r,
+                   int k, double tol, const std::int64_t* boff, double* b, cudaStream_t s) {
+  if (npairs == 0) return;
+  const size_t smem = size_t(r * k + k * k + r * r + 2 * k * r + k) * sizeof(double);
+  HP_CUDA(cudaFuncSetAttribute(bsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  bsolve_kernel<<<npairs, kSvdThreads, smem, s>>>(gpu_, middle, vg, r, k, tol, boff, b);
+  HP_CUDA(cudaGetLastError());
+}
+
+}  // namespace hpeel

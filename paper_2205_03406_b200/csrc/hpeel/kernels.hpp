@@ -1,0 +1,174 @@
+// Launchers for the sm_100a kernels (K1..K7). Plain
+// pointers and sizes; every pointer is device memory unless noted.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.cuh"
+
+namespace hpeel {
+
+// ---------------------------------------------------------------- K1 payload
+/// Gaussian payload rows of the boxes at one level, fwd (phase 0) in columns
+/// [0, r) and adjoint (phase 1) in [r, 2r) of the row-major N x gld buffer g;
+/// columns [2r, gld) are zeroed. Rows of positions not covered stay untouched.
+/// pos_box[pos] = box id at this level (or -1), local[pos] = rank of the point
+/// in the box's input-ordered point list (proj/src/coloring.cpp:252-259).
+void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const int* pos_box,
+                             const int* local, std::uint64_t seed, int level, cudaStream_t s);
+
+// ---------------------------------------------------------------- K2 apply
+/// One CTA tile: up to 64 consecutive tree rows of a box against the payload
+/// rows of one color class.
+struct SampleTask {
+  std::int64_t row0;
+  std::int64_t out;  // element offset of (tile row 0, col 0) in `out`
+  int rows;
+  int color;
+  int ld;
+  int pad;
+};
+/// out[task.out + i + (ocol0 + c) * ld] = sum_j K(row0+i, j) g[j * gld + gcol0 + c]
+/// over payload rows j of the task's color (pay_pos[pay_off[c] .. pay_off[c+1])),
+/// c < ncols. `trans` applies K^T (adjoint of a non-symmetric dense operator).
+void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
+                         const std::int64_t* pay_off, const int* pay_pos, const double* g,
+                         int gld, int gcol0, int ncols, double* out, int ocol0,
+                         cudaStream_t s);
+
+/// Leaf-phase identity probes (proj/src/coloring.cpp:271-277):
+/// out[task.out + i + t * ld] = sum_{v in color} K(row0+i, start_v + t), t < |v|,
+/// for t < w. Boxes of color c are pay_box[pay_off[c]..pay_off[c+1]) with
+/// tree ranges (box_start, box_count).
+void launch_identity_apply(const DevOp& op, const SampleTask* tasks, int ntasks,
+                           const std::int64_t* pay_off, const int* pay_box,
+                           const std::int64_t* box_start, const std::int64_t* box_count, int w,
+                           double* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- K3 peel
+/// Coefficient task: T = op(B) * sum_v F[rows of v]^T P_v (k x w), written at
+/// t_out. F is a factor block (col-major, ld = frows) whose first row is tree
+/// position f_row0; P_v are payload rows (gaussian rows of g at column gcol0,
+/// or identity when gcol0 < 0). B is k x k col-major, transposed if btrans.
+struct CoeffTask {
+  std::int64_t f;      // factor offset
+  std::int64_t b;      // B offset
+  std::int64_t t_out;  // output offset (k x w col-major)
+  std::int64_t f_row0; // tree position of factor row 0
+  int frows;
+  int seg_begin;       // payload segments [seg_begin, seg_end) in seg arrays
+  int seg_end;
+  int btrans;
+};
+/// segments: tree ranges (seg_start, seg_count) of the payload boxes.
+void launch_peel_coeff(const CoeffTask* tasks, int ntasks, const double* factors,
+                       const double* bmat, const std::int64_t* seg_start,
+                       const std::int64_t* seg_count, const double* g, int gld, int gcol0, int k,
+                       int w, double* tbuf, cudaStream_t s);
+
+/// Apply task: out[out + i + (ocol0 + c) * ld] += alpha * sum_terms F_term[frow_off + i, :] T_term[:, c]
+/// for i < rows (<= 64), c < w. Terms in CSR (term_off[task] .. term_off[task+1]).
+struct PeelTask {
+  std::int64_t out;
+  int rows;
+  int ld;
+  int term_begin;
+  int term_end;
+};
+struct PeelTerm {
+  std::int64_t f;     // factor element offset of row 0 of the tile
+  std::int64_t t;     // coefficient offset (k x w)
+  int fld;            // factor leading dimension
+  int pad;
+};
+void launch_peel_apply(const PeelTask* tasks, int ntasks, const PeelTerm* terms,
+                       const double* factors, const double* tbuf, int k, int w, double* out,
+                       int ocol0, double alpha, cudaStream_t s);
+
+// ---------------------------------------------------------------- K4 QR
+/// One block of a batched QR stage (col-major offsets into the stage buffers).
+struct QrBlock {
+  std::int64_t a;    // input block (ld lda); chunk stage overwrites it with reflectors
+  std::int64_t out;  // chunk: R rows in the parent stacked matrix; top/backprop: Q output (ld ldo)
+  std::int64_t tau;  // chunk/backprop: tau offset
+  std::int64_t c;    // backprop: parent Q rows for this chunk (ld ldc)
+  int rows;
+  int lda;
+  int ldo;
+  int ldc;
+  int rank_slot;     // top: index into ranks (or -1)
+  int pad;
+};
+int qr_rows_max(int cols);
+/// Unpivoted Householder QR of each chunk in place (reflectors below the
+/// diagonal), tau at tau + aux, R (min(rows,cols) x cols, upper) copied into
+/// the parent stacked matrix at out (ld = ldo).
+void launch_qr_chunk(const QrBlock* blocks, int nb, double* data, double* rout, double* tau,
+                     int cols, cudaStream_t s);
+/// Column-pivoted Householder QR of each top block, keep = first columns with
+/// |R_jj| > tol * |R_00| capped at kmax (proj/src/linalg.cpp:53-78); writes
+/// Q(:, :keep) to out (ld = ldo, kmax columns, zero beyond keep) and keep to
+/// ranks[rank_slot].
+void launch_qr_top(const QrBlock* blocks, int nb, double* data, double* outbuf, int* ranks,
+                   int cols, int kmax, double tol, cudaStream_t s);
+/// TSQR back-propagation: out(rows x kmax) = H_chunk [C; 0], C = r x kmax
+/// block of the parent Q at aux (ld = parent ld in rank_slot).
+void launch_qr_backprop(const QrBlock* blocks, int nb, const double* data, const double* tau,
+                        const double* parent, double* outbuf, int cols, int kmax,
+                        cudaStream_t s);
+
+// ---------------------------------------------------------------- K5 B
+/// out = X^T Y partial sums over row chunks: X (rows x nx, ld lx), Y (rows x ny,
+/// ld ly). Tasks write nx x ny col-major partials; summed in task order by
+/// launch_sum_partials.
+struct GramTask {
+  std::int64_t x;
+  std::int64_t y;
+  std::int64_t out;
+  int rows;
+  int lx;
+  int ly;
+  int x_rowmajor;  // X is row-major with row stride lx (payload buffer)
+  int y_rowmajor;
+  int pad;
+};
+void launch_gram(const GramTask* tasks, int ntasks, const double* xbase, const double* ybase,
+                 int nx, int ny, double* out, cudaStream_t s);
+/// dst[d + i] = sum_{p in [off[d], off[d+1])} src[p * len + i]
+void launch_sum_partials(const std::int64_t* off, int ndst, const double* src, int len,
+                         double* dst, cudaStream_t s);
+
+/// Per pair: left = pinv(gpU) * middle, B = (pinv(VG^T) * left^T)^T with the
+/// SVD cutoff tol * sigma_1 (proj/src/linalg.cpp:110-127, proj/src/peeling.cpp:252-269).
+/// gpU r x k, middle r x r, VG k x r (all col-major, packed per pair at
+/// stride), B k x k written at b + pair * k * k.
+void launch_bsolve(int npairs, const double* gpu_, const double* middle, const double* vg,
+                   int r, int k, double tol, const std::int64_t* boff, double* b, cudaStream_t s);
+
+// ---------------------------------------------------------------- misc
+/// dst[i * dsr + c * dsc] = src[map[i] * ssr + c * ssc] (map == nullptr: identity).
+void launch_permute_rows(const double* src, std::int64_t ssr, std::int64_t ssc, const int* map,
+                         std::int64_t rows, int w, double* dst, std::int64_t dsr, std::int64_t dsc,
+                         cudaStream_t s);
+
+/// y = K x or K^T x (tree order, x and y col-major n x w): full black-box
+/// apply used by the power-method verifier (proj/src/linalg.cpp:179-196).
+void launch_full_apply(const DevOp& op, bool trans, const double* x, int w, double* y,
+                       cudaStream_t s);
+
+/// Dense leaf blocks of H1Rep::apply (proj/src/hmatrix.cpp:59-73): for box b,
+/// y[rows of b] += sum over tasks [off[b], off[b+1]) of D x[cols] (or D^T for
+/// the adjoint, where the task's columns are the output rows). x, y row-major.
+struct DenseTask {
+  std::int64_t d;     // block offset, col-major rows x cols
+  std::int64_t row0;  // tree position of the block rows (lambda)
+  std::int64_t col0;  // tree position of the block cols (mu)
+  int rows, cols;
+};
+void launch_dense_apply(const DenseTask* tasks, const int* box_off, int nboxes,
+                        const double* dense, const double* x, int w, bool adjoint, double* y,
+                        std::int64_t ldy, cudaStream_t s);
+
+}  // namespace hpeel
