@@ -1,0 +1,334 @@
+#!/usr/bin/env python3
+"""Benchmark: H-matrix (H1) compression time on B200 (BASELINE.json metric).
+
+One step = one full ``compress()`` of the workload (all H1 levels + leaf
+phase) with the operator and tree already resident (points in HBM, tree on
+the host). Default workload: config 3 (N = 262144 starfish curve, on-the-fly
+log kernel, quadtree leaf 128, k = 32, p = 10) -- the largest BASELINE config
+whose factors fit one GPU; config 4's N = 2^20 is quoted on 8 GPUs.
+
+  python bench.py [--gpus N --steps K --warmup W --config c3 --impl ours|reference]
+
+Prints one JSON line (rank 0). Times: CUDA events on the device around the
+synchronous compress call (max over ranks); L2 is flushed (512 MiB write)
+before every timed step. ``e2e`` repeats the step through the public API with
+host buffers: points H2D, tree build, compress, full factor export D2H.
+``--impl reference`` times the CPU oracle (oracle/, the restated reference
+algorithm: per-color dense test matrices through the black box) on a bounded
+sample and extrapolates to the full workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA.8x8x4 peak on this pool's B200 (profiles/r01_fp64_peaks.txt)
+FP64_PEAK_SOURCE = "measured DMMA m8n8k4 peak, profiles/r01_fp64_peaks.txt (MEASURED_PEAKS.json has no FP64 entry)"
+METRIC = "H-matrix compression time (s)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override N (scaled workload)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
+    return ws, rank, local
+
+
+def dist_max(x, ws, impl):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if impl == "ours" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_operator(hp, w, pts):
+    if w.dense:
+        # config 1: explicit dense A = log|x_i - x_j| (A_ii = 0) as the black box
+        x = pts
+        same = np.eye(len(x), dtype=bool)
+        diff = x[:, None, :] - x[None, :, :]
+        with np.errstate(divide="ignore"):
+            a = np.log(np.sqrt(np.sum(diff * diff, axis=2)))
+        a[same] = 0.0
+        return hp.dense_operator(a)
+    return hp.kernel_operator(w.kernel, pts, w.param)
+
+
+def k2_roofline(report):
+    """Dominant kernel K2 (sample_apply): executed useful FP64 flops / device time."""
+    flops = sum(ph["apply_flops"] for ph in report["phases"] if ph["phase"] == "h1")
+    ms = sum(ph["apply_ms"] for ph in report["phases"] if ph["phase"] == "h1")
+    launches = sum(1 for ph in report["phases"] if ph["phase"] == "h1")
+    ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    return {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None, "kernel": "sample_apply_kernel (K2)",
+            "launches_per_step": launches, "avg_launch_ms": round(ms / max(launches, 1), 3),
+            "flops_per_step": flops, "peak_source": FP64_PEAK_SOURCE}
+
+
+def flush_l2(torch):
+    buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    buf.fill_(1.0)
+    del buf
+
+
+def cpu_reference_sample(w, pts, threads, budget_s=12.0):
+    """Time the reference algorithm's black-box pattern on the host: the
+    per-color dense test matrix through an on-the-fly kernel operator
+    (residual_samples, proj/src/peeling.cpp:165-170), on a row subset, then
+    extrapolate to every color of every level (the plan is computed exactly
+    by the host layer). Black-box work dominates the reference's compression
+    time; the extrapolation counts only that part."""
+    import paper_2205_03406_b200 as hp
+    import oracle as O
+    from concurrent.futures import ThreadPoolExecutor
+    tree = hp.build_tree(pts, w.leaf)
+    r = w.rank + w.oversample
+    n = w.n
+    colors_cols = []  # (number of colors, width) per apply phase
+    for l in range(2, tree.depth + 1):
+        if not tree.admissible_pairs(l):
+            continue
+        p = hp.plan(tree, l, "h1", r, 7, 0)
+        colors_cols.append((2 * p.n_colors, r))   # forward + adjoint
+    pl = hp.plan(tree, tree.depth, "leaf", tree.max_leaf_size, 7, 0)
+    colors_cols.append((pl.n_colors, tree.max_leaf_size))
+    rng = np.random.default_rng(0)
+    x = np.asarray(pts, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[:, None]
+
+    def rows_apply(i0, i1, omega):
+        same = (np.arange(i0, i1)[:, None] == np.arange(n)[None, :]) if w.kernel != "exp" else None
+        kb = O.kernel_matrix(w.kernel, x[i0:i1], x, same, w.param)
+        return kb @ omega
+
+    per_row = {}
+    for width in sorted({c for _, c in colors_cols}):
+        omega = rng.standard_normal((n, width))
+        chunk = 64
+        done_rows, t0 = 0, time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:
+            while time.perf_counter() - t0 < budget_s / 2 and done_rows < n:
+                starts = list(range(done_rows, min(n, done_rows + chunk * threads), chunk))
+                list(ex.map(lambda s: rows_apply(s, min(n, s + chunk), omega), starts))
+                done_rows = min(n, done_rows + chunk * threads)
+        per_row[width] = (time.perf_counter() - t0) / done_rows
+    total = sum(nc * n * per_row[c] for nc, c in colors_cols)
+    sample = (f"oracle per-color black-box apply (kernel rows x full N @ dense Omega_c) on row subsets, "
+              f"{threads} threads, extrapolated over {sum(nc for nc, _ in colors_cols)} color applies "
+              f"(all levels fwd+adj + leaf); QR/B/peeling time excluded")
+    return total, sample
+
+
+def run_reference(args, ws, rank):
+    import paper_2205_03406_b200.configs as cfg
+    if rank != 0:
+        return
+    w = cfg.CONFIGS[args.config] if not args.n else cfg.scaled(args.config, args.n)
+    pts = w.points()
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sample = cpu_reference_sample(w, pts, threads, budget_s=4.0 if i < args.warmup else 12.0)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": w.name, "n": w.n, "description": w.description},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2205_03406_b200 as hp
+    import paper_2205_03406_b200.configs as cfg
+    w = cfg.CONFIGS[args.config] if not args.n else cfg.scaled(args.config, args.n)
+    torch.cuda.set_device(local)
+    pts = w.points()
+    tree = hp.build_tree(pts, w.leaf)
+    op = make_operator(hp, w, pts)
+    kw = dict(rank=w.rank, oversample=w.oversample, seed=7)
+    for _ in range(args.warmup):
+        rep = hp.compress(op, tree, **kw)
+        del rep
+    torch.cuda.synchronize()
+    times = []
+    launches0 = hp.launch_count()
+    last = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(torch)
+            barrier(ws)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rep = hp.compress(op, tree, **kw)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e-3)
+            last = rep
+    launches = hp.launch_count() - launches0
+    t_step = dist_max(float(np.mean(times)), ws, "ours")
+    report = last.report
+    roof = k2_roofline(report)
+    fdoubles, ddoubles = last.sizes()
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hf = np.empty(fdoubles)
+        hd = np.empty(max(ddoubles, 1))
+        etimes = []
+        h2d = pts.size * 8
+        for i in range(max(1, min(args.steps, 2))):
+            barrier(ws)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            host_pts = np.array(pts, copy=True)
+            t_tree = hp.build_tree(host_pts, w.leaf)
+            o2 = make_operator(hp, w, host_pts)
+            r2 = hp.compress(o2, t_tree, **kw)
+            d2h = r2.export(hf, hd)
+            hp.device_synchronize()
+            etimes.append(time.perf_counter() - t0)
+            del r2, o2
+        e2e = {"value": dist_max(float(np.mean(etimes)), ws, "ours"), "unit": "s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "includes": "points H2D, tree build, compress, export of all factors + dense blocks D2H"}
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        v, sample = cpu_reference_sample(w, pts, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": "s", "cores": os.cpu_count() or 1, "kind": "port", "sample": sample}
+    if rank != 0:
+        return
+    phases = [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in ph.items()
+               if k in ("phase", "level", "colors", "apply_ms", "peel_ms", "qr_ms", "bsolve_ms", "wall_ms_total")}
+              for ph in report["phases"]]
+    line = {
+        "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 2),
+        "higher_is_better": False, "scaling": "weak" if ws > 1 else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.n, "description": w.description, "rank": w.rank,
+                   "oversample": w.oversample, "leaf": w.leaf, "parallelism": f"replicas{ws}" if ws > 1 else "single",
+                   "l2": "flushed (512 MiB write) before every timed step"},
+        "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "report": {"forward_cols": report["forward_cols"], "adjoint_cols": report["adjoint_cols"],
+                   "max_sampling_colors": report["max_sampling_colors"], "net_flops": report["net_flops"],
+                   "wall_s_net": round(report["wall_s_net"], 4), "phases": phases},
+        "storage_doubles": last.storage()["total"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -53,6 +53,9 @@ typedef struct hp_rep hp_rep;
 
 const char* hp_last_error(void);
 int hp_device_count(int* count);
+/* kernels launched by this library so far (bench.py gpu_launches) */
+int64_t hp_launch_count(void);
+int hp_device_synchronize(void);
 
 /* ---- RNG: proj/include/hpeel/rng.hpp:37-50, proj/src/rng.cpp:31-59 ---- */
 uint64_t hp_mix_seed(uint64_t seed, uint64_t tag);
@@ -156,6 +159,8 @@ int hp_rel_error_power_method(const hp_rep* rep, const hp_op* op, int iters, uin
  *      (columns [0, r) phase 0, [r, 2r) phase 1; rows not in a level box = 0). */
 int hp_debug_payload(const hp_tree* tree, int level, int r, uint64_t seed, int device,
                      double* out);
+/* device natural log used by the log-kernel black box, for accuracy tests */
+int hp_debug_log(const double* x, int64_t n, int device, double* out);
 
 #ifdef __cplusplus
 }

@@ -35,6 +35,15 @@ def device_count() -> int:
     return n.value
 
 
+def launch_count() -> int:
+    """Kernels launched by libhpeel_b200 so far in this process."""
+    return int(lib().hp_launch_count())
+
+
+def device_synchronize() -> None:
+    check(lib().hp_device_synchronize())
+
+
 def mix_seed(seed: int, *tags: int) -> int:
     for t in tags:
         seed = lib().hp_mix_seed(seed, t)
@@ -437,6 +446,14 @@ def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, s
     out = C.c_double(0.0)
     check(lib().hp_rel_error_power_method(rep._h, ref._h, int(iters), int(seed), C.byref(out)))
     return out.value
+
+
+def debug_log(x, device: int = 0) -> np.ndarray:
+    """Device log used by the log-kernel black box (accuracy probe)."""
+    x = np.ascontiguousarray(x, dtype=np.float64).ravel()
+    out = np.zeros_like(x)
+    check(lib().hp_debug_log(dptr(x), x.size, device, dptr(out)))
+    return out
 
 
 def debug_payload(tree: BoxTree, level: int, r: int, seed: int, device: int = 0) -> np.ndarray:

@@ -28,6 +28,8 @@ lp = C.POINTER(C.c_int64)
 _SIGNATURES = {
     "hp_last_error": (C.c_char_p, []),
     "hp_device_count": (C.c_int, [ip]),
+    "hp_launch_count": (i64, []),
+    "hp_device_synchronize": (C.c_int, []),
     "hp_mix_seed": (u64, [u64, u64]),
     "hp_gaussian_matrix": (C.c_int, [i64, i64, u64, dp]),
     "hp_random_cloud": (C.c_int, [i64, C.c_int, u64, dp]),
@@ -67,6 +69,7 @@ _SIGNATURES = {
     "hp_rep_captured": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
     "hp_rel_error_power_method": (C.c_int, [P, P, C.c_int, u64, dp]),
     "hp_debug_payload": (C.c_int, [P, C.c_int, C.c_int, u64, C.c_int, dp]),
+    "hp_debug_log": (C.c_int, [dp, i64, C.c_int, dp]),
 }
 
 

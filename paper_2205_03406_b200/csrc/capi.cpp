@@ -33,6 +33,8 @@ struct hp_rep {
 };
 
 namespace hpeel {
+std::int64_t& launch_counter();
+void debug_fast_log(const double* x, std::int64_t n, double* y, int device);
 Matrix debug_payload(const BoxTree& tree, const TreeLayout& lay, int level, int r,
                      std::uint64_t seed, int device);
 }
@@ -79,6 +81,15 @@ int hp_device_count(int* count) {
   return guard([&] {
     need(count, "count");
     if (cudaGetDeviceCount(count) != cudaSuccess) *count = 0;
+  });
+}
+
+int64_t hp_launch_count(void) { return launch_counter(); }
+
+int hp_device_synchronize(void) {
+  return guard([&] {
+    const cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
   });
 }
 
@@ -576,6 +587,14 @@ int hp_debug_payload(const hp_tree* t, int level, int r, uint64_t seed, int devi
     need(out, "out");
     const Matrix m = debug_payload(*t->tree, *t->layout, level, r, seed, device);
     std::memcpy(out, m.data(), size_t(m.size()) * 8);
+  });
+}
+
+int hp_debug_log(const double* x, int64_t n, int device, double* out) {
+  return guard([&] {
+    need(x, "x");
+    need(out, "out");
+    debug_fast_log(x, n, out, device);
   });
 }
 

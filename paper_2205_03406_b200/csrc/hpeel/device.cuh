@@ -18,6 +18,15 @@ namespace hpeel {
                                " at " + __FILE__ + ":" + std::to_string(__LINE__));  \
   } while (0)
 
+/// Count of kernel launches issued by this library (reported by bench.py as
+/// gpu_launches; read through hp_launch_count).
+std::int64_t& launch_counter();
+#define HP_LAUNCHED()                     \
+  do {                                    \
+    HP_CUDA(cudaGetLastError());          \
+    ++::hpeel::launch_counter();          \
+  } while (0)
+
 /// Black-box kinds behind the LinearOperator boundary
 /// (proj/include/hpeel/linear_operator.hpp:12-24). kDense is the reference's
 /// DenseOperator (proj/include/hpeel/operators.hpp:56-69) held in HBM; the
@@ -39,6 +48,48 @@ struct DevOp {
   int symmetric = 1;           // A == A^T: forward and adjoint share K(i, j)
 };
 
+/// 1/d to ~1 ulp: MUFU.RCP64H seed + two Newton steps (FP64 pipe only).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
+}
+
+/// Natural log for positive normal x, |error| <= ~2 ulp (checked against
+/// glibc in tests/test_gpu_kernels.py). x = 2^e m with m in [sqrt2/2, sqrt2),
+/// log m = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716: series to z^8
+/// (truncation < 3e-17 relative). ~21 FP64 ops vs ~56 for the libdevice log.
+__device__ __forceinline__ double fast_log(double x) {
+  int hi = __double2hiint(x);
+  const int lo = __double2loint(x);
+  int e = (hi >> 20) - 1023;
+  int mhi = (hi & 0x000fffff) | 0x3ff00000;
+  if (mhi > 0x3ff6a09e) {  // m > sqrt(2): use m / 2
+    mhi -= 0x00100000;
+    e += 1;
+  }
+  const double m = __hiloint2double(mhi, lo);
+  const double f = m - 1.0;
+  const double s = f * fast_rcp(2.0 + f);
+  const double z = s * s;
+  double p = 1.0 / 19.0;
+  p = fma(p, z, 1.0 / 17.0);
+  p = fma(p, z, 1.0 / 15.0);
+  p = fma(p, z, 1.0 / 13.0);
+  p = fma(p, z, 1.0 / 11.0);
+  p = fma(p, z, 1.0 / 9.0);
+  p = fma(p, z, 1.0 / 7.0);
+  p = fma(p, z, 1.0 / 5.0);
+  p = fma(p, z, 1.0 / 3.0);
+  const double s2 = s + s;
+  const double lm = fma(s2 * z, p, s2);
+  const double de = double(e);
+  return fma(de, 6.93147180369123816490e-01, fma(de, 1.90821492927058770002e-10, lm));
+}
+
 /// K(x_i, x_j) for the on-the-fly kinds, from coordinates already in
 /// registers. `same` is true iff i == j (tree positions).
 template <int KIND, int DIM>
@@ -52,8 +103,12 @@ __device__ __forceinline__ double kernel_value(const double* xi, const double* x
   }
   if (KIND == kOpLog) {
     if (same) return 0.0;
-    if (DIM == 1) return log(fabs(xi[0] - xj[0]));
-    return 0.5 * log(r2);
+    // subnormal / zero distances (coincident points) take the libdevice path
+    if (DIM == 1) {
+      const double d = fabs(xi[0] - xj[0]);
+      return d >= 2.2250738585072014e-308 ? fast_log(d) : log(d);
+    }
+    return r2 >= 2.2250738585072014e-308 ? 0.5 * fast_log(r2) : 0.5 * log(r2);
   } else if (KIND == kOpInvDist4Pi) {
     if (same) return 0.0;
     return rsqrt(r2) * 0.07957747154594767;  // 1 / (4 pi)

@@ -1,0 +1,523 @@
+// H1 peeling driver (Alg. 4.1) on the device.
+//
+// Control follows compress()/run_h1()/extract_leaf()
+// (proj/src/peeling.cpp:211-275, :490-524, :576-639) step for step: the same
+// plans (make_plan, :98-154), colors, payload seeds, rank-drop and
+// pseudo-inverse tolerances, and the same error behaviour. What changes is
+// where the work runs: every level's host plan (coloring, task lists, QR
+// and peeling structure) is built on host threads up front, and the device
+// executes the levels back to back on one stream -- K1 payload, K2 apply on
+// the sample rows the extraction reads, K3 peeling restricted to nonzero
+// payload rows, batched K4 QR and K5 B-solves -- with no host round trip.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <future>
+#include <memory>
+#include <set>
+#include <sstream>
+#include <stdexcept>
+
+#include "engine.cuh"
+#include "rng.hpp"
+
+namespace hpeel {
+
+using namespace detail;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+constexpr int kForwardPhase = 0;  // proj/src/peeling.cpp:19-20
+
+std::int64_t gemm_flops(std::int64_t m, std::int64_t n, std::int64_t k) { return 2 * m * n * k; }
+std::int64_t svd_flops(std::int64_t m, std::int64_t n) {
+  return m >= n ? 6 * m * n * n + 11 * n * n * n : 6 * n * m * m + 11 * m * m * m;
+}
+
+// Reference flop count of H1Rep::apply_truncated(level) for one width-w
+// product (proj/src/hmatrix.cpp:86-100).
+std::int64_t truncated_apply_flops(const H1Rep& rep, int level, std::int64_t w, const Engine& e) {
+  std::int64_t f = 0;
+  for (int l = 2; l <= std::min<int>(level, int(rep.levels.size()) - 1); ++l) {
+    const auto& ld = rep.levels[size_t(l)];
+    for (size_t p = 0; p < ld.pairs.size(); ++p) {
+      const std::int64_t ma = e.count(ld.pairs[p].first), mb = e.count(ld.pairs[p].second);
+      f += gemm_flops(ld.kv[p], w, mb) + gemm_flops(ld.ku[p], w, ld.kv[p]) + gemm_flops(ma, w, ld.ku[p]);
+    }
+  }
+  return f;
+}
+
+struct LevelWork {
+  int level = 0;
+  bool empty = true;
+  bool symmetric = true;
+  int nc = 0;
+  std::int64_t fwd_cols = 0;
+  size_t np = 0;
+  std::vector<int> pcolor, swap;
+  std::vector<std::int64_t> soff;
+  std::vector<std::int64_t> pay_off;
+  std::vector<int> pay_pos;
+  std::vector<int> pos_box, local;
+  std::vector<SampleTask> tasks;
+  double evals = 0;
+  bool has_peel = false;
+  PeelPlan peel;
+  QrPlan qr;
+  GramPlan g_mid, g_gpu, g_vg;
+};
+
+LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig& cfg) {
+  LevelWork w;
+  w.level = l;
+  const auto& ld = rep.levels[size_t(l)];
+  if (ld.pairs.empty()) return w;
+  w.empty = false;
+  {
+    std::set<std::pair<int, int>> all(ld.pairs.begin(), ld.pairs.end());
+    for (auto [a, b] : ld.pairs)
+      if (!all.count({b, a})) w.symmetric = false;
+  }
+  if (!w.symmetric) return w;
+  const int r = e.r, k = e.k;
+  const SamplingPlan plan = make_plan(e.tree, e.adj, l, SampleMode::kH1, r, cfg.seed, kForwardPhase);
+  w.nc = plan.colors();
+  std::vector<std::vector<int>> color_boxes(size_t(w.nc));
+  w.pay_off.assign(size_t(w.nc) + 1, 0);
+  for (int c = 0; c < w.nc; ++c) {
+    for (auto [box, tag] : plan.matrices[size_t(c)].payload) {
+      color_boxes[size_t(c)].push_back(box);
+      for (std::int64_t q = 0; q < e.count(box); ++q) w.pay_pos.push_back(int(e.start(box) + q));
+    }
+    w.pay_off[size_t(c) + 1] = std::int64_t(w.pay_pos.size());
+    w.fwd_cols += plan.matrices[size_t(c)].payload.empty() ? 0 : r;
+  }
+  const size_t np = ld.pairs.size();
+  w.np = np;
+  w.pcolor.resize(np);
+  w.soff.assign(np + 1, 0);
+  w.swap.resize(np);
+  for (size_t p = 0; p < np; ++p) {
+    w.pcolor[p] = plan.block_to_matrix.at(ld.pairs[p]);
+    w.soff[p + 1] = w.soff[p] + std::int64_t(e.count(ld.pairs[p].first)) * 2 * r;
+    w.swap[p] = pair_index(ld.pairs, ld.pairs[p].second, ld.pairs[p].first);
+  }
+  // K1: pos -> box, local rank
+  w.pos_box.assign(size_t(e.n), -1);
+  w.local.assign(size_t(e.n), 0);
+  for (int b : e.tree.level_boxes(l)) {
+    const int* lr = e.lay.local_flat.data() + e.lay.local_off[size_t(b)];
+    for (int q = 0; q < e.count(b); ++q) {
+      w.pos_box[size_t(e.start(b) + q)] = b;
+      w.local[size_t(e.start(b) + q)] = lr[q];
+    }
+  }
+  // K2 tasks, largest payload lists first (tail balance)
+  for (size_t p = 0; p < np; ++p) {
+    const int a = ld.pairs[p].first;
+    const int rows = e.count(a);
+    for (int t0 = 0; t0 < rows; t0 += kTile)
+      w.tasks.push_back(SampleTask{e.start(a) + t0, w.soff[p] + t0, std::min(kTile, rows - t0),
+                                   w.pcolor[p], rows, 0});
+    w.evals += double(rows) * double(w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])]);
+  }
+  std::stable_sort(w.tasks.begin(), w.tasks.end(), [&](const SampleTask& x, const SampleTask& y) {
+    return w.pay_off[size_t(x.color) + 1] - w.pay_off[size_t(x.color)] >
+           w.pay_off[size_t(y.color) + 1] - w.pay_off[size_t(y.color)];
+  });
+  // K3 (prev_level = l - 1 >= 2)
+  if (l - 1 >= 2) {
+    std::vector<SampleBlock> blocks(np);
+    for (size_t p = 0; p < np; ++p) blocks[p] = SampleBlock{ld.pairs[p].first, w.pcolor[p], w.soff[p]};
+    w.peel = plan_peel(e, rep, blocks, color_boxes, l - 1, r, true);
+    w.has_peel = true;
+  }
+  // K5a middle = G'_a^T Y_p; K4 QR; K5b grams
+  const int gld = 2 * r;
+  std::vector<GramReq> mid(np), gu(np), vg(np);
+  std::vector<QrRequest> qr;
+  qr.reserve(2 * np);
+  for (size_t p = 0; p < np; ++p) {
+    const auto [a, b] = ld.pairs[p];
+    const int rows = e.count(a);
+    mid[p] = GramReq{e.start(a) * gld + r, w.soff[p], rows, gld, rows, 1, 0};
+    gu[p] = GramReq{e.start(a) * gld + r, ld.uoff[p], rows, gld, rows, 1, 0};
+    vg[p] = GramReq{ld.voff[p], e.start(b) * gld, e.count(b), e.count(b), gld, 0, 1};
+    qr.push_back(QrRequest{w.soff[p], ld.uoff[p], rows, rows, int(p)});
+    qr.push_back(QrRequest{w.soff[p] + std::int64_t(rows) * r, ld.voff[size_t(w.swap[p])], rows, rows,
+                           int(np + size_t(w.swap[p]))});
+  }
+  w.g_mid = plan_gram(mid, r, r);
+  w.g_gpu = plan_gram(gu, r, k);
+  w.g_vg = plan_gram(vg, k, r);
+  w.qr = plan_qr(qr, r, k);
+  return w;
+}
+
+struct LeafWork {
+  int nc = 0;
+  int w = 0;
+  std::int64_t fwd_cols = 0;
+  std::vector<std::int64_t> pay_off;
+  std::vector<int> pay_box;
+  std::vector<SampleTask> tasks;
+  double evals = 0;
+  bool has_peel = false;
+  PeelPlan peel;
+  std::vector<std::pair<int, int>> pairs;
+  std::vector<std::int64_t> off;
+  std::int64_t total = 0;
+};
+
+LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg) {
+  LeafWork lw;
+  const BoxTree& tree = e.tree;
+  lw.w = tree.max_leaf_size();
+  const SamplingPlan plan =
+      make_plan(tree, e.adj, tree.depth(), SampleMode::kLeaf, lw.w, cfg.seed, kForwardPhase);
+  lw.nc = plan.colors();
+  std::vector<std::vector<int>> color_boxes(size_t(lw.nc));
+  lw.pay_off.assign(size_t(lw.nc) + 1, 0);
+  for (int c = 0; c < lw.nc; ++c) {
+    for (auto [box, tag] : plan.matrices[size_t(c)].payload) {
+      color_boxes[size_t(c)].push_back(box);
+      lw.pay_box.push_back(box);
+    }
+    lw.pay_off[size_t(c) + 1] = std::int64_t(lw.pay_box.size());
+    lw.fwd_cols += plan.matrices[size_t(c)].payload.empty() ? 0 : lw.w;
+  }
+  lw.pairs = dense_pairs(tree, e.adj);
+  const size_t nd = lw.pairs.size();
+  lw.off.resize(nd);
+  std::vector<SampleBlock> blocks(nd);
+  for (size_t p = 0; p < nd; ++p) {
+    const auto [lam, mu] = lw.pairs[p];
+    const int c = plan.block_to_matrix.at(lw.pairs[p]);
+    const int rows = e.count(lam);
+    lw.off[p] = lw.total;
+    for (int t0 = 0; t0 < rows; t0 += kTile)
+      lw.tasks.push_back(SampleTask{e.start(lam) + t0, lw.total + t0, std::min(kTile, rows - t0), c, rows, 0});
+    blocks[p] = SampleBlock{lam, c, lw.total};
+    std::int64_t nnz = 0;
+    for (std::int64_t q = lw.pay_off[size_t(c)]; q < lw.pay_off[size_t(c) + 1]; ++q)
+      nnz += e.count(lw.pay_box[size_t(q)]);
+    lw.evals += double(rows) * double(nnz);
+    lw.total += std::int64_t(rows) * lw.w;
+  }
+  if (tree.depth() >= 2) {
+    lw.peel = plan_peel(e, rep, blocks, color_boxes, tree.depth(), lw.w, false);
+    lw.has_peel = true;
+  }
+  return lw;
+}
+
+struct LevelTimers {
+  Events apply, peel, mid, qr, bsolve;
+};
+
+}  // namespace
+
+void PeelConfig::validate() const {
+  if (rank < 1) throw std::invalid_argument("fixed rank must be >= 1");
+  if (oversample < 0) throw std::invalid_argument("negative oversampling");
+}
+
+std::string RunReport::to_csv() const {
+  std::ostringstream out;
+  out << "phase,level,colors,forward_cols,adjoint_cols,wall_ms_total,wall_ms_net,net_flops\n";
+  for (const PhaseReport& p : phases) {
+    out << p.phase << ',' << p.level << ',' << p.colors << ',' << p.forward_cols << ','
+        << p.adjoint_cols << ',' << p.wall_ms_total << ',' << p.wall_ms_net << ','
+        << p.net_flops << '\n';
+  }
+  return out.str();
+}
+
+PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tree,
+                    const PeelConfig& config) {
+  if (!tree) throw std::invalid_argument("null tree");
+  if (op.rows() != tree->num_points() || op.cols() != tree->num_points())
+    throw std::invalid_argument("operator and tree dimensions differ");
+  config.validate();
+  if (config.format != PeelFormat::kH1)
+    throw std::invalid_argument("only format h1 is on the device hot path");
+  if (config.strategy != ColoringStrategy::kGraph)
+    throw std::invalid_argument("only the graph coloring strategy is on the device hot path");
+  if (op.kind() != kOpDense && op.dim() != tree->dim())
+    throw std::invalid_argument("operator and tree dimensions differ");
+  const int r = config.sample_width();
+  const int k = config.rank;
+  if (2 * r > 160) throw std::invalid_argument("sample width k + p > 80 is not supported");
+
+  DeviceGuard guard(op.device());
+  const auto t_begin = Clock::now();
+  auto adj = std::make_shared<const AdjacencyInfo>(adjacency(*tree));
+  auto lay = std::make_shared<const TreeLayout>(tree_layout(*tree));
+
+  cudaStream_t s;
+  HP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  PeelResult result;
+  auto rep = std::make_shared<H1Rep>();
+  rep->tree = tree;
+  rep->adj = adj;
+  rep->layout = lay;
+  rep->rank = k;
+  rep->device = op.device();
+  rep->levels.resize(size_t(tree->depth()) + 1);
+  RunReport& report = result.report;
+  int* h_ranks = nullptr;
+
+  try {
+    Engine e(*tree, *adj, *lay, op, s);
+    e.r = r;
+    e.k = k;
+    const Index n = tree->num_points();
+
+    // Factor arena: U (|I_a| x k), V (|I_b| x k), B (k x k) per pair, all levels.
+    std::int64_t ftotal = 0, rank_total = 0;
+    for (int l = 2; l <= tree->depth(); ++l) {
+      auto& ld = rep->levels[size_t(l)];
+      ld.pairs = admissible_pairs(*tree, *adj, l);
+      const size_t np = ld.pairs.size();
+      ld.uoff.resize(np);
+      ld.voff.resize(np);
+      ld.boff.resize(np);
+      ld.ku.assign(np, 0);
+      ld.kv.assign(np, 0);
+      for (size_t p = 0; p < np; ++p) {
+        ld.uoff[p] = ftotal;
+        ftotal += std::int64_t(e.count(ld.pairs[p].first)) * k;
+        ld.voff[p] = ftotal;
+        ftotal += std::int64_t(e.count(ld.pairs[p].second)) * k;
+        ld.boff[p] = ftotal;
+        ftotal += std::int64_t(k) * k;
+      }
+      rank_total += 2 * std::int64_t(np);
+    }
+    rep->factor_doubles = ftotal;
+    HP_CUDA(cudaMalloc(&rep->d_factors, size_t(std::max<std::int64_t>(ftotal, 1)) * 8));
+    HP_CUDA(cudaMallocHost(&h_ranks, size_t(std::max<std::int64_t>(rank_total, 1)) * sizeof(int)));
+
+    // Host plans of every level and of the leaf phase, built concurrently.
+    std::vector<std::future<LevelWork>> futs(size_t(tree->depth()) + 1);
+    for (int l = 2; l <= tree->depth(); ++l)
+      futs[size_t(l)] = std::async(std::launch::async, build_level, std::cref(e), std::cref(*rep), l,
+                                   std::cref(config));
+    auto leaf_fut = std::async(std::launch::async, build_leaf, std::cref(e), std::cref(*rep),
+                               std::cref(config));
+
+    const int gld = 2 * r;
+    DevBuf<double> g(size_t(n) * size_t(gld), s);
+    std::vector<std::unique_ptr<LevelTimers>> timers(size_t(tree->depth()) + 1);
+    std::vector<std::int64_t> rank_off(size_t(tree->depth()) + 1, 0);
+    std::vector<double> evals(size_t(tree->depth()) + 1, 0.0), peel_flops(size_t(tree->depth()) + 1, 0.0);
+    std::vector<int> colors(size_t(tree->depth()) + 1, 0);
+    std::vector<std::int64_t> fcols(size_t(tree->depth()) + 1, 0);
+    std::int64_t roff = 0;
+    int built = 1;
+
+    for (int l = 2; l <= tree->depth(); ++l) {
+      LevelWork w = futs[size_t(l)].get();
+      if (w.empty) continue;  // proj/src/peeling.cpp:221 (built_level not advanced)
+      if (!w.symmetric) throw std::logic_error("asymmetric admissibility structure");
+      if (l - 1 >= 2 && l - 1 > built)
+        throw std::runtime_error("h1 apply: representation incomplete for level " + std::to_string(l - 1));
+      auto& ld = rep->levels[size_t(l)];
+      const size_t np = w.np;
+      auto tm = std::make_unique<LevelTimers>();
+      colors[size_t(l)] = w.nc;
+      fcols[size_t(l)] = w.fwd_cols;
+      evals[size_t(l)] = w.evals;
+      peel_flops[size_t(l)] = w.peel.coeff_flops + w.peel.apply_flops;
+
+      // K1 payload
+      DevBuf<int> d_pos_box, d_local;
+      d_pos_box.upload(w.pos_box, s);
+      d_local.upload(w.local, s);
+      launch_payload_gaussian(g.get(), gld, r, n, d_pos_box.get(), d_local.get(), config.seed, l, s);
+
+      // K2 apply (forward + adjoint samples of every pair's row block)
+      DevBuf<SampleTask> d_tasks;
+      d_tasks.upload(w.tasks, s);
+      DevBuf<std::int64_t> d_pay_off;
+      d_pay_off.upload(w.pay_off, s);
+      DevBuf<int> d_pay_pos;
+      d_pay_pos.upload(w.pay_pos, s);
+      DevBuf<double> samples(size_t(w.soff[np]), s);
+      HP_CUDA(cudaEventRecord(tm->apply.a, s));
+      if (op.symmetric()) {
+        launch_sample_apply(e.dop, false, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
+                            d_pay_pos.get(), g.get(), gld, 0, 2 * r, samples.get(), 0, s);
+      } else {
+        launch_sample_apply(e.dop, false, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
+                            d_pay_pos.get(), g.get(), gld, 0, r, samples.get(), 0, s);
+        launch_sample_apply(e.dop, true, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
+                            d_pay_pos.get(), g.get(), gld, r, r, samples.get(), r, s);
+      }
+      HP_CUDA(cudaEventRecord(tm->apply.b, s));
+
+      // K3 peel
+      HP_CUDA(cudaEventRecord(tm->peel.a, s));
+      if (w.has_peel) run_peel(w.peel, e, *rep, g.get(), gld, r, false, samples.get(), r, s);
+      HP_CUDA(cudaEventRecord(tm->peel.b, s));
+
+      if (config.capture_samples) {
+        HP_CUDA(cudaStreamSynchronize(s));
+        std::vector<Matrix> cap;
+        for (size_t p = 0; p < np; ++p) {
+          const int rows = e.count(ld.pairs[p].first);
+          Matrix m(rows, 2 * r);
+          HP_CUDA(cudaMemcpy(m.data(), samples.get() + w.soff[p], size_t(rows) * 2 * r * 8,
+                             cudaMemcpyDeviceToHost));
+          cap.push_back(std::move(m));
+        }
+        rep->captured[l] = std::move(cap);
+      }
+
+      // K5a: middle = G'_a^T Y_p before the QR overwrites Y
+      DevBuf<double> middle(np * size_t(r) * size_t(r), s), gpu(np * size_t(r) * size_t(k), s),
+          vg(np * size_t(k) * size_t(r), s);
+      HP_CUDA(cudaEventRecord(tm->mid.a, s));
+      run_gram(w.g_mid, g.get(), samples.get(), middle.get(), s);
+      HP_CUDA(cudaEventRecord(tm->mid.b, s));
+
+      // K4 QR: U_p from Y_p, V_swap(p) from Z_p
+      DevBuf<int> d_ranks(2 * np, s);
+      HP_CUDA(cudaEventRecord(tm->qr.a, s));
+      run_qr(w.qr, samples.get(), rep->d_factors, d_ranks.get(), r, k, s);
+      HP_CUDA(cudaEventRecord(tm->qr.b, s));
+
+      // K5b: gpU = G'^T U, VG = V^T G, B
+      HP_CUDA(cudaEventRecord(tm->bsolve.a, s));
+      run_gram(w.g_gpu, g.get(), rep->d_factors, gpu.get(), s);
+      run_gram(w.g_vg, rep->d_factors, g.get(), vg.get(), s);
+      DevBuf<std::int64_t> d_boff;
+      d_boff.upload(ld.boff, s);
+      launch_bsolve(int(np), gpu.get(), middle.get(), vg.get(), r, k, kPinvCutoff, d_boff.get(),
+                    rep->d_factors, s);
+      HP_CUDA(cudaEventRecord(tm->bsolve.b, s));
+      HP_CUDA(cudaMemcpyAsync(h_ranks + roff, d_ranks.get(), 2 * np * sizeof(int), cudaMemcpyDeviceToHost, s));
+      rank_off[size_t(l)] = roff;
+      roff += 2 * std::int64_t(np);
+      timers[size_t(l)] = std::move(tm);
+      built = l;
+    }
+    rep->built_level = tree->depth();
+
+    // ------------------------------------------------------------- leaf phase
+    LeafWork lw = leaf_fut.get();
+    rep->dense.pairs = lw.pairs;
+    rep->dense.off = lw.off;
+    rep->dense_doubles = lw.total;
+    HP_CUDA(cudaMalloc(&rep->d_dense, size_t(std::max<std::int64_t>(lw.total, 1)) * 8));
+    Events leaf_apply, leaf_peel;
+    {
+      DevBuf<SampleTask> d_tasks;
+      d_tasks.upload(lw.tasks, s);
+      DevBuf<std::int64_t> d_pay_off;
+      d_pay_off.upload(lw.pay_off, s);
+      DevBuf<int> d_pay_box;
+      d_pay_box.upload(lw.pay_box, s);
+      HP_CUDA(cudaEventRecord(leaf_apply.a, s));
+      launch_identity_apply(e.dop, d_tasks.get(), int(lw.tasks.size()), d_pay_off.get(), d_pay_box.get(),
+                            e.d_box_start.get(), e.d_box_count.get(), lw.w, rep->d_dense, s);
+      HP_CUDA(cudaEventRecord(leaf_apply.b, s));
+      HP_CUDA(cudaEventRecord(leaf_peel.a, s));
+      if (lw.has_peel) run_peel(lw.peel, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
+      HP_CUDA(cudaEventRecord(leaf_peel.b, s));
+    }
+    HP_CUDA(cudaStreamSynchronize(s));
+    if (config.capture_samples) {
+      for (size_t p = 0; p < lw.pairs.size(); ++p) {
+        const int rows = e.count(lw.pairs[p].first);
+        Matrix m(rows, lw.w);
+        HP_CUDA(cudaMemcpy(m.data(), rep->d_dense + lw.off[p], size_t(rows) * lw.w * 8, cudaMemcpyDeviceToHost));
+        rep->captured_leaf.push_back(std::move(m));
+      }
+    }
+    rep->dense_ready = true;
+
+    // ------------------------------------------------------------- report
+    double blackbox_ms = 0.0;
+    for (int l = 2; l <= tree->depth(); ++l) {
+      auto& ld = rep->levels[size_t(l)];
+      if (!timers[size_t(l)]) continue;
+      const size_t np = ld.pairs.size();
+      for (size_t p = 0; p < np; ++p) {
+        ld.ku[p] = h_ranks[rank_off[size_t(l)] + std::int64_t(p)];
+        ld.kv[p] = h_ranks[rank_off[size_t(l)] + std::int64_t(np + p)];
+      }
+    }
+    for (int l = 2; l <= tree->depth(); ++l) {
+      const auto& tm = timers[size_t(l)];
+      if (!tm) continue;
+      const auto& ld = rep->levels[size_t(l)];
+      PhaseReport ph;
+      ph.phase = "h1";
+      ph.level = l;
+      ph.colors = colors[size_t(l)];
+      ph.forward_cols = fcols[size_t(l)];
+      ph.adjoint_cols = fcols[size_t(l)];
+      ph.kernel_evals = evals[size_t(l)];
+      ph.apply_flops = evals[size_t(l)] * 2.0 * 2.0 * r;
+      ph.peel_flops = peel_flops[size_t(l)];
+      ph.apply_ms = tm->apply.ms();
+      ph.peel_ms = tm->peel.ms();
+      ph.qr_ms = tm->qr.ms();
+      ph.bsolve_ms = tm->bsolve.ms() + tm->mid.ms();
+      ph.wall_ms_total = ph.apply_ms + ph.peel_ms + ph.qr_ms + ph.bsolve_ms;
+      ph.wall_ms_net = ph.wall_ms_total - ph.apply_ms;
+      blackbox_ms += ph.apply_ms;
+      if (l - 1 >= 2) ph.net_flops += 2 * std::int64_t(ph.colors) * truncated_apply_flops(*rep, l - 1, r, e);
+      // QR (flops.hpp:18-20) and the B solve (peeling.cpp:262-268)
+      for (size_t p = 0; p < ld.pairs.size(); ++p) {
+        const std::int64_t ma = e.count(ld.pairs[p].first), mb = e.count(ld.pairs[p].second);
+        const std::int64_t ku = ld.ku[p], kv = ld.kv[p];
+        ph.net_flops += 2 * ma * r * r + 2 * mb * r * r;
+        ph.net_flops += gemm_flops(r, r, ma) + gemm_flops(r, ku, ma) + gemm_flops(kv, r, mb);
+        if (ku > 0) ph.net_flops += svd_flops(r, ku) + gemm_flops(ku, r, r);
+        if (kv > 0) ph.net_flops += svd_flops(r, kv) + gemm_flops(kv, ku, r);
+      }
+      report.phases.push_back(ph);
+    }
+    {
+      PhaseReport ph;
+      ph.phase = "leaf";
+      ph.level = tree->depth();
+      ph.colors = lw.nc;
+      ph.forward_cols = lw.fwd_cols;
+      ph.kernel_evals = lw.evals;
+      ph.peel_flops = lw.peel.coeff_flops + lw.peel.apply_flops;
+      ph.apply_ms = leaf_apply.ms();
+      ph.peel_ms = leaf_peel.ms();
+      ph.wall_ms_total = ph.apply_ms + ph.peel_ms;
+      ph.wall_ms_net = ph.peel_ms;
+      blackbox_ms += ph.apply_ms;
+      if (tree->depth() >= 2) ph.net_flops += std::int64_t(lw.nc) * truncated_apply_flops(*rep, tree->depth(), lw.w, e);
+      report.phases.push_back(ph);
+    }
+    for (const PhaseReport& p : report.phases) {
+      report.forward_cols += p.forward_cols;
+      report.adjoint_cols += p.adjoint_cols;
+      report.net_flops += p.net_flops;
+      if (p.phase != "leaf") report.max_sampling_colors = std::max(report.max_sampling_colors, p.colors);
+    }
+    report.wall_s_total = std::chrono::duration<double>(Clock::now() - t_begin).count();
+    report.wall_s_net = report.wall_s_total - blackbox_ms * 1e-3;
+  } catch (...) {
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (h_ranks) cudaFreeHost(h_ranks);
+    throw;
+  }
+  HP_CUDA(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+  cudaFreeHost(h_ranks);
+  result.rep = rep;
+  return result;
+}
+
+}  // namespace hpeel

@@ -1,0 +1,305 @@
+// Engine and batched task builders (see engine.cuh).
+#include "engine.cuh"
+
+#include <algorithm>
+#include <limits>
+#include <unordered_map>
+
+namespace hpeel::detail {
+
+Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
+               const DeviceOperator& o, cudaStream_t st)
+    : tree(t), adj(a), lay(l), op(o), s(st) {
+  n = tree.num_points();
+  DevBuf<int> perm;
+  perm.upload(lay.perm, s);
+  dop.kind = op.kind();
+  dop.dim = op.dim();
+  dop.n = n;
+  dop.param = op.param();
+  dop.symmetric = op.symmetric() ? 1 : 0;
+  if (op.kind() == kOpDense) {
+    DevBuf<double> tmp(size_t(n) * size_t(n), s);
+    at.alloc(size_t(n) * size_t(n), s);
+    // rows then columns: at[s + t n] = a[perm[s] + perm[t] n]
+    launch_permute_rows(op.device_matrix(), 1, n, perm.get(), n, int(n), tmp.get(), 1, n, s);
+    launch_permute_rows(tmp.get(), n, 1, perm.get(), n, int(n), at.get(), n, 1, s);
+    dop.a = at.get();
+  } else {
+    xt.alloc(size_t(op.dim()) * size_t(n), s);
+    launch_permute_rows(op.device_points(), 1, n, perm.get(), n, op.dim(), xt.get(), 1, n, s);
+    dop.x = xt.get();
+  }
+  d_box_start.upload(lay.start, s);
+  d_box_count.upload(lay.count, s);
+  anc.assign(size_t(tree.depth() + 1), std::vector<int>(size_t(tree.num_boxes()), -1));
+  for (const Box& b : tree.boxes()) {
+    int cur = b.id;
+    for (int lv = b.level; lv >= 0; --lv) {
+      anc[size_t(lv)][size_t(b.id)] = cur;
+      cur = tree.box(cur).parent;
+    }
+  }
+  HP_CUDA(cudaStreamSynchronize(s));
+}
+
+int pair_index(const std::vector<std::pair<int, int>>& pairs, int a, int b) {
+  auto it = std::lower_bound(pairs.begin(), pairs.end(), std::make_pair(a, b));
+  if (it == pairs.end() || *it != std::make_pair(a, b)) return -1;
+  return int(it - pairs.begin());
+}
+
+std::pair<int, int> first_range(const std::vector<std::pair<int, int>>& pairs, int a) {
+  const int lo_key = std::numeric_limits<int>::min();
+  auto lo = std::lower_bound(pairs.begin(), pairs.end(), std::make_pair(a, lo_key));
+  auto hi = std::lower_bound(pairs.begin(), pairs.end(), std::make_pair(a + 1, lo_key));
+  return {int(lo - pairs.begin()), int(hi - pairs.begin())};
+}
+
+// ---------------------------------------------------------------- K4
+
+QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
+  QrPlan pl;
+  const int rm = qr_rows_max(r);
+  for (const QrRequest& q : reqs) {
+    if (q.rows <= rm) {
+      pl.direct.push_back(QrBlock{q.a, q.out, 0, 0, q.rows, q.rows, q.ldo, 0, q.rank_slot, 0});
+      continue;
+    }
+    // TSQR: chunks of <= rm rows, stacked R factors reduced the same way.
+    std::int64_t cur_off = q.a;
+    int cur_rows = q.rows, cur_ld = q.rows;
+    std::int64_t cur_c = -1;  // Q of the current stacked matrix (workspace)
+    int round = 0;
+    while (cur_rows > rm) {
+      const int nch = (cur_rows + rm - 1) / rm;
+      const int base = cur_rows / nch, extra = cur_rows % nch;
+      int next_rows = 0;
+      for (int i = 0; i < nch; ++i) next_rows += std::min(base + (i < extra ? 1 : 0), r);
+      const std::int64_t stacked = pl.wsize;
+      pl.wsize += std::int64_t(next_rows) * r;
+      const std::int64_t c_next = pl.wsize;
+      pl.wsize += std::int64_t(next_rows) * kmax;
+      if (int(pl.chunk_rounds.size()) <= round) {
+        pl.chunk_rounds.resize(size_t(round) + 1);
+        pl.back_rounds.resize(size_t(round) + 1);
+      }
+      int row = 0, srow = 0;
+      for (int i = 0; i < nch; ++i) {
+        const int cr = base + (i < extra ? 1 : 0);
+        const std::int64_t tau = pl.tausize;
+        pl.tausize += r;
+        pl.chunk_rounds[size_t(round)].push_back(
+            QrBlock{cur_off + row, stacked + srow, tau, 0, cr, cur_ld, next_rows, 0, -1, 0});
+        QrBlock bp{};
+        bp.a = cur_off + row;
+        bp.tau = tau;
+        bp.c = c_next + srow;
+        bp.ldc = next_rows;
+        bp.rows = cr;
+        bp.lda = cur_ld;
+        bp.out = round == 0 ? q.out + row : cur_c + row;
+        bp.ldo = round == 0 ? q.ldo : cur_rows;
+        bp.rank_slot = -1;
+        pl.back_rounds[size_t(round)].push_back(bp);
+        row += cr;
+        srow += std::min(cr, r);
+      }
+      cur_off = stacked;
+      cur_rows = next_rows;
+      cur_ld = next_rows;
+      cur_c = c_next;
+      ++round;
+    }
+    pl.tops.push_back(QrBlock{cur_off, cur_c, 0, 0, cur_rows, cur_ld, cur_rows, 0, q.rank_slot, 0});
+  }
+  return pl;
+}
+
+void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, int kmax,
+            cudaStream_t s) {
+  DevBuf<double> w(size_t(std::max<std::int64_t>(pl.wsize, 1)), s);
+  DevBuf<double> tau(size_t(std::max<std::int64_t>(pl.tausize, 1)), s);
+  if (!pl.direct.empty()) {
+    DevBuf<QrBlock> d;
+    d.upload(pl.direct, s);
+    launch_qr_top(d.get(), int(pl.direct.size()), data, out, d_ranks, r, kmax, kQrRankDropTol, s);
+  }
+  for (size_t rd = 0; rd < pl.chunk_rounds.size(); ++rd) {
+    DevBuf<QrBlock> d;
+    d.upload(pl.chunk_rounds[rd], s);
+    launch_qr_chunk(d.get(), int(pl.chunk_rounds[rd].size()), rd == 0 ? data : w.get(), w.get(),
+                    tau.get(), r, s);
+  }
+  if (!pl.tops.empty()) {
+    DevBuf<QrBlock> d;
+    d.upload(pl.tops, s);
+    launch_qr_top(d.get(), int(pl.tops.size()), w.get(), w.get(), d_ranks, r, kmax, kQrRankDropTol, s);
+  }
+  for (size_t rd = pl.back_rounds.size(); rd-- > 0;) {
+    DevBuf<QrBlock> d;
+    d.upload(pl.back_rounds[rd], s);
+    launch_qr_backprop(d.get(), int(pl.back_rounds[rd].size()), rd == 0 ? data : w.get(), tau.get(),
+                       w.get(), rd == 0 ? out : w.get(), r, kmax, s);
+  }
+}
+
+// ---------------------------------------------------------------- K5 grams
+
+GramPlan plan_gram(const std::vector<GramReq>& reqs, int nx, int ny) {
+  constexpr int kChunk = 512;
+  GramPlan pl;
+  pl.nx = nx;
+  pl.ny = ny;
+  pl.off.assign(reqs.size() + 1, 0);
+  for (size_t i = 0; i < reqs.size(); ++i) {
+    const GramReq& q = reqs[i];
+    for (int r0 = 0; r0 < q.rows; r0 += kChunk) {
+      GramTask t{};
+      t.x = q.x + (q.x_rowmajor ? std::int64_t(r0) * q.lx : r0);
+      t.y = q.y + (q.y_rowmajor ? std::int64_t(r0) * q.ly : r0);
+      t.out = std::int64_t(pl.tasks.size()) * nx * ny;
+      t.rows = std::min(kChunk, q.rows - r0);
+      t.lx = q.lx;
+      t.ly = q.ly;
+      t.x_rowmajor = q.x_rowmajor;
+      t.y_rowmajor = q.y_rowmajor;
+      pl.tasks.push_back(t);
+    }
+    pl.off[i + 1] = std::int64_t(pl.tasks.size());
+  }
+  return pl;
+}
+
+void run_gram(const GramPlan& pl, const double* xb, const double* yb, double* out,
+              cudaStream_t s) {
+  if (pl.tasks.empty()) return;
+  DevBuf<GramTask> d_tasks;
+  d_tasks.upload(pl.tasks, s);
+  DevBuf<std::int64_t> d_off;
+  d_off.upload(pl.off, s);
+  DevBuf<double> partial(pl.tasks.size() * size_t(pl.nx) * size_t(pl.ny), s);
+  launch_gram(d_tasks.get(), int(pl.tasks.size()), xb, yb, pl.nx, pl.ny, partial.get(), s);
+  launch_sum_partials(d_off.get(), int(pl.off.size()) - 1, partial.get(), pl.nx * pl.ny, out, s);
+}
+
+// ---------------------------------------------------------------- K3
+
+PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBlock>& blocks,
+                   const std::vector<std::vector<int>>& payload_boxes, int top_level, int w,
+                   bool with_adjoint) {
+  PeelPlan pp;
+  const int k = e.k;
+  // group[(lp, box, c)] -> payload boxes of color c under `box` (level lp)
+  struct Key {
+    int lp, box, c;
+    bool operator==(const Key& o) const { return lp == o.lp && box == o.box && c == o.c; }
+  };
+  struct KeyHash {
+    size_t operator()(const Key& x) const {
+      return (size_t(x.lp) * 1000003u + size_t(x.box)) * 1000033u + size_t(x.c);
+    }
+  };
+  std::unordered_map<Key, std::vector<int>, KeyHash> groups;
+  for (int c = 0; c < int(payload_boxes.size()); ++c) {
+    for (int v : payload_boxes[size_t(c)]) {
+      const int lv = e.tree.box(v).level;
+      for (int lp = 2; lp <= std::min(lv, top_level); ++lp)
+        groups[Key{lp, e.anc[size_t(lp)][size_t(v)], c}].push_back(v);
+    }
+  }
+  std::unordered_map<std::uint64_t, int> tidx;  // (side, lp, q, c) -> coefficient or -1
+  auto coeff = [&](int side, int lp, int q, int c) -> int {
+    const std::uint64_t key = ((std::uint64_t(side) * 64 + std::uint64_t(lp)) * (1ull << 28) +
+                               std::uint64_t(q)) * (1ull << 24) + std::uint64_t(c);
+    auto it = tidx.find(key);
+    if (it != tidx.end()) return it->second;
+    const auto& ld = rep.levels[size_t(lp)];
+    const auto [x, y] = ld.pairs[size_t(q)];
+    const int src = side == 0 ? y : x;
+    auto g = groups.find(Key{lp, src, c});
+    if (g == groups.end()) return tidx[key] = -1;
+    CoeffTask t{};
+    t.f = side == 0 ? ld.voff[size_t(q)] : ld.uoff[size_t(q)];
+    t.btrans = side == 0 ? 0 : 1;
+    t.b = ld.boff[size_t(q)];
+    t.f_row0 = e.start(src);
+    t.frows = e.count(src);
+    t.seg_begin = int(pp.seg_start.size());
+    for (int v : g->second) {
+      pp.seg_start.push_back(e.start(v));
+      pp.seg_count.push_back(e.count(v));
+      pp.coeff_flops += 2.0 * double(e.count(v)) * k * w;
+    }
+    pp.coeff_flops += 2.0 * k * k * w;
+    t.seg_end = int(pp.seg_start.size());
+    auto& list = side == 0 ? pp.coeff_fwd : pp.coeff_adj;
+    t.t_out = std::int64_t(list.size()) * k * w;
+    list.push_back(t);
+    return tidx[key] = int(list.size()) - 1;
+  };
+  for (const SampleBlock& sb : blocks) {
+    const int a = sb.box;
+    const int la = e.tree.box(a).level;
+    const int rows = e.count(a);
+    for (int t0 = 0; t0 < rows; t0 += kTile) {
+      const int trows = std::min(kTile, rows - t0);
+      PeelTask tf{sb.off + t0, trows, rows, int(pp.terms_fwd.size()), 0};
+      PeelTask ta{sb.off + t0, trows, rows, int(pp.terms_adj.size()), 0};
+      for (int lp = 2; lp <= std::min(la, top_level); ++lp) {
+        const auto& ld = rep.levels[size_t(lp)];
+        if (ld.pairs.empty()) continue;
+        const int ap = e.anc[size_t(lp)][size_t(a)];
+        const std::int64_t roff = e.start(a) - e.start(ap) + t0;
+        const auto [q0, q1] = first_range(ld.pairs, ap);
+        for (int q = q0; q < q1; ++q) {
+          const int ti = coeff(0, lp, q, sb.color);
+          if (ti < 0) continue;
+          pp.terms_fwd.push_back(PeelTerm{ld.uoff[size_t(q)] + roff, std::int64_t(ti) * k * w, e.count(ap), 0});
+          pp.apply_flops += 2.0 * trows * k * w;
+        }
+        if (!with_adjoint) continue;
+        for (int x : e.adj.interaction[size_t(ap)]) {
+          const int q = pair_index(ld.pairs, x, ap);
+          if (q < 0) continue;
+          const int ti = coeff(1, lp, q, sb.color);
+          if (ti < 0) continue;
+          pp.terms_adj.push_back(PeelTerm{ld.voff[size_t(q)] + roff, std::int64_t(ti) * k * w, e.count(ap), 0});
+          pp.apply_flops += 2.0 * trows * k * w;
+        }
+      }
+      tf.term_end = int(pp.terms_fwd.size());
+      ta.term_end = int(pp.terms_adj.size());
+      if (tf.term_end > tf.term_begin) pp.tasks_fwd.push_back(tf);
+      if (with_adjoint && ta.term_end > ta.term_begin) pp.tasks_adj.push_back(ta);
+    }
+  }
+  return pp;
+}
+
+void run_peel(const PeelPlan& pp, const Engine& e, const H1Rep& rep, const double* g, int gld,
+              int w, bool identity, double* samples, int adj_col, cudaStream_t s) {
+  const int k = e.k;
+  DevBuf<std::int64_t> d_ss, d_sc;
+  d_ss.upload(pp.seg_start, s);
+  d_sc.upload(pp.seg_count, s);
+  for (int side = 0; side < 2; ++side) {
+    const auto& coeff = side == 0 ? pp.coeff_fwd : pp.coeff_adj;
+    const auto& tasks = side == 0 ? pp.tasks_fwd : pp.tasks_adj;
+    const auto& terms = side == 0 ? pp.terms_fwd : pp.terms_adj;
+    if (coeff.empty() || tasks.empty()) continue;
+    DevBuf<CoeffTask> d_coeff;
+    d_coeff.upload(coeff, s);
+    DevBuf<double> tbuf(coeff.size() * size_t(k) * size_t(w), s);
+    launch_peel_coeff(d_coeff.get(), int(coeff.size()), rep.d_factors, rep.d_factors, d_ss.get(),
+                      d_sc.get(), g, gld, identity ? -1 : (side == 0 ? 0 : e.r), k, w, tbuf.get(), s);
+    DevBuf<PeelTask> d_tasks;
+    d_tasks.upload(tasks, s);
+    DevBuf<PeelTerm> d_terms;
+    d_terms.upload(terms, s);
+    launch_peel_apply(d_tasks.get(), int(tasks.size()), d_terms.get(), rep.d_factors, tbuf.get(), k,
+                      w, samples, side == 0 ? 0 : adj_col, -1.0, s);
+  }
+}
+
+}  // namespace hpeel::detail

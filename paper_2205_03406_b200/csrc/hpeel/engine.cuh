@@ -1,0 +1,157 @@
+// Device-side plumbing shared by the driver (driver.cu) and the
+// representation/verifier code (rep.cu): stream-ordered buffers, event
+// timers, the per-tree Engine (tree-order coordinates, box ranges, ancestor
+// table) and the batched QR / Gram / peeling task builders.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "kernels.hpp"
+#include "peeling.hpp"
+
+namespace hpeel::detail {
+
+template <class T>
+class DevBuf {
+ public:
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), s_(o.s_) { o.p_ = nullptr; o.n_ = 0; }
+  ~DevBuf() { release(); }
+  void alloc(size_t n, cudaStream_t s) {
+    release();
+    n_ = n;
+    s_ = s;
+    if (n) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.size(), s);
+    if (!v.empty())
+      HP_CUDA(cudaMemcpyAsync(p_, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void release() {
+    if (p_) cudaFreeAsync(p_, s_);
+    p_ = nullptr;
+    n_ = 0;
+  }
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+
+struct Events {
+  cudaEvent_t a = nullptr, b = nullptr;
+  Events() {
+    HP_CUDA(cudaEventCreate(&a));
+    HP_CUDA(cudaEventCreate(&b));
+  }
+  Events(const Events&) = delete;
+  ~Events() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  float ms() const {
+    float t = 0.f;
+    HP_CUDA(cudaEventElapsedTime(&t, a, b));
+    return t;
+  }
+};
+
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int dev) {
+    HP_CUDA(cudaGetDevice(&prev_));
+    if (prev_ != dev) HP_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev_); }
+
+ private:
+  int prev_ = 0;
+};
+
+constexpr int kTile = 64;  // rows per K2 / K3 CTA
+
+// Tree-order copy of the black box and the box tables, for one tree.
+struct Engine {
+  const BoxTree& tree;
+  const AdjacencyInfo& adj;
+  const TreeLayout& lay;
+  const DeviceOperator& op;
+  cudaStream_t s;
+  int r = 0, k = 0;
+  Index n = 0;
+  DevBuf<double> xt;  // tree-order coordinates (dim x n SoA)
+  DevBuf<double> at;  // tree-order dense matrix
+  DevOp dop;
+  DevBuf<std::int64_t> d_box_start, d_box_count;
+  std::vector<std::vector<int>> anc;  // anc[l][box] = ancestor at level l (or -1)
+
+  Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l, const DeviceOperator& o,
+         cudaStream_t st);
+  std::int64_t start(int b) const { return lay.start[size_t(b)]; }
+  int count(int b) const { return int(lay.count[size_t(b)]); }
+};
+
+int pair_index(const std::vector<std::pair<int, int>>& pairs, int a, int b);
+std::pair<int, int> first_range(const std::vector<std::pair<int, int>>& pairs, int a);
+
+// ---------------------------------------------------------------- K4 plan
+struct QrRequest {
+  std::int64_t a;
+  std::int64_t out;
+  int rows;
+  int ldo;
+  int rank_slot;
+};
+struct QrPlan {
+  std::vector<QrBlock> direct, tops;
+  std::vector<std::vector<QrBlock>> chunk_rounds, back_rounds;
+  std::int64_t wsize = 0, tausize = 0;
+};
+QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax);
+void run_qr(const QrPlan& plan, double* data, double* out, int* d_ranks, int r, int kmax,
+            cudaStream_t s);
+
+// ---------------------------------------------------------------- K5 grams
+struct GramReq {
+  std::int64_t x, y;
+  int rows, lx, ly, x_rowmajor, y_rowmajor;
+};
+struct GramPlan {
+  std::vector<GramTask> tasks;
+  std::vector<std::int64_t> off;
+  int nx = 0, ny = 0;
+};
+GramPlan plan_gram(const std::vector<GramReq>& reqs, int nx, int ny);
+void run_gram(const GramPlan& plan, const double* xb, const double* yb, double* out,
+              cudaStream_t s);
+
+// ---------------------------------------------------------------- K3 plan
+struct PeelPlan {
+  std::vector<CoeffTask> coeff_fwd, coeff_adj;
+  std::vector<std::int64_t> seg_start, seg_count;
+  std::vector<PeelTask> tasks_fwd, tasks_adj;
+  std::vector<PeelTerm> terms_fwd, terms_adj;
+  double coeff_flops = 0, apply_flops = 0;
+};
+struct SampleBlock {
+  int box;
+  int color;
+  std::int64_t off;  // sample block offset (col-major, ld = |I_box|)
+};
+PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBlock>& blocks,
+                   const std::vector<std::vector<int>>& payload_boxes, int top_level, int w,
+                   bool with_adjoint);
+void run_peel(const PeelPlan& pp, const Engine& e, const H1Rep& rep, const double* g, int gld,
+              int w, bool identity, double* samples, int adj_col, cudaStream_t s);
+
+}  // namespace hpeel::detail

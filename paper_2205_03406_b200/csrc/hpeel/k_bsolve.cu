@@ -246,7 +246,7 @@ void launch_gram(const GramTask* tasks, int ntasks, const double* xbase, const d
     HP_CUDA(cudaFuncSetAttribute(gram_kernel<EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                  int(smem)));                                               \
     gram_kernel<EE><<<ntasks, kGramThreads, smem, s>>>(tasks, xbase, ybase, nx, ny, out);   \
-    HP_CUDA(cudaGetLastError());                                                            \
+    HP_LAUNCHED();                                                            \
     return;                                                                                 \
   }
   HP_G(2) HP_G(4) HP_G(8) HP_G(12) HP_G(16) HP_G(20) HP_G(25) HP_G(32)
@@ -258,7 +258,7 @@ void launch_sum_partials(const std::int64_t* off, int ndst, const double* src, i
                          double* dst, cudaStream_t s) {
   if (ndst == 0) return;
   sum_partials_kernel<<<ndst, 128, 0, s>>>(off, src, len, dst);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_bsolve(int npairs, const double* gpu_, const double* middle, const double* vg, int r,
@@ -267,7 +267,7 @@ void launch_bsolve(int npairs, const double* gpu_, const double* middle, const d
   const size_t smem = size_t(r * k + k * k + r * r + 2 * k * r + k) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(bsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   bsolve_kernel<<<npairs, kSvdThreads, smem, s>>>(gpu_, middle, vg, r, k, tol, boff, b);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 }  // namespace hpeel

@@ -57,7 +57,7 @@ void launch_permute_rows(const double* src, std::int64_t ssr, std::int64_t ssc, 
   if (total == 0) return;
   const unsigned blocks = unsigned(std::min<std::int64_t>((total + 255) / 256, 148 * 16));
   gather_rows_kernel<<<blocks, 256, 0, s>>>(src, ssr, ssc, map, rows, w, dst, dsr, dsc);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_dense_apply(const DenseTask* tasks, const int* box_off, int nboxes,
@@ -65,7 +65,14 @@ void launch_dense_apply(const DenseTask* tasks, const int* box_off, int nboxes,
                         std::int64_t ldy, cudaStream_t s) {
   if (nboxes == 0) return;
   dense_apply_kernel<<<nboxes, 256, 0, s>>>(tasks, box_off, dense, x, w, adjoint ? 1 : 0, y, ldy);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
+}  // namespace hpeel
+
+namespace hpeel {
+std::int64_t& launch_counter() {
+  static std::int64_t count = 0;
+  return count;
+}
 }  // namespace hpeel

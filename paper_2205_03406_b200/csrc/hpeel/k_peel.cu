@@ -7,7 +7,9 @@
 // U_q (B_q (V_q^T Omega_c(I_y))) for every color over all N rows. Here
 // coefficient tasks form T_{q,c} = B_q * sum_{v in P_c, v in y} V_q[v]^T G_v
 // once (k x r), and apply tasks subtract U_q[rows of a] T_{q,c} from each
-// level-l sample block whose box a lies under x.
+// level-l sample block whose box a lies under x. Both contractions run on
+// FP64 DMMA (m8n8k4) with shared-memory operand tiles in conflict-free
+// strides (== 4 mod 16 doubles) and cp.async double buffering.
 #include <cuda_runtime.h>
 
 #include "kernels.hpp"
@@ -16,64 +18,195 @@ namespace hpeel {
 
 namespace {
 
-constexpr int kCoeffThreads = 256;
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// M (k x w) accumulated in registers, E entries per thread; then T = op(B) M
-// through shared memory.
-template <int E>
-__global__ void __launch_bounds__(kCoeffThreads)
-peel_coeff_kernel(const CoeffTask* __restrict__ tasks, const double* __restrict__ factors,
-                  const double* __restrict__ bmat, const std::int64_t* __restrict__ seg_start,
-                  const std::int64_t* __restrict__ seg_count, const double* __restrict__ g,
-                  int gld, int gcol0, int k, int w, double* __restrict__ tbuf) {
-  extern __shared__ double sm[];  // k*w (M) then k*k (B)
-  const CoeffTask task = tasks[blockIdx.x];
-  const int tid = threadIdx.x;
-  const int kw = k * w;
-  double acc[E];
-#pragma unroll
-  for (int u = 0; u < E; ++u) acc[u] = 0.0;
-  const double* f = factors + task.f;
+__host__ __device__ constexpr int stride4(int n) { return ((n + 11) / 16) * 16 + 4; }
 
-  for (int sg = task.seg_begin; sg < task.seg_end; ++sg) {
-    const std::int64_t s0 = seg_start[sg] - task.f_row0;
-    const std::int64_t cnt = seg_count[sg];
-    if (gcol0 >= 0) {
-      // Gaussian payload: M[i][c] += sum_t F[s0+t][i] * G[pos][c]
-      for (std::int64_t t = 0; t < cnt; ++t) {
-        const std::int64_t row = s0 + t;
-        const double* grow = g + (seg_start[sg] + t) * gld + gcol0;
+constexpr int kThreads = 128;
+constexpr int kRows = 64;  // apply tile rows (4 warps x 16)
+constexpr int kFS = kRows + 4;
+
+// ------------------------------------------------------------------ apply
+// out[rows, c0 + c] += alpha * sum_terms F[rows, :k] T[:k, c0 + c]
+// F tile staged column-major (ld kFS), T staged column-major (ld ts).
+template <int NT>
+__global__ void __launch_bounds__(kThreads)
+peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelTerm* __restrict__ terms,
+                  const double* __restrict__ factors, const double* __restrict__ tbuf, int k,
+                  int w, double* __restrict__ out, int ocol0, double alpha) {
+  extern __shared__ __align__(16) double sm[];
+  const int kp = (k + 3) & ~3;
+  const int ts = stride4(kp);
+  const int fsz = kp * kFS, tsz = NT * 8 * ts;
+  auto fs = [&](int b) { return sm + b * (fsz + tsz); };
+  auto tsm = [&](int b) { return sm + b * (fsz + tsz) + fsz; };
+  const PeelTask task = tasks[blockIdx.x];
+  const int c0 = blockIdx.y * NT * 8;
+  const int ncol = min(NT * 8, w - c0);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < 2 * (fsz + tsz); e += kThreads) sm[e] = 0.0;
+  __syncthreads();
+
+  auto issue = [&](int buf, int q) {
+    const PeelTerm term = terms[q];
+    for (int e = tid; e < kRows * k; e += kThreads) {
+      const int i = e % kRows, l = e / kRows;
+      if (i < task.rows) cp_async8(fs(buf) + l * kFS + i, factors + term.f + i + std::int64_t(l) * term.fld);
+    }
+    for (int e = tid; e < ncol * k; e += kThreads) {
+      const int l = e % k, c = e / k;
+      cp_async8(tsm(buf) + c * ts + l, tbuf + term.t + l + std::int64_t(c0 + c) * k);
+    }
+    cp_async_commit();
+  };
+
+  double acc[2][NT][2];
 #pragma unroll
-        for (int u = 0; u < E; ++u) {
-          const int e = tid + u * kCoeffThreads;
-          if (e < kw) {
-            const int i = e % k, c = e / k;
-            acc[u] = fma(f[row + std::int64_t(i) * task.frows], grow[c], acc[u]);
-          }
-        }
-      }
-    } else {
-      // Identity payload [I | 0]: M[i][t] += F[s0+t][i] for t < min(cnt, w)
+  for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int u = 0; u < E; ++u) {
-        const int e = tid + u * kCoeffThreads;
-        if (e < kw) {
-          const int i = e % k, c = e / k;
-          if (c < cnt) acc[u] += f[s0 + c + std::int64_t(i) * task.frows];
-        }
+    for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+
+  if (task.term_begin < task.term_end) issue(0, task.term_begin);
+  int buf = 0;
+  for (int q = task.term_begin; q < task.term_end; ++q, buf ^= 1) {
+    cp_async_wait_all();
+    __syncthreads();
+    if (q + 1 < task.term_end) issue(buf ^ 1, q + 1);
+    const double* a0p = fs(buf) + (lane & 3) * kFS + warp * 16 + (lane >> 2);
+    const double* bp = tsm(buf) + (lane >> 2) * ts + (lane & 3);
+    for (int kk = 0; kk < kp; kk += 4) {
+      const double a0 = a0p[kk * kFS], a1 = a0p[kk * kFS + 8];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const double b = bp[nt * 8 * ts + kk];
+        dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a0, b);
+        dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, b);
       }
     }
   }
-  double* ms = sm;
-  double* bs = sm + kw;
 #pragma unroll
-  for (int u = 0; u < E; ++u) {
-    const int e = tid + u * kCoeffThreads;
-    if (e < kw) ms[e] = acc[u];  // (i, c) at i + c*k: col-major k x w
+  for (int m = 0; m < 2; ++m) {
+    const int rr = warp * 16 + m * 8 + (lane >> 2);
+    if (rr >= task.rows) continue;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = nt * 8 + (lane & 3) * 2 + h;
+        if (c < ncol) out[task.out + rr + std::int64_t(ocol0 + c0 + c) * task.ld] += alpha * acc[m][nt][h];
+      }
   }
-  for (int e = tid; e < k * k; e += kCoeffThreads) bs[e] = bmat[task.b + e];
+}
+
+// ------------------------------------------------------------------ coeff
+// Gaussian payloads: M (k x w) = sum_v F[v rows]^T G[v rows, gcol0 : gcol0 + w]
+// on DMMA (A = F^T staged [m][t], B = G staged [t][c]), then T = op(B) M.
+constexpr int kCK = 32;  // payload rows per stage
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads)
+peel_coeff_dmma_kernel(const CoeffTask* __restrict__ tasks, const double* __restrict__ factors,
+                       const double* __restrict__ bmat, const std::int64_t* __restrict__ seg_start,
+                       const std::int64_t* __restrict__ seg_count, const double* __restrict__ g,
+                       int gld, int gcol0, int k, int w, double* __restrict__ tbuf) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int S = stride4(NT * 8);
+  constexpr int FS = stride4(kCK);  // F^T rows (one per factor column m), kCK payload rows each
+  const int mt = (k + 7) / 8;       // m-tiles (<= 8)
+  auto fs = [&](int b) { return sm + b * mt * 8 * FS; };
+  auto gs = [&](int b) { return sm + 2 * mt * 8 * FS + b * kCK * S; };
+  double* ms = sm + 2 * mt * 8 * FS + 2 * kCK * S;  // k x w col-major (after the loop)
+  double* bs = ms + k * w;
+  const CoeffTask task = tasks[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < 2 * (mt * 8 * FS + kCK * S); e += kThreads) sm[e] = 0.0;
   __syncthreads();
-  for (int e = tid; e < kw; e += kCoeffThreads) {
+
+  auto issue = [&](int buf, int sg, std::int64_t r0) {
+    const std::int64_t left = seg_count[sg] - r0;
+    const int cnt = left < kCK ? int(left) : kCK;
+    const std::int64_t frow = seg_start[sg] - task.f_row0 + r0;
+    const std::int64_t gpos = seg_start[sg] + r0;
+    for (int e = tid; e < cnt * k; e += kThreads) {
+      const int t = e % cnt, m = e / cnt;
+      cp_async8(fs(buf) + m * FS + t, factors + task.f + frow + t + std::int64_t(m) * task.frows);
+    }
+    for (int e = tid; e < cnt * w; e += kThreads) {
+      const int t = e / w, c = e - t * w;
+      cp_async8(gs(buf) + t * S + c, g + (gpos + t) * gld + gcol0 + c);
+    }
+    cp_async_commit();
+    return cnt;
+  };
+
+  double acc[2][NT][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+
+  int sg = task.seg_begin;
+  std::int64_t r0 = 0;
+  int buf = 0;
+  int cnt_cur = 0;
+  if (sg < task.seg_end) cnt_cur = issue(0, sg, 0);
+  while (sg < task.seg_end) {
+    int nsg = sg;
+    std::int64_t nr0 = r0 + kCK;
+    if (nr0 >= seg_count[nsg]) {
+      ++nsg;
+      nr0 = 0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    int cnt_next = 0;
+    if (nsg < task.seg_end) cnt_next = issue(buf ^ 1, nsg, nr0);
+    // rows past the chunk end hold stale rows of earlier chunks: zero G there
+    if (cnt_cur < kCK) {
+      for (int e = tid; e < (kCK - cnt_cur) * S; e += kThreads) gs(buf)[cnt_cur * S + e] = 0.0;
+      __syncthreads();
+    }
+#pragma unroll
+    for (int mm = 0; mm < 2; ++mm) {
+      const int mtile = warp + 4 * mm;
+      if (mtile >= mt) continue;
+      const double* ap = fs(buf) + (mtile * 8 + (lane >> 2)) * FS + (lane & 3);
+      const double* bp = gs(buf) + (lane & 3) * S + (lane >> 2);
+#pragma unroll
+      for (int kk = 0; kk < kCK; kk += 4) {
+        const double a = ap[kk];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma8x8x4(acc[mm][nt][0], acc[mm][nt][1], a, bp[kk * S + nt * 8]);
+      }
+    }
+    sg = nsg;
+    r0 = nr0;
+    cnt_cur = cnt_next;
+    buf ^= 1;
+  }
+  __syncthreads();
+  // M -> shared (col-major k x w), B -> shared
+#pragma unroll
+  for (int mm = 0; mm < 2; ++mm) {
+    const int mtile = warp + 4 * mm;
+    if (mtile >= mt) continue;
+    const int m = mtile * 8 + (lane >> 2);
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = nt * 8 + (lane & 3) * 2 + h;
+        if (m < k && c < w) ms[m + c * k] = acc[mm][nt][h];
+      }
+  }
+  for (int e = tid; e < k * k; e += kThreads) bs[e] = bmat[task.b + e];
+  __syncthreads();
+  for (int e = tid; e < k * w; e += kThreads) {
     const int i = e % k, c = e / k;
     double t = 0.0;
     if (task.btrans) {
@@ -85,49 +218,61 @@ peel_coeff_kernel(const CoeffTask* __restrict__ tasks, const double* __restrict_
   }
 }
 
-constexpr int kApplyThreads = 256;
-constexpr int kApplyRows = 64;
+// Identity payloads [I | 0] (leaf phase): M[:, t] = sum_v F[row v_t, :]^T for
+// t < |v|, a gather; then T = op(B) M.
+__global__ void __launch_bounds__(256)
+peel_coeff_identity_kernel(const CoeffTask* __restrict__ tasks, const double* __restrict__ factors,
+                           const double* __restrict__ bmat, const std::int64_t* __restrict__ seg_start,
+                           const std::int64_t* __restrict__ seg_count, int k, int w,
+                           double* __restrict__ tbuf) {
+  extern __shared__ __align__(16) double sm[];
+  double* ms = sm;
+  double* bs = sm + k * w;
+  const CoeffTask task = tasks[blockIdx.x];
+  const double* f = factors + task.f;
+  for (int e = threadIdx.x; e < k * w; e += blockDim.x) {
+    const int i = e % k, c = e / k;
+    double acc = 0.0;
+    for (int sg = task.seg_begin; sg < task.seg_end; ++sg)
+      if (c < seg_count[sg]) acc += f[seg_start[sg] - task.f_row0 + c + std::int64_t(i) * task.frows];
+    ms[e] = acc;
+  }
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) bs[e] = bmat[task.b + e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * w; e += blockDim.x) {
+    const int i = e % k, c = e / k;
+    double t = 0.0;
+    if (task.btrans) {
+      for (int l = 0; l < k; ++l) t = fma(bs[l + i * k], ms[l + c * k], t);
+    } else {
+      for (int l = 0; l < k; ++l) t = fma(bs[i + l * k], ms[l + c * k], t);
+    }
+    tbuf[task.t_out + e] = t;
+  }
+}
 
-// acc (64 x w) in registers (E = ceil(64 w / 256) entries per thread).
-template <int E>
-__global__ void __launch_bounds__(kApplyThreads)
-peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelTerm* __restrict__ terms,
-                  const double* __restrict__ factors, const double* __restrict__ tbuf, int k,
-                  int w, double* __restrict__ out, int ocol0, double alpha) {
-  extern __shared__ double sm[];  // F tile (64 x k, col-major) then T (k x w)
-  double* fs = sm;
-  double* ts = sm + kApplyRows * k;
-  const PeelTask task = tasks[blockIdx.x];
-  const int tid = threadIdx.x;
-  double acc[E];
-#pragma unroll
-  for (int u = 0; u < E; ++u) acc[u] = 0.0;
-  for (int q = task.term_begin; q < task.term_end; ++q) {
-    const PeelTerm term = terms[q];
-    __syncthreads();
-    for (int e = tid; e < kApplyRows * k; e += kApplyThreads) {
-      const int i = e % kApplyRows, l = e / kApplyRows;
-      fs[e] = i < task.rows ? factors[term.f + i + std::int64_t(l) * term.fld] : 0.0;
-    }
-    for (int e = tid; e < k * w; e += kApplyThreads) ts[e] = tbuf[term.t + e];
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < E; ++u) {
-      const int e = tid + u * kApplyThreads;
-      const int i = e % kApplyRows, c = e / kApplyRows;
-      if (c < w) {
-        double t = acc[u];
-        for (int l = 0; l < k; ++l) t = fma(fs[i + l * kApplyRows], ts[l + c * k], t);
-        acc[u] = t;
-      }
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < E; ++u) {
-    const int e = tid + u * kApplyThreads;
-    const int i = e % kApplyRows, c = e / kApplyRows;
-    if (c < w && i < task.rows) out[task.out + i + std::int64_t(ocol0 + c) * task.ld] += alpha * acc[u];
-  }
+template <int NT>
+void coeff_nt(const CoeffTask* tasks, int ntasks, const double* factors, const double* bmat,
+              const std::int64_t* ss, const std::int64_t* sc, const double* g, int gld, int gcol0,
+              int k, int w, double* tbuf, cudaStream_t s) {
+  constexpr int S = stride4(NT * 8);
+  constexpr int FS = stride4(kCK);
+  const int mt = (k + 7) / 8;
+  const size_t smem = size_t(2 * mt * 8 * FS + 2 * kCK * S + k * w + k * k) * sizeof(double);
+  HP_CUDA(cudaFuncSetAttribute(peel_coeff_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  peel_coeff_dmma_kernel<NT><<<ntasks, kThreads, smem, s>>>(tasks, factors, bmat, ss, sc, g, gld, gcol0, k, w, tbuf);
+  HP_LAUNCHED();
+}
+
+template <int NT>
+void apply_nt(const PeelTask* tasks, int ntasks, const PeelTerm* terms, const double* factors,
+              const double* tbuf, int k, int w, double* out, int ocol0, double alpha, cudaStream_t s) {
+  const int kp = (k + 3) & ~3;
+  const size_t smem = size_t(2 * (kp * kFS + NT * 8 * stride4(kp))) * sizeof(double);
+  HP_CUDA(cudaFuncSetAttribute(peel_apply_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const dim3 grid(unsigned(ntasks), unsigned((w + NT * 8 - 1) / (NT * 8)));
+  peel_apply_kernel<NT><<<grid, kThreads, smem, s>>>(tasks, terms, factors, tbuf, k, w, out, ocol0, alpha);
+  HP_LAUNCHED();
 }
 
 }  // namespace
@@ -137,40 +282,37 @@ void launch_peel_coeff(const CoeffTask* tasks, int ntasks, const double* factors
                        const std::int64_t* seg_count, const double* g, int gld, int gcol0, int k,
                        int w, double* tbuf, cudaStream_t s) {
   if (ntasks == 0) return;
-  const int e = (k * w + kCoeffThreads - 1) / kCoeffThreads;
-  const size_t smem = size_t(k * w + k * k) * sizeof(double);
-#define HP_C(EE)                                                                              \
-  if (e <= EE) {                                                                              \
-    HP_CUDA(cudaFuncSetAttribute(peel_coeff_kernel<EE>,                                       \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));    \
-    peel_coeff_kernel<EE><<<ntasks, kCoeffThreads, smem, s>>>(tasks, factors, bmat, seg_start, \
-                                                              seg_count, g, gld, gcol0, k, w, tbuf); \
-    HP_CUDA(cudaGetLastError());                                                              \
-    return;                                                                                   \
+  if (k > 64) throw std::invalid_argument("peel: rank k > 64 is not supported");
+  if (gcol0 < 0) {
+    const size_t smem = size_t(k * w + k * k) * sizeof(double);
+    HP_CUDA(cudaFuncSetAttribute(peel_coeff_identity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    peel_coeff_identity_kernel<<<ntasks, 256, smem, s>>>(tasks, factors, bmat, seg_start, seg_count, k, w, tbuf);
+    HP_LAUNCHED();
+    return;
   }
-  HP_C(2) HP_C(4) HP_C(8) HP_C(12) HP_C(16) HP_C(24) HP_C(32) HP_C(48) HP_C(64)
+  const int nt = (w + 7) / 8;
+#define HP_C(N) \
+  case N: return coeff_nt<N>(tasks, ntasks, factors, bmat, seg_start, seg_count, g, gld, gcol0, k, w, tbuf, s);
+  switch (nt) {
+    HP_C(1) HP_C(2) HP_C(3) HP_C(4) HP_C(5) HP_C(6) HP_C(7) HP_C(8) HP_C(9) HP_C(10)
+    default: throw std::invalid_argument("peel coefficient width > 80 is not supported");
+  }
 #undef HP_C
-  throw std::invalid_argument("peel coefficient block too large (k * w > 16384)");
 }
 
 void launch_peel_apply(const PeelTask* tasks, int ntasks, const PeelTerm* terms,
                        const double* factors, const double* tbuf, int k, int w, double* out,
                        int ocol0, double alpha, cudaStream_t s) {
   if (ntasks == 0) return;
-  const int e = (kApplyRows * w + kApplyThreads - 1) / kApplyThreads;
-  const size_t smem = size_t(kApplyRows * k + k * w) * sizeof(double);
-#define HP_A(EE)                                                                              \
-  if (e <= EE) {                                                                              \
-    HP_CUDA(cudaFuncSetAttribute(peel_apply_kernel<EE>,                                       \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));    \
-    peel_apply_kernel<EE><<<ntasks, kApplyThreads, smem, s>>>(tasks, terms, factors, tbuf, k, w, \
-                                                              out, ocol0, alpha);                    \
-    HP_CUDA(cudaGetLastError());                                                              \
-    return;                                                                                   \
+  if (k > 64) throw std::invalid_argument("peel: rank k > 64 is not supported");
+  const int nt = (w + 7) / 8;
+#define HP_A(N) \
+  case N: return apply_nt<N>(tasks, ntasks, terms, factors, tbuf, k, w, out, ocol0, alpha, s);
+  switch (nt) {
+    HP_A(1) HP_A(2) HP_A(3) HP_A(4) HP_A(5) HP_A(6) HP_A(7) HP_A(8) HP_A(9) HP_A(10)
+    default: return apply_nt<8>(tasks, ntasks, terms, factors, tbuf, k, w, out, ocol0, alpha, s);
   }
-  HP_A(2) HP_A(4) HP_A(8) HP_A(12) HP_A(16) HP_A(20) HP_A(24) HP_A(32) HP_A(48) HP_A(64)
 #undef HP_A
-  throw std::invalid_argument("peel apply width too large (w > 256)");
 }
 
 }  // namespace hpeel

@@ -234,7 +234,7 @@ void launch_qr_chunk(const QrBlock* blocks, int nb, double* data, double* rout, 
   const size_t smem = size_t(qr_rows_max(cols)) * size_t(cols) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(qr_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   qr_chunk_kernel<<<nb, kQrThreads, smem, s>>>(blocks, data, rout, tau, cols);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_qr_top(const QrBlock* blocks, int nb, double* data, double* outbuf, int* ranks,
@@ -244,7 +244,7 @@ void launch_qr_top(const QrBlock* blocks, int nb, double* data, double* outbuf, 
   const size_t smem = size_t(qr_rows_max(cols)) * size_t(cols + kQrWarps) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(qr_top_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   qr_top_kernel<<<nb, kQrThreads, smem, s>>>(blocks, data, outbuf, ranks, cols, kmax, tol);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_qr_backprop(const QrBlock* blocks, int nb, const double* data, const double* tau,
@@ -254,7 +254,7 @@ void launch_qr_backprop(const QrBlock* blocks, int nb, const double* data, const
   const size_t smem = size_t(qr_rows_max(cols)) * size_t(cols + kQrWarps) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(qr_backprop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   qr_backprop_kernel<<<nb, kQrThreads, smem, s>>>(blocks, data, tau, parent, outbuf, cols, kmax);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 }  // namespace hpeel

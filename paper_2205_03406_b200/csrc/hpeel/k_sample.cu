@@ -45,42 +45,77 @@ __global__ void payload_gaussian_kernel(double* g, int gld, int r, std::int64_t 
 }
 
 constexpr int kBM = 64;       // rows per CTA (4 warps x 16)
-constexpr int kBK = 32;       // payload rows per smem stage
+constexpr int kBK = 32;       // payload rows per shared-memory stage
 constexpr int kThreads = 128;
+constexpr int kKS = kBK + 4;  // kernel-tile row stride (== 4 mod 16: conflict-free A fragments)
 
 __host__ __device__ constexpr int smem_stride(int nt) {
-  // row stride (doubles) == 4 mod 16: conflict-free B-fragment reads
+  // payload row stride (doubles) == 4 mod 16: conflict-free B-fragment reads
   return ((nt * 8 + 11) / 16) * 16 + 4;
 }
 
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Per payload chunk (32 rows): (1) all 128 threads evaluate the 64 x 32 kernel
+// tile into shared memory (16 independent evaluations per thread: full ILP
+// on the FP64 pipe), (2) each warp runs 2 x NT DMMA.8x8x4 per k-step over its
+// 16 rows. The next chunk's payload rows stream in with cp.async meanwhile.
+template <int NT>
+constexpr size_t sample_smem_bytes() {
+  return size_t(2 * kBK * smem_stride(NT) + kBM * kKS) * sizeof(double);
+}
+
 template <int NT, int KIND, int DIM, bool TRANS>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, NT <= 10 ? 4 : (NT <= 14 ? 3 : 2))
 sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
                     const std::int64_t* __restrict__ pay_off, const int* __restrict__ pay_pos,
                     const double* __restrict__ g, int gld, int gcol0, int ncols,
                     double* __restrict__ out, int ocol0) {
   constexpr int S = smem_stride(NT);
-  __shared__ __align__(16) double gs[kBK * S];
-  __shared__ double xs[DIM > 0 ? DIM : 1][kBK];
-  __shared__ int js[kBK];
+  constexpr int D = DIM > 0 ? DIM : 1;
+  extern __shared__ __align__(16) double dyn_smem[];
+  double(*gs)[kBK * S] = reinterpret_cast<double(*)[kBK * S]>(dyn_smem);
+  double* ks = dyn_smem + 2 * kBK * S;
+  __shared__ double xs[2][D][kBK];
+  __shared__ double xr[D][kBM];
+  __shared__ int js[2][kBK];
 
   const SampleTask task = tasks[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
 
-  // Rows owned by this lane in the A/C fragments.
-  std::int64_t irow[2];
-  double xi[2][DIM > 0 ? DIM : 1];
-#pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    int rr = warp * 16 + m * 8 + (lane >> 2);
-    if (rr >= task.rows) rr = task.rows - 1;
-    irow[m] = task.row0 + rr;
+  for (int e = tid; e < 2 * kBK * S; e += kThreads) (&gs[0][0])[e] = 0.0;
+  if (tid < kBM) {
+    const int rr = tid < task.rows ? tid : task.rows - 1;
     if constexpr (KIND != kOpDense) {
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) xi[m][d] = op.x[d * n + irow[m]];
+      for (int d = 0; d < DIM; ++d) xr[d][tid] = op.x[d * n + task.row0 + rr];
     }
   }
+  __syncthreads();
+
+  const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
+  auto issue = [&](int buf, std::int64_t base) {
+    const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
+    for (int idx = tid; idx < cnt * ncols; idx += kThreads) {
+      const int t = idx / ncols, c = idx - t * ncols;
+      cp_async8(&gs[buf][t * S + c], g + std::int64_t(pay_pos[base + t]) * gld + gcol0 + c);
+    }
+    cp_async_commit();
+    if (tid < kBK) {
+      const int pos = tid < cnt ? pay_pos[base + tid] : -1;
+      js[buf][tid] = pos;
+      if constexpr (KIND != kOpDense) {
+#pragma unroll
+        for (int d = 0; d < DIM; ++d) xs[buf][d][tid] = pos >= 0 ? op.x[d * n + pos] : 0.0;
+      }
+    }
+  };
 
   double acc[2][NT][2];
 #pragma unroll
@@ -88,52 +123,53 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 
-  const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
-  for (std::int64_t base = p0; base < p1; base += kBK) {
-    const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
+  if (p0 < p1) issue(0, p0);
+  int buf = 0;
+  for (std::int64_t base = p0; base < p1; base += kBK, buf ^= 1) {
+    cp_async_wait_all();
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kBK * NT * 8; idx += kThreads) {
-      const int t = idx / (NT * 8), c = idx - t * (NT * 8);
-      double v = 0.0;
-      if (t < cnt && c < ncols) v = g[std::int64_t(pay_pos[base + t]) * gld + gcol0 + c];
-      gs[t * S + c] = v;
-    }
-    if (threadIdx.x < kBK) {
-      const int t = threadIdx.x;
-      const int pos = t < cnt ? pay_pos[base + t] : -1;
-      js[t] = pos;
+    if (base + kBK < p1) issue(buf ^ 1, base + kBK);
+
+    // (1) kernel tile: lane = payload column, warp strides over the 64 rows
+    {
+      const int jpos = js[buf][lane];
+      double xj[D];
       if constexpr (KIND != kOpDense) {
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) xs[d][t] = pos >= 0 ? op.x[d * n + pos] : 0.0;
+        for (int d = 0; d < DIM; ++d) xj[d] = xs[buf][d][lane];
       }
-    }
-    __syncthreads();
-#pragma unroll 2
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      const int t = ks * 4 + (lane & 3);
-      const int jpos = js[t];
-      double a[2];
 #pragma unroll
-      for (int m = 0; m < 2; ++m) {
+      for (int u = 0; u < kBM / 4; ++u) {
+        const int row = warp + 4 * u;
+        const std::int64_t ipos = task.row0 + (row < task.rows ? row : task.rows - 1);
         double v = 0.0;
         if (jpos >= 0) {
           if constexpr (KIND == kOpDense) {
-            v = TRANS ? op.a[std::int64_t(jpos) + irow[m] * n] : op.a[irow[m] + std::int64_t(jpos) * n];
+            v = TRANS ? op.a[std::int64_t(jpos) + ipos * n] : op.a[ipos + std::int64_t(jpos) * n];
           } else {
-            double xj[DIM > 0 ? DIM : 1];
+            double xi[D];
 #pragma unroll
-            for (int d = 0; d < DIM; ++d) xj[d] = xs[d][t];
-            v = kernel_value<KIND, DIM>(xi[m], xj, irow[m] == jpos, op.param);
+            for (int d = 0; d < DIM; ++d) xi[d] = xr[d][row];
+            v = kernel_value<KIND, DIM>(xi, xj, ipos == jpos, op.param);
           }
         }
-        a[m] = v;
+        ks[row * kKS + lane] = v;
       }
-      const double* brow = gs + t * S + (lane >> 2);
+    }
+    __syncthreads();
+
+    // (2) DMMA over the tile
+    const double* arow0 = ks + (warp * 16 + (lane >> 2)) * kKS + (lane & 3);
+    const double* arow1 = arow0 + 8 * kKS;
+    const double* brow = gs[buf] + (lane & 3) * S + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < kBK / 4; ++kk) {
+      const double a0 = arow0[kk * 4], a1 = arow1[kk * 4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const double b = brow[nt * 8];
-        dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a[0], b);
-        dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a[1], b);
+        const double b = brow[kk * 4 * S + nt * 8];
+        dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a0, b);
+        dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, b);
       }
     }
   }
@@ -152,18 +188,20 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
     }
   }
 }
-
 template <int NT, int KIND, int DIM>
 void launch_nt_kind_dim(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
                         const std::int64_t* pay_off, const int* pay_pos, const double* g, int gld,
                         int gcol0, int ncols, double* out, int ocol0, cudaStream_t s) {
   // kernel kinds are symmetric: only the explicit dense operator has a transpose
+  constexpr size_t smem = sample_smem_bytes<NT>();
   if (KIND == kOpDense && trans) {
-    sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense><<<ntasks, kThreads, 0, s>>>(
-        op, tasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0);
+    auto* fn = sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense>;
+    HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0);
   } else {
-    sample_apply_kernel<NT, KIND, DIM, false><<<ntasks, kThreads, 0, s>>>(
-        op, tasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0);
+    auto* fn = sample_apply_kernel<NT, KIND, DIM, false>;
+    HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0);
   }
 }
 
@@ -279,7 +317,7 @@ void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const in
   const std::int64_t total = n * gld;
   const unsigned blocks = unsigned(std::min<std::int64_t>((total + 255) / 256, 148 * 32));
   payload_gaussian_kernel<<<blocks, 256, 0, s>>>(g, gld, r, n, pos_box, local, seed, level);
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
@@ -301,7 +339,7 @@ void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, i
       throw std::invalid_argument("sample width 2r > 160 is not supported by the apply kernel");
   }
 #undef HP_CASE
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_identity_apply(const DevOp& op, const SampleTask* tasks, int ntasks,
@@ -317,7 +355,7 @@ void launch_identity_apply(const DevOp& op, const SampleTask* tasks, int ntasks,
   else if (op.kind == kOpInvDist4Pi) { if (op.dim == 1) HP_ID(kOpInvDist4Pi, 1); else if (op.dim == 2) HP_ID(kOpInvDist4Pi, 2); else HP_ID(kOpInvDist4Pi, 3); }
   else { if (op.dim == 1) HP_ID(kOpExp, 1); else if (op.dim == 2) HP_ID(kOpExp, 2); else HP_ID(kOpExp, 3); }
 #undef HP_ID
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 void launch_full_apply(const DevOp& op, bool trans, const double* x, int w, double* y,
@@ -333,7 +371,7 @@ void launch_full_apply(const DevOp& op, bool trans, const double* x, int w, doub
   else if (op.kind == kOpInvDist4Pi) { if (op.dim == 1) HP_FA(kOpInvDist4Pi, 1); else if (op.dim == 2) HP_FA(kOpInvDist4Pi, 2); else HP_FA(kOpInvDist4Pi, 3); }
   else { if (op.dim == 1) HP_FA(kOpExp, 1); else if (op.dim == 2) HP_FA(kOpExp, 2); else HP_FA(kOpExp, 3); }
 #undef HP_FA
-  HP_CUDA(cudaGetLastError());
+  HP_LAUNCHED();
 }
 
 }  // namespace hpeel

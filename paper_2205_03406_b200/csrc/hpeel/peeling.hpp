@@ -55,6 +55,7 @@ struct PhaseReport {
   double qr_ms = 0.0;            // K4
   double bsolve_ms = 0.0;        // K5 (incl. gram reductions)
   double apply_flops = 0.0;      // FMAs*2 executed by K2 on needed rows
+  double peel_flops = 0.0;       // FMAs*2 executed by K3 (coefficients + subtraction)
   double kernel_evals = 0.0;
 };
 
