@@ -55,6 +55,8 @@ const char* hp_last_error(void);
 int hp_device_count(int* count);
 /* kernels launched by this library so far (bench.py gpu_launches) */
 int64_t hp_launch_count(void);
+/* profiling only: 1 = K2 skips kernel evaluation, 2 = K2 skips DMMA, 0 = normal */
+void hp_debug_set_k2_mode(int mode);
 int hp_device_synchronize(void);
 
 /* ---- RNG: proj/include/hpeel/rng.hpp:37-50, proj/src/rng.cpp:31-59 ---- */

@@ -29,6 +29,7 @@ _SIGNATURES = {
     "hp_last_error": (C.c_char_p, []),
     "hp_device_count": (C.c_int, [ip]),
     "hp_launch_count": (i64, []),
+    "hp_debug_set_k2_mode": (None, [C.c_int]),
     "hp_device_synchronize": (C.c_int, []),
     "hp_mix_seed": (u64, [u64, u64]),
     "hp_gaussian_matrix": (C.c_int, [i64, i64, u64, dp]),

@@ -34,6 +34,7 @@ struct hp_rep {
 
 namespace hpeel {
 std::int64_t& launch_counter();
+void set_k2_mode(int mode);
 void debug_fast_log(const double* x, std::int64_t n, double* y, int device);
 Matrix debug_payload(const BoxTree& tree, const TreeLayout& lay, int level, int r,
                      std::uint64_t seed, int device);
@@ -85,6 +86,8 @@ int hp_device_count(int* count) {
 }
 
 int64_t hp_launch_count(void) { return launch_counter(); }
+
+void hp_debug_set_k2_mode(int mode) { set_k2_mode(mode); }
 
 int hp_device_synchronize(void) {
   return guard([&] {

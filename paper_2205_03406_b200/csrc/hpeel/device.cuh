@@ -46,7 +46,11 @@ struct DevOp {
   const double* a = nullptr;   // kOpDense: n x n col-major, tree order
   double param = 1.0;          // kOpExp length scale
   int symmetric = 1;           // A == A^T: forward and adjoint share K(i, j)
+  const double* ltab = nullptr;  // fast_log table (3 x kLogTab doubles, device)
 };
+
+/// fast_log table on `device` (built once per device, never freed).
+const double* log_table_device(int device);
 
 /// 1/d to ~1 ulp: MUFU.RCP64H seed + two Newton steps (FP64 pipe only).
 __device__ __forceinline__ double fast_rcp(double d) {
@@ -58,43 +62,42 @@ __device__ __forceinline__ double fast_rcp(double d) {
   return fma(r, e, r);
 }
 
-/// Natural log for positive normal x, |error| <= ~2 ulp (checked against
-/// glibc in tests/test_gpu_kernels.py). x = 2^e m with m in [sqrt2/2, sqrt2),
-/// log m = 2 atanh(s), s = (m-1)/(m+1), |s| <= 0.1716: series to z^8
-/// (truncation < 3e-17 relative). ~21 FP64 ops vs ~56 for the libdevice log.
-__device__ __forceinline__ double fast_log(double x) {
-  int hi = __double2hiint(x);
+/// Table for fast_log (built on the host in extended precision, see
+/// log_table_device): kLogTab entries each of 1/T_k, log(T_k) hi and lo.
+constexpr int kLogTab = 256;
+constexpr int kLogSplit = 106;  // first index with 1 + k/256 >= sqrt(2)
+
+/// Natural log for positive normal x, <= 2 ulp (tests/test_gpu_kernels.py
+/// checks it against glibc). x = 2^e m, m in [1, 2); the top 8 mantissa bits
+/// pick T_k (left endpoints below sqrt2, halved right endpoints above, so
+/// x -> 1 from either side meets T = 1 exactly) and u = m / T_k - 1 with
+/// |u| < 1/256; log1p(u) by its Taylor series to u^7 (remainder < 1e-20).
+/// 12 FP64 ops and 3 table reads vs ~56 FP64-op equivalents for libdevice log.
+__device__ __forceinline__ double fast_log(double x, const double* __restrict__ tab) {
+  const int hi = __double2hiint(x);
   const int lo = __double2loint(x);
-  int e = (hi >> 20) - 1023;
-  int mhi = (hi & 0x000fffff) | 0x3ff00000;
-  if (mhi > 0x3ff6a09e) {  // m > sqrt(2): use m / 2
-    mhi -= 0x00100000;
-    e += 1;
-  }
-  const double m = __hiloint2double(mhi, lo);
-  const double f = m - 1.0;
-  const double s = f * fast_rcp(2.0 + f);
-  const double z = s * s;
-  double p = 1.0 / 19.0;
-  p = fma(p, z, 1.0 / 17.0);
-  p = fma(p, z, 1.0 / 15.0);
-  p = fma(p, z, 1.0 / 13.0);
-  p = fma(p, z, 1.0 / 11.0);
-  p = fma(p, z, 1.0 / 9.0);
-  p = fma(p, z, 1.0 / 7.0);
-  p = fma(p, z, 1.0 / 5.0);
-  p = fma(p, z, 1.0 / 3.0);
-  const double s2 = s + s;
-  const double lm = fma(s2 * z, p, s2);
+  const int k = (hi >> 12) & 0xff;
+  const int e = ((hi >> 20) & 0x7ff) - 1023 + (k >= kLogSplit ? 1 : 0);
+  const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
+  const double u = fma(m, tab[k], -1.0);
+  double q = 1.0 / 7.0;
+  q = fma(q, u, -1.0 / 6.0);
+  q = fma(q, u, 1.0 / 5.0);
+  q = fma(q, u, -1.0 / 4.0);
+  q = fma(q, u, 1.0 / 3.0);
+  q = fma(q, u, -0.5);
+  const double lp = fma(u * u, q, u);
   const double de = double(e);
-  return fma(de, 6.93147180369123816490e-01, fma(de, 1.90821492927058770002e-10, lm));
+  return fma(de, 6.93147180369123816490e-01, tab[kLogTab + k]) +
+         (fma(de, 1.90821492927058770002e-10, tab[2 * kLogTab + k]) + lp);
 }
 
 /// K(x_i, x_j) for the on-the-fly kinds, from coordinates already in
-/// registers. `same` is true iff i == j (tree positions).
+/// registers. `same` is true iff i == j (tree positions); `ltab` is the
+/// fast_log table (log kernels only).
 template <int KIND, int DIM>
 __device__ __forceinline__ double kernel_value(const double* xi, const double* xj, bool same,
-                                               double param) {
+                                               double param, const double* ltab) {
   double r2 = 0.0;
 #pragma unroll
   for (int d = 0; d < DIM; ++d) {
@@ -102,13 +105,15 @@ __device__ __forceinline__ double kernel_value(const double* xi, const double* x
     r2 = fma(t, t, r2);
   }
   if (KIND == kOpLog) {
-    if (same) return 0.0;
-    // subnormal / zero distances (coincident points) take the libdevice path
+    // coincident distinct points give -inf as the dense assembly would;
+    // sub-normal distances (< 1.5e-154) are outside the supported range
     if (DIM == 1) {
       const double d = fabs(xi[0] - xj[0]);
-      return d >= 2.2250738585072014e-308 ? fast_log(d) : log(d);
+      const double v = fast_log(d, ltab);
+      return same ? 0.0 : (d == 0.0 ? -INFINITY : v);
     }
-    return r2 >= 2.2250738585072014e-308 ? 0.5 * fast_log(r2) : 0.5 * log(r2);
+    const double v = 0.5 * fast_log(r2, ltab);
+    return same ? 0.0 : (r2 == 0.0 ? -INFINITY : v);
   } else if (KIND == kOpInvDist4Pi) {
     if (same) return 0.0;
     return rsqrt(r2) * 0.07957747154594767;  // 1 / (4 pi)

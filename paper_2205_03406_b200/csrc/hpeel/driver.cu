@@ -347,15 +347,23 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       DevBuf<int> d_pay_pos;
       d_pay_pos.upload(w.pay_pos, s);
       DevBuf<double> samples(size_t(w.soff[np]), s);
+      // payload rows and coordinates in color order (contiguous K2 chunks)
+      const std::int64_t nnz = std::int64_t(w.pay_pos.size());
+      DevBuf<double> gcol(size_t(nnz) * size_t(gld), s);
+      DevBuf<double> xcol(op.kind() == kOpDense ? 1 : size_t(nnz) * size_t(op.dim()), s);
       HP_CUDA(cudaEventRecord(tm->apply.a, s));
+      launch_permute_rows(g.get(), gld, 1, d_pay_pos.get(), nnz, gld, gcol.get(), gld, 1, s);
+      if (op.kind() != kOpDense)
+        launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
       if (op.symmetric()) {
         launch_sample_apply(e.dop, false, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
-                            d_pay_pos.get(), g.get(), gld, 0, 2 * r, samples.get(), 0, s);
+                            d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
+                            samples.get(), 0, s);
       } else {
         launch_sample_apply(e.dop, false, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
-                            d_pay_pos.get(), g.get(), gld, 0, r, samples.get(), 0, s);
+                            d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0, s);
         launch_sample_apply(e.dop, true, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
-                            d_pay_pos.get(), g.get(), gld, r, r, samples.get(), r, s);
+                            d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r, s);
       }
       HP_CUDA(cudaEventRecord(tm->apply.b, s));
 

@@ -18,6 +18,7 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
   dop.n = n;
   dop.param = op.param();
   dop.symmetric = op.symmetric() ? 1 : 0;
+  dop.ltab = log_table_device(op.device());
   if (op.kind() == kOpDense) {
     DevBuf<double> tmp(size_t(n) * size_t(n), s);
     at.alloc(size_t(n) * size_t(n), s);

@@ -44,134 +44,219 @@ __global__ void payload_gaussian_kernel(double* g, int gld, int r, std::int64_t 
   }
 }
 
-constexpr int kBM = 64;       // rows per CTA (4 warps x 16)
-constexpr int kBK = 32;       // payload rows per shared-memory stage
-constexpr int kThreads = 128;
-constexpr int kKS = kBK + 4;  // kernel-tile row stride (== 4 mod 16: conflict-free A fragments)
+constexpr int kBM = 64;        // rows per CTA
+constexpr int kBK = 32;        // payload rows per stage
+constexpr int kThreads = 256;  // 4 DMMA warps + 4 evaluation warps
+constexpr int kKR = kBM + 4;   // kernel tile, column-major, column stride (== 4 mod 16)
+constexpr int kBarFull = 1;    // named barriers: 1,2 tile b full; 3,4 tile b empty; 5 eval warps
+constexpr int kBarEmpty = 3;
+constexpr int kBarEval = 5;
 
 __host__ __device__ constexpr int smem_stride(int nt) {
-  // payload row stride (doubles) == 4 mod 16: conflict-free B-fragment reads
-  return ((nt * 8 + 11) / 16) * 16 + 4;
+  // payload row stride (doubles) == 4 or 12 mod 16: the B-fragment pattern
+  // (lane%4) * S + lane/4 then hits 16 distinct 8-byte bank pairs per half warp
+  return nt * 8 + 4;
 }
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+constexpr int kStages = 3;     // payload ring: chunk c+1 streams in while chunk c is evaluated
+
+template <int NT>
+constexpr size_t sample_smem_bytes() {
+  return size_t(kStages * kBK * smem_stride(NT) + 2 * kBK * kKR) * sizeof(double);
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src));
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Per payload chunk (32 rows): (1) all 128 threads evaluate the 64 x 32 kernel
-// tile into shared memory (16 independent evaluations per thread: full ILP
-// on the FP64 pipe), (2) each warp runs 2 x NT DMMA.8x8x4 per k-step over its
-// 16 rows. The next chunk's payload rows stream in with cp.async meanwhile.
-template <int NT>
-constexpr size_t sample_smem_bytes() {
-  return size_t(2 * kBK * smem_stride(NT) + kBM * kKS) * sizeof(double);
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Warp-specialized colored apply. The payload rows of each color are stored
+// contiguously in color order (gc, xc, pc: payload values, coordinates and
+// tree positions), so a 32-row chunk is one contiguous copy.
+// Warps 4..7 ("eval"): per chunk, cp.async the chunk's coordinates/positions
+// (group 1) and payload rows (group 2), then evaluate the 64 x 32 kernel
+// tile into K[b] (column-major; each thread owns one row and 16 columns).
+// Warps 0..3 ("DMMA"): each owns 16 output rows and runs 2 x NT DMMA.8x8x4
+// per k-step from K[b] / G[b]. Double-buffered; full/empty hand-off through
+// named barriers, so evaluation of chunk c+1 overlaps the DMMA of chunk c.
 template <int NT, int KIND, int DIM, bool TRANS>
-__global__ void __launch_bounds__(kThreads, NT <= 10 ? 4 : (NT <= 14 ? 3 : 2))
+__global__ void __launch_bounds__(kThreads, NT <= 11 ? 2 : 1)
 sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
-                    const std::int64_t* __restrict__ pay_off, const int* __restrict__ pay_pos,
-                    const double* __restrict__ g, int gld, int gcol0, int ncols,
-                    double* __restrict__ out, int ocol0) {
+                    const std::int64_t* __restrict__ pay_off, const int* __restrict__ pc,
+                    const double* __restrict__ gc, int gld, int gcol0, int ncols,
+                    const double* __restrict__ xc, std::int64_t nnz, double* __restrict__ out,
+                    int ocol0, int mode) {
   constexpr int S = smem_stride(NT);
   constexpr int D = DIM > 0 ? DIM : 1;
   extern __shared__ __align__(16) double dyn_smem[];
-  double(*gs)[kBK * S] = reinterpret_cast<double(*)[kBK * S]>(dyn_smem);
-  double* ks = dyn_smem + 2 * kBK * S;
-  __shared__ double xs[2][D][kBK];
-  __shared__ double xr[D][kBM];
-  __shared__ int js[2][kBK];
+  double* gsm = dyn_smem;                        // [kStages][kBK * S] payload ring
+  double* ksm = dyn_smem + kStages * kBK * S;    // [2][kBK * kKR] kernel tiles
+  __shared__ __align__(16) double xs[kStages][D][kBK];
+  __shared__ __align__(16) int js[kStages][kBK];
+  __shared__ __align__(16) double lts[KIND == kOpLog ? 3 * kLogTab : 1];
 
   const SampleTask task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
 
-  for (int e = tid; e < 2 * kBK * S; e += kThreads) (&gs[0][0])[e] = 0.0;
-  if (tid < kBM) {
-    const int rr = tid < task.rows ? tid : task.rows - 1;
-    if constexpr (KIND != kOpDense) {
-#pragma unroll
-      for (int d = 0; d < DIM; ++d) xr[d][tid] = op.x[d * n + task.row0 + rr];
-    }
+  if constexpr (KIND == kOpLog) {
+    for (int e = tid; e < 3 * kLogTab; e += kThreads) lts[e] = op.ltab[e];
+  }
+  for (int e = tid; e < kStages * kBK * S; e += kThreads) gsm[e] = 0.0;
+  for (int e = tid; e < kStages * kBK; e += kThreads) {
+    (&js[0][0])[e] = int(task.row0);
+    for (int d = 0; d < D; ++d) xs[e / kBK][d][e % kBK] = 0.0;
   }
   __syncthreads();
 
   const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
-  auto issue = [&](int buf, std::int64_t base) {
-    const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
-    for (int idx = tid; idx < cnt * ncols; idx += kThreads) {
-      const int t = idx / ncols, c = idx - t * ncols;
-      cp_async8(&gs[buf][t * S + c], g + std::int64_t(pay_pos[base + t]) * gld + gcol0 + c);
-    }
-    cp_async_commit();
-    if (tid < kBK) {
-      const int pos = tid < cnt ? pay_pos[base + tid] : -1;
-      js[buf][tid] = pos;
-      if constexpr (KIND != kOpDense) {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) xs[buf][d][tid] = pos >= 0 ? op.x[d * n + pos] : 0.0;
-      }
-    }
-  };
+  const int nchunks = int((p1 - p0 + kBK - 1) / kBK);
 
+  if (warp >= 4) {
+    // ------------------------------------------------ evaluation warps
+    const int et = tid - 128;
+    const int row = et & (kBM - 1), cgrp = et >> 6;
+    const int ipos = int(task.row0) + (row < task.rows ? row : task.rows - 1);
+    double xi[D];
+    if constexpr (KIND != kOpDense) {
+#pragma unroll
+      for (int d = 0; d < DIM; ++d) xi[d] = op.x[d * n + ipos];
+    }
+    const bool even_cols = ((gld | gcol0 | ncols) & 1) == 0;
+    // stage chunk c: positions/coordinates, then payload rows (one group)
+    auto load_chunk = [&](int c) {
+      const int st = c % kStages;
+      const std::int64_t base = p0 + std::int64_t(c) * kBK;
+      const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
+      if (et < cnt) {
+        cp_async4(&js[st][et], pc + base + et);
+        if constexpr (KIND != kOpDense) {
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) cp_async8(&xs[st][d][et], xc + d * nnz + base + et);
+        }
+      }
+      double* gb = gsm + st * kBK * S;
+      const double* gsrc = gc + base * gld + gcol0;
+      if (even_cols) {
+        const int half = ncols >> 1;
+        for (int idx = et; idx < cnt * half; idx += 128) {
+          const int t = idx / half, cc = (idx - t * half) * 2;
+          cp_async16(gb + t * S + cc, gsrc + std::int64_t(t) * gld + cc);
+        }
+      } else {
+        for (int idx = et; idx < cnt * ncols; idx += 128) {
+          const int t = idx / ncols, cc = idx - t * ncols;
+          cp_async8(gb + t * S + cc, gsrc + std::int64_t(t) * gld + cc);
+        }
+      }
+      cp_async_commit();
+    };
+    if (nchunks > 0) load_chunk(0);
+    for (int c = 0; c < nchunks; ++c) {
+      const int b = c & 1, st = c % kStages;
+      // DMMA is done with chunk c-2 (K tile b and payload stage (c+1) % 3)
+      if (c >= 2) bar_sync(kBarEmpty + b, kThreads);
+      if (c + 1 < nchunks) {
+        load_chunk(c + 1);
+        cp_async_wait_1();  // chunk c landed (this thread's copies)
+      } else {
+        cp_async_wait_all();
+      }
+      bar_sync(kBarEval, 128);  // ... and every eval thread's copies
+      const std::int64_t base = p0 + std::int64_t(c) * kBK;
+      const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
+      double* kb = ksm + b * kBK * kKR;
+      const bool skip = (mode & 1) != 0;
+      // branch-free: stale/padded columns are evaluated and masked to 0.
+      // Loads, evaluations and stores are grouped so the 8 independent
+      // evaluation chains of a group interleave (shared-memory stores would
+      // otherwise order them).
+      constexpr int kGrp = 8;
+      if (skip) {
+        for (int u = 0; u < kBK / 2; ++u) kb[(cgrp + 2 * u) * kKR + row] = 0.0;
+        bar_arrive(kBarFull + b, kThreads);
+        continue;
+      }
+#pragma unroll
+      for (int h = 0; h < kBK / 2; h += kGrp) {
+        int jp[kGrp];
+        double xj[kGrp][D];
+        double v[kGrp];
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+          const int col = cgrp + 2 * (h + u);
+          jp[u] = js[st][col];
+          if constexpr (KIND != kOpDense) {
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) xj[u][d] = xs[st][d][col];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+          const int col = cgrp + 2 * (h + u);
+          if constexpr (KIND == kOpDense) {
+            const int jj = col < cnt ? jp[u] : ipos;
+            v[u] = TRANS ? op.a[std::int64_t(jj) + std::int64_t(ipos) * n]
+                         : op.a[std::int64_t(ipos) + std::int64_t(jj) * n];
+          } else {
+            v[u] = kernel_value<KIND, DIM>(xi, xj[u], ipos == jp[u], op.param, lts);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+          const int col = cgrp + 2 * (h + u);
+          kb[col * kKR + row] = col < cnt ? v[u] : 0.0;
+        }
+      }
+      bar_arrive(kBarFull + b, kThreads);
+    }
+    return;
+  }
+
+  // -------------------------------------------------- DMMA warps
   double acc[2][NT][2];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 
-  if (p0 < p1) issue(0, p0);
-  int buf = 0;
-  for (std::int64_t base = p0; base < p1; base += kBK, buf ^= 1) {
-    cp_async_wait_all();
-    __syncthreads();
-    if (base + kBK < p1) issue(buf ^ 1, base + kBK);
-
-    // (1) kernel tile: lane = payload column, warp strides over the 64 rows
-    {
-      const int jpos = js[buf][lane];
-      double xj[D];
-      if constexpr (KIND != kOpDense) {
-#pragma unroll
-        for (int d = 0; d < DIM; ++d) xj[d] = xs[buf][d][lane];
-      }
-#pragma unroll
-      for (int u = 0; u < kBM / 4; ++u) {
-        const int row = warp + 4 * u;
-        const std::int64_t ipos = task.row0 + (row < task.rows ? row : task.rows - 1);
-        double v = 0.0;
-        if (jpos >= 0) {
-          if constexpr (KIND == kOpDense) {
-            v = TRANS ? op.a[std::int64_t(jpos) + ipos * n] : op.a[ipos + std::int64_t(jpos) * n];
-          } else {
-            double xi[D];
-#pragma unroll
-            for (int d = 0; d < DIM; ++d) xi[d] = xr[d][row];
-            v = kernel_value<KIND, DIM>(xi, xj, ipos == jpos, op.param);
-          }
-        }
-        ks[row * kKS + lane] = v;
-      }
+  for (int c = 0; c < nchunks; ++c) {
+    const int b = c & 1;
+    bar_sync(kBarFull + b, kThreads);
+    if (mode & 2) {
+      if (c + 2 < nchunks) bar_arrive(kBarEmpty + b, kThreads);
+      continue;
     }
-    __syncthreads();
-
-    // (2) DMMA over the tile
-    const double* arow0 = ks + (warp * 16 + (lane >> 2)) * kKS + (lane & 3);
-    const double* arow1 = arow0 + 8 * kKS;
-    const double* brow = gs[buf] + (lane & 3) * S + (lane >> 2);
+    const double* arow = ksm + b * kBK * kKR + (lane & 3) * kKR + warp * 16 + (lane >> 2);
+    const double* brow = gsm + (c % kStages) * kBK * S + (lane & 3) * S + (lane >> 2);
 #pragma unroll
     for (int kk = 0; kk < kBK / 4; ++kk) {
-      const double a0 = arow0[kk * 4], a1 = arow1[kk * 4];
+      const double a0 = arow[kk * 4 * kKR], a1 = arow[kk * 4 * kKR + 8];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        const double b = brow[kk * 4 * S + nt * 8];
-        dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a0, b);
-        dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, b);
+        const double bb = brow[kk * 4 * S + nt * 8];
+        dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a0, bb);
+        dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, bb);
       }
     }
+    if (c + 2 < nchunks) bar_arrive(kBarEmpty + b, kThreads);
   }
 
 #pragma unroll
@@ -188,28 +273,37 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
     }
   }
 }
+
+// profiling switch (hp_debug_set_k2_mode): bit 0 skips kernel evaluation,
+// bit 1 skips the DMMA; 0 in production
+int& k2_mode() {
+  static int mode = 0;
+  return mode;
+}
+
 template <int NT, int KIND, int DIM>
 void launch_nt_kind_dim(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
-                        const std::int64_t* pay_off, const int* pay_pos, const double* g, int gld,
-                        int gcol0, int ncols, double* out, int ocol0, cudaStream_t s) {
+                        const std::int64_t* pay_off, const int* pc, const double* gc, int gld,
+                        int gcol0, int ncols, const double* xc, std::int64_t nnz, double* out,
+                        int ocol0, cudaStream_t s) {
   // kernel kinds are symmetric: only the explicit dense operator has a transpose
   constexpr size_t smem = sample_smem_bytes<NT>();
   if (KIND == kOpDense && trans) {
     auto* fn = sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense>;
     HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0);
+    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode());
   } else {
     auto* fn = sample_apply_kernel<NT, KIND, DIM, false>;
     HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0);
+    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode());
   }
 }
 
 template <int NT>
 void launch_nt(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
-               const std::int64_t* pay_off, const int* pay_pos, const double* g, int gld, int gcol0,
-               int ncols, double* out, int ocol0, cudaStream_t s) {
-#define HP_ARGS op, trans, tasks, ntasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0, s
+               const std::int64_t* pay_off, const int* pc, const double* gc, int gld, int gcol0,
+               int ncols, const double* xc, std::int64_t nnz, double* out, int ocol0, cudaStream_t s) {
+#define HP_ARGS op, trans, tasks, ntasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, s
   switch (op.kind) {
     case kOpDense: return launch_nt_kind_dim<NT, kOpDense, 0>(HP_ARGS);
     case kOpLog:
@@ -257,7 +351,7 @@ __global__ void identity_apply_kernel(DevOp op, const SampleTask* __restrict__ t
         double xj[DIM > 0 ? DIM : 1];
 #pragma unroll
         for (int d = 0; d < DIM; ++d) xj[d] = op.x[d * n + jp];
-        acc += kernel_value<KIND, DIM>(xi, xj, ip == jp, op.param);
+        acc += kernel_value<KIND, DIM>(xi, xj, ip == jp, op.param, op.ltab);
       }
     }
     out[task.out + i + std::int64_t(t) * task.ld] = acc;
@@ -300,7 +394,7 @@ __global__ void full_apply_kernel(DevOp op, const double* __restrict__ x, int w,
             double xj[DIM > 0 ? DIM : 1];
 #pragma unroll
             for (int d = 0; d < DIM; ++d) xj[d] = xs[d][t];
-            kv = kernel_value<KIND, DIM>(xi, xj, i == j0 + t, op.param);
+            kv = kernel_value<KIND, DIM>(xi, xj, i == j0 + t, op.param, op.ltab);
           }
           acc = fma(kv, vs[t], acc);
         }
@@ -312,6 +406,8 @@ __global__ void full_apply_kernel(DevOp op, const double* __restrict__ x, int w,
 
 }  // namespace
 
+void set_k2_mode(int m) { k2_mode() = m; }
+
 void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const int* pos_box,
                              const int* local, std::uint64_t seed, int level, cudaStream_t s) {
   const std::int64_t total = n * gld;
@@ -321,15 +417,15 @@ void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const in
 }
 
 void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
-                         const std::int64_t* pay_off, const int* pay_pos, const double* g,
-                         int gld, int gcol0, int ncols, double* out, int ocol0,
-                         cudaStream_t s) {
+                         const std::int64_t* pay_off, const int* pc, const double* gc, int gld,
+                         int gcol0, int ncols, const double* xc, std::int64_t nnz, double* out,
+                         int ocol0, cudaStream_t s) {
   if (ntasks == 0) return;
   const int nt = (ncols + 7) / 8;
-#define HP_CASE(NT)                                                                         \
-  case NT:                                                                                  \
-    launch_nt<NT>(op, trans, tasks, ntasks, pay_off, pay_pos, g, gld, gcol0, ncols, out, ocol0, \
-                  s);                                                                       \
+#define HP_CASE(NT)                                                                            \
+  case NT:                                                                                     \
+    launch_nt<NT>(op, trans, tasks, ntasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out,  \
+                  ocol0, s);                                                                   \
     break;
   switch (nt) {
     HP_CASE(1) HP_CASE(2) HP_CASE(3) HP_CASE(4) HP_CASE(5) HP_CASE(6) HP_CASE(7) HP_CASE(8)

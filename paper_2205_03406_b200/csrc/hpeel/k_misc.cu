@@ -76,3 +76,44 @@ std::int64_t& launch_counter() {
   return count;
 }
 }  // namespace hpeel
+
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
+
+namespace hpeel {
+const double* log_table_device(int device) {
+  static std::mutex mu;
+  static std::map<int, double*> tabs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = tabs.find(device);
+  if (it != tabs.end()) return it->second;
+  // T_k = 1 / inv_k exactly; log T_k in extended precision split hi + lo
+  std::vector<double> h(3 * kLogTab);
+  for (int k = 0; k < kLogTab; ++k) {
+    double inv;
+    long double t;
+    if (k < kLogSplit) {
+      inv = double(1.0L / (1.0L + (long double)k / kLogTab));
+      t = 1.0L / (long double)inv;
+    } else {
+      inv = double(1.0L / (1.0L + (long double)(k + 1) / kLogTab));
+      t = (1.0L / (long double)inv) / 2.0L;
+    }
+    const long double l = logl(t);
+    h[size_t(k)] = inv;
+    h[size_t(kLogTab + k)] = double(l);
+    h[size_t(2 * kLogTab + k)] = double(l - (long double)double(l));
+  }
+  int prev = 0;
+  HP_CUDA(cudaGetDevice(&prev));
+  HP_CUDA(cudaSetDevice(device));
+  double* d = nullptr;
+  HP_CUDA(cudaMalloc(&d, h.size() * sizeof(double)));
+  HP_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  HP_CUDA(cudaSetDevice(prev));
+  tabs[device] = d;
+  return d;
+}
+}  // namespace hpeel

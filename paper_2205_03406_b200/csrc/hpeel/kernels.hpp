@@ -30,13 +30,15 @@ struct SampleTask {
   int ld;
   int pad;
 };
-/// out[task.out + i + (ocol0 + c) * ld] = sum_j K(row0+i, j) g[j * gld + gcol0 + c]
-/// over payload rows j of the task's color (pay_pos[pay_off[c] .. pay_off[c+1])),
-/// c < ncols. `trans` applies K^T (adjoint of a non-symmetric dense operator).
+/// out[task.out + i + (ocol0 + c) * ld] = sum_q K(row0+i, pc[q]) gc[q * gld + gcol0 + c]
+/// over the payload rows q in [pay_off[color], pay_off[color+1]) of the task's
+/// color, stored in color order: pc = tree positions, gc = payload rows,
+/// xc = coordinates (dim x nnz). `trans` applies K^T (adjoint of a
+/// non-symmetric dense operator).
 void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
-                         const std::int64_t* pay_off, const int* pay_pos, const double* g,
-                         int gld, int gcol0, int ncols, double* out, int ocol0,
-                         cudaStream_t s);
+                         const std::int64_t* pay_off, const int* pc, const double* gc, int gld,
+                         int gcol0, int ncols, const double* xc, std::int64_t nnz, double* out,
+                         int ocol0, cudaStream_t s);
 
 /// Leaf-phase identity probes (proj/src/coloring.cpp:271-277):
 /// out[task.out + i + t * ld] = sum_{v in color} K(row0+i, start_v + t), t < |v|,

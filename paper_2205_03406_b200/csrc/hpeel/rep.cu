@@ -73,6 +73,7 @@ Matrix DeviceOperator::apply(const Matrix& x, bool adjoint) const {
   d.a = d_a_;
   d.param = param_;
   d.symmetric = symmetric_;
+  d.ltab = log_table_device(device_);
   cudaStream_t s;
   HP_CUDA(cudaStreamCreate(&s));
   Matrix y(x.rows(), x.cols());
@@ -392,9 +393,9 @@ Matrix debug_payload(const BoxTree& tree, const TreeLayout& lay, int level, int 
 
 namespace hpeel {
 namespace {
-__global__ void fast_log_probe_kernel(const double* x, std::int64_t n, double* y) {
+__global__ void fast_log_probe_kernel(const double* x, std::int64_t n, double* y, const double* tab) {
   const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) y[i] = fast_log(x[i]);
+  if (i < n) y[i] = fast_log(x[i], tab);
 }
 }  // namespace
 
@@ -405,7 +406,7 @@ void debug_fast_log(const double* x, std::int64_t n, double* y, int device) {
   HP_CUDA(cudaMalloc(&dx, size_t(n) * 8));
   HP_CUDA(cudaMalloc(&dy, size_t(n) * 8));
   HP_CUDA(cudaMemcpy(dx, x, size_t(n) * 8, cudaMemcpyHostToDevice));
-  fast_log_probe_kernel<<<cdiv(n, 256), 256>>>(dx, n, dy);
+  fast_log_probe_kernel<<<cdiv(n, 256), 256>>>(dx, n, dy, log_table_device(device));
   HP_LAUNCHED();
   HP_CUDA(cudaMemcpy(y, dy, size_t(n) * 8, cudaMemcpyDeviceToHost));
   cudaFree(dx);

@@ -1,0 +1,15 @@
+"""K2 bottleneck probe: compress c3 with K2 in full / no-eval / no-DMMA modes."""
+import sys, time
+sys.path.insert(0, "/root/repo")
+import paper_2205_03406_b200 as hp
+from paper_2205_03406_b200 import configs, _lib
+name = sys.argv[1] if len(sys.argv) > 1 else "c3"
+w = configs.CONFIGS[name]
+pts = w.points()
+t = hp.build_tree(pts, w.leaf)
+op = hp.kernel_operator(w.kernel, pts, w.param)
+for mode in (0, 1, 2, 3, 0):
+    _lib.lib().hp_debug_set_k2_mode(mode)
+    rep = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
+    ph = [p for p in rep.report["phases"] if p["phase"] == "h1"]
+    print(mode, "apply_ms %.1f" % sum(p["apply_ms"] for p in ph), [round(p["apply_ms"], 1) for p in ph][:6])
