@@ -384,6 +384,29 @@ def build_graph(sets):
     """proj/src/coloring.cpp:154-167, the literal pairwise scan (vectorized
     over j through Python sets; same edge set)."""
     n = len(sets)
+    if 0 < n <= 6000:
+        # the same pairwise predicate, evaluated for all (i, j) at once with
+        # incidence matrices: payload-hits-zero either way, or one box with
+        # two different payload tags
+        nb = 1 + max(max([b for s in sets for b, _ in s.payload] + [0]),
+                     max([z for s in sets for z in s.zero] + [0]))
+        P = np.zeros((n, nb), dtype=np.float32)
+        Z = np.zeros((n, nb), dtype=np.float32)
+        T = [np.zeros((n, nb), dtype=np.float32) for _ in range(3)]
+        for i, s in enumerate(sets):
+            for b, t in s.payload:
+                P[i, b] = 1.0
+                T[t][i, b] = 1.0
+            for z in s.zero:
+                Z[i, z] = 1.0
+        hit = (P @ Z.T) > 0
+        inc = hit | hit.T
+        for a in range(3):
+            for b in range(3):
+                if a != b:
+                    inc |= (T[a] @ T[b].T) > 0
+        np.fill_diagonal(inc, False)
+        return [list(np.nonzero(inc[i])[0].astype(int)) for i in range(n)]
     zeros = [set(s.zero) for s in sets]
     pays = [dict(s.payload) for s in sets]
     edges = [[] for _ in range(n)]
@@ -415,6 +438,33 @@ def dsatur_color(edges):
     color = [-1] * n
     if n == 0:
         return color, 0
+    if n <= 20000:
+        # same rule by direct arg-max over the uncolored vertices: key
+        # (saturation, uncolored degree, -v), ties impossible
+        col = np.full(n, -1, dtype=np.int64)
+        seen = np.zeros((n, 64), dtype=bool)
+        sat = np.zeros(n, dtype=np.int64)
+        udeg = np.array([len(e) for e in edges], dtype=np.int64)
+        adj = [np.asarray(e, dtype=np.int64) for e in edges]
+        ncol = 0
+        bits = np.int64(1) << 20  # > n and > any degree: lexicographic key
+        order = bits - 1 - np.arange(n, dtype=np.int64)
+        for _ in range(n):
+            key = np.where(col < 0, (sat * bits + udeg) * bits + order, -1)
+            v = int(np.argmax(key))
+            used = seen[v]
+            c = int(np.argmin(used)) if not used.all() else used.size
+            if c >= seen.shape[1]:
+                seen = np.concatenate([seen, np.zeros((n, seen.shape[1]), dtype=bool)], axis=1)
+            col[v] = c
+            ncol = max(ncol, c + 1)
+            nb = adj[v]
+            nb = nb[col[nb] < 0]
+            udeg[nb] -= 1
+            fresh = nb[~seen[nb, c]]
+            seen[fresh, c] = True
+            sat[fresh] += 1
+        return [int(x) for x in col], ncol
     seen = [set() for _ in range(n)]
     udeg = [len(e) for e in edges]
     stamp = [0] * n

@@ -1,0 +1,155 @@
+"""Bit-exact parity of the product's host planning layer (C++ behind the C
+ABI) with the oracle: trees, adjacency, admissible/dense pairs, constraint
+sets, incompatibility graphs, DSatur/tile colorings and per-color payload
+lists. Runs without a GPU."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2205_03406_b200 import configs
+
+
+def geometries():
+    yield "worked-1d", O.equispaced_1d(512), 64
+    yield "figure", O.equispaced_1d(400), 100
+    yield "random-2d", O.random_cloud(700, 2, 31), 48
+    yield "random-2d-b", O.random_cloud(1000, 2, 99), 50
+    yield "lopsided", np.concatenate([0.001 * np.arange(150) / 150.0, np.arange(150) / 150.0])[:, None], 32
+    yield "grid-2d", O.uniform_grid_points(16, 2), 1
+    yield "grid-3d", O.uniform_grid_points(8, 3), 1
+    yield "c1", configs.make_points("c1", 4096), 64
+    yield "c2-scaled", configs.make_points("c2", 8192), 64
+    yield "c3-scaled", configs.make_points("c3", 8192), 128
+    yield "c4-scaled", configs.make_points("c4", 16384), 256
+    yield "c5-scaled", configs.make_points("c5", 8192), 256
+
+
+GEOMS = list(geometries())
+
+
+@pytest.mark.parametrize("name,pts,leaf", GEOMS, ids=[g[0] for g in GEOMS])
+def test_tree_and_adjacency_bit_exact(hp, name, pts, leaf):
+    t = hp.build_tree(pts, leaf)
+    ot = O.BoxTree(O.PointCloud(pts), leaf)
+    oadj = O.adjacency(ot)
+    assert (t.depth, t.num_boxes, t.num_points) == (ot.depth, ot.num_boxes, ot.num_points)
+    assert t.fully_populated == ot.is_fully_populated()
+    assert t.max_leaf_size == ot.max_leaf_size()
+    for b in ot.boxes:
+        assert t.box_level(b.id) == b.level
+        assert t.box_parent(b.id) == b.parent
+        assert tuple(t.box_coord(b.id)) == b.coord
+        assert t.box_points(b.id) == [int(p) for p in b.points]
+        assert t.children(b.id) == b.children
+        assert t.neighbors(b.id) == oadj.neighbors[b.id]
+        assert t.interaction(b.id) == oadj.interaction[b.id]
+        assert t.coarse_leaf_neighbors(b.id) == oadj.coarse_leaf_neighbors[b.id]
+        assert t.dense_partners(b.id) == oadj.dense_partners[b.id]
+    assert t.cross_level_adjacencies == oadj.cross_level_adjacencies
+    for l in range(2, ot.depth + 1):
+        assert t.admissible_pairs(l) == O.admissible_pairs(ot, oadj, l)
+    assert t.dense_pairs() == O.dense_pairs(ot, oadj)
+
+
+def _compare_plan(hp, t, ot, oadj, level, mode, omode):
+    p = hp.plan(t, level, mode, 12, 7, 0)
+    sets = O.build_constraints(ot, oadj, level, omode)
+    assert p.n_vertices == len(sets)
+    for got, want in zip(p.sets, sets):
+        assert tuple(tuple(x) for x in got["payload"]) == want.payload
+        assert tuple(got["zero"]) == want.zero
+        assert [tuple(o) for o in got["owners"]] == want.owners
+    if len(sets) <= 2500:  # literal O(V^2) oracle scan
+        edges = O.build_graph(sets)
+        assert p.edges == edges
+        col, n = O.plan_coloring(ot, sets, edges, omode)
+        assert p.color == col and p.n_colors == n
+        dcol, dn = O.dsatur_color(edges)
+        assert p.dsatur_color == dcol and p.dsatur_colors == dn
+        mats = O.assemble_test_matrices(sets, col, n, ot, level, 12, 7, 0)
+        assert p.color_payload == [[b for b, _ in m.payload] for m in mats]
+    return p
+
+
+@pytest.mark.parametrize("name,pts,leaf", GEOMS, ids=[g[0] for g in GEOMS])
+def test_h1_and_leaf_plans_bit_exact(hp, name, pts, leaf):
+    t = hp.build_tree(pts, leaf)
+    ot = O.BoxTree(O.PointCloud(pts), leaf)
+    oadj = O.adjacency(ot)
+    for l in range(2, ot.depth + 1):
+        _compare_plan(hp, t, ot, oadj, l, "h1", O.H1)
+    _compare_plan(hp, t, ot, oadj, ot.depth, "leaf", O.LEAF)
+
+
+def test_inverted_index_graph_equals_pairwise_scan(hp):
+    """build_graph's inverted index gives the literal scan's edge set
+    (proj/src/coloring.cpp:154-167) on every level of an adaptive tree."""
+    pts = configs.make_points("c3", 16384)
+    t = hp.build_tree(pts, 128)
+    for l in range(2, t.depth + 1):
+        fast = hp.plan(t, l, "h1", 8, 1, 0)
+        slow = hp.plan(t, l, "h1", 8, 1, 0, pairwise=True)
+        assert fast.edges == slow.edges and fast.color == slow.color
+    fast = hp.plan(t, t.depth, "leaf", 8, 1, 0)
+    slow = hp.plan(t, t.depth, "leaf", 8, 1, 0, pairwise=True)
+    assert fast.edges == slow.edges and fast.color == slow.color
+
+
+def test_worked_example_known_answers(hp):
+    """proj/tests/test_coloring.cpp:151-182, proj/tests/python/test_smoke.py:14-26."""
+    t = hp.build_tree(hp.equispaced_1d(512), 64)
+    assert t.depth == 3 and t.num_points == 512
+    assert len(t.admissible_pairs(3)) == 18 and len(t.admissible_pairs(2)) == 6
+    h1 = hp.level_coloring(t, 3, "h1")
+    assert h1["n_vertices"] == 12 and h1["n_colors"] == 6
+    assert hp.level_coloring(t, 2, "h1")["n_colors"] == 4
+    assert hp.level_coloring(t, 3, "unif-stage1") == {"n_vertices": 8, "n_edges": 22, "n_colors": 5}
+    assert hp.level_coloring(t, 3, "leaf")["n_colors"] == 3
+
+
+def test_dsatur_known_answers(hp):
+    """proj/tests/test_coloring.cpp:91-126."""
+    cyc = [sorted([(i + 1) % 5, (i - 1) % 5]) for i in range(5)]
+    assert hp.dsatur(cyc)["num_colors"] == 3
+    k33 = [[3, 4, 5]] * 3 + [[0, 1, 2]] * 3
+    assert hp.dsatur(k33)["num_colors"] == 2
+    t = hp.build_tree(hp.equispaced_1d(4096), 32)
+    p = hp.plan(t, t.depth, "h1", 4, 0, 0)
+    v = p.n_vertices
+    deg = max(len(e) for e in p.edges)
+    assert p.queue_ops <= 4.0 * (deg + 1.0) * v * max(1.0, np.log2(v))
+
+
+def test_gaussian_stream_and_realize_bit_exact(hp):
+    """Host RNG equals the frozen stream (libm path, bit for bit), and
+    BlockTestMatrix::realize matches the oracle on every color."""
+    for rows, cols, seed in [(4, 3, 7), (17, 13, 2**62 + 3), (1, 1, 0)]:
+        assert np.array_equal(hp.gaussian_matrix(rows, cols, seed), O.gaussian_matrix_libm(rows, cols, seed))
+    assert np.array_equal(hp.random_cloud(9, 3, 11), O.random_cloud(9, 3, 11))
+    assert hp.mix_seed(7, 0xC1) == O.mix_seed(7, 0xC1)
+    t = hp.build_tree(hp.equispaced_1d(512), 64)
+    ot = O.BoxTree(O.PointCloud(O.equispaced_1d(512)), 64)
+    oadj = O.adjacency(ot)
+    for mode, omode, level in [("h1", O.H1, 3), ("leaf", O.LEAF, 3)]:
+        width = 12 if mode == "h1" else 64
+        p = hp.plan(t, level, mode, width, 77, 1)
+        sets = O.build_constraints(ot, oadj, level, omode)
+        col, n = O.plan_coloring(ot, sets, O.build_graph(sets), omode)
+        mats = O.assemble_test_matrices(sets, col, n, ot, level, width, 77, 1)
+        for c in range(n):
+            got = p.realize(c)
+            want = mats[c].realize(ot)
+            assert np.max(np.abs(got - want)) <= 4e-16 * max(1.0, np.max(np.abs(want)))
+
+
+def test_error_behaviour(hp):
+    """Exception mapping of the C ABI: invalid_argument -> ValueError,
+    runtime_error -> RuntimeError (proj/src/box_tree.cpp:130-133)."""
+    with pytest.raises(RuntimeError):
+        hp.build_tree(np.zeros((10, 1)), 2)
+    with pytest.raises(ValueError):
+        hp.build_tree(np.zeros((0, 1)), 2)
+    with pytest.raises(ValueError):
+        hp.build_tree(np.array([[0.0], [np.nan]]), 2)
+    with pytest.raises(ValueError):
+        hp.build_tree(hp.equispaced_1d(16), 0)
