@@ -2,8 +2,10 @@
 #include "coloring.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <queue>
 #include <stdexcept>
+#include <thread>
 #include <tuple>
 
 #include "rng.hpp"
@@ -167,24 +169,36 @@ IncompatibilityGraph build_graph(const std::vector<ConstraintSet>& sets) {
       }
     }
   }
-  for (size_t i = 0; i < sets.size(); ++i) {
+  // Neighbors of i, each list built independently (threads over vertices):
+  // sets that zero one of i's payload boxes, sets whose payload box i zeroes,
+  // and sets carrying one of i's payload boxes with another tag.
+  auto neighbors = [&](size_t i, std::vector<int>& e) {
     for (auto& [box, tag] : sets[i].payload) {
-      for (int k = zoff[size_t(box)]; k < zoff[size_t(box) + 1]; ++k) {
-        const int j = zsets[size_t(k)];
-        if (j == int(i)) continue;
-        g.edges[i].push_back(j);
-        g.edges[size_t(j)].push_back(int(i));
-      }
-      for (int k = poff[size_t(box)]; k < poff[size_t(box) + 1]; ++k) {
-        const int j = psets[size_t(k)];
-        if (j != int(i) && ptags[size_t(k)] != tag) g.edges[i].push_back(j);
-      }
+      for (int k = zoff[size_t(box)]; k < zoff[size_t(box) + 1]; ++k) e.push_back(zsets[size_t(k)]);
+      for (int k = poff[size_t(box)]; k < poff[size_t(box) + 1]; ++k)
+        if (ptags[size_t(k)] != tag) e.push_back(psets[size_t(k)]);
     }
-  }
-  for (auto& e : g.edges) {
+    for (int z : sets[i].zero)
+      for (int k = poff[size_t(z)]; k < poff[size_t(z) + 1]; ++k) e.push_back(psets[size_t(k)]);
     std::sort(e.begin(), e.end());
     e.erase(std::unique(e.begin(), e.end()), e.end());
-  }
+    auto self = std::lower_bound(e.begin(), e.end(), int(i));
+    if (self != e.end() && *self == int(i)) e.erase(self);
+  };
+  const size_t n = sets.size();
+  const unsigned nt = n < 4096 ? 1u : std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (;;) {
+      const size_t b = next.fetch_add(256);
+      if (b >= n) return;
+      for (size_t i = b; i < std::min(n, b + 256); ++i) neighbors(i, g.edges[i]);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
   return g;
 }
 
@@ -206,40 +220,67 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
   Coloring out;
   out.color.assign(size_t(n), -1);
   if (n == 0) return out;
-  std::vector<std::vector<int>> seen(static_cast<size_t>(n));  // sorted distinct neighbor colors
+  // Max-heap of (saturation, uncolored degree, -v) with lazy keys: a vertex's
+  // live entry always carries its current saturation and an uncolored degree
+  // >= the current one. A popped entry with an outdated saturation is dropped
+  // (a newer one exists), one with an outdated degree is re-pushed with the
+  // current key; a popped entry that is exactly current dominates every other
+  // vertex's true key, so the selection equals the reference's eager heap
+  // (proj/src/coloring.cpp:184-213) with far fewer queue operations.
+  // neighbor colors as a flat bitset (W words per vertex, grown on demand)
+  size_t words = 4;
+  std::vector<std::uint64_t> seen(size_t(n) * words, 0);
+  std::vector<int> sat(static_cast<size_t>(n), 0);
   std::vector<int> udeg(static_cast<size_t>(n));
-  std::vector<std::uint64_t> stamp(size_t(n), 0);
-  using Entry = std::tuple<int, int, int, std::uint64_t>;
-  std::priority_queue<Entry> heap;
+  using Entry = std::tuple<int, int, int>;
+  std::vector<Entry> init;
+  init.reserve(size_t(n));
   for (int v = 0; v < n; ++v) {
     udeg[size_t(v)] = int(graph.edges[size_t(v)].size());
-    heap.emplace(0, udeg[size_t(v)], -v, 0);
-    ++out.queue_ops;
+    init.emplace_back(0, udeg[size_t(v)], -v);
   }
+  std::priority_queue<Entry> heap(std::less<Entry>(), std::move(init));
+  out.queue_ops += size_t(n);
   int done = 0;
   while (done < n) {
-    auto [sat, ud, negv, st] = heap.top();
+    auto [s, ud, negv] = heap.top();
     heap.pop();
     ++out.queue_ops;
     const int v = -negv;
-    if (out.color[size_t(v)] != -1 || st != stamp[size_t(v)]) continue;
-    int c = 0;
-    for (int used : seen[size_t(v)]) {
-      if (used == c) ++c;
-      else if (used > c) break;
+    if (out.color[size_t(v)] != -1 || s != sat[size_t(v)]) continue;
+    if (ud != udeg[size_t(v)]) {
+      heap.emplace(s, udeg[size_t(v)], negv);
+      ++out.queue_ops;
+      continue;
+    }
+    // smallest color absent among the neighbors
+    const std::uint64_t* row = seen.data() + size_t(v) * words;
+    size_t wi = 0;
+    while (wi < words && row[wi] == ~std::uint64_t(0)) ++wi;
+    const int c = int(64 * wi) + (wi < words ? __builtin_ctzll(~row[wi]) : 0);
+    if (size_t(c) >= 64 * words) {
+      std::vector<std::uint64_t> grown(size_t(n) * words * 2, 0);
+      for (size_t u = 0; u < size_t(n); ++u)
+        std::copy(seen.begin() + std::ptrdiff_t(u * words), seen.begin() + std::ptrdiff_t((u + 1) * words),
+                  grown.begin() + std::ptrdiff_t(u * words * 2));
+      seen.swap(grown);
+      words *= 2;
     }
     out.color[size_t(v)] = c;
     out.num_colors = std::max(out.num_colors, c + 1);
     ++done;
+    const size_t cw = size_t(c) >> 6;
+    const std::uint64_t cb = std::uint64_t(1) << (c & 63);
     for (int w : graph.edges[size_t(v)]) {
       if (out.color[size_t(w)] != -1) continue;
       --udeg[size_t(w)];
-      auto& sw = seen[size_t(w)];
-      auto pos = std::lower_bound(sw.begin(), sw.end(), c);
-      if (pos == sw.end() || *pos != c) sw.insert(pos, c);
-      ++stamp[size_t(w)];
-      heap.emplace(int(sw.size()), udeg[size_t(w)], -w, stamp[size_t(w)]);
-      ++out.queue_ops;
+      std::uint64_t& word = seen[size_t(w) * words + cw];
+      if (!(word & cb)) {
+        word |= cb;
+        ++sat[size_t(w)];
+        heap.emplace(sat[size_t(w)], udeg[size_t(w)], -w);
+        ++out.queue_ops;
+      }
     }
   }
   return out;
