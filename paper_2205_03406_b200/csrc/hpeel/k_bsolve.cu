@@ -171,10 +171,157 @@ __device__ void pinv_weights(const double* c, int m, int n, double tol, double* 
   __syncthreads();
 }
 
+// Column-pivoted Householder QR of the first `ncand` columns of the m x ntot
+// shared matrix a (ld m); every reflector is also applied to the trailing
+// columns (right-hand sides), which end up holding Q^T rhs. perm[j] = original
+// column at pivot position j; the R diagonal stays on a's diagonal.
+__device__ void pivqr_augmented(double* a, int m, int ncand, int ntot, int* perm, double* nrm,
+                                double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = threadIdx.x; j < ncand; j += kSvdThreads) perm[j] = j;
+  __syncthreads();
+  const int kk = m < ncand ? m : ncand;
+  for (int j = 0; j < kk; ++j) {
+    for (int c = j + warp; c < ncand; c += kSvdWarps) {
+      const double* ac = a + c * m;
+      double s = 0.0;
+      for (int i = j + lane; i < m; i += 32) s = fma(ac[i], ac[i], s);
+      s = wsum(s);
+      if (lane == 0) nrm[c] = s;
+    }
+    __syncthreads();
+    int p = j;
+    double best = nrm[j];
+    for (int c = j + 1; c < ncand; ++c)
+      if (nrm[c] > best) { best = nrm[c]; p = c; }
+    if (p != j) {
+      for (int i = threadIdx.x; i < m; i += kSvdThreads) {
+        const double t = a[i + j * m];
+        a[i + j * m] = a[i + p * m];
+        a[i + p * m] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = perm[j];
+        perm[j] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    // reflector from column j (dlarfg), applied to columns j+1 .. ntot-1
+    double* col = a + j * m;
+    double part = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < m; i += kSvdThreads) part += col[i] * col[i];
+    part = wsum(part);
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    double sigma = 0.0;
+    for (int w = 0; w < kSvdWarps; ++w) sigma += red[w];
+    const double alpha = col[j];
+    double tau = 0.0;
+    if (sigma > 0.0) {
+      const double beta = alpha >= 0.0 ? -sqrt(alpha * alpha + sigma) : sqrt(alpha * alpha + sigma);
+      tau = (beta - alpha) / beta;
+      const double scale = 1.0 / (alpha - beta);
+      __syncthreads();
+      for (int i = j + 1 + threadIdx.x; i < m; i += kSvdThreads) col[i] *= scale;
+      if (threadIdx.x == 0) col[j] = beta;
+    }
+    __syncthreads();
+    if (tau != 0.0) {
+      for (int c = j + 1 + warp; c < ntot; c += kSvdWarps) {
+        double* ac = a + c * m;
+        double s = lane == 0 ? ac[j] : 0.0;
+        for (int i = j + 1 + lane; i < m; i += 32) s = fma(col[i], ac[i], s);
+        s = wsum(s) * tau;
+        if (lane == 0) ac[j] -= s;
+        for (int i = j + 1 + lane; i < m; i += 32) ac[i] = fma(-s, col[i], ac[i]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// pinv(C) X through the pivoted QR above (C = a[:, :n], X = a[:, n:n+nr]):
+// out (n x nr, ld n) = P R^{-1} (Q^T X)[:rank] with zero rows for exactly-zero
+// pivots. Returns false (uniformly) when a nonzero |R_jj| <= 1e-10 |R_00|,
+// i.e. when the SVD cutoff 1e-12 sigma_1 of pinv_apply could drop a value.
+__device__ bool qr_pinv_apply(double* a, int m, int n, int nr, int* perm, double* nrm,
+                              double* red, double* out) {
+  pivqr_augmented(a, m, n, n + nr, perm, nrm, red);
+  const int kk = m < n ? m : n;
+  __shared__ int rank_s, ok_s;
+  if (threadIdx.x == 0) {
+    const double r0 = kk > 0 ? fabs(a[0]) : 0.0;
+    int rank = 0;
+    int ok = 1;
+    while (rank < kk && fabs(a[rank + rank * m]) > 0.0) {
+      if (fabs(a[rank + rank * m]) <= 1e-10 * r0) ok = 0;
+      ++rank;
+    }
+    rank_s = rank;
+    ok_s = ok;
+  }
+  __syncthreads();
+  const int rank = rank_s;
+  for (int e = threadIdx.x; e < n * nr; e += kSvdThreads) out[e] = 0.0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < nr; c += kSvdThreads) {
+    const double* y = a + (n + c) * m;
+    for (int i = rank - 1; i >= 0; --i) {
+      double s = y[i];
+      for (int l = i + 1; l < rank; ++l) s = fma(-a[i + l * m], out[perm[l] + c * n], s);
+      out[perm[i] + c * n] = s / a[i + i * m];
+    }
+  }
+  __syncthreads();
+  return ok_s != 0;
+}
+
+// B for every pair by pivoted-QR least squares; pairs whose conditioning
+// could interact with the SVD cutoff are flagged for bsolve_kernel.
+__global__ void __launch_bounds__(kSvdThreads)
+bsolve_qr_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle,
+                 const double* __restrict__ vg, int r, int k, const std::int64_t* __restrict__ boff,
+                 double* __restrict__ bout, int* __restrict__ flags) {
+  extern __shared__ double sm[];
+  double* a = sm;                   // r x (k + max(r, k))
+  double* left = a + r * (k + (r > k ? r : k));  // k x r
+  double* out2 = left + k * r;      // k x k
+  double* nrm = out2 + k * k;       // k
+  __shared__ double red[kSvdWarps];
+  __shared__ int perm[160];
+  const std::int64_t p = blockIdx.x;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < r * k; e += kSvdThreads) a[e] = gpu_[p * r * k + e];
+  for (int e = tid; e < r * r; e += kSvdThreads) a[r * k + e] = middle[p * r * r + e];
+  __syncthreads();
+  const bool ok1 = qr_pinv_apply(a, r, k, r, perm, nrm, red, left);
+  // [ (V^T G)^T | left^T ]
+  for (int e = tid; e < r * k; e += kSvdThreads) {
+    const int i = e % r, j = e / r;
+    a[e] = vg[p * k * r + j + std::int64_t(i) * k];
+  }
+  for (int e = tid; e < r * k; e += kSvdThreads) {
+    const int i = e % r, j = e / r;  // column j of left^T = row j of left
+    a[r * k + e] = left[j + i * k];
+  }
+  __syncthreads();
+  const bool ok2 = qr_pinv_apply(a, r, k, k, perm, nrm, red, out2);
+  if (ok1 && ok2) {
+    for (int e = tid; e < k * k; e += kSvdThreads) {
+      const int i = e % k, j = e / k;
+      bout[boff[p] + e] = out2[j + i * k];  // B = out2^T
+    }
+  }
+  if (tid == 0) flags[p] = (ok1 && ok2) ? 0 : 1;
+}
+
 __global__ void __launch_bounds__(kSvdThreads)
 bsolve_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle,
               const double* __restrict__ vg, int r, int k, double tol,
-              const std::int64_t* __restrict__ boff, double* __restrict__ bout) {
+              const std::int64_t* __restrict__ boff, double* __restrict__ bout,
+              const int* __restrict__ flags) {
+  if (flags && flags[blockIdx.x] == 0) return;
   extern __shared__ double sm[];
   double* c = sm;              // r x k
   double* v = c + r * k;       // k x k
@@ -264,10 +411,20 @@ void launch_sum_partials(const std::int64_t* off, int ndst, const double* src, i
 void launch_bsolve(int npairs, const double* gpu_, const double* middle, const double* vg, int r,
                    int k, double tol, const std::int64_t* boff, double* b, cudaStream_t s) {
   if (npairs == 0) return;
+  if (r > 160 || k > 160) throw std::invalid_argument("bsolve: widths above 160 unsupported");
+  int* flags = nullptr;
+  HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), size_t(npairs) * sizeof(int), s));
+  const size_t smem_qr =
+      size_t(r * (k + std::max(r, k)) + k * r + k * k + k) * sizeof(double);
+  HP_CUDA(cudaFuncSetAttribute(bsolve_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_qr)));
+  bsolve_qr_kernel<<<npairs, kSvdThreads, smem_qr, s>>>(gpu_, middle, vg, r, k, boff, b, flags);
+  HP_LAUNCHED();
+  // fallback: one-sided Jacobi SVD with the 1e-12 cutoff for flagged pairs
   const size_t smem = size_t(r * k + k * k + r * r + 2 * k * r + k) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(bsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  bsolve_kernel<<<npairs, kSvdThreads, smem, s>>>(gpu_, middle, vg, r, k, tol, boff, b);
+  bsolve_kernel<<<npairs, kSvdThreads, smem, s>>>(gpu_, middle, vg, r, k, tol, boff, b, flags);
   HP_LAUNCHED();
+  HP_CUDA(cudaFreeAsync(flags, s));
 }
 
 }  // namespace hpeel
