@@ -126,6 +126,21 @@ int hp_op_apply(const hp_op* op, int adjoint, const double* x, int64_t w, double
 int hp_compress(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
                 int format, int strategy, int capture, hp_rep** out);
 void hp_rep_free(hp_rep* rep);
+
+/* ---- multi-GPU (one process per GPU): NCCL communicator.
+ *      Rank 0 calls hp_comm_unique_id and distributes the 128 bytes. ---- */
+typedef struct hp_comm hp_comm;
+int hp_comm_unique_id(unsigned char* id128);
+int hp_comm_create(const unsigned char* id128, int rank, int world, int device, hp_comm** out);
+void hp_comm_free(hp_comm* comm);
+/* compress with the black-box apply and leaf probes sharded over `comm`
+ * (NULL: single GPU); emulate_shards > 1 splits the launches as that many
+ * ranks would, in this process (tests) */
+int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
+                   int format, int strategy, int capture, hp_comm* comm, int emulate_shards,
+                   hp_rep** out);
+/* the work partition every rank computes: world + 1 boundaries */
+int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bounds);
 /* totals[0..5] = forward_cols, adjoint_cols, max_sampling_colors,
  * wall_s_total, wall_s_net, net_flops; *nphases = phase count */
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases);

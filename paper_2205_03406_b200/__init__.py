@@ -426,9 +426,41 @@ class CompressedRep:
         return b.value
 
 
+class Comm:
+    """NCCL communicator of one rank (one process per GPU)."""
+
+    def __init__(self, unique_id: bytes, rank: int, world: int, device: int = 0):
+        h = C.c_void_p()
+        check(lib().hp_comm_create(unique_id, int(rank), int(world), int(device), C.byref(h)))
+        self._h = h
+        self.rank, self.world, self.device = rank, world, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().hp_comm_unique_id(buf))
+        return buf.raw
+
+    def __del__(self):
+        try:
+            lib().hp_comm_free(self._h)
+        except Exception:
+            pass
+
+
+def partition_ranges(work, world: int):
+    """Contiguous work-balanced ranges every rank computes identically."""
+    work = np.ascontiguousarray(work, dtype=np.float64)
+    out = np.zeros(world + 1, dtype=np.int64)
+    check(lib().hp_partition_ranges(dptr(work), work.size, int(world), lptr(out)))
+    return [int(v) for v in out]
+
+
 def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, oversample: int = 10,
-             tol: float = 0.0, seed: int = 0, strategy: str = "graph", capture: bool = False) -> CompressedRep:
-    """compress_py (module.cpp:65-93) on the device; fixed-rank H1 only."""
+             tol: float = 0.0, seed: int = 0, strategy: str = "graph", capture: bool = False,
+             comm: "Comm | None" = None, emulate_shards: int = 0) -> CompressedRep:
+    """compress_py (module.cpp:65-93) on the device; fixed-rank H1 only.
+    `comm`: shard the black-box apply over the ranks of an NCCL group."""
     if format not in FORMATS:
         raise ValueError("unknown format: " + format)
     if strategy not in STRATEGIES:
@@ -436,8 +468,9 @@ def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, ov
     if tol > 0.0:
         raise ValueError("relative-tolerance truncation is outside the H1 fixed-rank hot path")
     h = C.c_void_p()
-    check(lib().hp_compress(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
-                            STRATEGIES[strategy], int(capture), C.byref(h)))
+    check(lib().hp_compress_ex(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
+                               STRATEGIES[strategy], int(capture), comm._h if comm else None,
+                               int(emulate_shards), C.byref(h)))
     return CompressedRep(h.value, tree, rank, oversample)
 
 

@@ -57,6 +57,12 @@ _SIGNATURES = {
     "hp_op_apply": (C.c_int, [P, C.c_int, dp, i64, dp]),
     "hp_compress": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
     "hp_rep_free": (None, [P]),
+    "hp_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "hp_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
+    "hp_comm_free": (None, [P]),
+    "hp_compress_ex": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, P, C.c_int,
+                                 C.POINTER(P)]),
+    "hp_partition_ranges": (C.c_int, [dp, i64, C.c_int, lp]),
     "hp_rep_report": (C.c_int, [P, dp, lp]),
     "hp_rep_phase": (C.c_int, [P, i64, lp, dp]),
     "hp_rep_csv": (C.c_int, [P, C.c_char_p, i64, lp]),

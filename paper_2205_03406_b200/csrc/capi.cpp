@@ -10,6 +10,7 @@
 #include "hpeel/coloring.hpp"
 #include "hpeel/peeling.hpp"
 #include "hpeel/rng.hpp"
+#include "hpeel/shard.hpp"
 
 using namespace hpeel;
 
@@ -30,6 +31,9 @@ struct hp_op {
 };
 struct hp_rep {
   PeelResult result;
+};
+struct hp_comm {
+  std::unique_ptr<Comm> comm;
 };
 
 namespace hpeel {
@@ -422,6 +426,62 @@ int hp_compress(const hp_op* op, const hp_tree* tree, int rank, int oversample, 
 }
 
 void hp_rep_free(hp_rep* rep) { delete rep; }
+
+int hp_comm_unique_id(unsigned char* id128) {
+  return guard([&] {
+    need(id128, "id");
+    Comm::unique_id(id128);
+  });
+}
+
+int hp_comm_create(const unsigned char* id128, int rank, int world, int device, hp_comm** out) {
+  return guard([&] {
+    need(out, "out");
+    if (world > 1) need(id128, "id");
+    auto c = std::make_unique<hp_comm>();
+    c->comm = std::make_unique<Comm>(id128, rank, world, device);
+    *out = c.release();
+  });
+}
+
+void hp_comm_free(hp_comm* comm) { delete comm; }
+
+int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
+                   int format, int strategy, int capture, hp_comm* comm, int emulate_shards,
+                   hp_rep** out) {
+  return guard([&] {
+    need(op, "op");
+    need(tree, "tree");
+    need(out, "out");
+    if (format < 0 || format > 3) throw std::invalid_argument("unknown format");
+    if (emulate_shards < 0) throw std::invalid_argument("negative shard count");
+    PeelConfig cfg;
+    cfg.rank = rank;
+    cfg.oversample = oversample;
+    cfg.leaf_capacity = tree->tree->leaf_capacity();
+    cfg.seed = seed;
+    cfg.format = PeelFormat(format);
+    cfg.strategy = strategy == HP_STRATEGY_FALLBACK_PATTERN ? ColoringStrategy::kFallbackPattern
+                                                            : ColoringStrategy::kGraph;
+    cfg.capture_samples = capture != 0;
+    cfg.comm = comm ? comm->comm.get() : nullptr;
+    cfg.emulate_shards = emulate_shards;
+    if (cfg.comm && cfg.comm->device() != op->op->device())
+      throw std::invalid_argument("communicator and operator on different devices");
+    auto r = std::make_unique<hp_rep>();
+    r->result = compress(*op->op, tree->tree, cfg);
+    *out = r.release();
+  });
+}
+
+int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bounds) {
+  return guard([&] {
+    need(bounds, "bounds");
+    if (n > 0) need(work, "work");
+    const auto b = partition_ranges(std::vector<double>(work, work + n), world);
+    std::memcpy(bounds, b.data(), b.size() * sizeof(int64_t));
+  });
+}
 
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases) {
   return guard([&] {

@@ -21,6 +21,7 @@
 
 #include "engine.cuh"
 #include "rng.hpp"
+#include "shard.hpp"
 
 namespace hpeel {
 
@@ -309,6 +310,24 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     auto leaf_fut = std::async(std::launch::async, build_leaf, std::cref(e), std::cref(*rep),
                                std::cref(config));
 
+    // Sharding: ranks launch K2/K6 for contiguous work-balanced
+    // ranges and broadcast their rows; emulate_shards splits the launches the
+    // same way inside one process (tests).
+    const int world = config.comm ? config.comm->world() : std::max(1, config.emulate_shards);
+    const int my_rank = config.comm ? config.comm->rank() : -1;
+    auto shard_tasks = [&](const std::vector<SampleTask>& tasks, const std::vector<double>& work,
+                           const std::vector<std::int64_t>& item_off, std::vector<std::int64_t>& seg) {
+      const auto b = partition_ranges(work, world);
+      seg.assign(size_t(world) + 1, 0);
+      for (int q = 0; q <= world; ++q) seg[size_t(q)] = item_off[size_t(b[size_t(q)])];
+      std::vector<std::vector<SampleTask>> lists(static_cast<size_t>(world));
+      for (const SampleTask& t : tasks) {
+        const int q = int(std::upper_bound(seg.begin(), seg.end(), t.out) - seg.begin()) - 1;
+        lists[size_t(std::min(std::max(q, 0), world - 1))].push_back(t);
+      }
+      return lists;
+    };
+
     const int gld = 2 * r;
     DevBuf<double> g(size_t(n) * size_t(gld), s);
     std::vector<std::unique_ptr<LevelTimers>> timers(size_t(tree->depth()) + 1);
@@ -339,9 +358,14 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       d_local.upload(w.local, s);
       launch_payload_gaussian(g.get(), gld, r, n, d_pos_box.get(), d_local.get(), config.seed, l, s);
 
-      // K2 apply (forward + adjoint samples of every pair's row block)
-      DevBuf<SampleTask> d_tasks;
-      d_tasks.upload(w.tasks, s);
+      // K2 apply (forward + adjoint samples of every pair's row block),
+      // split into work-balanced contiguous pair ranges across ranks
+      std::vector<double> pair_work(np);
+      for (size_t p = 0; p < np; ++p)
+        pair_work[p] = double(e.count(ld.pairs[p].first)) *
+                       double(w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])]);
+      std::vector<std::int64_t> seg;
+      const auto lists = shard_tasks(w.tasks, pair_work, w.soff, seg);
       DevBuf<std::int64_t> d_pay_off;
       d_pay_off.upload(w.pay_off, s);
       DevBuf<int> d_pay_pos;
@@ -355,16 +379,23 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       launch_permute_rows(g.get(), gld, 1, d_pay_pos.get(), nnz, gld, gcol.get(), gld, 1, s);
       if (op.kind() != kOpDense)
         launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
-      if (op.symmetric()) {
-        launch_sample_apply(e.dop, false, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
-                            d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
-                            samples.get(), 0, s);
-      } else {
-        launch_sample_apply(e.dop, false, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
-                            d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0, s);
-        launch_sample_apply(e.dop, true, d_tasks.get(), int(w.tasks.size()), d_pay_off.get(),
-                            d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r, s);
+      for (int sr = 0; sr < int(lists.size()); ++sr) {
+        if (my_rank >= 0 && sr != my_rank) continue;
+        const auto& tl = lists[size_t(sr)];
+        DevBuf<SampleTask> d_tasks;
+        d_tasks.upload(tl, s);
+        if (op.symmetric()) {
+          launch_sample_apply(e.dop, false, d_tasks.get(), int(tl.size()), d_pay_off.get(),
+                              d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
+                              samples.get(), 0, s);
+        } else {
+          launch_sample_apply(e.dop, false, d_tasks.get(), int(tl.size()), d_pay_off.get(),
+                              d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0, s);
+          launch_sample_apply(e.dop, true, d_tasks.get(), int(tl.size()), d_pay_off.get(),
+                              d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r, s);
+        }
       }
+      if (config.comm) config.comm->broadcast_segments(samples.get(), seg, s);
       HP_CUDA(cudaEventRecord(tm->apply.b, s));
 
       // K3 peel
@@ -423,18 +454,42 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     HP_CUDA(cudaMalloc(&rep->d_dense, size_t(std::max<std::int64_t>(lw.total, 1)) * 8));
     Events leaf_apply, leaf_peel;
     {
-      DevBuf<SampleTask> d_tasks;
-      d_tasks.upload(lw.tasks, s);
+      std::vector<double> dwork(lw.pairs.size());
+      std::vector<std::int64_t> doff(lw.off);
+      doff.push_back(lw.total);
+      for (size_t p = 0; p < lw.pairs.size(); ++p)
+        dwork[p] = double(e.count(lw.pairs[p].first)) * double(lw.w);
+      std::vector<std::int64_t> seg;
+      const auto lists = shard_tasks(lw.tasks, dwork, doff, seg);
       DevBuf<std::int64_t> d_pay_off;
       d_pay_off.upload(lw.pay_off, s);
       DevBuf<int> d_pay_box;
       d_pay_box.upload(lw.pay_box, s);
       HP_CUDA(cudaEventRecord(leaf_apply.a, s));
-      launch_identity_apply(e.dop, d_tasks.get(), int(lw.tasks.size()), d_pay_off.get(), d_pay_box.get(),
-                            e.d_box_start.get(), e.d_box_count.get(), lw.w, rep->d_dense, s);
+      for (int sr = 0; sr < int(lists.size()); ++sr) {
+        if (my_rank >= 0 && sr != my_rank) continue;
+        DevBuf<SampleTask> d_tasks;
+        d_tasks.upload(lists[size_t(sr)], s);
+        launch_identity_apply(e.dop, d_tasks.get(), int(lists[size_t(sr)].size()), d_pay_off.get(),
+                              d_pay_box.get(), e.d_box_start.get(), e.d_box_count.get(), lw.w,
+                              rep->d_dense, s);
+      }
       HP_CUDA(cudaEventRecord(leaf_apply.b, s));
       HP_CUDA(cudaEventRecord(leaf_peel.a, s));
-      if (lw.has_peel) run_peel(lw.peel, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
+      if (lw.has_peel) {
+        if (my_rank >= 0) {
+          // peel this rank's dense blocks only, then share them
+          PeelPlan mine = lw.peel;
+          const std::int64_t lo = seg[size_t(my_rank)], hi = seg[size_t(my_rank) + 1];
+          mine.tasks_fwd.erase(std::remove_if(mine.tasks_fwd.begin(), mine.tasks_fwd.end(),
+                                              [&](const PeelTask& t) { return t.out < lo || t.out >= hi; }),
+                               mine.tasks_fwd.end());
+          run_peel(mine, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
+        } else {
+          run_peel(lw.peel, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
+        }
+      }
+      if (config.comm) config.comm->broadcast_segments(rep->d_dense, seg, s);
       HP_CUDA(cudaEventRecord(leaf_peel.b, s));
     }
     HP_CUDA(cudaStreamSynchronize(s));

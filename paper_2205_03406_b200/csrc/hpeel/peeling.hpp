@@ -28,6 +28,8 @@ inline constexpr double kPinvCutoff = 1e-12;     // proj/include/hpeel/linalg.hp
 enum class PeelFormat : std::uint8_t { kH1 = 0, kUnifH1 = 1, kH1PlusUnif = 2, kH2 = 3 };
 enum class ColoringStrategy : std::uint8_t { kGraph = 0, kFallbackPattern = 1 };
 
+class Comm;  // shard.hpp
+
 struct PeelConfig {
   int rank = 8;          // TruncationSpec::fixed_rank(k, p) (proj/src/linalg.cpp:24-31)
   int oversample = 10;
@@ -36,6 +38,8 @@ struct PeelConfig {
   PeelFormat format = PeelFormat::kH1;
   ColoringStrategy strategy = ColoringStrategy::kGraph;
   bool capture_samples = false;  // keep post-peel sample blocks on the host (tests)
+  Comm* comm = nullptr;          // multi-GPU: this process's rank in the NCCL group
+  int emulate_shards = 0;        // tests: split K2/K6 launches as `n` ranks would
   int sample_width() const { return rank + oversample; }
   void validate() const;
 };
