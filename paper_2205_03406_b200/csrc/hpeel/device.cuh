@@ -62,34 +62,32 @@ __device__ __forceinline__ double fast_rcp(double d) {
   return fma(r, e, r);
 }
 
-/// Table for fast_log (built on the host in extended precision, see
-/// log_table_device): kLogTab entries each of 1/T_k, log(T_k) hi and lo.
-constexpr int kLogTab = 256;
-constexpr int kLogSplit = 106;  // first index with 1 + k/256 >= sqrt(2)
+/// Table for half_log (built on the host in extended precision, see
+/// log_table_device): kLogTab entries each of 1/(2 T_k) and 0.5 log(T_k').
+constexpr int kLogTab = 1025;
+constexpr int kLogSplit = 425;  // k >= kLogSplit (T_k >= sqrt 2): reduce m / 2 against T_k / 2
 
-/// Natural log for positive normal x, <= 2 ulp (tests/test_gpu_kernels.py
-/// checks it against glibc). x = 2^e m, m in [1, 2); the top 8 mantissa bits
-/// pick T_k (left endpoints below sqrt2, halved right endpoints above, so
-/// x -> 1 from either side meets T = 1 exactly) and u = m / T_k - 1 with
-/// |u| < 1/256; log1p(u) by its Taylor series to u^7 (remainder < 1e-20).
-/// 12 FP64 ops and 3 table reads vs ~56 FP64-op equivalents for libdevice log.
-__device__ __forceinline__ double fast_log(double x, const double* __restrict__ tab) {
+/// 0.5 * log(x) for positive normal x, <= 2 ulp of 0.5 log x
+/// (tests/test_gpu_kernels.py checks 2 * half_log against glibc log).
+/// x = 2^e m, m in [1, 2); the top 11 mantissa bits round to the nearest
+/// T_k = 1 + k/1024 (k in 0..1024; T = 1 is hit exactly from either side of
+/// x = 1, where the table value is 0) and v = (m / T_k - 1) / 2, |v| <= 2^-12,
+/// so 0.5 log1p(2v) is a degree-5 series (remainder < 5e-18 relative). The 1/2
+/// is folded into the table and the coefficients: 9 FP64 ops, one int->f64
+/// conversion and 2 table reads per call.
+__device__ __forceinline__ double half_log(double x, const double* __restrict__ tab) {
   const int hi = __double2hiint(x);
   const int lo = __double2loint(x);
-  const int k = (hi >> 12) & 0xff;
+  const int k = (((hi >> 9) & 0x7ff) + 1) >> 1;
   const int e = ((hi >> 20) & 0x7ff) - 1023 + (k >= kLogSplit ? 1 : 0);
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double u = fma(m, tab[k], -1.0);
-  double q = 1.0 / 7.0;
-  q = fma(q, u, -1.0 / 6.0);
-  q = fma(q, u, 1.0 / 5.0);
-  q = fma(q, u, -1.0 / 4.0);
-  q = fma(q, u, 1.0 / 3.0);
-  q = fma(q, u, -0.5);
-  const double lp = fma(u * u, q, u);
-  const double de = double(e);
-  return fma(de, 6.93147180369123816490e-01, tab[kLogTab + k]) +
-         (fma(de, 1.90821492927058770002e-10, tab[2 * kLogTab + k]) + lp);
+  const double v = fma(m, tab[k], -0.5);
+  // 0.5 log1p(2v) = v - v^2 + 4/3 v^3 - 2 v^4 + 16/5 v^5 - ...
+  double q = fma(16.0 / 5.0, v, -2.0);
+  q = fma(q, v, 4.0 / 3.0);
+  q = fma(q, v, -1.0);
+  const double lp = fma(v * v, q, v);
+  return fma(double(e), 3.46573590279972654709e-01, tab[kLogTab + k]) + lp;
 }
 
 /// K(x_i, x_j) for the on-the-fly kinds, from coordinates already in
@@ -105,15 +103,12 @@ __device__ __forceinline__ double kernel_value(const double* xi, const double* x
     r2 = fma(t, t, r2);
   }
   if (KIND == kOpLog) {
-    // coincident distinct points give -inf as the dense assembly would;
-    // sub-normal distances (< 1.5e-154) are outside the supported range
-    if (DIM == 1) {
-      const double d = fabs(xi[0] - xj[0]);
-      const double v = fast_log(d, ltab);
-      return same ? 0.0 : (d == 0.0 ? -INFINITY : v);
-    }
-    const double v = 0.5 * fast_log(r2, ltab);
-    return same ? 0.0 : (r2 == 0.0 ? -INFINITY : v);
+    // log|x - y| = 0.5 log r^2; coincident distinct points give -inf as the
+    // dense assembly would (integer test: r2 >= 0); sub-normal r^2
+    // (< 2.2e-308) is outside the supported range
+    const double v = half_log(r2, ltab);
+    const bool zero = (__double2hiint(r2) | __double2loint(r2)) == 0;
+    return same ? 0.0 : (zero ? -INFINITY : v);
   } else if (KIND == kOpInvDist4Pi) {
     if (same) return 0.0;
     return rsqrt(r2) * 0.07957747154594767;  // 1 / (4 pi)

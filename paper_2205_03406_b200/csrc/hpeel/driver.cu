@@ -63,7 +63,9 @@ struct LevelWork {
   std::vector<std::int64_t> pay_off;
   std::vector<int> pay_pos;
   std::vector<int> pos_box, local;
-  std::vector<SampleTask> tasks;
+  std::vector<K2Row> rowtab;               // K2 rows, grouped by shard and color
+  std::vector<std::vector<K2Task>> k2;     // K2 tiles per shard
+  std::vector<std::int64_t> seg;           // shard q owns samples [seg[q], seg[q+1])
   double evals = 0;
   bool has_peel = false;
   PeelPlan peel;
@@ -116,19 +118,44 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
       w.local[size_t(e.start(b) + q)] = lr[q];
     }
   }
-  // K2 tasks, largest payload lists first (tail balance)
+  // K2: split the pairs into work-balanced contiguous ranges, one per shard
+  // (DESIGN.md §7); inside a shard, the target rows of all pairs served by
+  // one color are packed into full tiles, largest payload lists first.
+  const int world = cfg.comm ? cfg.comm->world() : std::max(1, cfg.emulate_shards);
+  std::vector<double> pair_work(np);
   for (size_t p = 0; p < np; ++p) {
-    const int a = ld.pairs[p].first;
-    const int rows = e.count(a);
-    for (int t0 = 0; t0 < rows; t0 += kTile)
-      w.tasks.push_back(SampleTask{e.start(a) + t0, w.soff[p] + t0, std::min(kTile, rows - t0),
-                                   w.pcolor[p], rows, 0});
-    w.evals += double(rows) * double(w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])]);
+    const std::int64_t nnz = w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])];
+    pair_work[p] = double(e.count(ld.pairs[p].first)) * double(nnz);
+    w.evals += pair_work[p];
   }
-  std::stable_sort(w.tasks.begin(), w.tasks.end(), [&](const SampleTask& x, const SampleTask& y) {
-    return w.pay_off[size_t(x.color) + 1] - w.pay_off[size_t(x.color)] >
-           w.pay_off[size_t(y.color) + 1] - w.pay_off[size_t(y.color)];
-  });
+  const auto bounds = partition_ranges(pair_work, world);
+  w.seg.resize(size_t(world) + 1);
+  for (int q = 0; q <= world; ++q) w.seg[size_t(q)] = w.soff[size_t(bounds[size_t(q)])];
+  const int tile = k2_tile_rows(e.dop.symmetric ? 2 * r : r);
+  w.k2.resize(size_t(world));
+  std::vector<std::vector<int>> by_color(size_t(w.nc));
+  for (int q = 0; q < world; ++q) {
+    for (auto& v : by_color) v.clear();
+    for (std::int64_t p = bounds[size_t(q)]; p < bounds[size_t(q) + 1]; ++p)
+      by_color[size_t(w.pcolor[size_t(p)])].push_back(int(p));
+    auto& tl = w.k2[size_t(q)];
+    for (int c = 0; c < w.nc; ++c) {
+      const std::int64_t first = std::int64_t(w.rowtab.size());
+      for (int p : by_color[size_t(c)]) {
+        const int a = ld.pairs[size_t(p)].first;
+        const int rows = e.count(a);
+        for (int i = 0; i < rows; ++i)
+          w.rowtab.push_back(K2Row{w.soff[size_t(p)] + i, int(e.start(a) + i), rows});
+      }
+      const std::int64_t last = std::int64_t(w.rowtab.size());
+      for (std::int64_t t0 = first; t0 < last; t0 += tile)
+        tl.push_back(K2Task{t0, int(std::min<std::int64_t>(tile, last - t0)), c});
+    }
+    std::stable_sort(tl.begin(), tl.end(), [&](const K2Task& x, const K2Task& y) {
+      return w.pay_off[size_t(x.color) + 1] - w.pay_off[size_t(x.color)] >
+             w.pay_off[size_t(y.color) + 1] - w.pay_off[size_t(y.color)];
+    });
+  }
   // K3 (prev_level = l - 1 >= 2)
   if (l - 1 >= 2) {
     std::vector<SampleBlock> blocks(np);
@@ -358,14 +385,11 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       d_local.upload(w.local, s);
       launch_payload_gaussian(g.get(), gld, r, n, d_pos_box.get(), d_local.get(), config.seed, l, s);
 
-      // K2 apply (forward + adjoint samples of every pair's row block),
-      // split into work-balanced contiguous pair ranges across ranks
-      std::vector<double> pair_work(np);
-      for (size_t p = 0; p < np; ++p)
-        pair_work[p] = double(e.count(ld.pairs[p].first)) *
-                       double(w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])]);
-      std::vector<std::int64_t> seg;
-      const auto lists = shard_tasks(w.tasks, pair_work, w.soff, seg);
+      // K2 apply (forward + adjoint samples of every pair's row block); each
+      // shard launches its own tiles, then the shards' rows are broadcast
+      const std::vector<std::int64_t>& seg = w.seg;
+      DevBuf<K2Row> d_rowtab;
+      d_rowtab.upload(w.rowtab, s);
       DevBuf<std::int64_t> d_pay_off;
       d_pay_off.upload(w.pay_off, s);
       DevBuf<int> d_pay_pos;
@@ -379,19 +403,20 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       launch_permute_rows(g.get(), gld, 1, d_pay_pos.get(), nnz, gld, gcol.get(), gld, 1, s);
       if (op.kind() != kOpDense)
         launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
-      for (int sr = 0; sr < int(lists.size()); ++sr) {
+      for (int sr = 0; sr < int(w.k2.size()); ++sr) {
         if (my_rank >= 0 && sr != my_rank) continue;
-        const auto& tl = lists[size_t(sr)];
-        DevBuf<SampleTask> d_tasks;
+        const auto& tl = w.k2[size_t(sr)];
+        DevBuf<K2Task> d_tasks;
         d_tasks.upload(tl, s);
+        const int nt = int(tl.size());
         if (op.symmetric()) {
-          launch_sample_apply(e.dop, false, d_tasks.get(), int(tl.size()), d_pay_off.get(),
+          launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
                               d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
                               samples.get(), 0, s);
         } else {
-          launch_sample_apply(e.dop, false, d_tasks.get(), int(tl.size()), d_pay_off.get(),
+          launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
                               d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0, s);
-          launch_sample_apply(e.dop, true, d_tasks.get(), int(tl.size()), d_pay_off.get(),
+          launch_sample_apply(e.dop, true, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
                               d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r, s);
         }
       }

@@ -44,10 +44,7 @@ __global__ void payload_gaussian_kernel(double* g, int gld, int r, std::int64_t 
   }
 }
 
-constexpr int kBM = 64;        // rows per CTA
 constexpr int kBK = 32;        // payload rows per stage
-constexpr int kThreads = 256;  // 4 DMMA warps + 4 evaluation warps
-constexpr int kKR = kBM + 4;   // kernel tile, column-major, column stride (== 4 mod 16)
 constexpr int kBarFull = 1;    // named barriers: 1,2 tile b full; 3,4 tile b empty; 5 eval warps
 constexpr int kBarEmpty = 3;
 constexpr int kBarEval = 5;
@@ -60,10 +57,14 @@ __host__ __device__ constexpr int smem_stride(int nt) {
 
 constexpr int kStages = 3;     // payload ring: chunk c+1 streams in while chunk c is evaluated
 
-template <int NT>
+template <int NT, int ROWS>
 constexpr size_t sample_smem_bytes() {
-  return size_t(kStages * kBK * smem_stride(NT) + 2 * kBK * kKR) * sizeof(double);
+  return size_t(kStages * kBK * smem_stride(NT) + 2 * kBK * (ROWS + 4)) * sizeof(double);
 }
+
+/// Rows per K2 CTA: 128 (8 DMMA + 8 evaluation warps, one CTA per SM) when the
+/// accumulators fit 128 registers (2r <= 88), else 64 (4 + 4 warps).
+constexpr int k2_rows_for(int nt) { return nt <= 11 ? 128 : 64; }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -90,38 +91,43 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 // Warp-specialized colored apply. The payload rows of each color are stored
 // contiguously in color order (gc, xc, pc: payload values, coordinates and
 // tree positions), so a 32-row chunk is one contiguous copy.
-// Warps 4..7 ("eval"): per chunk, cp.async the chunk's coordinates/positions
+// Upper half of the warps ("eval"): per chunk, cp.async the chunk's coordinates/positions
 // (group 1) and payload rows (group 2), then evaluate the 64 x 32 kernel
 // tile into K[b] (column-major; each thread owns one row and 16 columns).
-// Warps 0..3 ("DMMA"): each owns 16 output rows and runs 2 x NT DMMA.8x8x4
+// Lower half ("DMMA"): each owns 16 output rows and runs 2 x NT DMMA.8x8x4
 // per k-step from K[b] / G[b]. Double-buffered; full/empty hand-off through
 // named barriers, so evaluation of chunk c+1 overlaps the DMMA of chunk c.
-template <int NT, int KIND, int DIM, bool TRANS>
-__global__ void __launch_bounds__(kThreads, NT <= 11 ? 2 : 1)
-sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
+template <int NT, int KIND, int DIM, bool TRANS, int ROWS>
+__global__ void __launch_bounds__(ROWS * 4, 1)
+sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __restrict__ rowtab,
                     const std::int64_t* __restrict__ pay_off, const int* __restrict__ pc,
                     const double* __restrict__ gc, int gld, int gcol0, int ncols,
                     const double* __restrict__ xc, std::int64_t nnz, double* __restrict__ out,
                     int ocol0, int mode) {
   constexpr int S = smem_stride(NT);
   constexpr int D = DIM > 0 ? DIM : 1;
+  constexpr int kThreads = ROWS * 4;   // ROWS/16 DMMA warps + ROWS/16 evaluation warps
+  constexpr int kEval = ROWS * 2;      // evaluation threads
+  constexpr int kKR = ROWS + 4;        // kernel tile column stride (== 4 mod 16)
+  constexpr int kBM = ROWS;
   extern __shared__ __align__(16) double dyn_smem[];
   double* gsm = dyn_smem;                        // [kStages][kBK * S] payload ring
   double* ksm = dyn_smem + kStages * kBK * S;    // [2][kBK * kKR] kernel tiles
   __shared__ __align__(16) double xs[kStages][D][kBK];
   __shared__ __align__(16) int js[kStages][kBK];
-  __shared__ __align__(16) double lts[KIND == kOpLog ? 3 * kLogTab : 1];
+  __shared__ __align__(16) double lts[KIND == kOpLog ? 2 * kLogTab : 1];
 
-  const SampleTask task = tasks[blockIdx.x];
+  const K2Task task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
+  const K2Row* rt = rowtab + task.rbeg;
 
   if constexpr (KIND == kOpLog) {
-    for (int e = tid; e < 3 * kLogTab; e += kThreads) lts[e] = op.ltab[e];
+    for (int e = tid; e < 2 * kLogTab; e += kThreads) lts[e] = op.ltab[e];
   }
   for (int e = tid; e < kStages * kBK * S; e += kThreads) gsm[e] = 0.0;
   for (int e = tid; e < kStages * kBK; e += kThreads) {
-    (&js[0][0])[e] = int(task.row0);
+    (&js[0][0])[e] = rt[0].pos;
     for (int d = 0; d < D; ++d) xs[e / kBK][d][e % kBK] = 0.0;
   }
   __syncthreads();
@@ -129,11 +135,11 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
   const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
   const int nchunks = int((p1 - p0 + kBK - 1) / kBK);
 
-  if (warp >= 4) {
+  if (warp >= ROWS / 16) {
     // ------------------------------------------------ evaluation warps
-    const int et = tid - 128;
-    const int row = et & (kBM - 1), cgrp = et >> 6;
-    const int ipos = int(task.row0) + (row < task.rows ? row : task.rows - 1);
+    const int et = tid - kEval;
+    const int row = et & (kBM - 1), cgrp = et / kBM;
+    const int ipos = rt[row < task.rows ? row : task.rows - 1].pos;
     double xi[D];
     if constexpr (KIND != kOpDense) {
 #pragma unroll
@@ -156,12 +162,12 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
       const double* gsrc = gc + base * gld + gcol0;
       if (even_cols) {
         const int half = ncols >> 1;
-        for (int idx = et; idx < cnt * half; idx += 128) {
+        for (int idx = et; idx < cnt * half; idx += kEval) {
           const int t = idx / half, cc = (idx - t * half) * 2;
           cp_async16(gb + t * S + cc, gsrc + std::int64_t(t) * gld + cc);
         }
       } else {
-        for (int idx = et; idx < cnt * ncols; idx += 128) {
+        for (int idx = et; idx < cnt * ncols; idx += kEval) {
           const int t = idx / ncols, cc = idx - t * ncols;
           cp_async8(gb + t * S + cc, gsrc + std::int64_t(t) * gld + cc);
         }
@@ -179,7 +185,7 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
       } else {
         cp_async_wait_all();
       }
-      bar_sync(kBarEval, 128);  // ... and every eval thread's copies
+      bar_sync(kBarEval, kEval);  // ... and every eval thread's copies
       const std::int64_t base = p0 + std::int64_t(c) * kBK;
       const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
       double* kb = ksm + b * kBK * kKR;
@@ -263,12 +269,13 @@ sample_apply_kernel(DevOp op, const SampleTask* __restrict__ tasks,
   for (int m = 0; m < 2; ++m) {
     const int rr = warp * 16 + m * 8 + (lane >> 2);
     if (rr >= task.rows) continue;
+    const K2Row dst = rt[rr];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = nt * 8 + (lane & 3) * 2 + h;
-        if (c < ncols) out[task.out + rr + std::int64_t(ocol0 + c) * task.ld] = acc[m][nt][h];
+        if (c < ncols) out[dst.out + std::int64_t(ocol0 + c) * dst.ld] = acc[m][nt][h];
       }
     }
   }
@@ -281,29 +288,37 @@ int& k2_mode() {
   return mode;
 }
 
+template <int NT, int KIND, int DIM, int R>
+void launch_rows(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab, int ntasks,
+                 const std::int64_t* pay_off, const int* pc, const double* gc, int gld, int gcol0,
+                 int ncols, const double* xc, std::int64_t nnz, double* out, int ocol0, cudaStream_t s) {
+  constexpr size_t smem = sample_smem_bytes<NT, R>();
+  if (KIND == kOpDense && trans) {
+    auto* fn = sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense, R>;
+    HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    fn<<<ntasks, R * 4, smem, s>>>(op, tasks, rowtab, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode());
+  } else {
+    auto* fn = sample_apply_kernel<NT, KIND, DIM, false, R>;
+    HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    fn<<<ntasks, R * 4, smem, s>>>(op, tasks, rowtab, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode());
+  }
+}
+
 template <int NT, int KIND, int DIM>
-void launch_nt_kind_dim(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
+void launch_nt_kind_dim(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab, int ntasks,
                         const std::int64_t* pay_off, const int* pc, const double* gc, int gld,
                         int gcol0, int ncols, const double* xc, std::int64_t nnz, double* out,
                         int ocol0, cudaStream_t s) {
   // kernel kinds are symmetric: only the explicit dense operator has a transpose
-  constexpr size_t smem = sample_smem_bytes<NT>();
-  if (KIND == kOpDense && trans) {
-    auto* fn = sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense>;
-    HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode());
-  } else {
-    auto* fn = sample_apply_kernel<NT, KIND, DIM, false>;
-    HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    fn<<<ntasks, kThreads, smem, s>>>(op, tasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode());
-  }
+  launch_rows<NT, KIND, DIM, k2_rows_for(NT)>(op, trans, tasks, rowtab, ntasks, pay_off, pc, gc, gld,
+                                              gcol0, ncols, xc, nnz, out, ocol0, s);
 }
 
 template <int NT>
-void launch_nt(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
+void launch_nt(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab, int ntasks,
                const std::int64_t* pay_off, const int* pc, const double* gc, int gld, int gcol0,
                int ncols, const double* xc, std::int64_t nnz, double* out, int ocol0, cudaStream_t s) {
-#define HP_ARGS op, trans, tasks, ntasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, s
+#define HP_ARGS op, trans, tasks, rowtab, ntasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, s
   switch (op.kind) {
     case kOpDense: return launch_nt_kind_dim<NT, kOpDense, 0>(HP_ARGS);
     case kOpLog:
@@ -406,6 +421,8 @@ __global__ void full_apply_kernel(DevOp op, const double* __restrict__ x, int w,
 
 }  // namespace
 
+int k2_tile_rows(int ncols) { return k2_rows_for((ncols + 7) / 8); }
+
 void set_k2_mode(int m) { k2_mode() = m; }
 
 void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const int* pos_box,
@@ -416,7 +433,7 @@ void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const in
   HP_LAUNCHED();
 }
 
-void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
+void launch_sample_apply(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab, int ntasks,
                          const std::int64_t* pay_off, const int* pc, const double* gc, int gld,
                          int gcol0, int ncols, const double* xc, std::int64_t nnz, double* out,
                          int ocol0, cudaStream_t s) {
@@ -424,7 +441,7 @@ void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, i
   const int nt = (ncols + 7) / 8;
 #define HP_CASE(NT)                                                                            \
   case NT:                                                                                     \
-    launch_nt<NT>(op, trans, tasks, ntasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out,  \
+    launch_nt<NT>(op, trans, tasks, rowtab, ntasks, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out,  \
                   ocol0, s);                                                                   \
     break;
   switch (nt) {

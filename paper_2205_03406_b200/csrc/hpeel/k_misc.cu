@@ -89,22 +89,16 @@ const double* log_table_device(int device) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = tabs.find(device);
   if (it != tabs.end()) return it->second;
-  // T_k = 1 / inv_k exactly; log T_k in extended precision split hi + lo
-  std::vector<double> h(3 * kLogTab);
+  // T_k = 1 / inv_k exactly (inv_k = 1 / (1 + k/1024) rounded); stored:
+  // inv_k / 2, and 0.5 log T_k' in extended precision, where T_k' = T_k
+  // below kLogSplit and T_k / 2 from it on (device.cuh half_log)
+  std::vector<double> h(2 * kLogTab);
   for (int k = 0; k < kLogTab; ++k) {
-    double inv;
-    long double t;
-    if (k < kLogSplit) {
-      inv = double(1.0L / (1.0L + (long double)k / kLogTab));
-      t = 1.0L / (long double)inv;
-    } else {
-      inv = double(1.0L / (1.0L + (long double)(k + 1) / kLogTab));
-      t = (1.0L / (long double)inv) / 2.0L;
-    }
-    const long double l = logl(t);
-    h[size_t(k)] = inv;
-    h[size_t(kLogTab + k)] = double(l);
-    h[size_t(2 * kLogTab + k)] = double(l - (long double)double(l));
+    const double inv = double(1.0L / (1.0L + (long double)k / 1024.0L));
+    long double t = 1.0L / (long double)inv;
+    if (k >= kLogSplit) t /= 2.0L;
+    h[size_t(k)] = inv / 2.0;
+    h[size_t(kLogTab + k)] = double(0.5L * logl(t));
   }
   int prev = 0;
   HP_CUDA(cudaGetDevice(&prev));

@@ -20,8 +20,8 @@ void launch_payload_gaussian(double* g, int gld, int r, std::int64_t n, const in
                              const int* local, std::uint64_t seed, int level, cudaStream_t s);
 
 // ---------------------------------------------------------------- K2 apply
-/// One CTA tile: up to 64 consecutive tree rows of a box against the payload
-/// rows of one color class.
+/// Leaf identity-apply tile: up to 64 consecutive tree rows of a box against
+/// the boxes of one color class.
 struct SampleTask {
   std::int64_t row0;
   std::int64_t out;  // element offset of (tile row 0, col 0) in `out`
@@ -30,15 +30,34 @@ struct SampleTask {
   int ld;
   int pad;
 };
-/// out[task.out + i + (ocol0 + c) * ld] = sum_q K(row0+i, pc[q]) gc[q * gld + gcol0 + c]
+/// K2 row table entry: one output row of a sample block (element offset of
+/// its column 0 and the block's column stride) and its tree position.
+struct K2Row {
+  std::int64_t out;
+  int pos;
+  int ld;
+};
+/// One K2 CTA: rows [rbeg, rbeg + rows) of the row table, all served by the
+/// payload of `color` (rows of several target boxes of the same color are
+/// packed into one tile).
+struct K2Task {
+  std::int64_t rbeg;
+  int rows;
+  int color;
+};
+/// For each task row R = rowtab[rbeg + i]:
+/// out[R.out + (ocol0 + c) * R.ld] = sum_q K(R.pos, pc[q]) gc[q * gld + gcol0 + c]
 /// over the payload rows q in [pay_off[color], pay_off[color+1]) of the task's
 /// color, stored in color order: pc = tree positions, gc = payload rows,
 /// xc = coordinates (dim x nnz). `trans` applies K^T (adjoint of a
 /// non-symmetric dense operator).
-void launch_sample_apply(const DevOp& op, bool trans, const SampleTask* tasks, int ntasks,
-                         const std::int64_t* pay_off, const int* pc, const double* gc, int gld,
-                         int gcol0, int ncols, const double* xc, std::int64_t nnz, double* out,
-                         int ocol0, cudaStream_t s);
+/// Rows per K2 CTA for an apply of `ncols` payload columns; K2Task.rows must
+/// not exceed it.
+int k2_tile_rows(int ncols);
+void launch_sample_apply(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab,
+                         int ntasks, const std::int64_t* pay_off, const int* pc, const double* gc,
+                         int gld, int gcol0, int ncols, const double* xc, std::int64_t nnz,
+                         double* out, int ocol0, cudaStream_t s);
 
 /// Leaf-phase identity probes (proj/src/coloring.cpp:271-277):
 /// out[task.out + i + t * ld] = sum_{v in color} K(row0+i, start_v + t), t < |v|,

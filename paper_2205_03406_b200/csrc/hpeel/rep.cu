@@ -395,7 +395,7 @@ namespace hpeel {
 namespace {
 __global__ void fast_log_probe_kernel(const double* x, std::int64_t n, double* y, const double* tab) {
   const std::int64_t i = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x;
-  if (i < n) y[i] = fast_log(x[i], tab);
+  if (i < n) y[i] = 2.0 * half_log(x[i], tab);
 }
 }  // namespace
 
