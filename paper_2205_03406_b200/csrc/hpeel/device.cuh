@@ -46,7 +46,7 @@ struct DevOp {
   const double* a = nullptr;   // kOpDense: n x n col-major, tree order
   double param = 1.0;          // kOpExp length scale
   int symmetric = 1;           // A == A^T: forward and adjoint share K(i, j)
-  const double* ltab = nullptr;  // fast_log table (3 x kLogTab doubles, device)
+  const double* ltab = nullptr;  // half_log table (2 x kLogTab doubles, device)
 };
 
 /// fast_log table on `device` (built once per device, never freed).
@@ -63,7 +63,7 @@ __device__ __forceinline__ double fast_rcp(double d) {
 }
 
 /// Table for half_log (built on the host in extended precision, see
-/// log_table_device): kLogTab entries each of 1/(2 T_k) and 0.5 log(T_k').
+/// log_table_device): kLogTab pairs {1/(2 T_k), 0.5 log(T_k')}, 16-byte aligned.
 constexpr int kLogTab = 1025;
 constexpr int kLogSplit = 425;  // k >= kLogSplit (T_k >= sqrt 2): reduce m / 2 against T_k / 2
 
@@ -73,27 +73,33 @@ constexpr int kLogSplit = 425;  // k >= kLogSplit (T_k >= sqrt 2): reduce m / 2 
 /// T_k = 1 + k/1024 (k in 0..1024; T = 1 is hit exactly from either side of
 /// x = 1, where the table value is 0) and v = (m / T_k - 1) / 2, |v| <= 2^-12,
 /// so 0.5 log1p(2v) is a degree-5 series (remainder < 5e-18 relative). The 1/2
-/// is folded into the table and the coefficients: 9 FP64 ops, one int->f64
-/// conversion and 2 table reads per call.
+/// is folded into the table and the coefficients; the exponent converts
+/// exactly through the 2^52 bias: 11 FP64 ops and one 16-byte table read.
 __device__ __forceinline__ double half_log(double x, const double* __restrict__ tab) {
   const int hi = __double2hiint(x);
   const int lo = __double2loint(x);
-  const int k = (((hi >> 9) & 0x7ff) + 1) >> 1;
-  const int e = ((hi >> 20) & 0x7ff) - 1023 + (k >= kLogSplit ? 1 : 0);
+  // k = round(1024 (m - 1)); e' + 1023 = biased exponent, plus one when the
+  // mantissa reaches the split (k >= kLogSplit): a carry into the exponent
+  const int k = ((hi & 0x000fffff) + 0x200) >> 10;
+  const int eb = (hi + (0x100000 - ((2 * kLogSplit - 1) << 9))) >> 20;
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
-  const double v = fma(m, tab[k], -0.5);
+  const double2 t = reinterpret_cast<const double2*>(tab)[k];
+  const double v = fma(m, t.x, -0.5);
   // 0.5 log1p(2v) = v - v^2 + 4/3 v^3 - 2 v^4 + 16/5 v^5 - ...
   double q = fma(16.0 / 5.0, v, -2.0);
   q = fma(q, v, 4.0 / 3.0);
   q = fma(q, v, -1.0);
   const double lp = fma(v * v, q, v);
-  return fma(double(e), 3.46573590279972654709e-01, tab[kLogTab + k]) + lp;
+  const double de = __hiloint2double(0x43300000, eb) - 4503599627371519.0;  // - (2^52 + 1023)
+  return fma(de, 3.46573590279972654709e-01, t.y) + lp;
 }
 
 /// K(x_i, x_j) for the on-the-fly kinds, from coordinates already in
 /// registers. `same` is true iff i == j (tree positions); `ltab` is the
-/// fast_log table (log kernels only).
-template <int KIND, int DIM>
+/// half_log table (log kernels only). CHECK = false drops the i == j and
+/// coincident-point cases, for callers that know neither occurs (K2 tiles
+/// whose row box is not in the payload, on clouds without duplicate points).
+template <int KIND, int DIM, bool CHECK = true>
 __device__ __forceinline__ double kernel_value(const double* xi, const double* xj, bool same,
                                                double param, const double* ltab) {
   double r2 = 0.0;
@@ -107,10 +113,11 @@ __device__ __forceinline__ double kernel_value(const double* xi, const double* x
     // dense assembly would (integer test: r2 >= 0); sub-normal r^2
     // (< 2.2e-308) is outside the supported range
     const double v = half_log(r2, ltab);
-    const bool zero = (__double2hiint(r2) | __double2loint(r2)) == 0;
-    return same ? 0.0 : (zero ? -INFINITY : v);
+    if (!CHECK) return v;
+    const bool zero = (__double2hiint(r2) | __double2loint(r2)) == 0;  // same => zero
+    return zero ? (same ? 0.0 : -INFINITY) : v;
   } else if (KIND == kOpInvDist4Pi) {
-    if (same) return 0.0;
+    if (CHECK && same) return 0.0;
     return rsqrt(r2) * 0.07957747154594767;  // 1 / (4 pi)
   } else {
     return exp(-sqrt(r2) / param);

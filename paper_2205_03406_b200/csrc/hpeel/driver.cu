@@ -66,6 +66,7 @@ struct LevelWork {
   std::vector<K2Row> rowtab;               // K2 rows, grouped by shard and color
   std::vector<std::vector<K2Task>> k2;     // K2 tiles per shard
   std::vector<std::int64_t> seg;           // shard q owns samples [seg[q], seg[q+1])
+  bool k2_checked = false;                 // some row box is in its own color's payload
   double evals = 0;
   bool has_peel = false;
   PeelPlan peel;
@@ -127,6 +128,15 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
     const std::int64_t nnz = w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])];
     pair_work[p] = double(e.count(ld.pairs[p].first)) * double(nnz);
     w.evals += pair_work[p];
+  }
+  {
+    // a valid H1 coloring never puts a row box into the payload serving it;
+    // if it did, K2 would have to test i == j
+    std::set<std::pair<int, int>> box_color;
+    for (int c = 0; c < w.nc; ++c)
+      for (int box : color_boxes[size_t(c)]) box_color.insert({box, c});
+    for (size_t p = 0; p < np; ++p)
+      if (box_color.count({ld.pairs[p].first, w.pcolor[p]})) w.k2_checked = true;
   }
   const auto bounds = partition_ranges(pair_work, world);
   w.seg.resize(size_t(world) + 1);
@@ -403,6 +413,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       launch_permute_rows(g.get(), gld, 1, d_pay_pos.get(), nnz, gld, gcol.get(), gld, 1, s);
       if (op.kind() != kOpDense)
         launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
+      const bool checked = w.k2_checked || e.has_dups;
       for (int sr = 0; sr < int(w.k2.size()); ++sr) {
         if (my_rank >= 0 && sr != my_rank) continue;
         const auto& tl = w.k2[size_t(sr)];
@@ -412,12 +423,14 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         if (op.symmetric()) {
           launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
                               d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
-                              samples.get(), 0, s);
+                              samples.get(), 0, checked, s);
         } else {
           launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
-                              d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0, s);
+                              d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0,
+                              checked, s);
           launch_sample_apply(e.dop, true, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
-                              d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r, s);
+                              d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r,
+                              checked, s);
         }
       }
       if (config.comm) config.comm->broadcast_segments(samples.get(), seg, s);

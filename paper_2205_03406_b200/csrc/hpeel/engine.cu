@@ -41,7 +41,30 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
       cur = tree.box(cur).parent;
     }
   }
+  int* h_flag = nullptr;
+  DevBuf<int> d_flag;
+  if (op.kind() != kOpDense) {
+    // coincident points can only share a leaf
+    std::vector<std::int64_t> ls, lc;
+    for (const Box& b : tree.boxes())
+      if (b.is_leaf() && lay.count[size_t(b.id)] > 1) {
+        ls.push_back(lay.start[size_t(b.id)]);
+        lc.push_back(lay.count[size_t(b.id)]);
+      }
+    DevBuf<std::int64_t> d_ls, d_lc;
+    d_ls.upload(ls, s);
+    d_lc.upload(lc, s);
+    d_flag.alloc(1, s);
+    HP_CUDA(cudaMemsetAsync(d_flag.get(), 0, sizeof(int), s));
+    launch_find_duplicates(xt.get(), op.dim(), n, d_ls.get(), d_lc.get(), int(ls.size()), d_flag.get(), s);
+    HP_CUDA(cudaMallocHost(&h_flag, sizeof(int)));
+    HP_CUDA(cudaMemcpyAsync(h_flag, d_flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  }
   HP_CUDA(cudaStreamSynchronize(s));
+  if (h_flag) {
+    has_dups = *h_flag != 0;
+    cudaFreeHost(h_flag);
+  }
 }
 
 int pair_index(const std::vector<std::pair<int, int>>& pairs, int a, int b) {

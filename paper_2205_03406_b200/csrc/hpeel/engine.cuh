@@ -93,6 +93,7 @@ struct Engine {
   DevBuf<double> at;  // tree-order dense matrix
   DevOp dop;
   DevBuf<std::int64_t> d_box_start, d_box_count;
+  bool has_dups = false;  // kernel kinds: two distinct points share coordinates
   std::vector<std::vector<int>> anc;  // anc[l][box] = ancestor at level l (or -1)
 
   Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l, const DeviceOperator& o,

@@ -83,6 +83,33 @@ std::int64_t& launch_counter() {
 #include <vector>
 
 namespace hpeel {
+namespace {
+__global__ void find_duplicates_kernel(const double* __restrict__ x, int dim, std::int64_t n,
+                                       const std::int64_t* __restrict__ leaf_start,
+                                       const std::int64_t* __restrict__ leaf_count, int* flag) {
+  const std::int64_t s0 = leaf_start[blockIdx.x];
+  const int m = int(leaf_count[blockIdx.x]);
+  const std::int64_t pairs = std::int64_t(m) * (m - 1) / 2;
+  for (std::int64_t q = threadIdx.x; q < pairs; q += blockDim.x) {
+    // q -> (i, j), i < j
+    int i = int((sqrt(8.0 * double(q) + 1.0) - 1.0) / 2.0) + 1;
+    while (std::int64_t(i) * (i - 1) / 2 > q) --i;
+    while (std::int64_t(i + 1) * i / 2 <= q) ++i;
+    const int j = int(q - std::int64_t(i) * (i - 1) / 2);
+    bool eq = true;
+    for (int d = 0; d < dim; ++d) eq = eq && x[d * n + s0 + i] == x[d * n + s0 + j];
+    if (eq) atomicOr(flag, 1);
+  }
+}
+}  // namespace
+
+void launch_find_duplicates(const double* x, int dim, std::int64_t n, const std::int64_t* leaf_start,
+                            const std::int64_t* leaf_count, int nleaves, int* flag, cudaStream_t s) {
+  if (nleaves == 0) return;
+  find_duplicates_kernel<<<nleaves, 256, 0, s>>>(x, dim, n, leaf_start, leaf_count, flag);
+  HP_LAUNCHED();
+}
+
 const double* log_table_device(int device) {
   static std::mutex mu;
   static std::map<int, double*> tabs;
@@ -90,15 +117,15 @@ const double* log_table_device(int device) {
   auto it = tabs.find(device);
   if (it != tabs.end()) return it->second;
   // T_k = 1 / inv_k exactly (inv_k = 1 / (1 + k/1024) rounded); stored:
-  // inv_k / 2, and 0.5 log T_k' in extended precision, where T_k' = T_k
+  // pairs {inv_k / 2, 0.5 log T_k'} (extended precision), where T_k' = T_k
   // below kLogSplit and T_k / 2 from it on (device.cuh half_log)
   std::vector<double> h(2 * kLogTab);
   for (int k = 0; k < kLogTab; ++k) {
     const double inv = double(1.0L / (1.0L + (long double)k / 1024.0L));
     long double t = 1.0L / (long double)inv;
     if (k >= kLogSplit) t /= 2.0L;
-    h[size_t(k)] = inv / 2.0;
-    h[size_t(kLogTab + k)] = double(0.5L * logl(t));
+    h[size_t(2 * k)] = inv / 2.0;
+    h[size_t(2 * k + 1)] = double(0.5L * logl(t));
   }
   int prev = 0;
   HP_CUDA(cudaGetDevice(&prev));

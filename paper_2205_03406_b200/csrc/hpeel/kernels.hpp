@@ -51,13 +51,30 @@ struct K2Task {
 /// color, stored in color order: pc = tree positions, gc = payload rows,
 /// xc = coordinates (dim x nnz). `trans` applies K^T (adjoint of a
 /// non-symmetric dense operator).
+/// `checked` = false promises that no tile row coincides with a payload row
+/// (position or coordinates), so the evaluation skips those tests.
 /// Rows per K2 CTA for an apply of `ncols` payload columns; K2Task.rows must
 /// not exceed it.
 int k2_tile_rows(int ncols);
 void launch_sample_apply(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab,
                          int ntasks, const std::int64_t* pay_off, const int* pc, const double* gc,
                          int gld, int gcol0, int ncols, const double* xc, std::int64_t nnz,
-                         double* out, int ocol0, cudaStream_t s);
+                         double* out, int ocol0, bool checked, cudaStream_t s);
+
+/// Fused K2 variant (k_apply3.cu): every warp evaluates its own DMMA A
+/// fragments; rows per CTA kFusedRows, sample width 2r <= 88. Selected by
+/// k2 mode bit 2 (hp_debug_set_k2_mode) while it is being evaluated.
+constexpr int kFusedRows = 128;
+void launch_sample_apply_fused(const DevOp& op, bool trans, const K2Task* tasks,
+                               const K2Row* rowtab, int ntasks, const std::int64_t* pay_off,
+                               const int* pc, const double* gc, int gld, int gcol0, int ncols,
+                               const double* xc, std::int64_t nnz, double* out, int ocol0,
+                               cudaStream_t s);
+
+/// flag |= 1 if two distinct points of one leaf (tree-order ranges
+/// [leaf_start, +leaf_count)) have identical coordinates (x: dim x n SoA).
+void launch_find_duplicates(const double* x, int dim, std::int64_t n, const std::int64_t* leaf_start,
+                            const std::int64_t* leaf_count, int nleaves, int* flag, cudaStream_t s);
 
 /// Leaf-phase identity probes (proj/src/coloring.cpp:271-277):
 /// out[task.out + i + t * ld] = sum_{v in color} K(row0+i, start_v + t), t < |v|,
