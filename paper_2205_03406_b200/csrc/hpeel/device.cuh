@@ -64,8 +64,9 @@ __device__ __forceinline__ double fast_rcp(double d) {
 
 /// Table for half_log (built on the host in extended precision, see
 /// log_table_device): kLogTab pairs {1/(2 T_k), 0.5 log(T_k')}, 16-byte aligned.
-constexpr int kLogTab = 1025;
-constexpr int kLogSplit = 425;  // k >= kLogSplit (T_k >= sqrt 2): reduce m / 2 against T_k / 2
+constexpr int kLogBits = 10;                      // T_k = 1 + k / 1024
+constexpr int kLogTab = (1 << kLogBits) + 1;
+constexpr int kLogSplit = 425;                    // first k with T_k >= sqrt 2: reduce m / 2 against T_k / 2
 
 /// 0.5 * log(x) for positive normal x, <= 2 ulp of 0.5 log x
 /// (tests/test_gpu_kernels.py checks 2 * half_log against glibc log).
@@ -78,10 +79,11 @@ constexpr int kLogSplit = 425;  // k >= kLogSplit (T_k >= sqrt 2): reduce m / 2 
 __device__ __forceinline__ double half_log(double x, const double* __restrict__ tab) {
   const int hi = __double2hiint(x);
   const int lo = __double2loint(x);
-  // k = round(1024 (m - 1)); e' + 1023 = biased exponent, plus one when the
+  // k = round(4096 (m - 1)); e' + 1023 = biased exponent, plus one when the
   // mantissa reaches the split (k >= kLogSplit): a carry into the exponent
-  const int k = ((hi & 0x000fffff) + 0x200) >> 10;
-  const int eb = (hi + (0x100000 - ((2 * kLogSplit - 1) << 9))) >> 20;
+  constexpr int kHalf = 1 << (19 - kLogBits);
+  const int k = ((hi & 0x000fffff) + kHalf) >> (20 - kLogBits);
+  const int eb = (hi + (0x100000 - ((kLogSplit << (20 - kLogBits)) - kHalf))) >> 20;
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);
   const double2 t = reinterpret_cast<const double2*>(tab)[k];
   const double v = fma(m, t.x, -0.5);

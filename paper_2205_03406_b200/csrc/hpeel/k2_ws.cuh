@@ -24,19 +24,29 @@ __host__ __device__ constexpr int smem_stride(int nt) {
   return nt * 8 + 4;
 }
 
-/// Dynamic shared memory of a K2 CTA: NK kernel tiles (kBK x (ROWS + 4)) and a
+/// Dynamic shared memory of a K2 CTA: NK kernel tiles (kBK x (ROWS + 4)), a
 /// payload ring of NK + 1 stages (chunk c + 1 streams in while chunk c is
-/// evaluated and the DMMA warps may still be NK - 1 chunks behind).
-__host__ __device__ constexpr size_t sample_smem_bytes(int nt, int rows, int nk) {
-  return size_t((nk + 1) * kBK * smem_stride(nt) + nk * kBK * (rows + 4)) * sizeof(double);
+/// evaluated and the DMMA warps may still be NK - 1 chunks behind) and,
+/// when `tab`, a shared-memory copy of the half_log table.
+__host__ __device__ constexpr size_t sample_smem_bytes(int nt, int rows, int nk, bool tab) {
+  return size_t((nk + 1) * kBK * smem_stride(nt) + nk * kBK * (rows + 4) + (tab ? 2 * kLogTab : 0)) *
+         sizeof(double);
 }
-/// Static shared memory: coordinates/positions ring and the log table.
+/// Static shared memory: coordinates/positions ring.
 __host__ __device__ constexpr size_t sample_static_bytes(int nk) {
-  return size_t(nk + 1) * kBK * (3 * 8 + 4) + 2 * kLogTab * 8;
+  return size_t(nk + 1) * kBK * (4 * 8 + 4);
 }
-/// Kernel tiles in flight: 3 when they fit the 227 KB per-CTA budget, else 2.
-__host__ __device__ constexpr int k2_ktiles(int nt, int rows) {
-  return sample_smem_bytes(nt, rows, 3) + sample_static_bytes(3) + 1024 <= 232448 ? 3 : 2;
+__host__ __device__ constexpr bool k2_fits(int nt, int rows, int nk, bool tab) {
+  return sample_smem_bytes(nt, rows, nk, tab) + sample_static_bytes(nk) + 1024 <= 232448;
+}
+/// Shared-memory plan: kernel tiles in flight (3 if they fit the 227 KB
+/// per-CTA budget, else 2) and whether the log table is staged in shared
+/// memory (log kernels; else it is read through L1). Encoded nk + 4 * tab.
+__host__ __device__ constexpr int k2_plan(int nt, int rows, bool log_kind) {
+  return (log_kind && k2_fits(nt, rows, 3, true))    ? 3 + 4
+         : (log_kind && k2_fits(nt, rows, 2, true))  ? 2 + 4
+         : k2_fits(nt, rows, 3, false)               ? 3
+                                                     : 2;
 }
 
 /// Rows per K2 CTA: 128 (8 DMMA + 8 evaluation warps, one CTA per SM) when the
@@ -65,24 +75,27 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
   constexpr int kEval = ROWS * 2;      // evaluation threads
   constexpr int kKR = ROWS + 4;        // kernel tile column stride (== 4 mod 16)
   constexpr int kBM = ROWS;
-  constexpr int NK = k2_ktiles(NT, ROWS);  // kernel tiles in flight
+  constexpr int kPlan = k2_plan(NT, ROWS, KIND == kOpLog);
+  constexpr int NK = kPlan & 3;                 // kernel tiles in flight
+  constexpr bool kTabSmem = (kPlan & 4) != 0;   // half_log table in shared memory
   constexpr int kStages = NK + 1;          // payload ring stages
   // named barriers: 1..NK tile b full, NK+1..2NK tile b empty, 2NK+1 eval warps
   constexpr int kBarFull = 1, kBarEmpty = 1 + NK, kBarEval = 1 + 2 * NK;
   extern __shared__ __align__(16) double dyn_smem[];
   double* gsm = dyn_smem;                        // [kStages][kBK * S] payload ring
   double* ksm = dyn_smem + kStages * kBK * S;    // [NK][kBK * kKR] kernel tiles
+  double* lts = ksm + NK * kBK * kKR;            // [2 * kLogTab] (kTabSmem)
+  const double* tab = kTabSmem ? lts : op.ltab;
   constexpr int DP = D == 3 ? 4 : D;  // point stride in smem (16-byte reads)
   __shared__ __align__(16) double xs[kStages][kBK][DP];
   __shared__ __align__(16) int js[kStages][kBK];
-  __shared__ __align__(16) double lts[KIND == kOpLog ? 2 * kLogTab : 1];
 
   const K2Task task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
   const K2Row* rt = rowtab + task.rbeg;
 
-  if constexpr (KIND == kOpLog) {
+  if constexpr (KIND == kOpLog && kTabSmem) {
     for (int e = tid; e < 2 * kLogTab; e += kThreads) lts[e] = op.ltab[e];
   }
   for (int e = tid; e < kStages * kBK * S; e += kThreads) gsm[e] = 0.0;
@@ -206,7 +219,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
               v[u] = TRANS ? op.a[std::int64_t(jj) + std::int64_t(ipos) * n]
                            : op.a[std::int64_t(ipos) + std::int64_t(jj) * n];
             } else {
-              v[u] = kernel_value<KIND, DIM, C>(xi, xj[u], C && ipos == jp[u], op.param, lts);
+              v[u] = kernel_value<KIND, DIM, C>(xi, xj[u], C && ipos == jp[u], op.param, tab);
             }
           }
 #pragma unroll
@@ -275,7 +288,8 @@ template <int NT, int KIND, int DIM, int R>
 void launch_rows(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* rowtab, int ntasks,
                  const std::int64_t* pay_off, const int* pc, const double* gc, int gld, int gcol0,
                  int ncols, const double* xc, std::int64_t nnz, double* out, int ocol0, int flags, cudaStream_t s) {
-  constexpr size_t smem = sample_smem_bytes(NT, R, k2_ktiles(NT, R));
+  constexpr int plan = k2_plan(NT, R, KIND == kOpLog);
+  constexpr size_t smem = sample_smem_bytes(NT, R, plan & 3, (plan & 4) != 0);
   if (KIND == kOpDense && trans) {
     auto* fn = sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense, R>;
     HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

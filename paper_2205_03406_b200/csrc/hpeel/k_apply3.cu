@@ -43,16 +43,13 @@ fused_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __re
   extern __shared__ __align__(16) double gsm[];  // [kFStages][kFK * S] payload ring
   __shared__ __align__(16) double xs[kFStages][D][kFK];
   __shared__ __align__(16) int js[kFStages][kFK];
-  __shared__ __align__(16) double lts[KIND == kOpLog ? 2 * kLogTab : 1];
+  const double* lts = op.ltab;  // half_log table read through L1
 
   const K2Task task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
   const K2Row* rt = rowtab + task.rbeg;
 
-  if constexpr (KIND == kOpLog) {
-    for (int e = tid; e < 2 * kLogTab; e += kThreads) lts[e] = op.ltab[e];
-  }
   for (int e = tid; e < kFStages * kFK * S; e += kThreads) gsm[e] = 0.0;
   for (int e = tid; e < kFStages * kFK; e += kThreads) {
     (&js[0][0])[e] = -1;

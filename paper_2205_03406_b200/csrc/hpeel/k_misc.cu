@@ -116,12 +116,12 @@ const double* log_table_device(int device) {
   std::lock_guard<std::mutex> lock(mu);
   auto it = tabs.find(device);
   if (it != tabs.end()) return it->second;
-  // T_k = 1 / inv_k exactly (inv_k = 1 / (1 + k/1024) rounded); stored:
+  // T_k = 1 / inv_k exactly (inv_k = 1 / (1 + k/2^kLogBits) rounded); stored:
   // pairs {inv_k / 2, 0.5 log T_k'} (extended precision), where T_k' = T_k
   // below kLogSplit and T_k / 2 from it on (device.cuh half_log)
   std::vector<double> h(2 * kLogTab);
   for (int k = 0; k < kLogTab; ++k) {
-    const double inv = double(1.0L / (1.0L + (long double)k / 1024.0L));
+    const double inv = double(1.0L / (1.0L + (long double)k / (long double)(1 << kLogBits)));
     long double t = 1.0L / (long double)inv;
     if (k >= kLogSplit) t /= 2.0L;
     h[size_t(2 * k)] = inv / 2.0;
