@@ -304,7 +304,8 @@ def run_ours(args, ws, rank, local):
     if rank != 0:
         return
     phases = [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in ph.items()
-               if k in ("phase", "level", "colors", "apply_ms", "peel_ms", "qr_ms", "bsolve_ms", "wall_ms_total")}
+               if k in ("phase", "level", "colors", "apply_ms", "peel_ms", "qr_ms", "bsolve_ms", "wall_ms_total",
+                        "host_wait_ms")}
               for ph in report["phases"]]
     line = {
         "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": args.gpus,
@@ -318,7 +319,8 @@ def run_ours(args, ws, rank, local):
         "clocks": clk.summary(),
         "report": {"forward_cols": report["forward_cols"], "adjoint_cols": report["adjoint_cols"],
                    "max_sampling_colors": report["max_sampling_colors"], "net_flops": report["net_flops"],
-                   "wall_s_net": round(report["wall_s_net"], 4), "phases": phases},
+                   "wall_s_net": round(report["wall_s_net"], 4), "setup_ms": round(report["setup_ms"], 1),
+                   "phases": phases},
         "storage_doubles": last.storage()["total"],
     }
     print(json.dumps(line), flush=True)

@@ -141,12 +141,12 @@ int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversampl
                    hp_rep** out);
 /* the work partition every rank computes: world + 1 boundaries */
 int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bounds);
-/* totals[0..5] = forward_cols, adjoint_cols, max_sampling_colors,
- * wall_s_total, wall_s_net, net_flops; *nphases = phase count */
+/* totals[0..6] = forward_cols, adjoint_cols, max_sampling_colors,
+ * wall_s_total, wall_s_net, net_flops, setup_ms; *nphases = phase count */
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases);
 /* per phase: is_leaf, level, colors, forward_cols, adjoint_cols, net_flops and
- * times[8] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
- * apply_flops, kernel_evals */
+ * times[9] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
+ * apply_flops, kernel_evals, host_wait_ms */
 int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times);
 /* RunReport::to_csv (proj/src/peeling.cpp:478-488) */
 int hp_rep_csv(const hp_rep* rep, char* buf, int64_t cap, int64_t* len);

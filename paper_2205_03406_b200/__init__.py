@@ -334,7 +334,7 @@ class CompressedRep:
         self.rank = rank
         self.width = rank + oversample
         self.format = "h1"
-        totals = np.zeros(6)
+        totals = np.zeros(7)
         nph = C.c_int64(0)
         check(lib().hp_rep_report(self._h, dptr(totals), C.byref(nph)))
         ln = C.c_int64(0)
@@ -344,19 +344,20 @@ class CompressedRep:
         phases = []
         for i in range(nph.value):
             ints = np.zeros(6, dtype=np.int64)
-            times = np.zeros(8)
+            times = np.zeros(9)
             check(lib().hp_rep_phase(self._h, i, lptr(ints), dptr(times)))
             phases.append({
                 "phase": "leaf" if ints[0] else "h1", "level": int(ints[1]), "colors": int(ints[2]),
                 "forward_cols": int(ints[3]), "adjoint_cols": int(ints[4]), "net_flops": int(ints[5]),
                 "wall_ms_total": times[0], "wall_ms_net": times[1], "apply_ms": times[2],
                 "peel_ms": times[3], "qr_ms": times[4], "bsolve_ms": times[5],
-                "apply_flops": times[6], "kernel_evals": times[7],
+                "apply_flops": times[6], "kernel_evals": times[7], "host_wait_ms": times[8],
             })
         self.report = {
             "forward_cols": int(totals[0]), "adjoint_cols": int(totals[1]),
             "max_sampling_colors": int(totals[2]), "wall_s_total": totals[3],
-            "wall_s_net": totals[4], "net_flops": int(totals[5]), "csv": buf.value.decode(),
+            "wall_s_net": totals[4], "net_flops": int(totals[5]), "setup_ms": totals[6],
+            "csv": buf.value.decode(),
             "phases": phases,
         }
 

@@ -494,6 +494,7 @@ int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases) {
       totals[3] = r.wall_s_total;
       totals[4] = r.wall_s_net;
       totals[5] = double(r.net_flops);
+      totals[6] = r.setup_ms;
     }
     if (nphases) *nphases = int64_t(r.phases.size());
   });
@@ -520,6 +521,7 @@ int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times)
       times[5] = ph.bsolve_ms;
       times[6] = ph.apply_flops;
       times[7] = ph.kernel_evals;
+      times[8] = ph.host_wait_ms;
     }
   });
 }

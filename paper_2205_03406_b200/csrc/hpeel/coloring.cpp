@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <queue>
 #include <stdexcept>
 #include <thread>
@@ -398,15 +401,30 @@ std::vector<BlockTestMatrix> assemble_test_matrices(const std::vector<Constraint
 SamplingPlan make_plan(const BoxTree& tree, const AdjacencyInfo& adj, int level, SampleMode mode,
                        int width, std::uint64_t seed, int phase) {
   SamplingPlan plan;
+  static const bool timing = std::getenv("HP_PLAN_TIMING") != nullptr;
+  using Clock = std::chrono::steady_clock;
+  auto t0 = Clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = Clock::now();
+    std::fprintf(stderr, "[plan l=%d mode=%d] %s %.1f ms\n", level, int(mode), what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   const auto sets = build_constraints(tree, adj, level, mode);
+  lap("constraints");
   if (sets.empty()) return plan;
   const auto graph = build_graph(sets);
+  lap("graph");
   const auto coloring = plan_coloring(tree, sets, graph, mode);
+  lap("coloring");
   plan.n_vertices = sets.size();
   plan.n_edges = graph.num_edges();
   plan.matrices = assemble_test_matrices(sets, coloring, tree, level, width, seed, phase);
+  lap("matrices");
   for (size_t i = 0; i < sets.size(); ++i)
     for (const auto& owner : sets[i].owners) plan.block_to_matrix[owner] = coloring.color[i];
+  lap("block map");
   return plan;
 }
 

@@ -15,6 +15,8 @@
 #include <chrono>
 #include <future>
 #include <memory>
+#include <cstdio>
+#include <cstdlib>
 #include <set>
 #include <sstream>
 #include <stdexcept>
@@ -87,7 +89,17 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
   }
   if (!w.symmetric) return w;
   const int r = e.r, k = e.k;
+  static const bool timing = std::getenv("HP_PLAN_TIMING") != nullptr;
+  auto t0 = Clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = Clock::now();
+    std::fprintf(stderr, "[build_level %d] %s %.1f ms\n", l, what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   const SamplingPlan plan = make_plan(e.tree, e.adj, l, SampleMode::kH1, r, cfg.seed, kForwardPhase);
+  lap("make_plan");
   w.nc = plan.colors();
   std::vector<std::vector<int>> color_boxes(size_t(w.nc));
   w.pay_off.assign(size_t(w.nc) + 1, 0);
@@ -150,16 +162,21 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
       by_color[size_t(w.pcolor[size_t(p)])].push_back(int(p));
     auto& tl = w.k2[size_t(q)];
     for (int c = 0; c < w.nc; ++c) {
+      // whole tiles of big boxes run in place; their remainders and the small
+      // boxes are packed through the row table
       const std::int64_t first = std::int64_t(w.rowtab.size());
       for (int p : by_color[size_t(c)]) {
         const int a = ld.pairs[size_t(p)].first;
         const int rows = e.count(a);
-        for (int i = 0; i < rows; ++i)
+        const int full = rows / tile * tile;
+        for (int t0 = 0; t0 < full; t0 += tile)
+          tl.push_back(K2Task{w.soff[size_t(p)] + t0, tile, c, rows, int(e.start(a) + t0)});
+        for (int i = full; i < rows; ++i)
           w.rowtab.push_back(K2Row{w.soff[size_t(p)] + i, int(e.start(a) + i), rows});
       }
       const std::int64_t last = std::int64_t(w.rowtab.size());
       for (std::int64_t t0 = first; t0 < last; t0 += tile)
-        tl.push_back(K2Task{t0, int(std::min<std::int64_t>(tile, last - t0)), c});
+        tl.push_back(K2Task{t0, int(std::min<std::int64_t>(tile, last - t0)), c, 0, 0});
     }
     std::stable_sort(tl.begin(), tl.end(), [&](const K2Task& x, const K2Task& y) {
       return w.pay_off[size_t(x.color) + 1] - w.pay_off[size_t(x.color)] >
@@ -170,7 +187,9 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
   if (l - 1 >= 2) {
     std::vector<SampleBlock> blocks(np);
     for (size_t p = 0; p < np; ++p) blocks[p] = SampleBlock{ld.pairs[p].first, w.pcolor[p], w.soff[p]};
+    lap("k2 tasks");
     w.peel = plan_peel(e, rep, blocks, color_boxes, l - 1, r, true);
+    lap("plan_peel");
     w.has_peel = true;
   }
   // K5a middle = G'_a^T Y_p; K4 QR; K5b grams
@@ -188,10 +207,13 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
     qr.push_back(QrRequest{w.soff[p] + std::int64_t(rows) * r, ld.voff[size_t(w.swap[p])], rows, rows,
                            int(np + size_t(w.swap[p]))});
   }
+  lap("pre-gram");
   w.g_mid = plan_gram(mid, r, r);
   w.g_gpu = plan_gram(gu, r, k);
   w.g_vg = plan_gram(vg, k, r);
+  lap("grams");
   w.qr = plan_qr(qr, r, k);
+  lap("plan_qr");
   return w;
 }
 
@@ -310,6 +332,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
 
   try {
     Engine e(*tree, *adj, *lay, op, s);
+    StagingScope staging(s);  // uploads below stay asynchronous
     e.r = r;
     e.k = k;
     const Index n = tree->num_points();
@@ -375,8 +398,23 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     std::int64_t roff = 0;
     int built = 1;
 
+    std::vector<double> wait_ms(size_t(tree->depth()) + 1, 0.0);
+    report.setup_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_begin).count();
     for (int l = 2; l <= tree->depth(); ++l) {
+      const auto t_wait = Clock::now();
       LevelWork w = futs[size_t(l)].get();
+      const auto t_got = Clock::now();
+      wait_ms[size_t(l)] = std::chrono::duration<double, std::milli>(t_got - t_wait).count();
+      struct IterTimer {  // HP_DRIVER_TIMING: host time spent issuing this level
+        int level;
+        Clock::time_point t0;
+        ~IterTimer() {
+          static const bool on = std::getenv("HP_DRIVER_TIMING") != nullptr;
+          if (on)
+            std::fprintf(stderr, "[driver] level %d issue %.1f ms\n", level,
+                         std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
+        }
+      } iter_timer{l, t_got};
       if (w.empty) continue;  // proj/src/peeling.cpp:221 (built_level not advanced)
       if (!w.symmetric) throw std::logic_error("asymmetric admissibility structure");
       if (l - 1 >= 2 && l - 1 > built)
@@ -485,11 +523,13 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     rep->built_level = tree->depth();
 
     // ------------------------------------------------------------- leaf phase
+    const auto t_leaf_wait = Clock::now();
     LeafWork lw = leaf_fut.get();
+    const double leaf_wait_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_leaf_wait).count();
     rep->dense.pairs = lw.pairs;
     rep->dense.off = lw.off;
     rep->dense_doubles = lw.total;
-    HP_CUDA(cudaMalloc(&rep->d_dense, size_t(std::max<std::int64_t>(lw.total, 1)) * 8));
+    HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_dense), size_t(std::max<std::int64_t>(lw.total, 1)) * 8, s));
     Events leaf_apply, leaf_peel;
     {
       std::vector<double> dwork(lw.pairs.size());
@@ -571,6 +611,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       ph.bsolve_ms = tm->bsolve.ms() + tm->mid.ms();
       ph.wall_ms_total = ph.apply_ms + ph.peel_ms + ph.qr_ms + ph.bsolve_ms;
       ph.wall_ms_net = ph.wall_ms_total - ph.apply_ms;
+      ph.host_wait_ms = wait_ms[size_t(l)];
       blackbox_ms += ph.apply_ms;
       if (l - 1 >= 2) ph.net_flops += 2 * std::int64_t(ph.colors) * truncated_apply_flops(*rep, l - 1, r, e);
       // QR (flops.hpp:18-20) and the B solve (peeling.cpp:262-268)
@@ -596,6 +637,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       ph.peel_ms = leaf_peel.ms();
       ph.wall_ms_total = ph.apply_ms + ph.peel_ms;
       ph.wall_ms_net = ph.peel_ms;
+      ph.host_wait_ms = leaf_wait_ms;
       blackbox_ms += ph.apply_ms;
       if (tree->depth() >= 2) ph.net_flops += std::int64_t(lw.nc) * truncated_apply_flops(*rep, tree->depth(), lw.w, e);
       report.phases.push_back(ph);

@@ -1,11 +1,60 @@
 // Engine and batched task builders (see engine.cuh).
 #include "engine.cuh"
 
+#include <mutex>
+
 #include <algorithm>
 #include <limits>
 #include <unordered_map>
 
 namespace hpeel::detail {
+
+namespace {
+std::mutex& pool_mutex() {
+  static std::mutex m;
+  return m;
+}
+std::vector<std::pair<char*, size_t>>& pool() {
+  static std::vector<std::pair<char*, size_t>> p;
+  return p;
+}
+}  // namespace
+
+PinnedStaging*& PinnedStaging::current() {
+  thread_local PinnedStaging* cur = nullptr;
+  return cur;
+}
+
+void* PinnedStaging::take(size_t bytes) {
+  bytes = (bytes + 255) / 256 * 256;
+  for (Chunk& c : chunks_)
+    if (c.size - c.used >= bytes) {
+      void* p = c.p + c.used;
+      c.used += bytes;
+      return p;
+    }
+  {
+    std::lock_guard<std::mutex> lock(pool_mutex());
+    auto& pl = pool();
+    for (size_t i = 0; i < pl.size(); ++i)
+      if (pl[i].second >= bytes) {
+        chunks_.push_back({pl[i].first, pl[i].second, bytes});
+        pl.erase(pl.begin() + std::ptrdiff_t(i));
+        return chunks_.back().p;
+      }
+  }
+  const size_t size = std::max<size_t>(bytes, size_t(64) << 20);
+  char* p = nullptr;
+  HP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), size));
+  chunks_.push_back({p, size, bytes});
+  return p;
+}
+
+void PinnedStaging::release_to_pool() {
+  std::lock_guard<std::mutex> lock(pool_mutex());
+  for (const Chunk& c : chunks_) pool().push_back({c.p, c.size});
+  chunks_.clear();
+}
 
 Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
                const DeviceOperator& o, cudaStream_t st)

@@ -7,12 +7,52 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "kernels.hpp"
 #include "peeling.hpp"
 
 namespace hpeel::detail {
+
+/// Pinned staging for host->device uploads (DevBuf::upload) inside a
+/// StagingScope: a pageable cudaMemcpyAsync waits for the stream to drain,
+/// which would tie the driver thread to the device and serialize host
+/// planning with device work. Chunks come from a process-wide pool and go
+/// back to it when the scope ends (after synchronizing its stream).
+class PinnedStaging {
+ public:
+  static PinnedStaging*& current();
+  void* take(size_t bytes);
+  void release_to_pool();
+
+ private:
+  struct Chunk {
+    char* p;
+    size_t size;
+    size_t used;
+  };
+  std::vector<Chunk> chunks_;
+};
+
+class StagingScope {
+ public:
+  explicit StagingScope(cudaStream_t s) : s_(s), prev_(PinnedStaging::current()) {
+    PinnedStaging::current() = &staging_;
+  }
+  ~StagingScope() {
+    cudaStreamSynchronize(s_);
+    PinnedStaging::current() = prev_;
+    staging_.release_to_pool();
+  }
+  StagingScope(const StagingScope&) = delete;
+  StagingScope& operator=(const StagingScope&) = delete;
+
+ private:
+  cudaStream_t s_;
+  PinnedStaging* prev_;
+  PinnedStaging staging_;
+};
 
 template <class T>
 class DevBuf {
@@ -31,8 +71,15 @@ class DevBuf {
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     alloc(v.size(), s);
-    if (!v.empty())
-      HP_CUDA(cudaMemcpyAsync(p_, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (v.empty()) return;
+    const size_t bytes = v.size() * sizeof(T);
+    if (PinnedStaging* st = PinnedStaging::current()) {
+      void* h = st->take(bytes);
+      std::memcpy(h, v.data(), bytes);
+      HP_CUDA(cudaMemcpyAsync(p_, h, bytes, cudaMemcpyHostToDevice, s));
+    } else {
+      HP_CUDA(cudaMemcpyAsync(p_, v.data(), bytes, cudaMemcpyHostToDevice, s));
+    }
   }
   void release() {
     if (p_) cudaFreeAsync(p_, s_);

@@ -93,14 +93,13 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
   const K2Task task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
-  const K2Row* rt = rowtab + task.rbeg;
 
   if constexpr (KIND == kOpLog && kTabSmem) {
     for (int e = tid; e < 2 * kLogTab; e += kThreads) lts[e] = op.ltab[e];
   }
   for (int e = tid; e < kStages * kBK * S; e += kThreads) gsm[e] = 0.0;
   for (int e = tid; e < kStages * kBK; e += kThreads) {
-    (&js[0][0])[e] = rt[0].pos;
+    (&js[0][0])[e] = k2_row(task, rowtab, 0).pos;
     for (int d = 0; d < DP; ++d) xs[e / kBK][e % kBK][d] = 0.0;
   }
   __syncthreads();
@@ -112,7 +111,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
     // ------------------------------------------------ evaluation warps
     const int et = tid - kEval;
     const int row = et & (kBM - 1), cgrp = et / kBM;
-    const int ipos = rt[row < task.rows ? row : task.rows - 1].pos;
+    const int ipos = k2_row(task, rowtab, row < task.rows ? row : task.rows - 1).pos;
     double xi[D];
     if constexpr (KIND != kOpDense) {
 #pragma unroll
@@ -272,7 +271,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
   for (int m = 0; m < 2; ++m) {
     const int rr = warp * 16 + m * 8 + (lane >> 2);
     if (rr >= task.rows) continue;
-    const K2Row dst = rt[rr];
+    const K2Row dst = k2_row(task, rowtab, rr);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll

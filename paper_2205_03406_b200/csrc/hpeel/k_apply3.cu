@@ -48,7 +48,6 @@ fused_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __re
   const K2Task task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const std::int64_t n = op.n;
-  const K2Row* rt = rowtab + task.rbeg;
 
   for (int e = tid; e < kFStages * kFK * S; e += kThreads) gsm[e] = 0.0;
   for (int e = tid; e < kFStages * kFK; e += kThreads) {
@@ -58,8 +57,8 @@ fused_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __re
 
   // this lane's two A rows and their points
   const int r0 = warp * 16 + (lane >> 2), r1 = r0 + 8;
-  const int ip0 = rt[r0 < task.rows ? r0 : task.rows - 1].pos;
-  const int ip1 = rt[r1 < task.rows ? r1 : task.rows - 1].pos;
+  const int ip0 = k2_row(task, rowtab, r0 < task.rows ? r0 : task.rows - 1).pos;
+  const int ip1 = k2_row(task, rowtab, r1 < task.rows ? r1 : task.rows - 1).pos;
   double xi0[D], xi1[D];
   if constexpr (KIND != kOpDense) {
 #pragma unroll
@@ -165,7 +164,7 @@ fused_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __re
   for (int m = 0; m < 2; ++m) {
     const int rr = warp * 16 + m * 8 + (lane >> 2);
     if (rr >= task.rows) continue;
-    const K2Row dst = rt[rr];
+    const K2Row dst = k2_row(task, rowtab, rr);
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll

@@ -37,15 +37,22 @@ struct K2Row {
   int pos;
   int ld;
 };
-/// One K2 CTA: rows [rbeg, rbeg + rows) of the row table, all served by the
-/// payload of `color` (rows of several target boxes of the same color are
-/// packed into one tile).
+/// One K2 CTA: `rows` output rows all served by the payload of `color`.
+/// ld > 0: one tile of a single box, row i = tree position pos + i written at
+/// base + i with column stride ld. ld == 0: rows rowtab[base + i] (rows of
+/// several small target boxes of the same color packed into one tile).
 struct K2Task {
-  std::int64_t rbeg;
+  std::int64_t base;
   int rows;
   int color;
+  int ld;
+  int pos;
 };
-/// For each task row R = rowtab[rbeg + i]:
+__host__ __device__ inline K2Row k2_row(const K2Task& t, const K2Row* rowtab, int i) {
+  if (t.ld > 0) return K2Row{t.base + i, t.pos + i, t.ld};
+  return rowtab[t.base + i];
+}
+/// For each task row R = k2_row(task, rowtab, i):
 /// out[R.out + (ocol0 + c) * R.ld] = sum_q K(R.pos, pc[q]) gc[q * gld + gcol0 + c]
 /// over the payload rows q in [pay_off[color], pay_off[color+1]) of the task's
 /// color, stored in color order: pc = tree positions, gc = payload rows,

@@ -61,6 +61,7 @@ struct PhaseReport {
   double apply_flops = 0.0;      // FMAs*2 executed by K2 on needed rows
   double peel_flops = 0.0;       // FMAs*2 executed by K3 (coefficients + subtraction)
   double kernel_evals = 0.0;
+  double host_wait_ms = 0.0;      // driver thread blocked on this phase's host plan
 };
 
 struct RunReport {
@@ -71,6 +72,7 @@ struct RunReport {
   double wall_s_total = 0.0;
   double wall_s_net = 0.0;
   std::int64_t net_flops = 0;
+  double setup_ms = 0.0;  // adjacency, layout, device operator staging, plan launch
   std::string to_csv() const;  // proj/src/peeling.cpp:478-488 columns
 };
 
