@@ -176,6 +176,12 @@ int hp_rel_error_power_method(const hp_rep* rep, const hp_op* op, int iters, uin
  *      (columns [0, r) phase 0, [r, 2r) phase 1; rows not in a level box = 0). */
 int hp_debug_payload(const hp_tree* tree, int level, int r, uint64_t seed, int device,
                      double* out);
+/* K4 probe: the batched range finder on nb blocks stacked column-major (block
+ * i is rows[i] x cols); q gets Q(:, :kmax) of each block stacked the same way
+ * (zero columns beyond the kept rank), ranks the kept ranks, *ms the device
+ * time of the QR stage. */
+int hp_debug_qr(const double* blocks, const int* rows, int nb, int cols, int kmax, int device,
+                double* q, int* ranks, double* ms);
 /* device natural log used by the log-kernel black box, for accuracy tests */
 int hp_debug_log(const double* x, int64_t n, int device, double* out);
 

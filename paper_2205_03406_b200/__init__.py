@@ -490,6 +490,27 @@ def debug_log(x, device: int = 0) -> np.ndarray:
     return out
 
 
+def debug_qr(blocks, kmax: int, device: int = 0):
+    """K4 probe: batched range finder (pivoted QR, keep rule, Q(:, :kmax)) of
+    equal-width blocks. Returns ([Q_i], ranks, device_ms)."""
+    blocks = [np.asarray(b, dtype=np.float64) for b in blocks]
+    if not blocks:
+        return [], np.zeros(0, dtype=np.int32), 0.0
+    cols = blocks[0].shape[1]
+    rows = np.array([b.shape[0] for b in blocks], dtype=np.int32)
+    flat = np.concatenate([np.asfortranarray(b).ravel(order="F") for b in blocks])
+    q = np.zeros(int((rows.astype(np.int64) * kmax).sum()))
+    ranks = np.zeros(len(blocks), dtype=np.int32)
+    ms = C.c_double(0.0)
+    check(lib().hp_debug_qr(dptr(flat), iptr(rows), len(blocks), cols, kmax, device, dptr(q),
+                            iptr(ranks), C.byref(ms)))
+    out, o = [], 0
+    for m in rows:
+        out.append(q[o:o + m * kmax].reshape((m, kmax), order="F"))
+        o += m * kmax
+    return out, ranks, ms.value
+
+
 def debug_payload(tree: BoxTree, level: int, r: int, seed: int, device: int = 0) -> np.ndarray:
     """K1 probe: n x 2r payload rows (input order) generated on the device."""
     out = np.zeros((tree.num_points, 2 * r), order="F")

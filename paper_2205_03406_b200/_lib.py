@@ -76,6 +76,7 @@ _SIGNATURES = {
     "hp_rep_captured": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
     "hp_rel_error_power_method": (C.c_int, [P, P, C.c_int, u64, dp]),
     "hp_debug_payload": (C.c_int, [P, C.c_int, C.c_int, u64, C.c_int, dp]),
+    "hp_debug_qr": (C.c_int, [dp, ip, C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, dp]),
     "hp_debug_log": (C.c_int, [dp, i64, C.c_int, dp]),
 }
 

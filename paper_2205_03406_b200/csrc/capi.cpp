@@ -42,6 +42,8 @@ void set_k2_mode(int mode);
 void debug_fast_log(const double* x, std::int64_t n, double* y, int device);
 Matrix debug_payload(const BoxTree& tree, const TreeLayout& lay, int level, int r,
                      std::uint64_t seed, int device);
+double debug_qr(const double* blocks, const int* rows, int nb, int cols, int kmax, int device,
+                double* q, int* ranks);
 }
 
 namespace {
@@ -652,6 +654,20 @@ int hp_debug_payload(const hp_tree* t, int level, int r, uint64_t seed, int devi
     need(out, "out");
     const Matrix m = debug_payload(*t->tree, *t->layout, level, r, seed, device);
     std::memcpy(out, m.data(), size_t(m.size()) * 8);
+  });
+}
+
+int hp_debug_qr(const double* blocks, const int* rows, int nb, int cols, int kmax, int device,
+                double* q, int* ranks, double* ms) {
+  return guard([&] {
+    need(blocks, "blocks");
+    need(rows, "rows");
+    need(q, "q");
+    need(ranks, "ranks");
+    if (nb < 0 || cols < 1 || cols > 160 || kmax < 0 || kmax > cols)
+      throw std::invalid_argument("debug_qr: bad sizes");
+    const double t = debug_qr(blocks, rows, nb, cols, kmax, device, q, ranks);
+    if (ms) *ms = t;
   });
 }
 

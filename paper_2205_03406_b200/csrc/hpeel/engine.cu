@@ -20,6 +20,20 @@ std::vector<std::pair<char*, size_t>>& pool() {
 }
 }  // namespace
 
+void retain_default_pool(int dev) {
+  static std::mutex mu;
+  static std::vector<char> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0) return;
+  if (size_t(dev) >= done.size()) done.resize(size_t(dev) + 1, 0);
+  if (done[size_t(dev)]) return;
+  cudaMemPool_t pool;
+  HP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  std::uint64_t thr = ~std::uint64_t(0);
+  HP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done[size_t(dev)] = 1;
+}
+
 PinnedStaging*& PinnedStaging::current() {
   thread_local PinnedStaging* cur = nullptr;
   return cur;
@@ -133,7 +147,12 @@ std::pair<int, int> first_range(const std::vector<std::pair<int, int>>& pairs, i
 
 QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
   QrPlan pl;
-  const int rm = qr_rows_max(r);
+  // register-resident kernels when the widths allow, else shared-memory ones
+  // (chunks must hold more than r rows or TSQR cannot shrink the stack)
+  pl.reg = qr_reg_cols(r) != 0 && qr_reg_cols(kmax) != 0 &&
+           std::min(qr_reg_rows_max(r), qr_reg_rows_max(kmax)) >= 2 * r;
+  const int rm = pl.reg ? std::min(qr_reg_rows_max(r), qr_reg_rows_max(kmax)) : qr_rows_max(r);
+  const int rc = pl.reg ? rm : qr_chunk_rows(r, kmax);  // TSQR chunk
   for (const QrRequest& q : reqs) {
     if (q.rows <= rm) {
       pl.direct.push_back(QrBlock{q.a, q.out, 0, 0, q.rows, q.rows, q.ldo, 0, q.rank_slot, 0});
@@ -145,7 +164,7 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
     std::int64_t cur_c = -1;  // Q of the current stacked matrix (workspace)
     int round = 0;
     while (cur_rows > rm) {
-      const int nch = (cur_rows + rm - 1) / rm;
+      const int nch = (cur_rows + rc - 1) / rc;
       const int base = cur_rows / nch, extra = cur_rows % nch;
       int next_rows = 0;
       for (int i = 0; i < nch; ++i) next_rows += std::min(base + (i < extra ? 1 : 0), r);
@@ -178,6 +197,7 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
         row += cr;
         srow += std::min(cr, r);
       }
+      if (next_rows >= cur_rows) throw std::logic_error("plan_qr: TSQR does not shrink");
       cur_off = stacked;
       cur_rows = next_rows;
       cur_ld = next_rows;
@@ -191,29 +211,52 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
 
 void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, int kmax,
             cudaStream_t s) {
+  auto max_rows = [](const std::vector<QrBlock>& v) {
+    int m = 1;
+    for (const QrBlock& b : v) m = std::max(m, b.rows);
+    return m;
+  };
   DevBuf<double> w(size_t(std::max<std::int64_t>(pl.wsize, 1)), s);
   DevBuf<double> tau(size_t(std::max<std::int64_t>(pl.tausize, 1)), s);
   if (!pl.direct.empty()) {
     DevBuf<QrBlock> d;
     d.upload(pl.direct, s);
-    launch_qr_top(d.get(), int(pl.direct.size()), data, out, d_ranks, r, kmax, kQrRankDropTol, s);
+    if (pl.reg)
+      launch_qr_reg(0, d.get(), int(pl.direct.size()), data, out, nullptr, d_ranks, r, kmax, kQrRankDropTol,
+                    max_rows(pl.direct), s);
+    else
+      launch_qr_top(d.get(), int(pl.direct.size()), data, out, d_ranks, r, kmax, kQrRankDropTol,
+                    max_rows(pl.direct), s);
   }
   for (size_t rd = 0; rd < pl.chunk_rounds.size(); ++rd) {
     DevBuf<QrBlock> d;
     d.upload(pl.chunk_rounds[rd], s);
-    launch_qr_chunk(d.get(), int(pl.chunk_rounds[rd].size()), rd == 0 ? data : w.get(), w.get(),
-                    tau.get(), r, s);
+    if (pl.reg)
+      launch_qr_reg(1, d.get(), int(pl.chunk_rounds[rd].size()), rd == 0 ? data : w.get(), w.get(),
+                    tau.get(), nullptr, r, kmax, 0.0, max_rows(pl.chunk_rounds[rd]), s);
+    else
+      launch_qr_chunk(d.get(), int(pl.chunk_rounds[rd].size()), rd == 0 ? data : w.get(), w.get(),
+                      tau.get(), r, max_rows(pl.chunk_rounds[rd]), s);
   }
   if (!pl.tops.empty()) {
     DevBuf<QrBlock> d;
     d.upload(pl.tops, s);
-    launch_qr_top(d.get(), int(pl.tops.size()), w.get(), w.get(), d_ranks, r, kmax, kQrRankDropTol, s);
+    if (pl.reg)
+      launch_qr_reg(0, d.get(), int(pl.tops.size()), w.get(), w.get(), nullptr, d_ranks, r, kmax,
+                    kQrRankDropTol, max_rows(pl.tops), s);
+    else
+      launch_qr_top(d.get(), int(pl.tops.size()), w.get(), w.get(), d_ranks, r, kmax, kQrRankDropTol,
+                    max_rows(pl.tops), s);
   }
   for (size_t rd = pl.back_rounds.size(); rd-- > 0;) {
     DevBuf<QrBlock> d;
     d.upload(pl.back_rounds[rd], s);
-    launch_qr_backprop(d.get(), int(pl.back_rounds[rd].size()), rd == 0 ? data : w.get(), tau.get(),
-                       w.get(), rd == 0 ? out : w.get(), r, kmax, s);
+    if (pl.reg)
+      launch_qr_reg_backprop(d.get(), int(pl.back_rounds[rd].size()), rd == 0 ? data : w.get(), tau.get(),
+                             w.get(), rd == 0 ? out : w.get(), r, kmax, max_rows(pl.back_rounds[rd]), s);
+    else
+      launch_qr_backprop(d.get(), int(pl.back_rounds[rd].size()), rd == 0 ? data : w.get(), tau.get(),
+                         w.get(), rd == 0 ? out : w.get(), r, kmax, max_rows(pl.back_rounds[rd]), s);
   }
 }
 

@@ -113,11 +113,17 @@ struct Events {
   }
 };
 
+/// Keep the device's default stream-ordered pool across synchronizations
+/// (release threshold = max), so repeated compress() calls reuse its memory
+/// instead of remapping it every time. Once per device.
+void retain_default_pool(int dev);
+
 class DeviceGuard {
  public:
   explicit DeviceGuard(int dev) {
     HP_CUDA(cudaGetDevice(&prev_));
     if (prev_ != dev) HP_CUDA(cudaSetDevice(dev));
+    retain_default_pool(dev);
   }
   ~DeviceGuard() { cudaSetDevice(prev_); }
 
@@ -164,6 +170,7 @@ struct QrPlan {
   std::vector<QrBlock> direct, tops;
   std::vector<std::vector<QrBlock>> chunk_rounds, back_rounds;
   std::int64_t wsize = 0, tausize = 0;
+  bool reg = false;  // register-resident kernels (k_qr2.cu)
 };
 QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax);
 void run_qr(const QrPlan& plan, double* data, double* out, int* d_ranks, int r, int kmax,

@@ -146,23 +146,39 @@ struct QrBlock {
   int rank_slot;     // top: index into ranks (or -1)
   int pad;
 };
+/// Rows of a block that the pivoted single-CTA QR (qr_top) holds in shared memory.
 int qr_rows_max(int cols);
+/// Rows per TSQR chunk (the back-propagation also stages kmax Q columns).
+int qr_chunk_rows(int cols, int kmax);
 /// Unpivoted Householder QR of each chunk in place (reflectors below the
 /// diagonal), tau at tau + aux, R (min(rows,cols) x cols, upper) copied into
-/// the parent stacked matrix at out (ld = ldo).
+/// the parent stacked matrix at out (ld = ldo). max_rows bounds the blocks'
+/// rows (sizes shared memory).
 void launch_qr_chunk(const QrBlock* blocks, int nb, double* data, double* rout, double* tau,
-                     int cols, cudaStream_t s);
+                     int cols, int max_rows, cudaStream_t s);
 /// Column-pivoted Householder QR of each top block, keep = first columns with
 /// |R_jj| > tol * |R_00| capped at kmax (proj/src/linalg.cpp:53-78); writes
 /// Q(:, :keep) to out (ld = ldo, kmax columns, zero beyond keep) and keep to
 /// ranks[rank_slot].
 void launch_qr_top(const QrBlock* blocks, int nb, double* data, double* outbuf, int* ranks,
-                   int cols, int kmax, double tol, cudaStream_t s);
+                   int cols, int kmax, double tol, int max_rows, cudaStream_t s);
 /// TSQR back-propagation: out(rows x kmax) = H_chunk [C; 0], C = r x kmax
-/// block of the parent Q at aux (ld = parent ld in rank_slot).
+/// block of the parent Q at c (ld = ldc).
 void launch_qr_backprop(const QrBlock* blocks, int nb, const double* data, const double* tau,
-                        const double* parent, double* outbuf, int cols, int kmax,
+                        const double* parent, double* outbuf, int cols, int kmax, int max_rows,
                         cudaStream_t s);
+
+/// Register-resident QR (k_qr2.cu) for cols <= 96: columns padded to
+/// qr_reg_cols(cols) (0 = unsupported), blocks of up to qr_reg_rows_max rows.
+/// mode 0 = launch_qr_top contract, mode 1 = launch_qr_chunk contract.
+int qr_reg_cols(int cols);
+int qr_reg_rows_max(int cols);
+void launch_qr_reg(int mode, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
+                   int* ranks, int cols, int kmax, double tol, int max_rows, cudaStream_t s);
+/// launch_qr_backprop contract, kmax <= 96, rows <= qr_reg_rows_max(kmax).
+void launch_qr_reg_backprop(const QrBlock* blocks, int nb, const double* data, const double* tau,
+                            const double* parent, double* outbuf, int cols, int kmax, int max_rows,
+                            cudaStream_t s);
 
 // ---------------------------------------------------------------- K5 B
 /// out = X^T Y partial sums over row chunks: X (rows x nx, ld lx), Y (rows x ny,

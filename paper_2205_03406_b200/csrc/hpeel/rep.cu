@@ -353,6 +353,42 @@ double rel_error_power_method(const H1Rep& rep, const DeviceOperator& op, int it
 
 namespace hpeel {
 
+// K4 probe (capi hp_debug_qr): the batched range finder on nb blocks stacked
+// column-major one after another (block i: rows[i] x cols, ld rows[i]); Q
+// (rows[i] x kmax each, stacked the same way) and the kept ranks come back.
+// Returns the device milliseconds of run_qr.
+double debug_qr(const double* blocks, const int* rows, int nb, int cols, int kmax, int device,
+                double* q, int* ranks) {
+  DeviceGuard guard(device);
+  cudaStream_t s;
+  HP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::vector<QrRequest> reqs;
+  std::int64_t a = 0, o = 0;
+  for (int i = 0; i < nb; ++i) {
+    reqs.push_back(QrRequest{a, o, rows[i], rows[i], i});
+    a += std::int64_t(rows[i]) * cols;
+    o += std::int64_t(rows[i]) * kmax;
+  }
+  const QrPlan plan = plan_qr(reqs, cols, kmax);
+  double ms = 0.0;
+  {
+    DevBuf<double> d_a(size_t(std::max<std::int64_t>(a, 1)), s), d_q(size_t(std::max<std::int64_t>(o, 1)), s);
+    DevBuf<int> d_r(size_t(std::max(nb, 1)), s);
+    HP_CUDA(cudaMemcpyAsync(d_a.get(), blocks, size_t(a) * 8, cudaMemcpyHostToDevice, s));
+    Events ev;
+    HP_CUDA(cudaEventRecord(ev.a, s));
+    run_qr(plan, d_a.get(), d_q.get(), d_r.get(), cols, kmax, s);
+    HP_CUDA(cudaEventRecord(ev.b, s));
+    HP_CUDA(cudaMemcpyAsync(q, d_q.get(), size_t(o) * 8, cudaMemcpyDeviceToHost, s));
+    HP_CUDA(cudaMemcpyAsync(ranks, d_r.get(), size_t(nb) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    HP_CUDA(cudaStreamSynchronize(s));
+    ms = ev.ms();
+  }
+  HP_CUDA(cudaStreamSynchronize(s));
+  cudaStreamDestroy(s);
+  return ms;
+}
+
 // K1 parity probe (capi hp_debug_payload): payload rows of every box at
 // `level`, n x 2r col-major in input order.
 Matrix debug_payload(const BoxTree& tree, const TreeLayout& lay, int level, int r,
