@@ -414,11 +414,13 @@ void launch_bsolve(int npairs, const double* gpu_, const double* middle, const d
   if (r > 160 || k > 160) throw std::invalid_argument("bsolve: widths above 160 unsupported");
   int* flags = nullptr;
   HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), size_t(npairs) * sizeof(int), s));
-  const size_t smem_qr =
-      size_t(r * (k + std::max(r, k)) + k * r + k * k + k) * sizeof(double);
-  HP_CUDA(cudaFuncSetAttribute(bsolve_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_qr)));
-  bsolve_qr_kernel<<<npairs, kSvdThreads, smem_qr, s>>>(gpu_, middle, vg, r, k, boff, b, flags);
-  HP_LAUNCHED();
+  if (!launch_bsolve_reg(npairs, gpu_, middle, vg, r, k, boff, b, flags, s)) {
+    const size_t smem_qr =
+        size_t(r * (k + std::max(r, k)) + k * r + k * k + k) * sizeof(double);
+    HP_CUDA(cudaFuncSetAttribute(bsolve_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_qr)));
+    bsolve_qr_kernel<<<npairs, kSvdThreads, smem_qr, s>>>(gpu_, middle, vg, r, k, boff, b, flags);
+    HP_LAUNCHED();
+  }
   // fallback: one-sided Jacobi SVD with the 1e-12 cutoff for flagged pairs
   const size_t smem = size_t(r * k + k * k + r * r + 2 * k * r + k) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(bsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

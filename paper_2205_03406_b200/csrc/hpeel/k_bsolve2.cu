@@ -1,0 +1,226 @@
+// K5 coupling-matrix solve, normal-equations variant (sm_100a).
+//
+// B = pinv(M1) middle pinv(M2)^T with M1 = G'^T U and M2 = (V^T G)^T
+// (proj/src/peeling.cpp:252-269). U and V have orthonormal columns (zero
+// columns beyond their kept rank) and G, G' are Gaussian test blocks, so M1
+// and M2 are r x k Gaussian matrices on their nonzero columns: full column
+// rank with condition numbers ~ (sqrt r + sqrt k) / (sqrt r - sqrt k) (~10-20
+// for the configured k, p). For such matrices pinv(M) X = (M^T M)^{-1} M^T X
+// through a Cholesky factorization agrees with the SVD-based pinv_apply to
+// ~cond^2 eps, and nothing falls under its 1e-12 sigma_1 cutoff. Exactly zero
+// columns (rank below k) get zero rows, as the pseudo-inverse gives. Any pair
+// whose Cholesky diagonal drops below 1e-2 of its largest entry (condition
+// ~1e2 or worse) is flagged and solved by the Jacobi-SVD kernel instead,
+// which implements pinv_apply itself.
+//
+// One CTA per pair: M and the right-hand side in shared memory (odd leading
+// dimensions, conflict-free column reads), Gram products accumulated in
+// registers, a right-looking Cholesky and column-per-thread triangular solves.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.hpp"
+
+namespace hpeel {
+
+namespace {
+
+constexpr int kBsThreads = 256;
+constexpr double kCholFlag = 1e-2;  // min L_jj / max L_jj before falling back
+
+// N = A^T A (lower, k x k, ld ldn) and Y = A^T X (k x nr), Y written over X
+// with ld k + 1 once every thread has read X. A: r x k (ld lda), X: r x nr.
+__device__ void gram_pair(const double* a, double* x, double* n, int r, int k, int nr, int lda, int ldx,
+                          int ldn) {
+  constexpr int kMaxY = 24;  // Y outputs per thread (k * nr <= 256 * 24)
+  double acc[kMaxY];
+#pragma unroll
+  for (int u = 0; u < kMaxY; ++u) {
+    const int e = threadIdx.x + u * kBsThreads;
+    acc[u] = 0.0;
+    if (e < k * nr) {
+      const int i = e % k, c = e / k;
+      const double* ai = a + i * lda;
+      const double* xc = x + c * ldx;
+      double s = 0.0;
+      for (int l = 0; l < r; ++l) s = fma(ai[l], xc[l], s);
+      acc[u] = s;
+    }
+  }
+  for (int e = threadIdx.x; e < k * k; e += kBsThreads) {
+    const int i = e % k, j = e / k;
+    if (i < j) continue;
+    const double* ai = a + i * lda;
+    const double* aj = a + j * lda;
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s = fma(ai[l], aj[l], s);
+    n[i + j * ldn] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kMaxY; ++u) {
+    const int e = threadIdx.x + u * kBsThreads;
+    if (e < k * nr) x[e % k + (e / k) * (k + 1)] = acc[u];
+  }
+  __syncthreads();
+}
+
+// In-place lower Cholesky of n (k x k, ld ldn). Exactly zero diagonals mark
+// null columns (zero rows in the solution). Returns false when a nonzero
+// pivot is small relative to the largest (or the matrix is not positive).
+__device__ bool cholesky(double* n, int k, int ldn, int* null_col) {
+  __shared__ int bad;
+  __shared__ double dmax;
+  if (threadIdx.x == 0) {
+    bad = 0;
+    dmax = 0.0;
+  }
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = n[j + j * ldn];
+      if (d == 0.0) {
+        null_col[j] = 1;
+      } else if (!(d > 0.0)) {
+        bad = 1;
+        null_col[j] = 1;
+        n[j + j * ldn] = 0.0;
+      } else {
+        null_col[j] = 0;
+        const double l = sqrt(d);
+        n[j + j * ldn] = l;
+        dmax = fmax(dmax, l);
+      }
+    }
+    __syncthreads();
+    const bool nul = null_col[j] != 0;
+    if (!nul) {
+      const double ljj = n[j + j * ldn];
+      for (int i = j + 1 + threadIdx.x; i < k; i += kBsThreads) n[i + j * ldn] /= ljj;
+    }
+    __syncthreads();
+    if (!nul) {
+      const int m = k - j - 1;
+      for (int e = threadIdx.x; e < m * m; e += kBsThreads) {
+        const int i = j + 1 + e % m, l = j + 1 + e / m;
+        if (i >= l) n[i + l * ldn] = fma(-n[i + j * ldn], n[l + j * ldn], n[i + l * ldn]);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < k; ++j)
+      if (!null_col[j] && n[j + j * ldn] < kCholFlag * dmax) bad = 1;
+  }
+  __syncthreads();
+  return bad == 0;
+}
+
+// y (k x nr, ld ldy) <- N^{-1} y with N = L L^T; null columns give zero rows.
+__device__ void chol_solve(const double* n, int k, int ldn, const int* null_col, double* y, int nr, int ldy) {
+  for (int c = threadIdx.x; c < nr; c += kBsThreads) {
+    double* yc = y + c * ldy;
+    for (int i = 0; i < k; ++i) {
+      if (null_col[i]) {
+        yc[i] = 0.0;
+        continue;
+      }
+      double s = yc[i];
+      for (int l = 0; l < i; ++l) s = fma(-n[i + l * ldn], yc[l], s);
+      yc[i] = s / n[i + i * ldn];
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      if (null_col[i]) continue;
+      double s = yc[i];
+      for (int l = i + 1; l < k; ++l) s = fma(-n[l + i * ldn], yc[l], s);
+      yc[i] = s / n[i + i * ldn];
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBsThreads)
+bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle,
+                   const double* __restrict__ vg, int r, int k, const std::int64_t* __restrict__ boff,
+                   double* __restrict__ bout, int* __restrict__ flags) {
+  extern __shared__ double sm[];
+  __shared__ int null_col[64];
+  const int lda = r + 1, ldx = r + 1, ldn = k + 1;
+  double* a = sm;                         // r x k (ld r + 1)
+  double* x = a + lda * k;                // r x r (ld r + 1); later k x r / k x k (ld k + 1)
+  double* n = x + ldx * (r > k ? r : k);  // k x k (ld k + 1)
+  const std::int64_t p = blockIdx.x;
+  const int t = threadIdx.x;
+  // 1) left = pinv(M1) middle, M1 = G'^T U (r x k), middle r x r
+  for (int e = t; e < r * k; e += kBsThreads) a[e % r + (e / r) * lda] = gpu_[p * r * k + e];
+  for (int e = t; e < r * r; e += kBsThreads) x[e % r + (e / r) * ldx] = middle[p * r * r + e];
+  __syncthreads();
+  gram_pair(a, x, n, r, k, r, lda, ldx, ldn);
+  const bool ok1 = cholesky(n, k, ldn, null_col);
+  chol_solve(n, k, ldn, null_col, x, r, k + 1);  // left (k x r, ld k + 1) in x
+  // 2) out2 = pinv(M2) left^T, M2 = (V^T G)^T (r x k): M2(i, c) = vg(c, i)
+  for (int e = t; e < r * k; e += kBsThreads) {
+    const int i = e % r, c = e / r;
+    a[i + c * lda] = vg[p * k * r + c + std::int64_t(i) * k];
+  }
+  __syncthreads();
+  {
+    // Y2 = M2^T left^T (k x k): Y2(c, d) = sum_i M2(i, c) left(d, i)
+    constexpr int kMaxY = 16;
+    double acc[kMaxY];
+#pragma unroll
+    for (int u = 0; u < kMaxY; ++u) {
+      const int e = t + u * kBsThreads;
+      acc[u] = 0.0;
+      if (e < k * k) {
+        const int c = e % k, d = e / k;
+        const double* ac = a + c * lda;
+        double s = 0.0;
+        for (int i = 0; i < r; ++i) s = fma(ac[i], x[d + i * (k + 1)], s);
+        acc[u] = s;
+      }
+    }
+    for (int e = t; e < k * k; e += kBsThreads) {
+      const int i = e % k, j = e / k;
+      if (i < j) continue;
+      const double* ai = a + i * lda;
+      const double* aj = a + j * lda;
+      double s = 0.0;
+      for (int l = 0; l < r; ++l) s = fma(ai[l], aj[l], s);
+      n[i + j * ldn] = s;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kMaxY; ++u) {
+      const int e = t + u * kBsThreads;
+      if (e < k * k) x[e % k + (e / k) * (k + 1)] = acc[u];
+    }
+    __syncthreads();
+  }
+  const bool ok2 = cholesky(n, k, ldn, null_col);
+  chol_solve(n, k, ldn, null_col, x, k, k + 1);  // out2 (k x k, ld k + 1)
+  const bool ok = ok1 && ok2;
+  if (ok)
+    for (int e = t; e < k * k; e += kBsThreads) {
+      const int i = e % k, j = e / k;  // B(i, j) = out2(j, i)
+      bout[boff[p] + e] = x[j + i * (k + 1)];
+    }
+  if (t == 0) flags[p] = ok ? 0 : 1;
+}
+
+}  // namespace
+
+bool launch_bsolve_reg(int npairs, const double* gpu_, const double* middle, const double* vg, int r, int k,
+                       const std::int64_t* boff, double* b, int* flags, cudaStream_t s) {
+  if (k > 64 || k > r || k * r > kBsThreads * 24 || k * k > kBsThreads * 16) return false;
+  const int mx = r > k ? r : k;
+  const size_t smem = size_t((r + 1) * k + (r + 1) * mx + (k + 1) * k) * sizeof(double);
+  if (smem > 220 * 1024) return false;
+  HP_CUDA(cudaFuncSetAttribute(bsolve_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  bsolve_chol_kernel<<<npairs, kBsThreads, smem, s>>>(gpu_, middle, vg, r, k, boff, b, flags);
+  HP_LAUNCHED();
+  return true;
+}
+
+}  // namespace hpeel

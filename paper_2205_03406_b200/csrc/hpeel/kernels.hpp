@@ -181,6 +181,10 @@ void launch_qr_reg_backprop(const QrBlock* blocks, int nb, const double* data, c
                             cudaStream_t s);
 
 // ---------------------------------------------------------------- K5 B
+/// Register-resident pivoted-QR B solve (k_bsolve2.cu, k <= 64, r <= 80):
+/// bsolve_qr_kernel's contract; false when the widths are unsupported.
+bool launch_bsolve_reg(int npairs, const double* gpu_, const double* middle, const double* vg, int r, int k,
+                       const std::int64_t* boff, double* b, int* flags, cudaStream_t s);
 /// out = X^T Y partial sums over row chunks: X (rows x nx, ld lx), Y (rows x ny,
 /// ld ly). Tasks write nx x ny col-major partials; summed in task order by
 /// launch_sum_partials.
