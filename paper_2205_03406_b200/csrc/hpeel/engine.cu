@@ -306,6 +306,7 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
                    bool with_adjoint) {
   PeelPlan pp;
   const int k = e.k;
+  const int nc = int(payload_boxes.size());
   // group[(lp, box, c)] -> payload boxes of color c under `box` (level lp)
   struct Key {
     int lp, box, c;
@@ -317,24 +318,28 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
     }
   };
   std::unordered_map<Key, std::vector<int>, KeyHash> groups;
-  for (int c = 0; c < int(payload_boxes.size()); ++c) {
+  for (int c = 0; c < nc; ++c) {
     for (int v : payload_boxes[size_t(c)]) {
       const int lv = e.tree.box(v).level;
       for (int lp = 2; lp <= std::min(lv, top_level); ++lp)
         groups[Key{lp, e.anc[size_t(lp)][size_t(v)], c}].push_back(v);
     }
   }
-  std::unordered_map<std::uint64_t, int> tidx;  // (side, lp, q, c) -> coefficient or -1
+  // coefficient index per (side, lp, q, c): -2 unknown, -1 none
+  std::vector<std::vector<int>> cidx[2];
+  for (int side = 0; side < 2; ++side) {
+    cidx[side].resize(size_t(top_level) + 1);
+    for (int lp = 2; lp <= top_level; ++lp)
+      cidx[side][size_t(lp)].assign(rep.levels[size_t(lp)].pairs.size() * size_t(nc), -2);
+  }
   auto coeff = [&](int side, int lp, int q, int c) -> int {
-    const std::uint64_t key = ((std::uint64_t(side) * 64 + std::uint64_t(lp)) * (1ull << 28) +
-                               std::uint64_t(q)) * (1ull << 24) + std::uint64_t(c);
-    auto it = tidx.find(key);
-    if (it != tidx.end()) return it->second;
+    int& slot = cidx[side][size_t(lp)][size_t(q) * size_t(nc) + size_t(c)];
+    if (slot != -2) return slot;
     const auto& ld = rep.levels[size_t(lp)];
     const auto [x, y] = ld.pairs[size_t(q)];
     const int src = side == 0 ? y : x;
     auto g = groups.find(Key{lp, src, c});
-    if (g == groups.end()) return tidx[key] = -1;
+    if (g == groups.end()) return slot = -1;
     CoeffTask t{};
     t.f = side == 0 ? ld.voff[size_t(q)] : ld.uoff[size_t(q)];
     t.btrans = side == 0 ? 0 : 1;
@@ -352,7 +357,35 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
     auto& list = side == 0 ? pp.coeff_fwd : pp.coeff_adj;
     t.t_out = std::int64_t(list.size()) * k * w;
     list.push_back(t);
-    return tidx[key] = int(list.size()) - 1;
+    return slot = int(list.size()) - 1;
+  };
+  // term list per (side, lp, ancestor box, color), shared by every tile of
+  // every target box under that ancestor: forward terms U_q T_{q,c} over the
+  // pairs (ap, x), adjoint terms V_q T'_{q,c} over the pairs (x, ap)
+  std::unordered_map<Key, std::pair<int, int>, KeyHash> lists[2];
+  auto term_list = [&](int side, int lp, int ap, int c) -> std::pair<int, int> {
+    auto it = lists[side].find(Key{lp, ap, c});
+    if (it != lists[side].end()) return it->second;
+    const auto& ld = rep.levels[size_t(lp)];
+    auto& terms = side == 0 ? pp.terms_fwd : pp.terms_adj;
+    const int b0 = int(terms.size());
+    if (side == 0) {
+      const auto [q0, q1] = first_range(ld.pairs, ap);
+      for (int q = q0; q < q1; ++q) {
+        const int ti = coeff(0, lp, q, c);
+        if (ti >= 0) terms.push_back(PeelTerm{ld.uoff[size_t(q)], std::int64_t(ti) * k * w, e.count(ap), 0});
+      }
+    } else {
+      for (int x : e.adj.interaction[size_t(ap)]) {
+        const int q = pair_index(ld.pairs, x, ap);
+        if (q < 0) continue;
+        const int ti = coeff(1, lp, q, c);
+        if (ti >= 0) terms.push_back(PeelTerm{ld.voff[size_t(q)], std::int64_t(ti) * k * w, e.count(ap), 0});
+      }
+    }
+    const std::pair<int, int> r{b0, int(terms.size())};
+    lists[side].emplace(Key{lp, ap, c}, r);
+    return r;
   };
   for (const SampleBlock& sb : blocks) {
     const int a = sb.box;
@@ -360,34 +393,29 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
     const int rows = e.count(a);
     for (int t0 = 0; t0 < rows; t0 += kTile) {
       const int trows = std::min(kTile, rows - t0);
-      PeelTask tf{sb.off + t0, trows, rows, int(pp.terms_fwd.size()), 0};
-      PeelTask ta{sb.off + t0, trows, rows, int(pp.terms_adj.size()), 0};
+      PeelTask tf{sb.off + t0, trows, rows, int(pp.refs_fwd.size()), 0};
+      PeelTask ta{sb.off + t0, trows, rows, int(pp.refs_adj.size()), 0};
       for (int lp = 2; lp <= std::min(la, top_level); ++lp) {
         const auto& ld = rep.levels[size_t(lp)];
         if (ld.pairs.empty()) continue;
         const int ap = e.anc[size_t(lp)][size_t(a)];
         const std::int64_t roff = e.start(a) - e.start(ap) + t0;
-        const auto [q0, q1] = first_range(ld.pairs, ap);
-        for (int q = q0; q < q1; ++q) {
-          const int ti = coeff(0, lp, q, sb.color);
-          if (ti < 0) continue;
-          pp.terms_fwd.push_back(PeelTerm{ld.uoff[size_t(q)] + roff, std::int64_t(ti) * k * w, e.count(ap), 0});
-          pp.apply_flops += 2.0 * trows * k * w;
+        const auto lf = term_list(0, lp, ap, sb.color);
+        if (lf.second > lf.first) {
+          pp.refs_fwd.push_back(PeelRef{lf.first, lf.second, roff});
+          pp.apply_flops += 2.0 * trows * k * w * (lf.second - lf.first);
         }
         if (!with_adjoint) continue;
-        for (int x : e.adj.interaction[size_t(ap)]) {
-          const int q = pair_index(ld.pairs, x, ap);
-          if (q < 0) continue;
-          const int ti = coeff(1, lp, q, sb.color);
-          if (ti < 0) continue;
-          pp.terms_adj.push_back(PeelTerm{ld.voff[size_t(q)] + roff, std::int64_t(ti) * k * w, e.count(ap), 0});
-          pp.apply_flops += 2.0 * trows * k * w;
+        const auto la2 = term_list(1, lp, ap, sb.color);
+        if (la2.second > la2.first) {
+          pp.refs_adj.push_back(PeelRef{la2.first, la2.second, roff});
+          pp.apply_flops += 2.0 * trows * k * w * (la2.second - la2.first);
         }
       }
-      tf.term_end = int(pp.terms_fwd.size());
-      ta.term_end = int(pp.terms_adj.size());
-      if (tf.term_end > tf.term_begin) pp.tasks_fwd.push_back(tf);
-      if (with_adjoint && ta.term_end > ta.term_begin) pp.tasks_adj.push_back(ta);
+      tf.ref_end = int(pp.refs_fwd.size());
+      ta.ref_end = int(pp.refs_adj.size());
+      if (tf.ref_end > tf.ref_begin) pp.tasks_fwd.push_back(tf);
+      if (with_adjoint && ta.ref_end > ta.ref_begin) pp.tasks_adj.push_back(ta);
     }
   }
   return pp;
@@ -402,6 +430,7 @@ void run_peel(const PeelPlan& pp, const Engine& e, const H1Rep& rep, const doubl
   for (int side = 0; side < 2; ++side) {
     const auto& coeff = side == 0 ? pp.coeff_fwd : pp.coeff_adj;
     const auto& tasks = side == 0 ? pp.tasks_fwd : pp.tasks_adj;
+    const auto& refs = side == 0 ? pp.refs_fwd : pp.refs_adj;
     const auto& terms = side == 0 ? pp.terms_fwd : pp.terms_adj;
     if (coeff.empty() || tasks.empty()) continue;
     DevBuf<CoeffTask> d_coeff;
@@ -411,10 +440,12 @@ void run_peel(const PeelPlan& pp, const Engine& e, const H1Rep& rep, const doubl
                       d_sc.get(), g, gld, identity ? -1 : (side == 0 ? 0 : e.r), k, w, tbuf.get(), s);
     DevBuf<PeelTask> d_tasks;
     d_tasks.upload(tasks, s);
+    DevBuf<PeelRef> d_refs;
+    d_refs.upload(refs, s);
     DevBuf<PeelTerm> d_terms;
     d_terms.upload(terms, s);
-    launch_peel_apply(d_tasks.get(), int(tasks.size()), d_terms.get(), rep.d_factors, tbuf.get(), k,
-                      w, samples, side == 0 ? 0 : adj_col, -1.0, s);
+    launch_peel_apply(d_tasks.get(), int(tasks.size()), d_refs.get(), d_terms.get(), rep.d_factors, tbuf.get(),
+                      k, w, samples, side == 0 ? 0 : adj_col, -1.0, s);
   }
 }
 

@@ -195,6 +195,7 @@ struct PeelPlan {
   std::vector<CoeffTask> coeff_fwd, coeff_adj;
   std::vector<std::int64_t> seg_start, seg_count;
   std::vector<PeelTask> tasks_fwd, tasks_adj;
+  std::vector<PeelRef> refs_fwd, refs_adj;
   std::vector<PeelTerm> terms_fwd, terms_adj;
   double coeff_flops = 0, apply_flops = 0;
 };

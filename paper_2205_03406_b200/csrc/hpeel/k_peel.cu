@@ -36,9 +36,10 @@ constexpr int kFS = kRows + 4;
 // F tile staged column-major (ld kFS), T staged column-major (ld ts).
 template <int NT>
 __global__ void __launch_bounds__(kThreads)
-peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelTerm* __restrict__ terms,
-                  const double* __restrict__ factors, const double* __restrict__ tbuf, int k,
-                  int w, double* __restrict__ out, int ocol0, double alpha) {
+peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict__ refs,
+                  const PeelTerm* __restrict__ terms, const double* __restrict__ factors,
+                  const double* __restrict__ tbuf, int k, int w, double* __restrict__ out, int ocol0,
+                  double alpha) {
   extern __shared__ __align__(16) double sm[];
   const int kp = (k + 3) & ~3;
   const int ts = stride4(kp);
@@ -52,11 +53,12 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelTerm* __restrict
   for (int e = tid; e < 2 * (fsz + tsz); e += kThreads) sm[e] = 0.0;
   __syncthreads();
 
-  auto issue = [&](int buf, int q) {
+  auto issue = [&](int buf, int q, std::int64_t roff) {
     const PeelTerm term = terms[q];
+    const double* f0 = factors + term.f + roff;
     for (int e = tid; e < kRows * k; e += kThreads) {
       const int i = e % kRows, l = e / kRows;
-      if (i < task.rows) cp_async8(fs(buf) + l * kFS + i, factors + term.f + i + std::int64_t(l) * term.fld);
+      if (i < task.rows) cp_async8(fs(buf) + l * kFS + i, f0 + i + std::int64_t(l) * term.fld);
     }
     for (int e = tid; e < ncol * k; e += kThreads) {
       const int l = e % k, c = e / k;
@@ -71,12 +73,24 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelTerm* __restrict
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 
-  if (task.term_begin < task.term_end) issue(0, task.term_begin);
+  // cursor over (ref, term): the next term after (ri, q)
+  auto next = [&](int& ri, int& q) {
+    ++q;
+    while (ri < task.ref_end && q >= refs[ri].term_end) {
+      ++ri;
+      if (ri < task.ref_end) q = refs[ri].term_begin;
+    }
+  };
+  int ri = task.ref_begin, q = ri < task.ref_end ? refs[ri].term_begin - 1 : 0;
+  next(ri, q);
+  if (ri < task.ref_end) issue(0, q, refs[ri].roff);
   int buf = 0;
-  for (int q = task.term_begin; q < task.term_end; ++q, buf ^= 1) {
+  for (; ri < task.ref_end; buf ^= 1) {
+    int nri = ri, nq = q;
+    next(nri, nq);
     cp_async_wait_all();
     __syncthreads();
-    if (q + 1 < task.term_end) issue(buf ^ 1, q + 1);
+    if (nri < task.ref_end) issue(buf ^ 1, nq, refs[nri].roff);
     const double* a0p = fs(buf) + (lane & 3) * kFS + warp * 16 + (lane >> 2);
     const double* bp = tsm(buf) + (lane >> 2) * ts + (lane & 3);
     for (int kk = 0; kk < kp; kk += 4) {
@@ -88,6 +102,8 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelTerm* __restrict
         dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, b);
       }
     }
+    ri = nri;
+    q = nq;
   }
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
@@ -265,13 +281,14 @@ void coeff_nt(const CoeffTask* tasks, int ntasks, const double* factors, const d
 }
 
 template <int NT>
-void apply_nt(const PeelTask* tasks, int ntasks, const PeelTerm* terms, const double* factors,
-              const double* tbuf, int k, int w, double* out, int ocol0, double alpha, cudaStream_t s) {
+void apply_nt(const PeelTask* tasks, int ntasks, const PeelRef* refs, const PeelTerm* terms,
+              const double* factors, const double* tbuf, int k, int w, double* out, int ocol0, double alpha,
+              cudaStream_t s) {
   const int kp = (k + 3) & ~3;
   const size_t smem = size_t(2 * (kp * kFS + NT * 8 * stride4(kp))) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(peel_apply_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const dim3 grid(unsigned(ntasks), unsigned((w + NT * 8 - 1) / (NT * 8)));
-  peel_apply_kernel<NT><<<grid, kThreads, smem, s>>>(tasks, terms, factors, tbuf, k, w, out, ocol0, alpha);
+  peel_apply_kernel<NT><<<grid, kThreads, smem, s>>>(tasks, refs, terms, factors, tbuf, k, w, out, ocol0, alpha);
   HP_LAUNCHED();
 }
 
@@ -300,17 +317,17 @@ void launch_peel_coeff(const CoeffTask* tasks, int ntasks, const double* factors
 #undef HP_C
 }
 
-void launch_peel_apply(const PeelTask* tasks, int ntasks, const PeelTerm* terms,
+void launch_peel_apply(const PeelTask* tasks, int ntasks, const PeelRef* refs, const PeelTerm* terms,
                        const double* factors, const double* tbuf, int k, int w, double* out,
                        int ocol0, double alpha, cudaStream_t s) {
   if (ntasks == 0) return;
   if (k > 64) throw std::invalid_argument("peel: rank k > 64 is not supported");
   const int nt = (w + 7) / 8;
 #define HP_A(N) \
-  case N: return apply_nt<N>(tasks, ntasks, terms, factors, tbuf, k, w, out, ocol0, alpha, s);
+  case N: return apply_nt<N>(tasks, ntasks, refs, terms, factors, tbuf, k, w, out, ocol0, alpha, s);
   switch (nt) {
     HP_A(1) HP_A(2) HP_A(3) HP_A(4) HP_A(5) HP_A(6) HP_A(7) HP_A(8) HP_A(9) HP_A(10)
-    default: return apply_nt<8>(tasks, ntasks, terms, factors, tbuf, k, w, out, ocol0, alpha, s);
+    default: return apply_nt<8>(tasks, ntasks, refs, terms, factors, tbuf, k, w, out, ocol0, alpha, s);
   }
 #undef HP_A
 }

@@ -115,20 +115,28 @@ void launch_peel_coeff(const CoeffTask* tasks, int ntasks, const double* factors
 
 /// Apply task: out[out + i + (ocol0 + c) * ld] += alpha * sum_terms F_term[frow_off + i, :] T_term[:, c]
 /// for i < rows (<= 64), c < w. Terms in CSR (term_off[task] .. term_off[task+1]).
+/// One output tile: rows [out, out + rows) (column stride ld) accumulate the
+/// term lists refs[ref_begin, ref_end).
 struct PeelTask {
   std::int64_t out;
   int rows;
   int ld;
+  int ref_begin;
+  int ref_end;
+};
+/// A shared term list [term_begin, term_end) read at row offset roff.
+struct PeelRef {
   int term_begin;
   int term_end;
+  std::int64_t roff;
 };
 struct PeelTerm {
-  std::int64_t f;     // factor element offset of row 0 of the tile
+  std::int64_t f;     // factor element offset of row 0 (plus the ref's roff)
   std::int64_t t;     // coefficient offset (k x w)
   int fld;            // factor leading dimension
   int pad;
 };
-void launch_peel_apply(const PeelTask* tasks, int ntasks, const PeelTerm* terms,
+void launch_peel_apply(const PeelTask* tasks, int ntasks, const PeelRef* refs, const PeelTerm* terms,
                        const double* factors, const double* tbuf, int k, int w, double* out,
                        int ocol0, double alpha, cudaStream_t s);
 

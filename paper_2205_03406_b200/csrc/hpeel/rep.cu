@@ -162,6 +162,7 @@ void H1Rep::apply_device(const double* x, int w, bool adjoint, double* y, cudaSt
     std::vector<CoeffTask> coeff;
     std::vector<std::int64_t> ss, sc;
     std::vector<PeelTask> tasks;
+    std::vector<PeelRef> refs;
     std::vector<PeelTerm> terms;
     for (size_t p = 0; p < ld.pairs.size(); ++p) {
       const auto [a, b] = ld.pairs[p];
@@ -185,14 +186,15 @@ void H1Rep::apply_device(const double* x, int w, bool adjoint, double* y, cudaSt
       by_box[adjoint ? ld.pairs[p].second : ld.pairs[p].first].push_back(int(p));
     for (auto& [box, ps] : by_box) {
       const int rows = int(layout->count[size_t(box)]);
+      const int tb = int(terms.size());
+      for (int p : ps)
+        terms.push_back(PeelTerm{adjoint ? ld.voff[size_t(p)] : ld.uoff[size_t(p)], std::int64_t(p) * k * w,
+                                 rows, 0});
+      const int te = int(terms.size());
       for (int t0 = 0; t0 < rows; t0 += kTile) {
-        PeelTask t{layout->start[size_t(box)] + t0, std::min(kTile, rows - t0), int(tree->num_points()),
-                   int(terms.size()), 0};
-        for (int p : ps)
-          terms.push_back(PeelTerm{(adjoint ? ld.voff[size_t(p)] : ld.uoff[size_t(p)]) + t0,
-                                   std::int64_t(p) * k * w, rows, 0});
-        t.term_end = int(terms.size());
-        tasks.push_back(t);
+        tasks.push_back(PeelTask{layout->start[size_t(box)] + t0, std::min(kTile, rows - t0),
+                                 int(tree->num_points()), int(refs.size()), int(refs.size()) + 1});
+        refs.push_back(PeelRef{tb, te, t0});
       }
     }
     DevBuf<CoeffTask> dc;
@@ -205,9 +207,11 @@ void H1Rep::apply_device(const double* x, int w, bool adjoint, double* y, cudaSt
                       0, k, w, tbuf.get(), s);
     DevBuf<PeelTask> dt;
     dt.upload(tasks, s);
+    DevBuf<PeelRef> dref;
+    dref.upload(refs, s);
     DevBuf<PeelTerm> dterm;
     dterm.upload(terms, s);
-    launch_peel_apply(dt.get(), int(tasks.size()), dterm.get(), d_factors, tbuf.get(), k, w, y, 0,
+    launch_peel_apply(dt.get(), int(tasks.size()), dref.get(), dterm.get(), d_factors, tbuf.get(), k, w, y, 0,
                       1.0, s);
     HP_CUDA(cudaStreamSynchronize(s));
   }
