@@ -260,6 +260,7 @@ def run_ours(args, ws, rank, local):
     last = None
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
+            last = rep = None  # the previous representation is released outside the timed region
             flush_l2(torch)
             barrier(ws)
             torch.cuda.synchronize()

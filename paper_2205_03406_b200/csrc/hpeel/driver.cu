@@ -359,7 +359,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       rank_total += 2 * std::int64_t(np);
     }
     rep->factor_doubles = ftotal;
-    HP_CUDA(cudaMalloc(&rep->d_factors, size_t(std::max<std::int64_t>(ftotal, 1)) * 8));
+    // stream-ordered from the retained device pool: repeated compress() calls reuse the memory
+    HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_factors), size_t(std::max<std::int64_t>(ftotal, 1)) * 8, s));
     HP_CUDA(cudaMallocHost(&h_ranks, size_t(std::max<std::int64_t>(rank_total, 1)) * sizeof(int)));
 
     // Host plans of every level and of the leaf phase, built concurrently.

@@ -91,8 +91,16 @@ Matrix DeviceOperator::apply(const Matrix& x, bool adjoint) const {
 // ---------------------------------------------------------------- rep
 
 H1Rep::~H1Rep() {
-  if (d_factors) cudaFree(d_factors);
-  if (d_dense) cudaFree(d_dense);
+  // pool allocations (cudaMallocAsync): return them to the retained pool
+  if (d_factors || d_dense) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (d_factors) cudaFreeAsync(d_factors, nullptr);
+    if (d_dense) cudaFreeAsync(d_dense, nullptr);
+    cudaStreamSynchronize(nullptr);
+    cudaSetDevice(prev);
+  }
 }
 
 std::int64_t H1Rep::storage_total() const {
