@@ -143,6 +143,13 @@ def make_operator(hp, w, pts, device=0):
     return hp.kernel_operator(w.kernel, pts, w.param, device)
 
 
+# DRAM bytes (read + write) of one K2 launch from `ncu --set full` (config 3,
+# level 7): the operands are L2-resident, far below the algorithmic bytes.
+K2_NCU_TRAFFIC = 902551808
+K2_NCU_SOURCE = ("profiles/r01_k2_ncu.txt: dram__bytes_read.sum + dram__bytes_write.sum of the level-7 launch "
+                 "(config 3; the write share is mostly the L2-flush buffer written back during the kernel)")
+
+
 def k2_roofline(report):
     """Dominant kernel K2 (sample_apply): executed useful FP64 flops / device time."""
     flops = sum(ph["apply_flops"] for ph in report["phases"] if ph["phase"] == "h1")
@@ -150,7 +157,8 @@ def k2_roofline(report):
     launches = sum(1 for ph in report["phases"] if ph["phase"] == "h1")
     ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
     return {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": None, "kernel": "sample_apply_kernel (K2)",
+            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": K2_NCU_TRAFFIC, "traffic_source": K2_NCU_SOURCE,
+            "kernel": "sample_apply_kernel (K2)",
             "launches_per_step": launches, "avg_launch_ms": round(ms / max(launches, 1), 3),
             "flops_per_step": flops, "peak_source": FP64_PEAK_SOURCE}
 
