@@ -283,29 +283,35 @@ def run_ours(args, ws, rank, local):
     t_step = dist_max(float(np.mean(times)), ws, "ours")
     report = last.report
     roof = k2_roofline(report)
-    fdoubles, ddoubles = last.sizes()
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        hf = np.empty(fdoubles)
-        hd = np.empty(max(ddoubles, 1))
+        # the caller's result arrays: page-locked host memory, allocated once
+        # outside the timed region (as the contract's pinned input buffers)
+        nf, nd = hp.export_sizes(tree, w.rank)
+        hf = hp.pinned_empty(nf)
+        hd = hp.pinned_empty(max(nd, 1))
+        host_pts_src = hp.pinned_empty(pts.size).reshape(pts.shape)
+        host_pts_src[...] = pts
         etimes = []
-        h2d = pts.size * 8
         for i in range(max(1, min(args.steps, 2))):
             barrier(ws)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            host_pts = np.array(pts, copy=True)
-            t_tree = hp.build_tree(host_pts, w.leaf)
-            o2 = make_operator(hp, w, host_pts, local)
-            r2 = hp.compress(o2, t_tree, **kw)
-            d2h = r2.export(hf, hd)
+            # points from host memory -> tree (host) + operator (H2D) ->
+            # compress with every level's factors and the dense blocks
+            # streamed D2H into hf / hd as soon as they are final
+            t_tree = hp.build_tree(host_pts_src, w.leaf)
+            o2 = make_operator(hp, w, host_pts_src, local)
+            r2 = hp.compress(o2, t_tree, **kw, export_to=(hf, hd))
             hp.device_synchronize()
             etimes.append(time.perf_counter() - t0)
             del r2, o2
+        d2h = (nf + nd) * 8
         e2e = {"value": dist_max(float(np.mean(etimes)), ws, "ours"), "unit": "s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "includes": "points H2D, tree build, compress, export of all factors + dense blocks D2H"}
+               "h2d_bytes_per_step": int(pts.size * 8), "d2h_bytes_per_step": int(d2h),
+               "includes": "points from pinned host memory: tree build, operator H2D, compress with every "
+                           "factor and dense block streamed D2H into pinned host arrays as levels finish"}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, sample = cpu_reference_sample(w, pts, os.cpu_count() or 1)

@@ -162,6 +162,21 @@ int hp_rep_storage(const hp_rep* rep, int64_t* total);
 int hp_rep_sizes(const hp_rep* rep, int64_t* factor_doubles, int64_t* dense_doubles);
 /* bulk device->host copy of all factors and dense blocks (internal layout) */
 int hp_rep_export(const hp_rep* rep, double* host_factors, double* host_dense, int64_t* bytes);
+/* sizes (doubles) of the host arrays hp_rep_export / hp_compress_export fill */
+int hp_export_sizes(const hp_tree* tree, int rank, int64_t* factor_doubles, int64_t* dense_doubles);
+/* pinned host memory (cudaHostAlloc) for the export arrays; hp_host_free releases it */
+int hp_host_alloc(int64_t bytes, void** out);
+void hp_host_free(void* p);
+/* compress (as hp_compress_ex) with a streamed export: each level's factors
+ * and then the dense leaf blocks are copied into host_factors / host_dense
+ * (hp_rep_export layout) on a second stream as soon as they are final, so
+ * with pinned arrays the device->host transfer overlaps the later levels.
+ * Returns when the export is complete. Replaces compress() followed by a
+ * host copy of the H1Rep (proj/include/hpeel/peeling.hpp:66-68). */
+int hp_compress_export(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
+                       int format, int strategy, hp_comm* comm, double* host_factors,
+                       int64_t factor_doubles, double* host_dense, int64_t dense_doubles,
+                       hp_rep** out);
 /* captured post-peel samples of pair `pair` at `level` (level < 0: leaf
  * probe block of dense pair `pair`): rows of the row box in box.points
  * order x (2r | leaf width) columns */

@@ -20,7 +20,7 @@ __all__ = [
     "gaussian_matrix", "mix_seed", "random_cloud", "equispaced_1d", "uniform_grid_points",
     "BoxTree", "build_tree", "Plan", "plan", "level_coloring", "dsatur",
     "Operator", "dense_operator", "kernel_operator", "CompressedRep", "compress",
-    "rel_error_power_method", "device_count", "debug_payload",
+    "rel_error_power_method", "device_count", "debug_payload", "export_sizes", "pinned_empty",
 ]
 
 MODES = {"h1": 0, "unif-stage1": 1, "unif-stage2": 2, "leaf": 3}
@@ -459,9 +459,12 @@ def partition_ranges(work, world: int):
 
 def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, oversample: int = 10,
              tol: float = 0.0, seed: int = 0, strategy: str = "graph", capture: bool = False,
-             comm: "Comm | None" = None, emulate_shards: int = 0) -> CompressedRep:
+             comm: "Comm | None" = None, emulate_shards: int = 0, export_to=None) -> CompressedRep:
     """compress_py (module.cpp:65-93) on the device; fixed-rank H1 only.
-    `comm`: shard the black-box apply over the ranks of an NCCL group."""
+    `comm`: shard the black-box apply over the ranks of an NCCL group.
+    `export_to=(host_factors, host_dense)`: float64 arrays of export_sizes()
+    filled with the representation while it is built (each level as soon as
+    it is final; asynchronous when they come from pinned_empty())."""
     if format not in FORMATS:
         raise ValueError("unknown format: " + format)
     if strategy not in STRATEGIES:
@@ -469,10 +472,51 @@ def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, ov
     if tol > 0.0:
         raise ValueError("relative-tolerance truncation is outside the H1 fixed-rank hot path")
     h = C.c_void_p()
+    if export_to is not None:
+        if capture or emulate_shards:
+            raise ValueError("export_to cannot be combined with capture or emulate_shards")
+        hf, hd = export_to
+        for a in (hf, hd):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+                raise ValueError("export arrays must be contiguous float64")
+        check(lib().hp_compress_export(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
+                                       STRATEGIES[strategy], comm._h if comm else None, dptr(hf), hf.size,
+                                       dptr(hd), hd.size, C.byref(h)))
+        return CompressedRep(h.value, tree, rank, oversample)
     check(lib().hp_compress_ex(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
                                STRATEGIES[strategy], int(capture), comm._h if comm else None,
                                int(emulate_shards), C.byref(h)))
     return CompressedRep(h.value, tree, rank, oversample)
+
+
+def export_sizes(tree: BoxTree, rank: int):
+    """(factor doubles, dense doubles) of the host arrays ``compress(...,
+    export_to=...)`` and ``CompressedRep.export`` fill for this tree and rank."""
+    f, d = C.c_int64(0), C.c_int64(0)
+    check(lib().hp_export_sizes(tree._h, int(rank), C.byref(f), C.byref(d)))
+    return f.value, d.value
+
+
+class _PinnedBlock:
+    def __init__(self, nbytes):
+        self.ptr = C.c_void_p()
+        check(lib().hp_host_alloc(int(nbytes), C.byref(self.ptr)))
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        if self.ptr and _lib._lib is not None:
+            _lib._lib.hp_host_free(self.ptr)
+            self.ptr = None
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """float64 array of n elements in page-locked host memory (cudaHostAlloc),
+    so device->host exports run asynchronously at full link speed."""
+    blk = _PinnedBlock(max(int(n), 1) * 8)
+    buf = (C.c_double * max(int(n), 1)).from_address(blk.ptr.value)
+    arr = np.frombuffer(buf, dtype=np.float64, count=int(n))
+    buf._hp_block = blk  # every view's base chain ends at buf: freed with the last view
+    return arr
 
 
 def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, seed: int = 0) -> float:

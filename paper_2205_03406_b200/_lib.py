@@ -73,6 +73,11 @@ _SIGNATURES = {
     "hp_rep_storage": (C.c_int, [P, lp]),
     "hp_rep_sizes": (C.c_int, [P, lp, lp]),
     "hp_rep_export": (C.c_int, [P, dp, dp, lp]),
+    "hp_export_sizes": (C.c_int, [P, C.c_int, lp, lp]),
+    "hp_host_alloc": (C.c_int, [i64, C.POINTER(P)]),
+    "hp_host_free": (None, [P]),
+    "hp_compress_export": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, P, dp, i64, dp, i64,
+                                     C.POINTER(P)]),
     "hp_rep_captured": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
     "hp_rel_error_power_method": (C.c_int, [P, P, C.c_int, u64, dp]),
     "hp_debug_payload": (C.c_int, [P, C.c_int, C.c_int, u64, C.c_int, dp]),

@@ -1,6 +1,8 @@
 // C ABI over the hpeel host layer and device engine (include/hpeel_b200.h).
 #include "../../include/hpeel_b200.h"
 
+#include <cuda_runtime.h>
+
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -609,6 +611,63 @@ int hp_rep_export(const hp_rep* rep, double* hf, double* hd, int64_t* bytes) {
     need(hd, "host_dense");
     const int64_t b = rep->result.rep->export_all(hf, hd);
     if (bytes) *bytes = b;
+  });
+}
+
+int hp_export_sizes(const hp_tree* tree, int rank, int64_t* factor_doubles, int64_t* dense_doubles) {
+  return guard([&] {
+    need(tree, "tree");
+    if (rank < 1) throw std::invalid_argument("fixed rank must be >= 1");
+    export_sizes(*tree->tree, rank, factor_doubles, dense_doubles);
+  });
+}
+
+int hp_host_alloc(int64_t bytes, void** out) {
+  return guard([&] {
+    need(out, "out");
+    if (bytes < 0) throw std::invalid_argument("negative size");
+    void* p = nullptr;
+    const cudaError_t e = cudaHostAlloc(&p, size_t(bytes > 0 ? bytes : 1), cudaHostAllocPortable);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+    *out = p;
+  });
+}
+
+void hp_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int hp_compress_export(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
+                       int format, int strategy, hp_comm* comm, double* host_factors,
+                       int64_t factor_doubles, double* host_dense, int64_t dense_doubles,
+                       hp_rep** out) {
+  return guard([&] {
+    need(op, "op");
+    need(tree, "tree");
+    need(out, "out");
+    need(host_factors, "host_factors");
+    need(host_dense, "host_dense");
+    if (format < 0 || format > 3) throw std::invalid_argument("unknown format");
+    std::int64_t nf = 0, nd = 0;
+    if (rank >= 1) export_sizes(*tree->tree, rank, &nf, &nd);
+    if (factor_doubles < nf || dense_doubles < nd)
+      throw std::invalid_argument("export arrays smaller than hp_export_sizes");
+    PeelConfig cfg;
+    cfg.rank = rank;
+    cfg.oversample = oversample;
+    cfg.leaf_capacity = tree->tree->leaf_capacity();
+    cfg.seed = seed;
+    cfg.format = PeelFormat(format);
+    cfg.strategy = strategy == HP_STRATEGY_FALLBACK_PATTERN ? ColoringStrategy::kFallbackPattern
+                                                            : ColoringStrategy::kGraph;
+    cfg.comm = comm ? comm->comm.get() : nullptr;
+    cfg.export_factors = host_factors;
+    cfg.export_dense = host_dense;
+    if (cfg.comm && cfg.comm->device() != op->op->device())
+      throw std::invalid_argument("communicator and operator on different devices");
+    auto r = std::make_unique<hp_rep>();
+    r->result = compress(*op->op, tree->tree, cfg);
+    *out = r.release();
   });
 }
 

@@ -236,8 +236,18 @@ LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg) {
   LeafWork lw;
   const BoxTree& tree = e.tree;
   lw.w = tree.max_leaf_size();
+  static const bool timing = std::getenv("HP_PLAN_TIMING") != nullptr;
+  auto t0 = Clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = Clock::now();
+    std::fprintf(stderr, "[build_leaf] %s %.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   const SamplingPlan plan =
       make_plan(tree, e.adj, tree.depth(), SampleMode::kLeaf, lw.w, cfg.seed, kForwardPhase);
+  lap("make_plan");
   lw.nc = plan.colors();
   std::vector<std::vector<int>> color_boxes(size_t(lw.nc));
   lw.pay_off.assign(size_t(lw.nc) + 1, 0);
@@ -267,10 +277,12 @@ LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg) {
     lw.evals += double(rows) * double(nnz);
     lw.total += std::int64_t(rows) * lw.w;
   }
+  lap("tasks");
   if (tree.depth() >= 2) {
     lw.peel = plan_peel(e, rep, blocks, color_boxes, tree.depth(), lw.w, false);
     lw.has_peel = true;
   }
+  lap("plan_peel");
   return lw;
 }
 
@@ -295,6 +307,92 @@ std::string RunReport::to_csv() const {
   }
   return out.str();
 }
+
+void export_sizes(const BoxTree& tree, int rank, std::int64_t* factor_doubles,
+                  std::int64_t* dense_doubles) {
+  const AdjacencyInfo adj = adjacency(tree);
+  std::int64_t f = 0, d = 0;
+  for (int l = 2; l <= tree.depth(); ++l)
+    for (auto [a, b] : admissible_pairs(tree, adj, l))
+      f += std::int64_t(tree.box(a).points.size() + tree.box(b).points.size()) * rank +
+           std::int64_t(rank) * rank;
+  const std::int64_t w = tree.max_leaf_size();
+  for (auto [lam, mu] : dense_pairs(tree, adj)) d += std::int64_t(tree.box(lam).points.size()) * w;
+  if (factor_doubles) *factor_doubles = f;
+  if (dense_doubles) *dense_doubles = d;
+}
+
+namespace {
+
+// Copies finished parts of the representation to the caller's host arrays on
+// a second stream, each after an event on the compute stream. Pinned
+// destinations overlap the later levels; pageable ones are copied at the end.
+class Exporter {
+ public:
+  Exporter(double* hf, double* hd, int device) : hf_(hf), hd_(hd) {
+    if (!hf_ && !hd_) return;
+    pinned_ = is_pinned(hf_) && is_pinned(hd_);
+    if (pinned_) HP_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+    (void)device;
+  }
+  ~Exporter() {
+    if (xs_) {
+      cudaStreamSynchronize(xs_);
+      cudaStreamDestroy(xs_);
+    }
+    for (cudaEvent_t ev : events_) cudaEventDestroy(ev);
+  }
+  bool active() const { return hf_ || hd_; }
+  // device [src, src + n) -> host dst once the work queued on s so far is done
+  void copy(double* dst, const double* src, std::int64_t n, cudaStream_t s) {
+    if (!dst || n <= 0) return;
+    if (!pinned_) {
+      deferred_.push_back({dst, src, n});
+      return;
+    }
+    cudaEvent_t ev;
+    HP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    events_.push_back(ev);
+    HP_CUDA(cudaEventRecord(ev, s));
+    HP_CUDA(cudaStreamWaitEvent(xs_, ev, 0));
+    HP_CUDA(cudaMemcpyAsync(dst, src, size_t(n) * 8, cudaMemcpyDeviceToHost, xs_));
+  }
+  void finish(cudaStream_t s) {
+    if (xs_) HP_CUDA(cudaStreamSynchronize(xs_));
+    if (!deferred_.empty()) {
+      HP_CUDA(cudaStreamSynchronize(s));
+      for (const auto& d : deferred_)
+        HP_CUDA(cudaMemcpy(d.dst, d.src, size_t(d.n) * 8, cudaMemcpyDeviceToHost));
+      deferred_.clear();
+    }
+  }
+  double* factors() const { return hf_; }
+  double* dense() const { return hd_; }
+
+ private:
+  static bool is_pinned(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  }
+  struct Deferred {
+    double* dst;
+    const double* src;
+    std::int64_t n;
+  };
+  double* hf_;
+  double* hd_;
+  bool pinned_ = false;
+  cudaStream_t xs_ = nullptr;
+  std::vector<cudaEvent_t> events_;
+  std::vector<Deferred> deferred_;
+};
+
+}  // namespace
 
 PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tree,
                     const PeelConfig& config) {
@@ -331,6 +429,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
   int* h_ranks = nullptr;
 
   try {
+    Exporter exporter(config.export_factors, config.export_dense, op.device());
     Engine e(*tree, *adj, *lay, op, s);
     StagingScope staging(s);  // uploads below stay asynchronous
     e.r = r;
@@ -519,6 +618,10 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       rank_off[size_t(l)] = roff;
       roff += 2 * std::int64_t(np);
       timers[size_t(l)] = std::move(tm);
+      if (exporter.active() && np > 0) {  // this level's U, V, B are final
+        const std::int64_t f0 = ld.uoff[0], f1 = ld.boff[np - 1] + std::int64_t(k) * k;
+        exporter.copy(exporter.factors() ? exporter.factors() + f0 : nullptr, rep->d_factors + f0, f1 - f0, s);
+      }
       built = l;
     }
     rep->built_level = tree->depth();
@@ -570,7 +673,9 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       }
       if (config.comm) config.comm->broadcast_segments(rep->d_dense, seg, s);
       HP_CUDA(cudaEventRecord(leaf_peel.b, s));
+      if (exporter.active()) exporter.copy(exporter.dense(), rep->d_dense, lw.total, s);
     }
+    exporter.finish(s);
     HP_CUDA(cudaStreamSynchronize(s));
     if (config.capture_samples) {
       for (size_t p = 0; p < lw.pairs.size(); ++p) {

@@ -40,6 +40,13 @@ struct PeelConfig {
   bool capture_samples = false;  // keep post-peel sample blocks on the host (tests)
   Comm* comm = nullptr;          // multi-GPU: this process's rank in the NCCL group
   int emulate_shards = 0;        // tests: split K2/K6 launches as `n` ranks would
+  // Streamed export: when set, every level's factor slice and the dense leaf
+  // blocks are copied to these host arrays (export_sizes() doubles each, the
+  // H1Rep::export_all layout) on a second stream as soon as they are final,
+  // overlapping the later levels' device work (pinned memory; pageable
+  // arrays are filled after the device loop).
+  double* export_factors = nullptr;
+  double* export_dense = nullptr;
   int sample_width() const { return rank + oversample; }
   void validate() const;
 };
@@ -169,6 +176,11 @@ struct PeelResult {
 /// proj/src/peeling.cpp:576-639 for format h1 (others: std::invalid_argument).
 PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tree,
                     const PeelConfig& config);
+
+/// Doubles of the factor arena and of the dense leaf blocks compress() will
+/// produce for this tree and rank (the export_all / export_* layout sizes).
+void export_sizes(const BoxTree& tree, int rank, std::int64_t* factor_doubles,
+                  std::int64_t* dense_doubles);
 
 /// proj/src/linalg.cpp:206-218 with both operators applied on the device.
 double rel_error_power_method(const H1Rep& rep, const DeviceOperator& op, int iters,

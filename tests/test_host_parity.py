@@ -153,3 +153,19 @@ def test_error_behaviour(hp):
         hp.build_tree(np.array([[0.0], [np.nan]]), 2)
     with pytest.raises(ValueError):
         hp.build_tree(hp.equispaced_1d(16), 0)
+
+
+def test_export_sizes_match_layout(hp):
+    """hp_export_sizes: U, V, B per admissible pair of every level plus the
+    |I_lam| x max_leaf_size dense probe blocks (H1Rep::export_all layout)."""
+    pts = O.random_cloud(3000, 2, O.mix_seed(7, 0xE3))
+    tree = hp.build_tree(pts, 32)
+    ot = O.BoxTree(O.PointCloud(pts), 32)
+    k = 9
+    want_f = 0
+    for level in range(2, tree.depth + 1):
+        for a, b in tree.admissible_pairs(level):
+            want_f += (len(ot.box(a).points) + len(ot.box(b).points)) * k + k * k
+    w = max(len(ot.box(v).points) for v in range(len(ot.boxes)) if not ot.box(v).children)
+    want_d = sum(len(ot.box(lam).points) * w for lam, _ in tree.dense_pairs())
+    assert hp.export_sizes(tree, k) == (want_f, want_d)
