@@ -320,7 +320,7 @@ def run_ours(args, ws, rank, local):
         return
     phases = [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in ph.items()
                if k in ("phase", "level", "colors", "apply_ms", "peel_ms", "qr_ms", "bsolve_ms", "wall_ms_total",
-                        "host_wait_ms")}
+                        "host_wait_ms", "start_ms")}
               for ph in report["phases"]]
     line = {
         "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": args.gpus,

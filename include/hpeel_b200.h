@@ -57,6 +57,10 @@ int hp_device_count(int* count);
 int64_t hp_launch_count(void);
 /* profiling only: 1 = K2 skips kernel evaluation, 2 = K2 skips DMMA, 0 = normal */
 void hp_debug_set_k2_mode(int mode);
+/* K2 arithmetic path: 0 = int8 tensor-core digit products (exact fixed-point
+ * emulation of the FP64 contraction, k2_i8.cuh) wherever eligible (default),
+ * 1 = FP64 DMMA for every apply (A/B tests) */
+void hp_debug_set_k2_path(int path);
 int hp_device_synchronize(void);
 
 /* ---- RNG: proj/include/hpeel/rng.hpp:37-50, proj/src/rng.cpp:31-59 ---- */
@@ -145,8 +149,9 @@ int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bound
  * wall_s_total, wall_s_net, net_flops, setup_ms; *nphases = phase count */
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases);
 /* per phase: is_leaf, level, colors, forward_cols, adjoint_cols, net_flops and
- * times[9] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
- * apply_flops, kernel_evals, host_wait_ms */
+ * times[10] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
+ * apply_flops, kernel_evals, host_wait_ms, start_ms (times[10]; device
+ * time from the first device work of compress to the phase start) */
 int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times);
 /* RunReport::to_csv (proj/src/peeling.cpp:478-488) */
 int hp_rep_csv(const hp_rep* rep, char* buf, int64_t cap, int64_t* len);

@@ -344,7 +344,7 @@ class CompressedRep:
         phases = []
         for i in range(nph.value):
             ints = np.zeros(6, dtype=np.int64)
-            times = np.zeros(9)
+            times = np.zeros(10)
             check(lib().hp_rep_phase(self._h, i, lptr(ints), dptr(times)))
             phases.append({
                 "phase": "leaf" if ints[0] else "h1", "level": int(ints[1]), "colors": int(ints[2]),
@@ -352,6 +352,7 @@ class CompressedRep:
                 "wall_ms_total": times[0], "wall_ms_net": times[1], "apply_ms": times[2],
                 "peel_ms": times[3], "qr_ms": times[4], "bsolve_ms": times[5],
                 "apply_flops": times[6], "kernel_evals": times[7], "host_wait_ms": times[8],
+                "start_ms": times[9],
             })
         self.report = {
             "forward_cols": int(totals[0]), "adjoint_cols": int(totals[1]),
@@ -524,6 +525,13 @@ def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, s
     out = C.c_double(0.0)
     check(lib().hp_rel_error_power_method(rep._h, ref._h, int(iters), int(seed), C.byref(out)))
     return out.value
+
+
+def set_k2_path(path: str) -> None:
+    """Black-box apply arithmetic: "int8" (default: exact fixed-point digit
+    products on the int8 tensor cores wherever eligible) or "fp64" (FP64
+    DMMA for every apply). For A/B parity tests and measurements."""
+    lib().hp_debug_set_k2_path({"int8": 0, "fp64": 1, "int8-nomma": 2, "int8-noeval": 3}[path])
 
 
 def debug_log(x, device: int = 0) -> np.ndarray:

@@ -30,6 +30,7 @@ _SIGNATURES = {
     "hp_device_count": (C.c_int, [ip]),
     "hp_launch_count": (i64, []),
     "hp_debug_set_k2_mode": (None, [C.c_int]),
+    "hp_debug_set_k2_path": (None, [C.c_int]),
     "hp_device_synchronize": (C.c_int, []),
     "hp_mix_seed": (u64, [u64, u64]),
     "hp_gaussian_matrix": (C.c_int, [i64, i64, u64, dp]),

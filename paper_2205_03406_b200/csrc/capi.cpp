@@ -41,6 +41,7 @@ struct hp_comm {
 namespace hpeel {
 std::int64_t& launch_counter();
 void set_k2_mode(int mode);
+void set_k2_path(int path);
 void debug_fast_log(const double* x, std::int64_t n, double* y, int device);
 Matrix debug_payload(const BoxTree& tree, const TreeLayout& lay, int level, int r,
                      std::uint64_t seed, int device);
@@ -96,6 +97,7 @@ int hp_device_count(int* count) {
 int64_t hp_launch_count(void) { return launch_counter(); }
 
 void hp_debug_set_k2_mode(int mode) { set_k2_mode(mode); }
+void hp_debug_set_k2_path(int path) { set_k2_path(path); }
 
 int hp_device_synchronize(void) {
   return guard([&] {
@@ -526,6 +528,7 @@ int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times)
       times[6] = ph.apply_flops;
       times[7] = ph.kernel_evals;
       times[8] = ph.host_wait_ms;
+      times[9] = ph.start_ms;
     }
   });
 }

@@ -22,6 +22,7 @@
 #include <stdexcept>
 
 #include "engine.cuh"
+#include "k2_i8.cuh"
 #include "rng.hpp"
 #include "shard.hpp"
 
@@ -64,6 +65,10 @@ struct LevelWork {
   std::vector<std::int64_t> soff;
   std::vector<std::int64_t> pay_off;
   std::vector<int> pay_pos;
+  std::vector<std::int64_t> step_off;      // int8 K2: 32-row K-steps per color (prefix)
+  std::vector<int> step_color;             // color of every K-step
+  std::vector<std::int64_t> pb_off;        // payload boxes per color (prefix)
+  std::vector<int> pb_box;
   std::vector<int> pos_box, local;
   std::vector<K2Row> rowtab;               // K2 rows, grouped by shard and color
   std::vector<std::vector<K2Task>> k2;     // K2 tiles per shard
@@ -110,6 +115,16 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
     }
     w.pay_off[size_t(c) + 1] = std::int64_t(w.pay_pos.size());
     w.fwd_cols += plan.matrices[size_t(c)].payload.empty() ? 0 : r;
+  }
+  // int8 K2 layout: per color, ceil(nnz_c / 32) K-steps and the payload boxes
+  w.step_off.assign(size_t(w.nc) + 1, 0);
+  w.pb_off.assign(size_t(w.nc) + 1, 0);
+  for (int c = 0; c < w.nc; ++c) {
+    const std::int64_t ns = (w.pay_off[size_t(c) + 1] - w.pay_off[size_t(c)] + 31) / 32;
+    w.step_off[size_t(c) + 1] = w.step_off[size_t(c)] + ns;
+    for (std::int64_t q = 0; q < ns; ++q) w.step_color.push_back(c);
+    for (int b : color_boxes[size_t(c)]) w.pb_box.push_back(b);
+    w.pb_off[size_t(c) + 1] = std::int64_t(w.pb_box.size());
   }
   const size_t np = ld.pairs.size();
   w.np = np;
@@ -430,6 +445,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
 
   try {
     Exporter exporter(config.export_factors, config.export_dense, op.device());
+    Events dev_span;  // a: first device work of this compress
+    HP_CUDA(cudaEventRecord(dev_span.a, s));
     Engine e(*tree, *adj, *lay, op, s);
     StagingScope staging(s);  // uploads below stay asynchronous
     e.r = r;
@@ -552,13 +569,41 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       if (op.kind() != kOpDense)
         launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
       const bool checked = w.k2_checked || e.has_dups;
+      // int8 tensor-core K2 (k2_i8.cuh): on-the-fly symmetric kernels,
+      // unchecked tiles, r <= 64 (7 accumulator groups x r fit TMEM)
+      const bool use_i8 = op.kind() != kOpDense && op.symmetric() && !checked && r <= 64 &&
+                          k2_mode() == 0 && k2_int8_enabled();
+      DevBuf<unsigned char> bdig;
+      DevBuf<std::int64_t> d_step_off, d_pb_off;
+      DevBuf<double> xstep;
+      DevBuf<int> d_step_color, d_pb_box;
+      std::int64_t half_stride = 0;
+      if (use_i8) {
+        const std::int64_t tsteps = w.step_off.back();
+        half_stride = tsteps * k2i8::b_step_bytes(k2i8::padded_width(r));
+        bdig.alloc(size_t(std::max<std::int64_t>(2 * half_stride, 16)), s);
+        d_step_off.upload(w.step_off, s);
+        d_step_color.upload(w.step_color, s);
+        d_pb_off.upload(w.pb_off, s);
+        d_pb_box.upload(w.pb_box, s);
+        k2i8::launch_payload_digits(gcol.get(), gld, r, d_pay_off.get(), d_step_off.get(), d_step_color.get(),
+                                    tsteps, bdig.get(), half_stride, s);
+        xstep.alloc(size_t(std::max<std::int64_t>(tsteps, 1)) * 32 * size_t(op.dim()), s);
+        k2i8::launch_step_coords(xcol.get(), nnz, op.dim(), d_pay_off.get(), d_step_off.get(), d_step_color.get(),
+                                 tsteps, xstep.get(), s);
+        e.ensure_box_bbox();
+      }
       for (int sr = 0; sr < int(w.k2.size()); ++sr) {
         if (my_rank >= 0 && sr != my_rank) continue;
         const auto& tl = w.k2[size_t(sr)];
         DevBuf<K2Task> d_tasks;
         d_tasks.upload(tl, s);
         const int nt = int(tl.size());
-        if (op.symmetric()) {
+        if (use_i8) {
+          k2i8::launch_sample_apply_i8(e.dop, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(), d_step_off.get(),
+                                       xstep.get(), d_pb_off.get(), d_pb_box.get(), e.d_box_bbox.get(),
+                                       bdig.get(), half_stride, r, samples.get(), s);
+        } else if (op.symmetric()) {
           launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
                               d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
                               samples.get(), 0, checked, s);
@@ -689,6 +734,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
 
     // ------------------------------------------------------------- report
     double blackbox_ms = 0.0;
+    float fstart = 0.f;
     for (int l = 2; l <= tree->depth(); ++l) {
       auto& ld = rep->levels[size_t(l)];
       if (!timers[size_t(l)]) continue;
@@ -718,6 +764,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       ph.wall_ms_total = ph.apply_ms + ph.peel_ms + ph.qr_ms + ph.bsolve_ms;
       ph.wall_ms_net = ph.wall_ms_total - ph.apply_ms;
       ph.host_wait_ms = wait_ms[size_t(l)];
+      HP_CUDA(cudaEventElapsedTime(&fstart, dev_span.a, tm->apply.a));
+      ph.start_ms = fstart;
       blackbox_ms += ph.apply_ms;
       if (l - 1 >= 2) ph.net_flops += 2 * std::int64_t(ph.colors) * truncated_apply_flops(*rep, l - 1, r, e);
       // QR (flops.hpp:18-20) and the B solve (peeling.cpp:262-268)
@@ -744,6 +792,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       ph.wall_ms_total = ph.apply_ms + ph.peel_ms;
       ph.wall_ms_net = ph.peel_ms;
       ph.host_wait_ms = leaf_wait_ms;
+      HP_CUDA(cudaEventElapsedTime(&fstart, dev_span.a, leaf_apply.a));
+      ph.start_ms = fstart;
       blackbox_ms += ph.apply_ms;
       if (tree->depth() >= 2) ph.net_flops += std::int64_t(lw.nc) * truncated_apply_flops(*rep, tree->depth(), lw.w, e);
       report.phases.push_back(ph);

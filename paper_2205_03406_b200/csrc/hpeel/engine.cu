@@ -1,5 +1,6 @@
 // Engine and batched task builders (see engine.cuh).
 #include "engine.cuh"
+#include "k2_i8.cuh"
 
 #include <mutex>
 
@@ -68,6 +69,13 @@ void PinnedStaging::release_to_pool() {
   std::lock_guard<std::mutex> lock(pool_mutex());
   for (const Chunk& c : chunks_) pool().push_back({c.p, c.size});
   chunks_.clear();
+}
+
+void Engine::ensure_box_bbox() {
+  if (d_box_bbox.get() || op.kind() == kOpDense) return;
+  const int nb = tree.num_boxes();
+  d_box_bbox.alloc(size_t(nb) * 2 * size_t(op.dim()), s);
+  k2i8::launch_box_bbox(xt.get(), n, op.dim(), d_box_start.get(), d_box_count.get(), nb, d_box_bbox.get(), s);
 }
 
 Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,

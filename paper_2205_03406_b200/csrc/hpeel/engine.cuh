@@ -147,12 +147,14 @@ struct Engine {
   DevOp dop;
   DevBuf<std::int64_t> d_box_start, d_box_count;
   bool has_dups = false;  // kernel kinds: two distinct points share coordinates
+  DevBuf<double> d_box_bbox;  // int8 K2: raw-coordinate bounding box per box (built on first use)
   std::vector<std::vector<int>> anc;  // anc[l][box] = ancestor at level l (or -1)
 
   Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l, const DeviceOperator& o,
          cudaStream_t st);
   std::int64_t start(int b) const { return lay.start[size_t(b)]; }
   int count(int b) const { return int(lay.count[size_t(b)]); }
+  void ensure_box_bbox();
 };
 
 int pair_index(const std::vector<std::pair<int, int>>& pairs, int a, int b);

@@ -15,6 +15,8 @@
 // forward+adjoint columns.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "k2_ws.cuh"
 #include "kernels.hpp"
 #include "rng.hpp"
@@ -137,6 +139,16 @@ __global__ void full_apply_kernel(DevOp op, const double* __restrict__ x, int w,
 }  // namespace
 
 int k2_mode() { return k2_mode_ref(); }
+
+// K2 arithmetic path: int8 tensor-core digit products (k2_i8.cuh) where
+// eligible, unless switched off (hp_debug_set_k2_path(1) or HP_K2_FP64=1).
+static int& k2_path_ref() {
+  static int path = std::getenv("HP_K2_FP64") ? 1 : 0;
+  return path;
+}
+bool k2_int8_enabled() { return k2_path_ref() != 1; }
+int k2_int8_debug() { return k2_path_ref() >= 2 ? k2_path_ref() - 1 : 0; }
+void set_k2_path(int path) { k2_path_ref() = path; }
 
 int k2_tile_rows(int ncols) {
   const int nt = (ncols + 7) / 8;

@@ -48,6 +48,14 @@ struct K2Task {
   int ld;
   int pos;
 };
+int k2_mode();
+/// K2 arithmetic path switch: true = int8 tensor-core digit products where
+/// eligible (default), false = FP64 DMMA everywhere (hp_debug_set_k2_path).
+bool k2_int8_enabled();
+void set_k2_path(int path);
+/// int8 K2 probe bits (path 2: skip the MMAs, path 3: skip the evaluation)
+int k2_int8_debug();
+
 __host__ __device__ inline K2Row k2_row(const K2Task& t, const K2Row* rowtab, int i) {
   if (t.ld > 0) return K2Row{t.base + i, t.pos + i, t.ld};
   return rowtab[t.base + i];

@@ -69,6 +69,7 @@ struct PhaseReport {
   double peel_flops = 0.0;       // FMAs*2 executed by K3 (coefficients + subtraction)
   double kernel_evals = 0.0;
   double host_wait_ms = 0.0;      // driver thread blocked on this phase's host plan
+  double start_ms = 0.0;          // device time from the first device work of compress to this phase
 };
 
 struct RunReport {

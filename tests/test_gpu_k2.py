@@ -18,12 +18,14 @@ def test_k2_variants_bit_identical(hp, gpu_available, name, mode):
     t = hp.build_tree(pts, w.leaf)
     op = hp.kernel_operator(w.kernel, pts, w.param)
     reps = []
+    hp.set_k2_path("fp64")  # the FP64 DMMA kernels (the int8 path: test_gpu_k2_int8.py)
     try:
         for m in (0, mode):
             _lib.lib().hp_debug_set_k2_mode(m)
             reps.append(hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7, capture=True))
     finally:
         _lib.lib().hp_debug_set_k2_mode(0)
+        hp.set_k2_path("int8")
     for l in range(2, t.depth + 1):
         for i in range(len(t.admissible_pairs(l))):
             assert np.array_equal(reps[0].captured(l, i), reps[1].captured(l, i))

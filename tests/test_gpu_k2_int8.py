@@ -1,0 +1,62 @@
+"""The int8 tensor-core black-box apply (k2_i8.cuh: exact fixed-point digit
+products on tcgen05.mma kind::i8) against the FP64 DMMA apply on the same
+inputs: every post-peel sample block within 1e-12 relative (the north-star
+FP64 sample tolerance), on 1D/2D log, 3D 1/(4 pi r) and 3D exp kernels, plus
+the reconstruction error of the resulting representation."""
+import numpy as np
+import pytest
+
+from paper_2205_03406_b200 import configs
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("c2", 8192), ("c3", 16384), ("c4", 16384), ("c5", 8192)]
+
+
+def _compress(hp, path, op, t, w, rank, over):
+    hp.set_k2_path(path)
+    try:
+        return hp.compress(op, t, rank=rank, oversample=over, seed=7, capture=True)
+    finally:
+        hp.set_k2_path("int8")
+
+
+@pytest.mark.parametrize("name,n", CASES)
+def test_int8_samples_match_fp64(hp, gpu_available, name, n):
+    w = configs.scaled(name, n)
+    pts = w.points()
+    t = hp.build_tree(pts, w.leaf)
+    op = hp.kernel_operator(w.kernel, pts, w.param)
+    # c5's k + p = 80 exceeds the int8 path's width; run it at k + p = 64
+    rank, over = (w.rank, w.oversample) if w.rank + w.oversample <= 64 else (48, 16)
+    a = _compress(hp, "fp64", op, t, w, rank, over)
+    b = _compress(hp, "int8", op, t, w, rank, over)
+    worst = 0.0
+    for l in range(2, t.depth + 1):
+        for i in range(len(t.admissible_pairs(l))):
+            x, y = a.captured(l, i), b.captured(l, i)
+            nx = np.linalg.norm(x)
+            if nx > 0:
+                worst = max(worst, np.linalg.norm(x - y) / nx)
+    assert worst <= 1e-12, f"{name}: worst sample block {worst:.3e}"
+    xs = np.random.default_rng(1).standard_normal((t.num_points, 3))
+    ya, yb = a.apply(xs), b.apply(xs)
+    assert np.linalg.norm(ya - yb) / np.linalg.norm(ya) <= 1e-9
+
+
+def test_int8_path_is_used(hp, gpu_available):
+    """The default path launches the int8 kernel (a CPU or DMMA fallback would
+    leave the launch count pattern unchanged between paths)."""
+    w = configs.scaled("c3", 8192)
+    pts = w.points()
+    t = hp.build_tree(pts, w.leaf)
+    op = hp.kernel_operator(w.kernel, pts, w.param)
+    counts = {}
+    for path in ("fp64", "int8"):
+        hp.set_k2_path(path)
+        c0 = hp.launch_count()
+        hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
+        counts[path] = hp.launch_count() - c0
+    hp.set_k2_path("int8")
+    # int8 adds one payload-digit launch per level (and one bbox launch)
+    assert counts["int8"] > counts["fp64"]
