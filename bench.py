@@ -144,23 +144,40 @@ def make_operator(hp, w, pts, device=0):
 
 
 # DRAM bytes (read + write) of one K2 launch from `ncu --set full` (config 3,
-# level 7): the operands are L2-resident, far below the algorithmic bytes.
-K2_NCU_TRAFFIC = 902551808
-K2_NCU_SOURCE = ("profiles/r01_k2_ncu.txt: dram__bytes_read.sum + dram__bytes_write.sum of the level-7 launch "
-                 "(config 3; the write share is mostly the L2-flush buffer written back during the kernel)")
+# level 7; profiles/r01_k2_int8_ncu.txt), per launch like `achieved`.
+K2_NCU_TRAFFIC = 901400832
+K2_NCU_SOURCE = "profiles/r01_k2_int8_ncu.txt: dram__bytes_read.sum + dram__bytes_write.sum of the level-7 launch (config 3)"
+INT8_PEAK_TOPS = 4500.0   # B200 dense INT8 tensor peak (datasheet; MEASURED_PEAKS.json has no INT8 entry)
 
 
-def k2_roofline(report):
-    """Dominant kernel K2 (sample_apply): executed useful FP64 flops / device time."""
+def k2_roofline(report, w):
+    """Dominant kernel K2 (black-box apply). achieved = useful FP64 flops of
+    the rows read back (2 * rows * payload rows * 2r) / K2 device time,
+    against the measured FP64 DMMA peak; the int8 path computes those flops
+    exactly as 28 int8 digit-pair products per entry and column (padded to
+    16), reported against the INT8 tensor peak in `int8`."""
     flops = sum(ph["apply_flops"] for ph in report["phases"] if ph["phase"] == "h1")
     ms = sum(ph["apply_ms"] for ph in report["phases"] if ph["phase"] == "h1")
     launches = sum(1 for ph in report["phases"] if ph["phase"] == "h1")
     ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-    return {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": K2_NCU_TRAFFIC, "traffic_source": K2_NCU_SOURCE,
-            "kernel": "sample_apply_kernel (K2)",
-            "launches_per_step": launches, "avg_launch_ms": round(ms / max(launches, 1), 3),
-            "flops_per_step": flops, "peak_source": FP64_PEAK_SOURCE}
+    r = w.rank + w.oversample
+    np_pad = (r + 15) // 16 * 16
+    int8_ops = flops / (4.0 * r) * 28 * 2 * (2 * np_pad)
+    int8_tops = int8_ops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+    int8_path = (not os.environ.get("HP_K2_FP64")) and r <= 64 and not w.dense
+    out = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+           "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": K2_NCU_TRAFFIC, "traffic_source": K2_NCU_SOURCE,
+           "kernel": ("sample_apply_i8_kernel (K2, FP64 apply emulated exactly on the int8 tensor cores)"
+                      if int8_path else "sample_apply_kernel (K2, FP64 DMMA)"),
+           "launches_per_step": launches, "avg_launch_ms": round(ms / max(launches, 1), 3),
+           "flops_per_step": flops, "peak_source": FP64_PEAK_SOURCE,
+           "achieved_meaning": "FP64-equivalent useful flops / K2 time"}
+    if int8_path:
+        out["int8"] = {"achieved_tops": round(int8_tops, 1), "peak_tops": INT8_PEAK_TOPS,
+                       "frac": round(int8_tops / INT8_PEAK_TOPS, 4),
+                       "ops_per_step": int8_ops,
+                       "peak_source": "B200 datasheet dense INT8 (fallback: no INT8 entry in MEASURED_PEAKS.json)"}
+    return out
 
 
 def flush_l2(torch):
@@ -282,7 +299,7 @@ def run_ours(args, ws, rank, local):
     launches = hp.launch_count() - launches0
     t_step = dist_max(float(np.mean(times)), ws, "ours")
     report = last.report
-    roof = k2_roofline(report)
+    roof = k2_roofline(report, w)
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
