@@ -164,7 +164,7 @@ def k2_roofline(report, w):
     np_pad = (r + 15) // 16 * 16
     int8_ops = flops / (4.0 * r) * 28 * 2 * (2 * np_pad)
     int8_tops = int8_ops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
-    int8_path = (not os.environ.get("HP_K2_FP64")) and r <= 64 and not w.dense
+    int8_path = any(ph.get("apply_path") == "int8" for ph in report["phases"] if ph["phase"] == "h1")
     out = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
            "frac": round(ach / FP64_PEAK_TFLOPS, 4), "traffic": K2_NCU_TRAFFIC, "traffic_source": K2_NCU_SOURCE,
            "kernel": ("sample_apply_i8_kernel (K2, FP64 apply emulated exactly on the int8 tensor cores)"
@@ -310,7 +310,7 @@ def run_ours(args, ws, rank, local):
         hd = hp.pinned_empty(max(nd, 1))
         host_pts_src = hp.pinned_empty(pts.size).reshape(pts.shape)
         host_pts_src[...] = pts
-        etimes = []
+        etimes, parts = [], []
         for i in range(max(1, min(args.steps, 2))):
             barrier(ws)
             torch.cuda.synchronize()
@@ -319,14 +319,21 @@ def run_ours(args, ws, rank, local):
             # compress with every level's factors and the dense blocks
             # streamed D2H into hf / hd as soon as they are final
             t_tree = hp.build_tree(host_pts_src, w.leaf)
+            t1 = time.perf_counter()
             o2 = make_operator(hp, w, host_pts_src, local)
+            t2 = time.perf_counter()
             r2 = hp.compress(o2, t_tree, **kw, export_to=(hf, hd))
             hp.device_synchronize()
-            etimes.append(time.perf_counter() - t0)
+            t3 = time.perf_counter()
+            etimes.append(t3 - t0)
+            parts.append((t1 - t0, t2 - t1, t3 - t2))
             del r2, o2
         d2h = (nf + nd) * 8
         e2e = {"value": dist_max(float(np.mean(etimes)), ws, "ours"), "unit": "s",
                "h2d_bytes_per_step": int(pts.size * 8), "d2h_bytes_per_step": int(d2h),
+               "breakdown_s": {"tree_build": round(float(np.mean([p[0] for p in parts])), 4),
+                               "operator_h2d": round(float(np.mean([p[1] for p in parts])), 4),
+                               "compress_with_export": round(float(np.mean([p[2] for p in parts])), 4)},
                "includes": "points from pinned host memory: tree build, operator H2D, compress with every "
                            "factor and dense block streamed D2H into pinned host arrays as levels finish"}
     cpu = None
@@ -337,7 +344,7 @@ def run_ours(args, ws, rank, local):
         return
     phases = [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in ph.items()
                if k in ("phase", "level", "colors", "apply_ms", "peel_ms", "qr_ms", "bsolve_ms", "wall_ms_total",
-                        "host_wait_ms", "start_ms")}
+                        "host_wait_ms", "start_ms", "apply_path")}
               for ph in report["phases"]]
     line = {
         "metric": METRIC, "value": round(t_step, 4), "unit": "s", "n_gpus": args.gpus,

@@ -148,7 +148,8 @@ int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bound
 /* totals[0..6] = forward_cols, adjoint_cols, max_sampling_colors,
  * wall_s_total, wall_s_net, net_flops, setup_ms; *nphases = phase count */
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases);
-/* per phase: is_leaf, level, colors, forward_cols, adjoint_cols, net_flops and
+/* per phase: ints[7] = is_leaf, level, colors, forward_cols, adjoint_cols, net_flops,
+ * apply_path (K2: 0 FP64 DMMA, 1 int8 tensor cores) and
  * times[10] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
  * apply_flops, kernel_evals, host_wait_ms, start_ms (times[10]; device
  * time from the first device work of compress to the phase start) */

@@ -343,12 +343,13 @@ class CompressedRep:
         check(lib().hp_rep_csv(self._h, buf, ln.value + 1, C.byref(ln)))
         phases = []
         for i in range(nph.value):
-            ints = np.zeros(6, dtype=np.int64)
+            ints = np.zeros(7, dtype=np.int64)
             times = np.zeros(10)
             check(lib().hp_rep_phase(self._h, i, lptr(ints), dptr(times)))
             phases.append({
                 "phase": "leaf" if ints[0] else "h1", "level": int(ints[1]), "colors": int(ints[2]),
                 "forward_cols": int(ints[3]), "adjoint_cols": int(ints[4]), "net_flops": int(ints[5]),
+                "apply_path": "int8" if ints[6] else "fp64",
                 "wall_ms_total": times[0], "wall_ms_net": times[1], "apply_ms": times[2],
                 "peel_ms": times[3], "qr_ms": times[4], "bsolve_ms": times[5],
                 "apply_flops": times[6], "kernel_evals": times[7], "host_wait_ms": times[8],

@@ -517,6 +517,7 @@ int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times)
       ints[3] = ph.forward_cols;
       ints[4] = ph.adjoint_cols;
       ints[5] = ph.net_flops;
+      ints[6] = ph.apply_path;
     }
     if (times) {
       times[0] = ph.wall_ms_total;

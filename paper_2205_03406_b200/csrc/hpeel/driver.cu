@@ -510,7 +510,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     std::vector<std::unique_ptr<LevelTimers>> timers(size_t(tree->depth()) + 1);
     std::vector<std::int64_t> rank_off(size_t(tree->depth()) + 1, 0);
     std::vector<double> evals(size_t(tree->depth()) + 1, 0.0), peel_flops(size_t(tree->depth()) + 1, 0.0);
-    std::vector<int> colors(size_t(tree->depth()) + 1, 0);
+    std::vector<int> colors(size_t(tree->depth()) + 1, 0), apply_path(size_t(tree->depth()) + 1, 0);
     std::vector<std::int64_t> fcols(size_t(tree->depth()) + 1, 0);
     std::int64_t roff = 0;
     int built = 1;
@@ -573,6 +573,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       // unchecked tiles, r <= 64 (7 accumulator groups x r fit TMEM)
       const bool use_i8 = op.kind() != kOpDense && op.symmetric() && !checked && r <= 64 &&
                           k2_mode() == 0 && k2_int8_enabled();
+      apply_path[size_t(l)] = use_i8 ? 1 : 0;
       DevBuf<unsigned char> bdig;
       DevBuf<std::int64_t> d_step_off, d_pb_off;
       DevBuf<double> xstep;
@@ -752,6 +753,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       ph.phase = "h1";
       ph.level = l;
       ph.colors = colors[size_t(l)];
+      ph.apply_path = apply_path[size_t(l)];
       ph.forward_cols = fcols[size_t(l)];
       ph.adjoint_cols = fcols[size_t(l)];
       ph.kernel_evals = evals[size_t(l)];

@@ -70,6 +70,7 @@ struct PhaseReport {
   double kernel_evals = 0.0;
   double host_wait_ms = 0.0;      // driver thread blocked on this phase's host plan
   double start_ms = 0.0;          // device time from the first device work of compress to this phase
+  int apply_path = 0;             // K2 arithmetic: 0 FP64 DMMA, 1 int8 tensor-core emulation
 };
 
 struct RunReport {
