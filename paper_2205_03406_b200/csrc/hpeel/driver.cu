@@ -732,6 +732,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       }
     }
     rep->dense_ready = true;
+    static const bool drv_timing = std::getenv("HP_DRIVER_TIMING") != nullptr;
+    const auto t_report = Clock::now();
 
     // ------------------------------------------------------------- report
     double blackbox_ms = 0.0;
@@ -807,6 +809,11 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       if (p.phase != "leaf") report.max_sampling_colors = std::max(report.max_sampling_colors, p.colors);
     }
     report.wall_s_total = std::chrono::duration<double>(Clock::now() - t_begin).count();
+    if (drv_timing)
+      std::fprintf(stderr, "[driver] device drained at %.1f ms, report %.1f ms, total %.1f ms\n",
+                   std::chrono::duration<double, std::milli>(t_report - t_begin).count(),
+                   std::chrono::duration<double, std::milli>(Clock::now() - t_report).count(),
+                   report.wall_s_total * 1e3);
     report.wall_s_net = report.wall_s_total - blackbox_ms * 1e-3;
   } catch (...) {
     cudaStreamSynchronize(s);

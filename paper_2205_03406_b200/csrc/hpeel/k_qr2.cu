@@ -51,9 +51,11 @@ __device__ __forceinline__ void set_row(double (&x)[RPT], int i, double v) {
 #undef HP_SET
 }
 
+// sum over the TPC threads of one column (lanes CPW apart, CPW = 32 / TPC)
+template <int TPC>
 __device__ __forceinline__ double group_sum(double v) {
-  v += __shfl_xor_sync(0xffffffffu, v, 8);
-  v += __shfl_xor_sync(0xffffffffu, v, 16);
+#pragma unroll
+  for (int o = 32 / TPC; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
@@ -67,13 +69,13 @@ __device__ __forceinline__ double tail_sq(const double (&x)[RPT], int r0, int j)
   return s;
 }
 
-template <int NC, int RPT>
+template <int NC, int RPT, int TPC>
 struct QrShared {
-  double v[2][4][RPT + 2];  // reflector (double-buffered), per row group (padded)
+  double v[2][TPC][RPT + 2];  // reflector (double-buffered), per row group (padded)
   double tau[NC];
   double beta[NC];
-  double best[2][NC / 8];   // per-warp argmax of the next step (double-buffered)
-  int bidx[2][NC / 8];
+  double best[2][NC * TPC / 32];   // per-warp argmax of the next step (double-buffered)
+  int bidx[2][NC * TPC / 32];
   int perm[NC];
   int keep;
 };
@@ -98,7 +100,7 @@ __device__ __forceinline__ double2 lds2(const double* p) {
 // x -= tau * v * (v^T x) over the column (all four row groups reduce). The
 // reflector is read in 8-row slices through volatile loads fenced on the
 // running sums, so at most one slice is live in registers next to the column.
-template <int RPT>
+template <int TPC, int RPT>
 __device__ __forceinline__ double reflect(double (&x)[RPT], const double* v, double tau) {
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -111,7 +113,7 @@ __device__ __forceinline__ double reflect(double (&x)[RPT], const double* v, dou
     }
     asm volatile("" : "+d"(s0), "+d"(s1));
   }
-  const double w = group_sum(s0 + s1) * tau;
+  const double w = group_sum<TPC>(s0 + s1) * tau;
 #pragma unroll
   for (int i0 = 0; i0 < RPT; i0 += 8) {
 #pragma unroll
@@ -131,16 +133,22 @@ __device__ __forceinline__ double reflect(double (&x)[RPT], const double* v, dou
 // tail norm and pivot-row value they computed in step j - 1 and publish it;
 // one barrier; every column applies it, then computes its exact remaining
 // norm (rows >= j + 1) and the warp-local argmax for step j + 1; one barrier.
-template <int NC, int RPT, int MODE>
-__global__ void __launch_bounds__(NC * 4, (NC * 4 * (RPT * 2 + 48) <= 32768) ? 2 : 1)
+// CTAs per SM the register budget allows (x[RPT] doubles + ~48 registers)
+__host__ __device__ constexpr int qr_min_blocks(int threads, int rpt) {
+  return threads * (rpt * 2 + 48) <= 32768 ? 2 : 1;
+}
+
+template <int NC, int RPT, int MODE, int TPC>
+__global__ void __launch_bounds__(NC * TPC, qr_min_blocks(NC * TPC, RPT))
 qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, double* tau_out,
               int* ranks, int n, int kmax, double tol) {
-  __shared__ __align__(16) QrShared<NC, RPT> sm;
+  constexpr int CPW = 32 / TPC;  // columns per warp
+  __shared__ __align__(16) QrShared<NC, RPT, TPC> sm;
   const QrBlock b = blocks[blockIdx.x];
   const int m = b.rows;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int g = (lane >> 3) & 3;
-  const int c = warp * 8 + (lane & 7);
+  const int g = lane / CPW;
+  const int c = warp * CPW + (lane % CPW);
   const int r0 = g * RPT;
   const bool valid = c < n;
 
@@ -162,13 +170,13 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
   double sig = 0.0, arow = 0.0;
   auto stats = [&](int j, int buf) {
     const int gj = j / RPT, ij = j - gj * RPT;
-    sig = group_sum(tail_sq(x, r0, j));
-    arow = __shfl_sync(0xffffffffu, get_row(x, ij), (lane & 7) | (gj << 3));
+    sig = group_sum<TPC>(tail_sq(x, r0, j));
+    arow = __shfl_sync(0xffffffffu, get_row(x, ij), (lane % CPW) + gj * CPW);
     if (MODE == 0) {
       double key = done ? -1.0 : fma(arow, arow, sig);
       int kidx = c;
 #pragma unroll
-      for (int o = 1; o < 8; o <<= 1) {
+      for (int o = 1; o < CPW; o <<= 1) {
         const double ok = __shfl_xor_sync(0xffffffffu, key, o);
         const int oi = __shfl_xor_sync(0xffffffffu, kidx, o);
         if (ok > key || (ok == key && oi < kidx)) {
@@ -193,7 +201,7 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
       double bk = sm.best[j & 1][0];
       p = sm.bidx[j & 1][0];
 #pragma unroll
-      for (int w = 1; w < NC / 8; ++w)
+      for (int w = 1; w < NC / CPW; ++w)
         if (sm.best[j & 1][w] > bk) {
           bk = sm.best[j & 1][w];
           p = sm.bidx[j & 1][w];
@@ -224,7 +232,7 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
     }
     __syncthreads();
     const double tau = sm.tau[j];
-    if (tau != 0.0) reflect(x, vj[g], done ? 0.0 : tau);
+    if (tau != 0.0) reflect<TPC>(x, vj[g], done ? 0.0 : tau);
     if (j + 1 < steps) stats(j + 1, (j + 1) & 1);
     __syncthreads();
   }
@@ -241,7 +249,7 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
       for (int i = 0; i < RPT; ++i)
         if (i < kk - r0) rdst[i] = r0 + i <= c ? x[i] : 0.0;
     }
-    for (int jj = t; jj < kk; jj += NC * 4) tau_out[b.tau + jj] = sm.tau[jj];
+    for (int jj = t; jj < kk; jj += NC * TPC) tau_out[b.tau + jj] = sm.tau[jj];
     return;
   }
 
@@ -265,7 +273,7 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
     if (owner) publish_v(vj, x, g, r0, j);
     __syncthreads();
     const double tau = sm.tau[j];
-    if (tau != 0.0) reflect(x, vj[g], li > j && li < keep ? tau : 0.0);
+    if (tau != 0.0) reflect<TPC>(x, vj[g], li > j && li < keep ? tau : 0.0);
     if (owner) {
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
@@ -275,7 +283,7 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
     }
   }
   // Q columns to out (zero beyond keep)
-  for (int e = t; e < m * kmax; e += NC * 4) {
+  for (int e = t; e < m * kmax; e += NC * TPC) {
     const int col = e / m;
     if (col >= keep) out[b.out + (e - col * m) + std::int64_t(col) * b.ldo] = 0.0;
   }
@@ -289,18 +297,19 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
 
 // out(rows x kmax) = H_0..H_{kk-1} [C; 0]: X columns on threads, reflectors
 // streamed from the chunk's in-place storage.
-template <int NC, int RPT>
-__global__ void __launch_bounds__(NC * 4, (NC * 4 * (RPT * 2 + 48) <= 32768) ? 2 : 1)
+template <int NC, int RPT, int TPC>
+__global__ void __launch_bounds__(NC * TPC, qr_min_blocks(NC * TPC, RPT))
 qr_reg_backprop_kernel(const QrBlock* __restrict__ blocks, const double* data,
                        const double* __restrict__ tau, const double* parent, double* outbuf, int n,
                        int kmax) {
-  __shared__ __align__(16) double vs[2][4][RPT + 2];
+  constexpr int CPW = 32 / TPC;
+  __shared__ __align__(16) double vs[2][TPC][RPT + 2];
   const QrBlock b = blocks[blockIdx.x];
   const int m = b.rows;
   const int kk = m < n ? m : n;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int g = (lane >> 3) & 3;
-  const int c = warp * 8 + (lane & 7);
+  const int g = lane / CPW;
+  const int c = warp * CPW + (lane % CPW);
   const int r0 = g * RPT;
   const bool valid = c < kmax;
   double x[RPT];
@@ -311,7 +320,7 @@ qr_reg_backprop_kernel(const QrBlock* __restrict__ blocks, const double* data,
     for (int i = 0; i < RPT; ++i) x[i] = i < lim ? src[i] : 0.0;
   }
   auto stage = [&](int j, int buf) {
-    for (int r = t; r < 4 * RPT; r += NC * 4) {
+    for (int r = t; r < TPC * RPT; r += NC * TPC) {
       const int gg = r / RPT, ii = r - gg * RPT;
       vs[buf][gg][ii] = r > j && r < m ? data[b.a + r + std::int64_t(j) * b.lda] : (r == j ? 1.0 : 0.0);
     }
@@ -321,7 +330,7 @@ qr_reg_backprop_kernel(const QrBlock* __restrict__ blocks, const double* data,
   for (int j = kk - 1; j >= 0; --j) {
     if (j > 0) stage(j - 1, (j - 1) & 1);
     const double tj = tau[b.tau + j];
-    if (tj != 0.0) reflect(x, vs[j & 1][g], valid ? tj : 0.0);
+    if (tj != 0.0) reflect<TPC>(x, vs[j & 1][g], valid ? tj : 0.0);
     __syncthreads();
   }
   if (valid) {
@@ -336,15 +345,28 @@ qr_reg_backprop_kernel(const QrBlock* __restrict__ blocks, const double* data,
 
 int qr_reg_cols(int cols) { return cols <= 32 ? 32 : cols <= 48 ? 48 : cols <= 64 ? 64 : cols <= 80 ? 80 : cols <= 96 ? 96 : 0; }
 
+// threads per column: 8 (a column's rows split over 8 threads: half the
+// dependent FMA chain of every Householder step and 1/2 the registers of the
+// 4-thread layout); HP_QR_TPC=4 selects the earlier layout for A/B runs
+// (NC <= 64; wider blocks keep 4 threads per column so a block still holds
+// 2r rows for TSQR within the register budget)
+#ifndef HP_QR_TPC
+#define HP_QR_TPC 8
+#endif
+constexpr int tpc_for(int nc) { return nc <= 64 ? HP_QR_TPC : 4; }
+
 int qr_reg_rows_max(int cols) {
   const int nc = qr_reg_cols(cols);
   if (nc == 0) return 0;
+  if (tpc_for(nc) == 8) return 8 * 32;
   return nc <= 64 ? 4 * 64 : 4 * 48;  // RPT cap: 64 (<= 256 threads) or 48 (register budget)
 }
 
 namespace {
 int rpt_for(int nc, int max_rows) {
-  const int need = (max_rows + 3) / 4;
+  const int tpc = tpc_for(nc);
+  const int need = (max_rows + tpc - 1) / tpc;
+  if (tpc == 8) return need <= 8 ? 8 : need <= 16 ? 16 : 32;
   const int cap = nc <= 64 ? 64 : 48;
   const int r = need <= 16 ? 16 : need <= 32 ? 32 : need <= 48 ? 48 : 64;
   return std::min(r, cap);
@@ -353,34 +375,57 @@ int rpt_for(int nc, int max_rows) {
 template <int NC, int RPT>
 void launch_reg(int mode, const QrBlock* blocks, int nb, double* data, double* out, double* tau, int* ranks,
                 int cols, int kmax, double tol, cudaStream_t s) {
+  constexpr int T = tpc_for(NC);
   if (mode == 0)
-    qr_reg_kernel<NC, RPT, 0><<<nb, NC * 4, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
+    qr_reg_kernel<NC, RPT, 0, T><<<nb, NC * T, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
   else
-    qr_reg_kernel<NC, RPT, 1><<<nb, NC * 4, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
+    qr_reg_kernel<NC, RPT, 1, T><<<nb, NC * T, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
 }
 
 template <int NC>
 void launch_reg_nc(int mode, int rpt, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
                    int* ranks, int cols, int kmax, double tol, cudaStream_t s) {
-  switch (rpt) {
-    case 16: return launch_reg<NC, 16>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-    case 32: return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-    case 48: return launch_reg<NC, 48>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-    default:
-      if constexpr (NC <= 64) return launch_reg<NC, 64>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+  if constexpr (tpc_for(NC) == 8) {
+    switch (rpt) {
+      case 8: return launch_reg<NC, 8>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+      case 16: return launch_reg<NC, 16>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+      default: return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+    }
+  } else {
+    switch (rpt) {
+      case 16: return launch_reg<NC, 16>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+      case 32: return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+      case 48: return launch_reg<NC, 48>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+      default:
+        if constexpr (NC <= 64) return launch_reg<NC, 64>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+    }
   }
+}
+
+template <int NC, int RPT>
+void launch_bp(const QrBlock* blocks, int nb, const double* data, const double* tau, const double* parent,
+               double* outbuf, int cols, int kmax, cudaStream_t s) {
+  constexpr int T = tpc_for(NC);
+  qr_reg_backprop_kernel<NC, RPT, T><<<nb, NC * T, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax);
 }
 
 template <int NC>
 void launch_bp_nc(int rpt, const QrBlock* blocks, int nb, const double* data, const double* tau,
                   const double* parent, double* outbuf, int cols, int kmax, cudaStream_t s) {
-  switch (rpt) {
-    case 16: qr_reg_backprop_kernel<NC, 16><<<nb, NC * 4, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax); return;
-    case 32: qr_reg_backprop_kernel<NC, 32><<<nb, NC * 4, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax); return;
-    case 48: qr_reg_backprop_kernel<NC, 48><<<nb, NC * 4, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax); return;
-    default:
-      if constexpr (NC <= 64)
-        qr_reg_backprop_kernel<NC, 64><<<nb, NC * 4, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax);
+  if constexpr (tpc_for(NC) == 8) {
+    switch (rpt) {
+      case 8: return launch_bp<NC, 8>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+      case 16: return launch_bp<NC, 16>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+      default: return launch_bp<NC, 32>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+    }
+  } else {
+    switch (rpt) {
+      case 16: return launch_bp<NC, 16>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+      case 32: return launch_bp<NC, 32>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+      case 48: return launch_bp<NC, 48>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+      default:
+        if constexpr (NC <= 64) return launch_bp<NC, 64>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+    }
   }
 }
 }  // namespace
@@ -390,7 +435,7 @@ void launch_qr_reg(int mode, const QrBlock* blocks, int nb, double* data, double
   if (nb == 0) return;
   const int nc = qr_reg_cols(cols);
   const int rpt = rpt_for(nc, max_rows);
-  if (max_rows > 4 * rpt || nc == 0) throw std::invalid_argument("qr_reg: block too large");
+  if (nc == 0 || max_rows > tpc_for(nc) * rpt) throw std::invalid_argument("qr_reg: block too large");
   switch (nc) {
     case 32: launch_reg_nc<32>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
     case 48: launch_reg_nc<48>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
@@ -407,7 +452,7 @@ void launch_qr_reg_backprop(const QrBlock* blocks, int nb, const double* data, c
   if (nb == 0) return;
   const int nc = qr_reg_cols(kmax);
   const int rpt = rpt_for(nc, max_rows);
-  if (max_rows > 4 * rpt || nc == 0) throw std::invalid_argument("qr_reg backprop: block too large");
+  if (nc == 0 || max_rows > tpc_for(nc) * rpt) throw std::invalid_argument("qr_reg backprop: block too large");
   switch (nc) {
     case 32: launch_bp_nc<32>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
     case 48: launch_bp_nc<48>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
