@@ -77,8 +77,15 @@ struct LevelWork {
   double evals = 0;
   bool has_peel = false;
   PeelPlan peel;
-  QrPlan qr;
-  GramPlan g_mid, g_gpu, g_vg;
+  // K4/K5 per shard: shard q owns pairs [fb[q], fb[q+1]) and
+  // computes their U, V (QR), grams and B; factor segments are then shared
+  struct Shard45 {
+    std::int64_t p0 = 0, p1 = 0;
+    QrPlan qr;
+    GramPlan g_mid, g_gpu, g_vg;
+  };
+  std::vector<Shard45> s45;
+  std::vector<std::int64_t> fb;
 };
 
 LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig& cfg) {
@@ -207,27 +214,38 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
     lap("plan_peel");
     w.has_peel = true;
   }
-  // K5a middle = G'_a^T Y_p; K4 QR; K5b grams
+  // K5a middle = G'_a^T Y_p; K4 QR; K5b grams -- per shard, on the pairs it
+  // owns (outputs by pair: U_p from Y_p, V_p from Z of swap(p))
   const int gld = 2 * r;
-  std::vector<GramReq> mid(np), gu(np), vg(np);
-  std::vector<QrRequest> qr;
-  qr.reserve(2 * np);
-  for (size_t p = 0; p < np; ++p) {
-    const auto [a, b] = ld.pairs[p];
-    const int rows = e.count(a);
-    mid[p] = GramReq{e.start(a) * gld + r, w.soff[p], rows, gld, rows, 1, 0};
-    gu[p] = GramReq{e.start(a) * gld + r, ld.uoff[p], rows, gld, rows, 1, 0};
-    vg[p] = GramReq{ld.voff[p], e.start(b) * gld, e.count(b), e.count(b), gld, 0, 1};
-    qr.push_back(QrRequest{w.soff[p], ld.uoff[p], rows, rows, int(p)});
-    qr.push_back(QrRequest{w.soff[p] + std::int64_t(rows) * r, ld.voff[size_t(w.swap[p])], rows, rows,
-                           int(np + size_t(w.swap[p]))});
+  {
+    std::vector<double> w45(np);
+    for (size_t p = 0; p < np; ++p)
+      w45[p] = double(e.count(ld.pairs[p].first) + e.count(ld.pairs[p].second)) * double(r) * double(r);
+    w.fb = partition_ranges(w45, world);
   }
-  lap("pre-gram");
-  w.g_mid = plan_gram(mid, r, r);
-  w.g_gpu = plan_gram(gu, r, k);
-  w.g_vg = plan_gram(vg, k, r);
-  lap("grams");
-  w.qr = plan_qr(qr, r, k);
+  w.s45.resize(size_t(world));
+  for (int q = 0; q < world; ++q) {
+    LevelWork::Shard45& sh = w.s45[size_t(q)];
+    sh.p0 = w.fb[size_t(q)];
+    sh.p1 = w.fb[size_t(q) + 1];
+    std::vector<GramReq> mid, gu, vg;
+    std::vector<QrRequest> qr;
+    for (std::int64_t p = sh.p0; p < sh.p1; ++p) {
+      const auto [a, b] = ld.pairs[size_t(p)];
+      const int rows = e.count(a), rows_b = e.count(b);
+      const std::int64_t sp = w.swap[size_t(p)];  // block (b, a): its adjoint columns give V_p
+      mid.push_back(GramReq{e.start(a) * gld + r, w.soff[size_t(p)], rows, gld, rows, 1, 0});
+      gu.push_back(GramReq{e.start(a) * gld + r, ld.uoff[size_t(p)], rows, gld, rows, 1, 0});
+      vg.push_back(GramReq{ld.voff[size_t(p)], e.start(b) * gld, rows_b, rows_b, gld, 0, 1});
+      qr.push_back(QrRequest{w.soff[size_t(p)], ld.uoff[size_t(p)], rows, rows, int(p)});
+      qr.push_back(QrRequest{w.soff[size_t(sp)] + std::int64_t(rows_b) * r, ld.voff[size_t(p)], rows_b, rows_b,
+                             int(np + size_t(p))});
+    }
+    sh.g_mid = plan_gram(mid, r, r);
+    sh.g_gpu = plan_gram(gu, r, k);
+    sh.g_vg = plan_gram(vg, k, r);
+    sh.qr = plan_qr(qr, r, k);
+  }
   lap("plan_qr");
   return w;
 }
@@ -638,27 +656,47 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         rep->captured[l] = std::move(cap);
       }
 
-      // K5a: middle = G'_a^T Y_p before the QR overwrites Y
+      // K5a: middle = G'_a^T Y_p before the QR overwrites Y; K4 QR; K5b grams
+      // and B -- each shard on its own pairs, then the shards' factor and
+      // rank segments are broadcast
       DevBuf<double> middle(np * size_t(r) * size_t(r), s), gpu(np * size_t(r) * size_t(k), s),
           vg(np * size_t(k) * size_t(r), s);
-      HP_CUDA(cudaEventRecord(tm->mid.a, s));
-      run_gram(w.g_mid, g.get(), samples.get(), middle.get(), s);
-      HP_CUDA(cudaEventRecord(tm->mid.b, s));
-
-      // K4 QR: U_p from Y_p, V_swap(p) from Z_p
       DevBuf<int> d_ranks(2 * np, s);
-      HP_CUDA(cudaEventRecord(tm->qr.a, s));
-      run_qr(w.qr, samples.get(), rep->d_factors, d_ranks.get(), r, k, s);
-      HP_CUDA(cudaEventRecord(tm->qr.b, s));
-
-      // K5b: gpU = G'^T U, VG = V^T G, B
-      HP_CUDA(cudaEventRecord(tm->bsolve.a, s));
-      run_gram(w.g_gpu, g.get(), rep->d_factors, gpu.get(), s);
-      run_gram(w.g_vg, rep->d_factors, g.get(), vg.get(), s);
       DevBuf<std::int64_t> d_boff;
       d_boff.upload(ld.boff, s);
-      launch_bsolve(int(np), gpu.get(), middle.get(), vg.get(), r, k, kPinvCutoff, d_boff.get(),
-                    rep->d_factors, s);
+      auto mine = [&](int sr) { return my_rank < 0 || sr == my_rank; };
+      HP_CUDA(cudaEventRecord(tm->mid.a, s));
+      for (int sr = 0; sr < int(w.s45.size()); ++sr)
+        if (mine(sr))
+          run_gram(w.s45[size_t(sr)].g_mid, g.get(), samples.get(),
+                   middle.get() + w.s45[size_t(sr)].p0 * r * r, s);
+      HP_CUDA(cudaEventRecord(tm->mid.b, s));
+      HP_CUDA(cudaEventRecord(tm->qr.a, s));
+      for (int sr = 0; sr < int(w.s45.size()); ++sr)
+        if (mine(sr)) run_qr(w.s45[size_t(sr)].qr, samples.get(), rep->d_factors, d_ranks.get(), r, k, s);
+      HP_CUDA(cudaEventRecord(tm->qr.b, s));
+      HP_CUDA(cudaEventRecord(tm->bsolve.a, s));
+      for (int sr = 0; sr < int(w.s45.size()); ++sr) {
+        if (!mine(sr)) continue;
+        const LevelWork::Shard45& sh = w.s45[size_t(sr)];
+        run_gram(sh.g_gpu, g.get(), rep->d_factors, gpu.get() + sh.p0 * r * k, s);
+        run_gram(sh.g_vg, rep->d_factors, g.get(), vg.get() + sh.p0 * k * r, s);
+        launch_bsolve(int(sh.p1 - sh.p0), gpu.get() + sh.p0 * r * k, middle.get() + sh.p0 * r * r,
+                      vg.get() + sh.p0 * k * r, r, k, kPinvCutoff, d_boff.get() + sh.p0, rep->d_factors, s);
+      }
+      if (config.comm && np > 0) {
+        const std::int64_t fend = ld.boff[np - 1] + std::int64_t(k) * k;
+        std::vector<std::int64_t> fseg(w.fb.size()), useg(w.fb.size()), vseg(w.fb.size());
+        for (size_t q = 0; q < w.fb.size(); ++q) {
+          const std::int64_t p = w.fb[q];
+          fseg[q] = p < std::int64_t(np) ? ld.uoff[size_t(p)] : fend;
+          useg[q] = p;
+          vseg[q] = std::int64_t(np) + p;
+        }
+        config.comm->broadcast_segments(rep->d_factors, fseg, s);
+        config.comm->broadcast_segments_i32(d_ranks.get(), useg, s);
+        config.comm->broadcast_segments_i32(d_ranks.get(), vseg, s);
+      }
       HP_CUDA(cudaEventRecord(tm->bsolve.b, s));
       HP_CUDA(cudaMemcpyAsync(h_ranks + roff, d_ranks.get(), 2 * np * sizeof(int), cudaMemcpyDeviceToHost, s));
       rank_off[size_t(l)] = roff;

@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include <algorithm>
+#include <map>
 #include <limits>
 #include <unordered_map>
 
@@ -224,47 +225,56 @@ void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, in
     for (const QrBlock& b : v) m = std::max(m, b.rows);
     return m;
   };
+  // register kernels: one launch per rows-per-thread class, so a block's
+  // arithmetic does not depend on which other blocks share its batch (sharded
+  // runs reproduce the unsharded factors bit for bit)
+  auto by_class = [&](const std::vector<QrBlock>& v, int cols, auto&& launch) {
+    if (v.empty()) return;
+    if (!pl.reg) {
+      DevBuf<QrBlock> d;
+      d.upload(v, s);
+      launch(d.get(), int(v.size()), max_rows(v));
+      return;
+    }
+    std::map<int, std::vector<QrBlock>> cls;
+    for (const QrBlock& b : v) cls[qr_reg_rpt(cols, b.rows)].push_back(b);
+    for (auto& [rpt, list] : cls) {
+      DevBuf<QrBlock> d;
+      d.upload(list, s);
+      launch(d.get(), int(list.size()), max_rows(list));
+    }
+  };
   DevBuf<double> w(size_t(std::max<std::int64_t>(pl.wsize, 1)), s);
   DevBuf<double> tau(size_t(std::max<std::int64_t>(pl.tausize, 1)), s);
-  if (!pl.direct.empty()) {
-    DevBuf<QrBlock> d;
-    d.upload(pl.direct, s);
+  by_class(pl.direct, r, [&](const QrBlock* d, int nb, int mr) {
     if (pl.reg)
-      launch_qr_reg(0, d.get(), int(pl.direct.size()), data, out, nullptr, d_ranks, r, kmax, kQrRankDropTol,
-                    max_rows(pl.direct), s);
+      launch_qr_reg(0, d, nb, data, out, nullptr, d_ranks, r, kmax, kQrRankDropTol, mr, s);
     else
-      launch_qr_top(d.get(), int(pl.direct.size()), data, out, d_ranks, r, kmax, kQrRankDropTol,
-                    max_rows(pl.direct), s);
-  }
+      launch_qr_top(d, nb, data, out, d_ranks, r, kmax, kQrRankDropTol, mr, s);
+  });
   for (size_t rd = 0; rd < pl.chunk_rounds.size(); ++rd) {
-    DevBuf<QrBlock> d;
-    d.upload(pl.chunk_rounds[rd], s);
-    if (pl.reg)
-      launch_qr_reg(1, d.get(), int(pl.chunk_rounds[rd].size()), rd == 0 ? data : w.get(), w.get(),
-                    tau.get(), nullptr, r, kmax, 0.0, max_rows(pl.chunk_rounds[rd]), s);
-    else
-      launch_qr_chunk(d.get(), int(pl.chunk_rounds[rd].size()), rd == 0 ? data : w.get(), w.get(),
-                      tau.get(), r, max_rows(pl.chunk_rounds[rd]), s);
+    by_class(pl.chunk_rounds[rd], r, [&](const QrBlock* d, int nb, int mr) {
+      if (pl.reg)
+        launch_qr_reg(1, d, nb, rd == 0 ? data : w.get(), w.get(), tau.get(), nullptr, r, kmax, 0.0, mr, s);
+      else
+        launch_qr_chunk(d, nb, rd == 0 ? data : w.get(), w.get(), tau.get(), r, mr, s);
+    });
   }
-  if (!pl.tops.empty()) {
-    DevBuf<QrBlock> d;
-    d.upload(pl.tops, s);
+  by_class(pl.tops, r, [&](const QrBlock* d, int nb, int mr) {
     if (pl.reg)
-      launch_qr_reg(0, d.get(), int(pl.tops.size()), w.get(), w.get(), nullptr, d_ranks, r, kmax,
-                    kQrRankDropTol, max_rows(pl.tops), s);
+      launch_qr_reg(0, d, nb, w.get(), w.get(), nullptr, d_ranks, r, kmax, kQrRankDropTol, mr, s);
     else
-      launch_qr_top(d.get(), int(pl.tops.size()), w.get(), w.get(), d_ranks, r, kmax, kQrRankDropTol,
-                    max_rows(pl.tops), s);
-  }
+      launch_qr_top(d, nb, w.get(), w.get(), d_ranks, r, kmax, kQrRankDropTol, mr, s);
+  });
   for (size_t rd = pl.back_rounds.size(); rd-- > 0;) {
-    DevBuf<QrBlock> d;
-    d.upload(pl.back_rounds[rd], s);
-    if (pl.reg)
-      launch_qr_reg_backprop(d.get(), int(pl.back_rounds[rd].size()), rd == 0 ? data : w.get(), tau.get(),
-                             w.get(), rd == 0 ? out : w.get(), r, kmax, max_rows(pl.back_rounds[rd]), s);
-    else
-      launch_qr_backprop(d.get(), int(pl.back_rounds[rd].size()), rd == 0 ? data : w.get(), tau.get(),
-                         w.get(), rd == 0 ? out : w.get(), r, kmax, max_rows(pl.back_rounds[rd]), s);
+    by_class(pl.back_rounds[rd], kmax, [&](const QrBlock* d, int nb, int mr) {
+      if (pl.reg)
+        launch_qr_reg_backprop(d, nb, rd == 0 ? data : w.get(), tau.get(), w.get(), rd == 0 ? out : w.get(), r,
+                               kmax, mr, s);
+      else
+        launch_qr_backprop(d, nb, rd == 0 ? data : w.get(), tau.get(), w.get(), rd == 0 ? out : w.get(), r, kmax,
+                           mr, s);
+    });
   }
 }
 

@@ -430,6 +430,8 @@ void launch_bp_nc(int rpt, const QrBlock* blocks, int nb, const double* data, co
 }
 }  // namespace
 
+int qr_reg_rpt(int cols, int rows) { return rpt_for(qr_reg_cols(cols), rows); }
+
 void launch_qr_reg(int mode, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
                    int* ranks, int cols, int kmax, double tol, int max_rows, cudaStream_t s) {
   if (nb == 0) return;

@@ -189,6 +189,9 @@ void launch_qr_backprop(const QrBlock* blocks, int nb, const double* data, const
 /// mode 0 = launch_qr_top contract, mode 1 = launch_qr_chunk contract.
 int qr_reg_cols(int cols);
 int qr_reg_rows_max(int cols);
+/// rows per thread the register kernels use for a block of `rows` rows; a
+/// block's arithmetic depends only on this, so batches are launched per class
+int qr_reg_rpt(int cols, int rows);
 void launch_qr_reg(int mode, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
                    int* ranks, int cols, int kmax, double tol, int max_rows, cudaStream_t s);
 /// launch_qr_backprop contract, kmax <= 96, rows <= qr_reg_rows_max(kmax).

@@ -38,7 +38,7 @@ struct NcclUniqueId {
   char internal[128];
 };
 using ncclComm_t = void*;
-enum NcclDataType { kNcclFloat64 = 8 };
+enum NcclDataType { kNcclInt32 = 2, kNcclFloat64 = 8 };
 enum NcclRedOp { kNcclMax = 2 };
 
 struct NcclApi {
@@ -114,6 +114,18 @@ void Comm::broadcast_segments(double* buf, const std::vector<std::int64_t>& off,
     if (n <= 0) continue;
     double* p = buf + off[size_t(r)];
     check(nccl().Broadcast(p, p, size_t(n), kNcclFloat64, r, comm_, s), "ncclBroadcast");
+  }
+  check(nccl().GroupEnd(), "ncclGroupEnd");
+}
+
+void Comm::broadcast_segments_i32(int* buf, const std::vector<std::int64_t>& off, cudaStream_t s) {
+  if (world_ == 1) return;
+  check(nccl().GroupStart(), "ncclGroupStart");
+  for (int r = 0; r < world_; ++r) {
+    const std::int64_t n = off[size_t(r) + 1] - off[size_t(r)];
+    if (n <= 0) continue;
+    int* p = buf + off[size_t(r)];
+    check(nccl().Broadcast(p, p, size_t(n), kNcclInt32, r, comm_, s), "ncclBroadcast");
   }
   check(nccl().GroupEnd(), "ncclGroupEnd");
 }

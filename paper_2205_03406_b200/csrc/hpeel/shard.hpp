@@ -4,7 +4,9 @@
 // the black-box apply (K2) and the leaf probes (K6) -- the dominant work --
 // are split into contiguous, work-balanced ranges of pairs, and each rank's
 // freshly computed sample rows are broadcast to the others with NCCL over
-// NVLink before the (replicated, deterministic) peeling, QR and B solves.
+// NVLink before the (replicated, deterministic) peeling; the per-pair QR and
+// B solves (K4/K5) are split by pair ranges as well and their factor and
+// rank segments broadcast.
 // NCCL is loaded at run time (libnccl.so.2; the torch-bundled copy when torch
 // already loaded it), so single-GPU use has no NCCL dependency.
 #pragma once
@@ -33,6 +35,7 @@ class Comm {
   int device() const { return device_; }
   /// In place: rank r's segment [off[r], off[r+1]) of `buf` reaches every rank.
   void broadcast_segments(double* buf, const std::vector<std::int64_t>& off, cudaStream_t s);
+  void broadcast_segments_i32(int* buf, const std::vector<std::int64_t>& off, cudaStream_t s);
   void all_reduce_max(double* dev_value, cudaStream_t s);
 
  private:

@@ -1,7 +1,8 @@
-"""Sharded black-box apply on one GPU by emulation: splitting the K2 / K6
-launches into the per-rank work ranges (as N ranks would before their NCCL
-broadcast) reproduces the single-rank samples, factors and dense blocks bit
-for bit (each tile is computed by exactly one rank)."""
+"""Sharded compression on one GPU by emulation: splitting the K2 / K6
+launches and the per-pair K4 QR / K5 B-solve batches into the per-rank work
+ranges (as N ranks would before their NCCL broadcasts of samples, factors and
+ranks) reproduces the single-rank samples, factors and dense blocks bit for
+bit (each tile and each pair is computed by exactly one rank)."""
 import numpy as np
 import pytest
 
@@ -10,9 +11,10 @@ from paper_2205_03406_b200 import configs
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("shards", [2, 3, 8])
-def test_emulated_shards_bit_identical(hp, gpu_available, shards):
-    w = configs.scaled("c3", 16384)
+@pytest.mark.parametrize("name,n,shards", [("c3", 16384, 2), ("c3", 16384, 3), ("c3", 16384, 8),
+                                           ("c4", 16384, 3)])
+def test_emulated_shards_bit_identical(hp, gpu_available, name, n, shards):
+    w = configs.scaled(name, n)
     pts = w.points()
     t = hp.build_tree(pts, w.leaf)
     op = hp.kernel_operator(w.kernel, pts, w.param)
