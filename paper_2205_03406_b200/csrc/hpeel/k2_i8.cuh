@@ -387,6 +387,16 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
                            bd0 + std::uint64_t(((g - a) * NP * kStepK) >> 4), kIdesc, (fresh && a == 0) ? 0u : 1u);
               }
             }
+            if (dbg & 4) {  // probe: every MMA issued twice (results invalid)
+#pragma unroll
+              for (int g = 0; g < kGroups; ++g) {
+#pragma unroll
+                for (int a = 0; a <= g; ++a) {
+                  umma_i8_ts(tmem + unsigned(g * NP), abuf + unsigned(a * 8),
+                             bd0 + std::uint64_t(((g - a) * NP * kStepK) >> 4), kIdesc, 1u);
+                }
+              }
+            }
           } else {
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {

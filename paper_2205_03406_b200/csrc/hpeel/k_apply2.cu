@@ -147,7 +147,7 @@ static int& k2_path_ref() {
   return path;
 }
 bool k2_int8_enabled() { return k2_path_ref() != 1; }
-int k2_int8_debug() { return k2_path_ref() >= 2 ? k2_path_ref() - 1 : 0; }
+int k2_int8_debug() { return k2_path_ref() >= 2 ? k2_path_ref() - 1 : 0; }  // 2: no MMA, 3: no eval, 5: MMAs x2, 7: no eval + MMAs x2
 void set_k2_path(int path) { k2_path_ref() = path; }
 
 int k2_tile_rows(int ncols) {
