@@ -183,6 +183,15 @@ int hp_compress_export(const hp_op* op, const hp_tree* tree, int rank, int overs
                        int format, int strategy, hp_comm* comm, double* host_factors,
                        int64_t factor_doubles, double* host_dense, int64_t dense_doubles,
                        hp_rep** out);
+/* .hrep files in the reference's format (save_rep / load_rep,
+ * proj/include/hpeel/hmatrix.hpp:150-152, proj/src/serialize.cpp:156-250);
+ * H1 only. hp_rep_load returns the representation and its embedded tree. */
+int hp_rep_save(const hp_rep* rep, const char* path);
+int hp_rep_load(const char* path, int device, hp_rep** out, hp_tree** tree_out);
+/* save_dense_matrix / load_dense_matrix (hmatrix.hpp:155-156): "HPEELDM1"
+ * files; load with out == NULL returns the shape only */
+int hp_save_dense_matrix(const char* path, const double* a, int64_t rows, int64_t cols);
+int hp_load_dense_matrix(const char* path, int64_t* rows, int64_t* cols, double* out, int64_t cap);
 /* captured post-peel samples of pair `pair` at `level` (level < 0: leaf
  * probe block of dense pair `pair`): rows of the row box in box.points
  * order x (2r | leaf width) columns */

@@ -18,7 +18,8 @@ __all__ = [
     "BlockTestMatrix", "payload_gaussian", "assemble_test_matrices", "make_plan",
     "qr_orthonormal", "pinv_apply", "DenseOperator", "KernelOperator", "H1Rep", "run_h1",
     "extract_leaf", "compress", "rel_error_power_method", "synth_rank_structured",
-    "kernel_matrix", "H1", "LEAF", "UNIF1",
+    "kernel_matrix", "H1", "LEAF", "UNIF1", "save_rep_bytes", "load_rep_bytes", "save_dense_matrix_bytes",
+    "REP_MAGIC", "DENSE_MAGIC",
 ]
 
 M64 = (1 << 64) - 1
@@ -903,3 +904,115 @@ def synth_rank_structured(tree, adj, k, seed):
         rows, cols = tree.box(lam).points, tree.box(mu).points
         a[np.ix_(rows, cols)] = gaussian_matrix(len(rows), len(cols), mix_seed(seed, 204, lam, mu))
     return a
+
+
+# ---------------------------------------------------------------- .hrep files
+# proj/src/serialize.cpp:14-270 (H1 format), little-endian; used by tests to
+# check the device writer/reader byte for byte.
+import struct as _struct
+
+REP_MAGIC = 0x3150524C45455048     # "HPEELRP1", serialize.cpp:12
+DENSE_MAGIC = 0x314D444C45455048   # "HPEELDM1", serialize.cpp:13
+FORMAT_H1 = 1                      # RepFormat::kH1, hmatrix.hpp:16
+
+
+def _put_matrix(out, m):
+    """Writer::put_matrix, serialize.cpp:31-36 (rows, cols, column-major)."""
+    m = np.asarray(m, dtype=np.float64)
+    out.append(_struct.pack("<qq", m.shape[0], m.shape[1]))
+    out.append(np.asfortranarray(m).tobytes(order="F"))
+
+
+def save_rep_bytes(rep, k, leaf_capacity):
+    """save_rep (serialize.cpp:156-188) for an oracle H1Rep: write_meta
+    (:128-138), write_tree (:97-109), per level 0..depth the std::map-ordered
+    blocks, then the dense blocks."""
+    tree = rep.tree
+    out = [_struct.pack("<Q", REP_MAGIC),
+           _struct.pack("<Bqiiiiib", FORMAT_H1, tree.num_points, tree.dim, tree.depth, leaf_capacity, k,
+                        rep.built_level, 1 if rep.dense_ready else 0)]
+    out.append(_struct.pack("<iiqi", tree.dim, tree.leaf_capacity, tree.num_points, len(tree.boxes)))
+    for b in tree.boxes:
+        out.append(_struct.pack("<ii", b.level, b.parent))
+        out.append(_struct.pack("<%dq" % tree.dim, *b.coord))
+        out.append(_struct.pack("<i", len(b.children)) + _struct.pack("<%di" % len(b.children), *b.children))
+        pts = [int(p) for p in b.points]
+        out.append(_struct.pack("<i", len(pts)) + _struct.pack("<%di" % len(pts), *pts))
+    for level in rep.levels:
+        out.append(_struct.pack("<i", len(level)))
+        for (a, b), (u, bb, v) in sorted(level.items()):
+            out.append(_struct.pack("<ii", a, b))
+            _put_matrix(out, u)
+            _put_matrix(out, bb)
+            _put_matrix(out, v)
+    dense = rep.dense if rep.dense_ready else {}
+    out.append(_struct.pack("<i", len(dense)))
+    for (lam, mu), d in sorted(dense.items()):
+        out.append(_struct.pack("<ii", lam, mu))
+        _put_matrix(out, d)
+    return b"".join(out)
+
+
+class _Reader:
+    def __init__(self, data):
+        self.data, self.pos = data, 0
+
+    def get(self, fmt):
+        v = _struct.unpack_from("<" + fmt, self.data, self.pos)
+        self.pos += _struct.calcsize("<" + fmt)
+        return v if len(v) > 1 else v[0]
+
+    def ints(self):
+        n = self.get("i")
+        return list(self.get("%di" % n)) if n > 1 else ([self.get("i")] if n == 1 else [])
+
+    def matrix(self):
+        r, c = self.get("qq")
+        a = np.frombuffer(self.data, dtype="<f8", count=r * c, offset=self.pos).reshape((r, c), order="F")
+        self.pos += 8 * r * c
+        return np.array(a)
+
+
+def load_rep_bytes(data):
+    """load_rep (serialize.cpp:190-218) for the H1 format: returns
+    (meta dict, boxes [(level, parent, coord, children, points)], levels
+    [{(a, b): (u, b, v)}], dense {(lam, mu): d})."""
+    r = _Reader(data)
+    if r.get("Q") != REP_MAGIC:
+        raise RuntimeError("not a representation file")
+    fmt, n, dim, depth, leaf, rank, built, dense_ready = r.get("Bqiiiiib")
+    meta = dict(format=fmt, n=n, dim=dim, depth=depth, leaf_capacity=leaf, rank=rank, built_level=built,
+                dense_ready=bool(dense_ready))
+    tdim, tleaf, tn, nboxes = r.get("iiqi")
+    boxes = []
+    for _ in range(nboxes):
+        level, parent = r.get("ii")
+        coord = r.get("%dq" % tdim)
+        coord = (coord,) if tdim == 1 else tuple(coord)
+        children = r.ints()
+        points = r.ints()
+        boxes.append((level, parent, coord, children, points))
+    if fmt != FORMAT_H1:
+        raise ValueError("only the H1 format is restated")
+    levels = []
+    for _ in range(depth + 1):
+        cnt = r.get("i")
+        lv = {}
+        for _ in range(cnt):
+            a, b = r.get("ii")
+            lv[(a, b)] = (r.matrix(), r.matrix(), r.matrix())
+        levels.append(lv)
+    dense = {}
+    for _ in range(r.get("i")):
+        lam, mu = r.get("ii")
+        dense[(lam, mu)] = r.matrix()
+    if r.pos != len(data):
+        raise RuntimeError("trailing bytes in representation file")
+    return meta, boxes, levels, dense
+
+
+def save_dense_matrix_bytes(m):
+    """save_dense_matrix, serialize.cpp:252-256."""
+    out = [_struct.pack("<Q", DENSE_MAGIC)]
+    _put_matrix(out, m)
+    return b"".join(out)

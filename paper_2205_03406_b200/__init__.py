@@ -21,6 +21,7 @@ __all__ = [
     "BoxTree", "build_tree", "Plan", "plan", "level_coloring", "dsatur",
     "Operator", "dense_operator", "kernel_operator", "CompressedRep", "compress",
     "rel_error_power_method", "device_count", "debug_payload", "export_sizes", "pinned_empty",
+    "load_rep", "save_dense_matrix", "load_dense_matrix",
 ]
 
 MODES = {"h1": 0, "unif-stage1": 1, "unif-stage2": 2, "leaf": 3}
@@ -422,6 +423,10 @@ class CompressedRep:
         check(lib().hp_rep_sizes(self._h, C.byref(f), C.byref(d)))
         return f.value, d.value
 
+    def save(self, path: str) -> None:
+        """save_rep (proj/src/serialize.cpp:156-188): the reference's .hrep file."""
+        check(lib().hp_rep_save(self._h, str(path).encode()))
+
     def export(self, host_factors: np.ndarray, host_dense: np.ndarray) -> int:
         """Bulk device->host copy of the whole representation; returns bytes."""
         b = C.c_int64(0)
@@ -489,6 +494,32 @@ def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, ov
                                STRATEGIES[strategy], int(capture), comm._h if comm else None,
                                int(emulate_shards), C.byref(h)))
     return CompressedRep(h.value, tree, rank, oversample)
+
+
+def load_rep(path: str, device: int = 0) -> "CompressedRep":
+    """load_rep (proj/src/serialize.cpp:190-250) onto `device`; H1 files only.
+    The representation's embedded tree is `rep.tree` (no point coordinates)."""
+    h, t = C.c_void_p(), C.c_void_p()
+    check(lib().hp_rep_load(str(path).encode(), int(device), C.byref(h), C.byref(t)))
+    tree = BoxTree(t.value, None)
+    return CompressedRep(h.value, tree, 1, 0)
+
+
+def save_dense_matrix(path: str, a) -> None:
+    """save_dense_matrix (serialize.cpp:252-256): "HPEELDM1" + matrix."""
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if a.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    check(lib().hp_save_dense_matrix(str(path).encode(), dptr(a), a.shape[0], a.shape[1]))
+
+
+def load_dense_matrix(path: str) -> np.ndarray:
+    """load_dense_matrix (serialize.cpp:258-264)."""
+    rows, cols = C.c_int64(0), C.c_int64(0)
+    check(lib().hp_load_dense_matrix(str(path).encode(), C.byref(rows), C.byref(cols), None, 0))
+    out = np.zeros((rows.value, cols.value), order="F")
+    check(lib().hp_load_dense_matrix(str(path).encode(), None, None, dptr(out), out.size))
+    return out
 
 
 def export_sizes(tree: BoxTree, rank: int):

@@ -79,6 +79,10 @@ _SIGNATURES = {
     "hp_host_free": (None, [P]),
     "hp_compress_export": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, P, dp, i64, dp, i64,
                                      C.POINTER(P)]),
+    "hp_rep_save": (C.c_int, [P, C.c_char_p]),
+    "hp_rep_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(P), C.POINTER(P)]),
+    "hp_save_dense_matrix": (C.c_int, [C.c_char_p, dp, i64, i64]),
+    "hp_load_dense_matrix": (C.c_int, [C.c_char_p, lp, lp, dp, i64]),
     "hp_rep_captured": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
     "hp_rel_error_power_method": (C.c_int, [P, P, C.c_int, u64, dp]),
     "hp_debug_payload": (C.c_int, [P, C.c_int, C.c_int, u64, C.c_int, dp]),

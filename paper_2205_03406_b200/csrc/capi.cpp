@@ -12,6 +12,7 @@
 #include "hpeel/coloring.hpp"
 #include "hpeel/peeling.hpp"
 #include "hpeel/rng.hpp"
+#include "hpeel/serialize.hpp"
 #include "hpeel/shard.hpp"
 
 using namespace hpeel;
@@ -672,6 +673,54 @@ int hp_compress_export(const hp_op* op, const hp_tree* tree, int rank, int overs
     auto r = std::make_unique<hp_rep>();
     r->result = compress(*op->op, tree->tree, cfg);
     *out = r.release();
+  });
+}
+
+int hp_rep_save(const hp_rep* rep, const char* path) {
+  return guard([&] {
+    need(rep, "rep");
+    need(path, "path");
+    save_rep(path, *rep->result.rep);
+  });
+}
+
+int hp_rep_load(const char* path, int device, hp_rep** out, hp_tree** tree_out) {
+  return guard([&] {
+    need(path, "path");
+    need(out, "out");
+    need(tree_out, "tree_out");
+    auto r = std::make_unique<hp_rep>();
+    r->result.rep = load_rep(path, device);
+    auto t = std::make_unique<hp_tree>();
+    t->tree = r->result.rep->tree;
+    t->adj = r->result.rep->adj;
+    t->layout = r->result.rep->layout;
+    *tree_out = t.release();
+    *out = r.release();
+  });
+}
+
+int hp_save_dense_matrix(const char* path, const double* a, int64_t rows, int64_t cols) {
+  return guard([&] {
+    need(path, "path");
+    if (rows < 0 || cols < 0) throw std::invalid_argument("negative shape");
+    if (rows * cols > 0) need(a, "a");
+    Matrix m(rows, cols);
+    if (rows * cols > 0) std::memcpy(m.data(), a, size_t(rows * cols) * 8);
+    save_dense_matrix(path, m);
+  });
+}
+
+int hp_load_dense_matrix(const char* path, int64_t* rows, int64_t* cols, double* out, int64_t cap) {
+  return guard([&] {
+    need(path, "path");
+    const Matrix m = load_dense_matrix(path);
+    if (rows) *rows = m.rows();
+    if (cols) *cols = m.cols();
+    if (out) {
+      if (cap < m.size()) throw std::invalid_argument("output buffer too small");
+      std::memcpy(out, m.data(), size_t(m.size()) * 8);
+    }
   });
 }
 

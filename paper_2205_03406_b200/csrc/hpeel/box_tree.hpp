@@ -43,6 +43,9 @@ class BoxTree {
   /// proj/src/box_tree.cpp:99-180. Throws std::runtime_error on degenerate
   /// geometry, std::invalid_argument on bad arguments.
   static BoxTree build(const PointCloud& cloud, int leaf_capacity);
+  /// proj/src/box_tree.cpp:182-196: rebuild from serialized boxes (level
+  /// lists, depth and child rows recomputed).
+  static BoxTree from_parts(int dim, int leaf_capacity, Index n, std::vector<Box> boxes);
 
   int dim() const { return dim_; }
   int depth() const { return depth_; }
