@@ -16,12 +16,13 @@ __device__ __forceinline__ std::uint64_t desc(unsigned addr, int layout, unsigne
 template <int N, int PAT>
 __global__ void bench(int iters, int groups, int layout, long long* cyc) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  __shared__ std::uint64_t bar;
+  __shared__ std::uint64_t bar, bar2;
   __shared__ unsigned tbase;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < 7 * 4096 + 7 * 256 * 32; i += blockDim.x) sm[i] = (unsigned char)(i * 7);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(sa(&bar2)));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -37,8 +38,10 @@ __global__ void bench(int iters, int groups, int layout, long long* cyc) {
   if (threadIdx.x == 0) {
     const long long t0 = clock64();
     int n = 0;
-    if (PAT == 1) {
+    if (PAT == 1 || PAT == 2) {
       for (int it = 0; it < iters; ++it) {
+        if (PAT == 2 && it > 0)  // commit after every 28 MMAs (as the K2 kernel does per K-step)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&bar2)));
 #pragma unroll
         for (int m = 0; m < 28; ++m) {
           const unsigned ad = sa(sm) + (m % 7) * 4096, bd = sa(sm) + 7 * 4096 + ((m / 7) % 7) * N * 32;
@@ -90,15 +93,9 @@ void run(int groups, int layout) {
 }
 
 int main() {
-  run<48>(7, 0);
-  run<48, 1>(1, 0);
-  run<48, 1>(2, 0);
-  run<48, 1>(4, 0);
   run<48, 1>(7, 0);
-  run<48, 1>(10, 0);
-  run<32, 1>(16, 0);
-  run<64, 1>(8, 0);
-  run<96, 1>(5, 0);
-  run<128, 1>(4, 0);
+  run<48, 2>(7, 0);
+  run<64, 1>(7, 0);
+  run<64, 2>(7, 0);
   return 0;
 }
