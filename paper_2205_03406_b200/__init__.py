@@ -564,7 +564,8 @@ def set_k2_path(path: str) -> None:
     products on the int8 tensor cores wherever eligible) or "fp64" (FP64
     DMMA for every apply). For A/B parity tests and measurements."""
     lib().hp_debug_set_k2_path({"int8": 0, "fp64": 1, "int8-nomma": 2, "int8-noeval": 3, "int8-mma2": 5,
-                                 "int8-noeval-mma2": 7}[path])
+                                 "int8-noeval-mma2": 7,
+                                 "int8-nodsmem": 9, "int8-noeval-nodsmem": 11}[path])
 
 
 def debug_log(x, device: int = 0) -> np.ndarray:

@@ -8,7 +8,7 @@ w = configs.CONFIGS[name] if len(sys.argv) < 3 else configs.scaled(name, int(sys
 pts = w.points()
 t = hp.build_tree(pts, w.leaf)
 op = hp.kernel_operator(w.kernel, pts, w.param)
-for path in ("int8", "int8", "int8-nomma", "int8-noeval", "int8-mma2", "int8-noeval-mma2", "fp64"):
+for path in ("int8", "int8", "int8-nomma", "int8-noeval", "int8-nodsmem", "int8-noeval-nodsmem", "fp64"):
     hp.set_k2_path(path)
     rep = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
     ap = sum(p["apply_ms"] for p in rep.report["phases"] if p["phase"] == "h1")

@@ -38,6 +38,25 @@ __global__ void bench(int iters, int groups, int layout, long long* cyc) {
   if (threadIdx.x == 0) {
     const long long t0 = clock64();
     int n = 0;
+    if (PAT == 3) {
+      for (int it = 0; it < iters; ++it) {
+        const unsigned abuf = tbase + 448 + (it & 1) * 0;  // one A buffer at columns 448..503
+#pragma unroll
+        for (int a = 0; a < 7; ++a)
+          asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(abuf + a * 8),
+                       "l"(desc(sa(sm) + a * 4096, layout, lbo, sbo)));
+#pragma unroll
+        for (int m = 0; m < 28; ++m) {
+          const unsigned bd = sa(sm) + 7 * 4096 + ((m / 7) % 7) * N * 32;
+          const unsigned d = tbase + unsigned(((m % groups) * N) % 448);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                       "r"(abuf + (m % 7) * 8), "l"(desc(bd, layout, lbo, sbo)), "r"(idesc), "r"(1u));
+          ++n;
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&bar2)));
+      }
+    } else
     if (PAT == 1 || PAT == 2) {
       for (int it = 0; it < iters; ++it) {
         if (PAT == 2 && it > 0)  // commit after every 28 MMAs (as the K2 kernel does per K-step)
@@ -93,9 +112,8 @@ void run(int groups, int layout) {
 }
 
 int main() {
-  run<48, 1>(7, 0);
   run<48, 2>(7, 0);
-  run<64, 1>(7, 0);
-  run<64, 2>(7, 0);
+  run<48, 3>(7, 0);
+  run<64, 3>(7, 0);
   return 0;
 }
