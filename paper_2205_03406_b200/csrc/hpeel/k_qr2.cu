@@ -169,6 +169,8 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
   // row j; MODE 0 also publishes the warp argmax of sig + arow^2
   double sig = 0.0, arow = 0.0;
   auto stats = [&](int j, int buf) {
+    // MODE 1 (no pivoting): only column j's warp needs its tail norm
+    if (MODE == 1 && j / CPW != warp) return;
     const int gj = j / RPT, ij = j - gj * RPT;
     sig = group_sum<TPC>(tail_sq(x, r0, j));
     arow = __shfl_sync(0xffffffffu, get_row(x, ij), (lane % CPW) + gj * CPW);

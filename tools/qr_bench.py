@@ -32,5 +32,5 @@ for rows, count in specs:
         assert ranks[i] == keep, (rows, i, ranks[i], keep)
         qa, qb = qs[i][:, :keep], qr_[:, :keep]
         worst = max(worst, np.abs(qa @ (qa.T @ qb) - qb).max() if keep else 0.0)
-    print(f"rows {rows:5d} x {r} count {count:6d}: {ms2:8.2f} ms  {flops / ms2 / 1e9:7.1f} GFLOP/s (2mn^2)  span err {worst:.1e}",
+    print(f"rows {rows:5d} x {r} count {count:6d}: {ms2:8.2f} ms  {flops / ms2 / 1e9:7.3f} TFLOP/s (2mn^2)  span err {worst:.1e}",
           flush=True)
