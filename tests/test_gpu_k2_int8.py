@@ -60,3 +60,26 @@ def test_int8_path_is_used(hp, gpu_available):
     hp.set_k2_path("int8")
     # int8 adds one payload-digit launch per level (and one bbox launch)
     assert counts["int8"] > counts["fp64"]
+
+
+def test_int8_full_size_c3_matches_fp64(hp, gpu_available):
+    """Config 3 at full size: colors have ~24k payload rows, so every int8
+    tile drains its int32 accumulators over more than one 16384-row window.
+    The two representations apply alike (the samples differ by ~1e-13; the
+    factors only through rank decisions at the 1e-14 pivot threshold)."""
+    w = configs.CONFIGS["c3"]
+    pts = w.points()
+    t = hp.build_tree(pts, w.leaf)
+    op = hp.kernel_operator(w.kernel, pts, w.param)
+    reps = {}
+    for path in ("fp64", "int8"):
+        hp.set_k2_path(path)
+        try:
+            reps[path] = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
+        finally:
+            hp.set_k2_path("int8")
+    h1 = {k: [p["apply_path"] for p in r.report["phases"] if p["phase"] == "h1"] for k, r in reps.items()}
+    assert set(h1["fp64"]) == {"fp64"} and set(h1["int8"]) == {"int8"}
+    x = np.random.default_rng(5).standard_normal((t.num_points, 4))
+    ya, yb = reps["fp64"].apply(x), reps["int8"].apply(x)
+    assert np.linalg.norm(ya - yb) / np.linalg.norm(ya) <= 1e-8
