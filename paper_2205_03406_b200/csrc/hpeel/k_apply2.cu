@@ -62,31 +62,70 @@ __global__ void identity_apply_kernel(DevOp op, const SampleTask* __restrict__ t
                                       const std::int64_t* __restrict__ box_start,
                                       const std::int64_t* __restrict__ box_count, int w,
                                       double* __restrict__ out) {
+  // the color's payload boxes (start, count) staged in shared memory in
+  // chunks, and the half_log table for log kernels: the per-box loop then has
+  // no dependent global loads before the coordinate reads
+  constexpr int kBoxChunk = 512;
+  __shared__ std::int64_t s_start[kBoxChunk];
+  __shared__ int s_count[kBoxChunk];
+  __shared__ __align__(16) double s_tab[KIND == kOpLog ? 2 * kLogTab : 2];
   const SampleTask task = tasks[blockIdx.x];
   const std::int64_t n = op.n;
-  for (int idx = threadIdx.x; idx < task.rows * w; idx += blockDim.x) {
-    const int t = idx / task.rows, i = idx - t * task.rows;
-    const std::int64_t ip = task.row0 + i;
-    double xi[DIM > 0 ? DIM : 1];
-    if constexpr (KIND != kOpDense) {
+  if constexpr (KIND == kOpLog) {
+    for (int e = threadIdx.x; e < 2 * kLogTab; e += blockDim.x) s_tab[e] = op.ltab[e];
+  }
+  const double* tab = KIND == kOpLog ? s_tab : op.ltab;
+  const std::int64_t q0 = pay_off[task.color], q1 = pay_off[task.color + 1];
+  const int nidx = task.rows * w;
+  // per-thread accumulators for kPer (row, column) entries per pass
+  constexpr int kPer = 16;
+  for (int base = 0; base < nidx; base += kPer * int(blockDim.x)) {
+    double acc[kPer];
 #pragma unroll
-      for (int d = 0; d < DIM; ++d) xi[d] = op.x[d * n + ip];
-    }
-    double acc = 0.0;
-    for (std::int64_t q = pay_off[task.color]; q < pay_off[task.color + 1]; ++q) {
-      const int v = pay_box[q];
-      if (t >= box_count[v]) continue;
-      const std::int64_t jp = box_start[v] + t;
-      if constexpr (KIND == kOpDense) {
-        acc += op.a[ip + jp * n];
-      } else {
-        double xj[DIM > 0 ? DIM : 1];
+    for (int u = 0; u < kPer; ++u) acc[u] = 0.0;
+    for (std::int64_t qc = q0; qc < q1; qc += kBoxChunk) {
+      const int nb = int(q1 - qc < kBoxChunk ? q1 - qc : kBoxChunk);
+      __syncthreads();
+      for (int e = threadIdx.x; e < nb; e += blockDim.x) {
+        const int v = pay_box[qc + e];
+        s_start[e] = box_start[v];
+        s_count[e] = int(box_count[v]);
+      }
+      __syncthreads();
 #pragma unroll
-        for (int d = 0; d < DIM; ++d) xj[d] = op.x[d * n + jp];
-        acc += kernel_value<KIND, DIM>(xi, xj, ip == jp, op.param, op.ltab);
+      for (int u = 0; u < kPer; ++u) {
+        const int idx = base + threadIdx.x + u * int(blockDim.x);
+        if (idx >= nidx) break;
+        const int t = idx / task.rows, i = idx - t * task.rows;
+        const std::int64_t ip = task.row0 + i;
+        double xi[DIM > 0 ? DIM : 1];
+        if constexpr (KIND != kOpDense) {
+#pragma unroll
+          for (int d = 0; d < DIM; ++d) xi[d] = op.x[d * n + ip];
+        }
+        double a = acc[u];
+        for (int b = 0; b < nb; ++b) {
+          if (t >= s_count[b]) continue;
+          const std::int64_t jp = s_start[b] + t;
+          if constexpr (KIND == kOpDense) {
+            a += op.a[ip + jp * n];
+          } else {
+            double xj[DIM > 0 ? DIM : 1];
+#pragma unroll
+            for (int d = 0; d < DIM; ++d) xj[d] = op.x[d * n + jp];
+            a += kernel_value<KIND, DIM>(xi, xj, ip == jp, op.param, tab);
+          }
+        }
+        acc[u] = a;
       }
     }
-    out[task.out + i + std::int64_t(t) * task.ld] = acc;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int idx = base + threadIdx.x + u * int(blockDim.x);
+      if (idx >= nidx) break;
+      const int t = idx / task.rows, i = idx - t * task.rows;
+      out[task.out + i + std::int64_t(t) * task.ld] = acc[u];
+    }
   }
 }
 
