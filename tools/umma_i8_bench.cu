@@ -38,11 +38,42 @@ __global__ void bench(int iters, int groups, int layout, long long* cyc) {
   if (threadIdx.x == 0) {
     const long long t0 = clock64();
     int n = 0;
-    if (PAT == 3) {
+    if (PAT == 5 || PAT == 6) {
+      // the K2 kernel's 28 digit-pair MMAs per K-step (SS): PAT 5 group-major
+      // (A plane changes every MMA), PAT 6 plane-major (7 - a MMAs per A plane)
+      for (int it = 0; it < iters; ++it) {
+        if (PAT == 5) {
+#pragma unroll
+          for (int g = 0; g < 7; ++g)
+#pragma unroll
+            for (int a = 0; a <= g; ++a) {
+              const unsigned ad = sa(sm) + a * 4096, bd = sa(sm) + 7 * 4096 + (g - a) * N * 32;
+              asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                           "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tbase + unsigned(g * N)),
+                           "l"(desc(ad, layout, lbo, sbo)), "l"(desc(bd, layout, lbo, sbo)), "r"(idesc), "r"(1u));
+              ++n;
+            }
+        } else {
+#pragma unroll
+          for (int a = 0; a < 7; ++a)
+#pragma unroll
+            for (int b = 0; a + b < 7; ++b) {
+              const unsigned ad = sa(sm) + a * 4096, bd = sa(sm) + 7 * 4096 + b * N * 32;
+              asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                           "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tbase + unsigned((a + b) * N)),
+                           "l"(desc(ad, layout, lbo, sbo)), "l"(desc(bd, layout, lbo, sbo)), "r"(idesc), "r"(1u));
+              ++n;
+            }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&bar2)));
+      }
+    } else
+    if (PAT == 3 || PAT == 4) {
       for (int it = 0; it < iters; ++it) {
         const unsigned abuf = tbase + 448 + (it & 1) * 0;  // one A buffer at columns 448..503
 #pragma unroll
         for (int a = 0; a < 7; ++a)
+          if (PAT == 3)
           asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(abuf + a * 8),
                        "l"(desc(sa(sm) + a * 4096, layout, lbo, sbo)));
 #pragma unroll
@@ -112,8 +143,9 @@ void run(int groups, int layout) {
 }
 
 int main() {
-  run<48, 2>(7, 0);
-  run<48, 3>(7, 0);
-  run<64, 3>(7, 0);
+  run<48, 5>(7, 0);
+  run<48, 6>(7, 0);
+  run<64, 5>(7, 0);
+  run<64, 6>(7, 0);
   return 0;
 }
