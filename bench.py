@@ -360,6 +360,7 @@ def run_ours(args, ws, rank, local):
                    "max_sampling_colors": report["max_sampling_colors"], "net_flops": report["net_flops"],
                    "wall_s_net": round(report["wall_s_net"], 4), "setup_ms": round(report["setup_ms"], 1),
                    "phases": phases},
+        "step_times_s": [round(t, 4) for t in times],
         "storage_doubles": last.storage()["total"],
     }
     print(json.dumps(line), flush=True)

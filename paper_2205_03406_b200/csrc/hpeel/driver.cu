@@ -600,7 +600,10 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       if (use_i8) {
         const std::int64_t tsteps = w.step_off.back();
         half_stride = tsteps * k2i8::b_step_bytes(k2i8::padded_width(r));
-        bdig.alloc(size_t(std::max<std::int64_t>(2 * half_stride, 16)), s);
+        bdig.alloc(size_t(std::max<std::int64_t>(2 * half_stride, 16)), s);  // same size in both layouts
+        // group split: the CTA pair adds two partial sums per sample element
+        if (k2i8::group_split(k2i8::padded_width(r)))
+          HP_CUDA(cudaMemsetAsync(samples.get(), 0, size_t(w.soff[np]) * sizeof(double), s));
         d_step_off.upload(w.step_off, s);
         d_step_color.upload(w.step_color, s);
         d_pb_off.upload(w.pb_off, s);

@@ -41,10 +41,19 @@ __global__ void payload_digits_kernel(const double* __restrict__ gc, int gld, in
     }
     pack_planes(uh, ul, w[q]);
   }
-  unsigned char* dst = bdig + half * half_stride + gstep * b_step_bytes(np) + (n >> 3) * 256 + kh * 128 + (n & 7) * 16;
+  unsigned char* dst;
+  std::int64_t plane;
+  if (group_split(np)) {  // [gstep][plane][2 np rows]: row half * np + n
+    const int n2 = half * np + n;
+    dst = bdig + gstep * b_step_bytes(2 * np) + (n2 >> 3) * 256 + kh * 128 + (n2 & 7) * 16;
+    plane = std::int64_t(2) * np * kStepK;
+  } else {
+    dst = bdig + half * half_stride + gstep * b_step_bytes(np) + (n >> 3) * 256 + kh * 128 + (n & 7) * 16;
+    plane = std::int64_t(np) * kStepK;
+  }
 #pragma unroll
   for (int a = 0; a < kPlanes; ++a)
-    *reinterpret_cast<uint4*>(dst + std::int64_t(a) * np * kStepK) = make_uint4(w[0][a], w[1][a], w[2][a], w[3][a]);
+    *reinterpret_cast<uint4*>(dst + std::int64_t(a) * plane) = make_uint4(w[0][a], w[1][a], w[2][a], w[3][a]);
 }
 
 __global__ void step_coords_kernel(const double* __restrict__ xc, std::int64_t nnz, int dim,

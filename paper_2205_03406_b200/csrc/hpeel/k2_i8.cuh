@@ -48,6 +48,13 @@ constexpr int kAPlane = kRows * kStepK;  // bytes of one A digit plane per K-ste
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 
 __host__ __device__ constexpr int padded_width(int r) { return (r + 15) / 16 * 16; }
+/// Group split (NP <= 48): CTA 0 of the pair accumulates digit-pair groups
+/// 0..kG0-1 and CTA 1 groups kG0..6, each for all 2 NP sample columns (one
+/// MMA of N = 2 NP per digit pair: 15 + 13 MMAs per K-step instead of 28 + 28
+/// of N = NP). Otherwise (NP = 64) CTA h owns column half h for all groups.
+constexpr int kG0 = 5;
+__host__ __device__ constexpr bool group_split(int np) { return kG0 * 2 * np <= 512 && (kGroups - kG0) * 2 * np <= 512; }
+__host__ __device__ constexpr int mma_n(int np) { return group_split(np) ? 2 * np : np; }
 __host__ __device__ constexpr int b_step_bytes(int np) { return kPlanes * np * kStepK; }
 /// Pipeline depth: 4 digit-tile (A) stages and 4 payload digit + coordinate
 /// (B) stages (a deeper B ring measured slower: 1.44 s vs 1.26 s on c3).
@@ -56,7 +63,7 @@ constexpr int kStaticSmem = 9216 + 1024;
 __host__ __device__ constexpr int b_ring_bytes(int np) { return b_step_bytes(np) + 3 * kStepK * 8; }
 __host__ __device__ constexpr int bstages_for(int np, bool tab) { return (void)np, (void)tab, 4; }
 __host__ __device__ constexpr size_t smem_bytes(int np, bool tab) {
-  return size_t(kAStages) * kPlanes * kAPlane + size_t(bstages_for(np, tab)) * b_ring_bytes(np) +
+  return size_t(kAStages) * kPlanes * kAPlane + size_t(bstages_for(np, tab)) * b_ring_bytes(mma_n(np)) +
          (tab ? 2 * kLogTab * 8 : 0) + 1024;
 }
 
@@ -254,11 +261,13 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
   constexpr int kBS = bstages_for(NP, kTab);
   // A digit planes staged in TMEM (two buffers of 7 x 8 columns after the
   // 7 accumulator groups) where they fit the 512 columns
+  constexpr bool kGS = group_split(NP);
+  constexpr int kN = mma_n(NP);  // MMA N (and TMEM columns per accumulator group)
   constexpr int kAcol = kGroups * NP;
-  constexpr bool kTS = kAcol + 2 * kPlanes * 8 <= 512 && kTSEnabled;
-  constexpr int kBStep = b_step_bytes(NP);
+  constexpr bool kTS = !kGS && kAcol + 2 * kPlanes * 8 <= 512 && kTSEnabled;
+  constexpr int kBStep = b_step_bytes(kN);
   constexpr int kXStep = DIM * kStepK * 8;  // coordinates of one K-step (dim-major)
-  constexpr unsigned kIdesc = umma_idesc(NP);
+  constexpr unsigned kIdesc = umma_idesc(kN);
   extern __shared__ __align__(1024) unsigned char smem[];
   unsigned char* sa = smem;                                   // [kStages][kPlanes][kAPlane]
   unsigned char* sb = smem + kStages * kPlanes * kAPlane;     // [kBS][kBStep]
@@ -281,7 +290,10 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
   const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
   const int nsteps = int((p1 - p0 + kStepK - 1) / kStepK);
   const std::int64_t step0 = step_off[task.color];
-  const unsigned char* bsrc = bdig + half * half_stride + step0 * kBStep;
+  const unsigned char* bsrc = bdig + (kGS ? 0 : half * half_stride) + step0 * kBStep;
+  // accumulator groups of this CTA
+  const int g_lo = kGS ? (half == 0 ? 0 : kG0) : 0;
+  const int g_hi = kGS ? (half == 0 ? kG0 : kGroups) : kGroups;
   const double* xsrc = xstep + step0 * (DIM * kStepK);
   const double* tab = kTab ? lts : op.ltab;
 
@@ -400,10 +412,11 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
           } else {
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
+              if (g < g_lo || g >= g_hi) continue;
 #pragma unroll
               for (int a = 0; a <= g; ++a) {
-                umma_i8(tmem + unsigned(g * NP), ad0 + std::uint64_t((a * kAPlane) >> 4),
-                        bd0 + std::uint64_t(((g - a) * NP * kStepK) >> 4), kIdesc, (fresh && a == 0) ? 0u : 1u);
+                umma_i8(tmem + unsigned((g - g_lo) * kN), ad0 + std::uint64_t((a * kAPlane) >> 4),
+                        bd0 + std::uint64_t(((g - a) * kN * kStepK) >> 4), kIdesc, (fresh && a == 0) ? 0u : 1u);
               }
             }
           }
@@ -461,7 +474,7 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
     unsigned char* a_dst = sa + (erow >> 3) * 256 + kh * 128 + (erow & 7) * 16 + k4 * 4;
     // epilogue: TMEM lanes (warp & 3) * 32 + lane = tile rows, column quarter (warp >> 2)
     const int orow = (warp & 3) * 32 + lane;
-    constexpr int kCq = NP / 4;  // columns per epilogue warp (multiple of 4)
+    constexpr int kCq = kN / 4;  // columns per epilogue warp (multiple of 4)
     const int cq = warp >> 2;
 
     double y[kCq];
@@ -502,11 +515,12 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
         const unsigned lane_base = tmem + (unsigned((warp & 3) * 32) << 16) + unsigned(cq * kCq);
 #pragma unroll
         for (int q = 0; q < kGroups; ++q) {
+          if (q < g_lo || q >= g_hi) continue;
           const double wg = ldexp(1.0, e - 8 - 8 * q);
 #pragma unroll
           for (int c0 = 0; c0 < kCq; c0 += 4) {
             int v[4];
-            tmem_ld4(lane_base + unsigned(q * NP + c0), v);
+            tmem_ld4(lane_base + unsigned((q - g_lo) * kN + c0), v);
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 4; ++c) y[c0 + c] = fma(double(v[c]), wg, y[c0 + c]);
@@ -522,7 +536,14 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
 #pragma unroll
       for (int c = 0; c < kCq; ++c) {
         const int col = cq * kCq + c;
-        if (col < r) out[dst.out + std::int64_t(half * r + col) * dst.ld] = y[c];
+        if constexpr (kGS) {
+          // both CTAs add their groups' partial sums into the zeroed sample
+          // block: two addends per element, so the result is order-independent
+          const int hh = col / NP, cc = col - hh * NP;
+          if (cc < r) atomicAdd(out + dst.out + std::int64_t(hh * r + cc) * dst.ld, y[c]);
+        } else {
+          if (col < r) out[dst.out + std::int64_t(half * r + col) * dst.ld] = y[c];
+        }
       }
     }
   }
@@ -563,9 +584,11 @@ void launch_kind(HP_K2I8_ARGS) {
   throw std::invalid_argument("k2 int8: unsupported dim / width");
 }
 
-/// Payload digit planes of one level: for every color's K-steps (step_off,
-/// step_color) and both column halves, bdig[half * half_stride + gstep *
-/// b_step_bytes(np) ...] (np = padded_width(r)).
+/// Payload digit planes of one level for every color's K-steps (step_off,
+/// step_color). Group split (group_split(np)): one N = 2 np tile per plane,
+/// rows [0, np) forward and [np, 2 np) adjoint columns, at bdig[gstep *
+/// b_step_bytes(2 np)]; otherwise per column half at bdig[half * half_stride
+/// + gstep * b_step_bytes(np)] (np = padded_width(r)).
 void launch_payload_digits(const double* gc, int gld, int r, const std::int64_t* pay_off,
                            const std::int64_t* step_off, const int* step_color, std::int64_t tsteps,
                            unsigned char* bdig, std::int64_t half_stride, cudaStream_t s);
