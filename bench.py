@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--n", type=int, default=0, help="override N (scaled workload)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0: off)")
     return ap.parse_args()
 
 
@@ -86,19 +87,22 @@ def barrier(ws):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
-    def __init__(self, gpu):
+    def __init__(self, gpu, period_ms=200):
         self.gpu = gpu
+        self.period_ms = period_ms
         self.rows = []
         self.proc = None
 
     def __enter__(self):
+        if self.period_ms <= 0:
+            return self
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap,power.draw")
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except FileNotFoundError:
@@ -280,21 +284,24 @@ def run_ours(args, ws, rank, local):
         rep = hp.compress(op, tree, **kw)
         del rep
     torch.cuda.synchronize()
-    times = []
+    times, walls = [], []
     launches0 = hp.launch_count()
     last = None
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_ms) as clk:
         for _ in range(args.steps):
             last = rep = None  # the previous representation is released outside the timed region
             flush_l2(torch)
             barrier(ws)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            w0 = time.perf_counter()
             e0.record()
             rep = hp.compress(op, tree, **kw)
             e1.record()
+            w1 = time.perf_counter()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) * 1e-3)
+            walls.append((w1 - w0, rep.report["wall_s_total"]))
             last = rep
     launches = hp.launch_count() - launches0
     t_step = dist_max(float(np.mean(times)), ws, "ours")
@@ -361,6 +368,7 @@ def run_ours(args, ws, rank, local):
                    "wall_s_net": round(report["wall_s_net"], 4), "setup_ms": round(report["setup_ms"], 1),
                    "phases": phases},
         "step_times_s": [round(t, 4) for t in times],
+        "step_host_wall_s": [[round(a, 4), round(b, 4)] for a, b in walls],
         "storage_doubles": last.storage()["total"],
     }
     print(json.dumps(line), flush=True)

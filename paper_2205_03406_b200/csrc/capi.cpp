@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -476,7 +479,12 @@ int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversampl
     if (cfg.comm && cfg.comm->device() != op->op->device())
       throw std::invalid_argument("communicator and operator on different devices");
     auto r = std::make_unique<hp_rep>();
+    static const bool timing = std::getenv("HP_DRIVER_TIMING") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     r->result = compress(*op->op, tree->tree, cfg);
+    if (timing)
+      std::fprintf(stderr, "[capi] compress() returned after %.1f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     *out = r.release();
   });
 }
