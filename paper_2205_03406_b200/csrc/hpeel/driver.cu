@@ -504,7 +504,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     rep->factor_doubles = ftotal;
     // stream-ordered from the retained device pool: repeated compress() calls reuse the memory
     HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_factors), size_t(std::max<std::int64_t>(ftotal, 1)) * 8, s));
-    HP_CUDA(cudaMallocHost(&h_ranks, size_t(std::max<std::int64_t>(rank_total, 1)) * sizeof(int)));
+    h_ranks = static_cast<int*>(persistent_pinned(size_t(std::max<std::int64_t>(rank_total, 1)) * sizeof(int), 0));
 
     // Host plans of every level and of the leaf phase, built concurrently.
     std::vector<std::future<LevelWork>> futs(size_t(tree->depth()) + 1);
@@ -876,12 +876,10 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
   } catch (...) {
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
-    if (h_ranks) cudaFreeHost(h_ranks);
     throw;
   }
   HP_CUDA(cudaStreamSynchronize(s));
   cudaStreamDestroy(s);
-  cudaFreeHost(h_ranks);
   result.rep = rep;
   return result;
 }

@@ -66,6 +66,27 @@ void* PinnedStaging::take(size_t bytes) {
   return p;
 }
 
+void* persistent_pinned(size_t bytes, int slot) {
+  // grow-only, per thread: cudaMallocHost / cudaFreeHost on every compress()
+  // serialized the return path behind the process's memory-map lock
+  struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+    ~Buf() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  thread_local Buf bufs[4];
+  Buf& b = bufs[slot];
+  if (b.n < bytes) {
+    if (b.p) cudaFreeHost(b.p);
+    b.p = nullptr;
+    HP_CUDA(cudaMallocHost(&b.p, bytes));
+    b.n = bytes;
+  }
+  return b.p;
+}
+
 void PinnedStaging::release_to_pool() {
   std::lock_guard<std::mutex> lock(pool_mutex());
   for (const Chunk& c : chunks_) pool().push_back({c.p, c.size});
@@ -129,13 +150,13 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
     d_flag.alloc(1, s);
     HP_CUDA(cudaMemsetAsync(d_flag.get(), 0, sizeof(int), s));
     launch_find_duplicates(xt.get(), op.dim(), n, d_ls.get(), d_lc.get(), int(ls.size()), d_flag.get(), s);
-    HP_CUDA(cudaMallocHost(&h_flag, sizeof(int)));
+    h_flag = static_cast<int*>(persistent_pinned(sizeof(int), 1));
     HP_CUDA(cudaMemcpyAsync(h_flag, d_flag.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   }
   HP_CUDA(cudaStreamSynchronize(s));
   if (h_flag) {
     has_dups = *h_flag != 0;
-    cudaFreeHost(h_flag);
+    // (persistent pinned buffer: not freed)
   }
 }
 

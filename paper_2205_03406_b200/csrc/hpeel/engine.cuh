@@ -35,6 +35,9 @@ class PinnedStaging {
   std::vector<Chunk> chunks_;
 };
 
+/// Grow-only pinned host buffer `slot` (< 4) of the calling thread.
+void* persistent_pinned(size_t bytes, int slot);
+
 class StagingScope {
  public:
   explicit StagingScope(cudaStream_t s) : s_(s), prev_(PinnedStaging::current()) {
