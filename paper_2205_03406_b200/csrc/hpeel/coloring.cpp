@@ -261,11 +261,6 @@ class KeyHeap {
   std::vector<std::uint64_t> h_;
 };
 
-// (saturation, uncolored degree, -v) packed so that integer order is the
-// DSatur order: 11 | 21 | 32 bits
-inline std::uint64_t dsatur_key(int sat, int udeg, int v) {
-  return (std::uint64_t(sat) << 53) | (std::uint64_t(udeg) << 32) | (0xFFFFFFFFull - std::uint64_t(unsigned(v)));
-}
 }  // namespace
 
 Coloring dsatur_color(const IncompatibilityGraph& graph) {
@@ -273,51 +268,53 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
   Coloring out;
   out.color.assign(size_t(n), -1);
   if (n == 0) return out;
-  // Max-heap of (saturation, uncolored degree, -v) with lazy keys: a vertex's
-  // live entry always carries its current saturation and an uncolored degree
-  // >= the current one. A popped entry with an outdated saturation is dropped
-  // (a newer one exists), one with an outdated degree is re-pushed with the
-  // current key; a popped entry that is exactly current dominates every other
-  // vertex's true key, so the selection equals the reference's eager heap
-  // (proj/src/coloring.cpp:184-213) with far fewer queue operations.
-  // Keys are packed into 64-bit integers in a 4-ary heap, per-vertex state is
-  // one 16-byte record (color, saturation, uncolored degree) plus a flat
-  // neighbor-color bitset of W words (grown on demand), and the neighbor
-  // sweep prefetches ahead: on the 3D leaf graphs (10^8 edges) the queue and
-  // the sweep are the whole cost.
+  // Selection = max (saturation, uncolored degree, -v) over uncolored
+  // vertices, as the reference's eager heap (proj/src/coloring.cpp:184-213).
+  // Queue: one lazy max-heap of (uncolored degree, -v) per saturation value;
+  // a vertex is pushed into bucket sat whenever its saturation rises, so the
+  // highest non-empty bucket holds every candidate. A popped entry whose
+  // vertex is colored or has moved to a higher bucket is dropped; one with an
+  // outdated degree is re-pushed with the current degree; a popped entry that
+  // is exactly current dominates its bucket -- the selection is identical to
+  // the eager heap with far fewer and shallower queue operations.
+  // Per-vertex state is one 16-byte record (color, saturation, uncolored
+  // degree) plus a flat neighbor-color bitset of W words (grown on demand),
+  // and the neighbor sweep prefetches ahead.
   struct VState {
     int color;
     int sat;
     int udeg;
     int pad;
   };
-  int max_deg = 0;
-  for (int v = 0; v < n; ++v) max_deg = std::max(max_deg, int(graph.edges[size_t(v)].size()));
-  if (max_deg >= (1 << 21) || n > 0x7FFFFFFF) throw std::logic_error("dsatur: graph too large for packed keys");
+  auto key = [](int udeg, int v) {
+    return (std::uint64_t(unsigned(udeg)) << 32) | (0xFFFFFFFFull - std::uint64_t(unsigned(v)));
+  };
   std::vector<VState> st(static_cast<size_t>(n));
   size_t words = 4;
   std::vector<std::uint64_t> seen(size_t(n) * words, 0);
-  KeyHeap heap;
-  heap.reserve(size_t(n) * 4);
+  std::vector<KeyHeap> bucket(1);
+  bucket[0].reserve(size_t(n));
   for (int v = 0; v < n; ++v) {
     const int d = int(graph.edges[size_t(v)].size());
     st[size_t(v)] = VState{-1, 0, d, 0};
-    heap.push(dsatur_key(0, d, v));
+    bucket[0].push(key(d, v));
   }
   out.queue_ops += size_t(n);
+  int top = 0;  // highest bucket that may be non-empty
   int done = 0;
   constexpr int kAhead = 12;
   while (done < n) {
-    const std::uint64_t key = heap.top();
-    heap.pop();
+    while (bucket[size_t(top)].empty()) --top;
+    KeyHeap& hb = bucket[size_t(top)];
+    const std::uint64_t k = hb.top();
+    hb.pop();
     ++out.queue_ops;
-    const int s = int(key >> 53);
-    const int ud = int((key >> 32) & 0x1FFFFF);
-    const int v = int(0xFFFFFFFFull - (key & 0xFFFFFFFFull));
+    const int ud = int(k >> 32);
+    const int v = int(0xFFFFFFFFull - (k & 0xFFFFFFFFull));
     VState& sv = st[size_t(v)];
-    if (sv.color != -1 || s != sv.sat) continue;
+    if (sv.color != -1 || sv.sat != top) continue;
     if (ud != sv.udeg) {
-      heap.push(dsatur_key(s, sv.udeg, v));
+      hb.push(key(sv.udeg, v));
       ++out.queue_ops;
       continue;
     }
@@ -334,7 +331,6 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
       seen.swap(grown);
       words *= 2;
     }
-    if (c >= (1 << 11) - 1) throw std::logic_error("dsatur: more than 2046 colors");
     sv.color = c;
     out.color[size_t(v)] = c;
     out.num_colors = std::max(out.num_colors, c + 1);
@@ -356,8 +352,10 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
       std::uint64_t& word = seen[size_t(w) * words + cw];
       if (!(word & cb)) {
         word |= cb;
-        ++sw.sat;
-        heap.push(dsatur_key(sw.sat, sw.udeg, w));
+        const int ns = ++sw.sat;
+        if (size_t(ns) >= bucket.size()) bucket.resize(size_t(ns) + 1);
+        bucket[size_t(ns)].push(key(sw.udeg, w));
+        if (ns > top) top = ns;
         ++out.queue_ops;
       }
     }
