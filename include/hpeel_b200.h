@@ -95,7 +95,10 @@ int hp_tree_layout(const hp_tree* tree, int* perm, int64_t* start, int64_t* coun
 
 /* ---- Sampling plan: build_constraints / build_graph / plan_coloring /
  *      assemble_test_matrices / make_plan (proj/src/coloring.cpp:55-332,
- *      proj/src/peeling.cpp:98-154; binding level_coloring module.cpp:190-205) */
+ *      proj/src/peeling.cpp:98-154; binding level_coloring module.cpp:190-205).
+ *      pairwise_graph: 0 inverted-index graph, 1 literal pairwise scan,
+ *      2 implicit graph (no edge lists; the path compress() uses for
+ *      single-payload sets) */
 int hp_plan_build(const hp_tree* tree, int level, int mode, int width, uint64_t seed, int phase,
                   int pairwise_graph, hp_plan** out);
 void hp_plan_free(hp_plan* plan);

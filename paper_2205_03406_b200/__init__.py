@@ -261,8 +261,10 @@ class Plan:
         return out
 
 
-def plan(tree, level, mode="h1", width=10, seed=0, phase=0, pairwise=False) -> Plan:
-    return Plan(tree, level, mode, width, seed, phase, pairwise)
+def plan(tree, level, mode="h1", width=10, seed=0, phase=0, pairwise=False, implicit=False) -> Plan:
+    """`pairwise`: literal O(V^2) graph scan; `implicit`: the driver's graph-free
+    DSatur (no edge lists: plan.graph() is empty)."""
+    return Plan(tree, level, mode, width, seed, phase, 2 if implicit else pairwise)
 
 
 def level_coloring(tree: BoxTree, level: int, mode: str) -> dict:

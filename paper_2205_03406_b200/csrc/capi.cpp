@@ -250,9 +250,18 @@ int hp_plan_build(const hp_tree* t, int level, int mode, int width, uint64_t see
     auto p = std::make_unique<hp_plan>();
     p->tree = t->tree;
     p->sets = build_constraints(*t->tree, *t->adj, level, m);
-    p->graph = pairwise_graph ? build_graph_pairwise(p->sets) : build_graph(p->sets);
-    p->dsatur = dsatur_color(p->graph);
-    p->coloring = plan_coloring(*t->tree, p->sets, p->graph, m);
+    if (pairwise_graph == 2) {  // implicit graph (the driver's path): no edge lists kept
+      if (!ImplicitGraph::applicable(p->sets)) throw std::invalid_argument("implicit graph needs single-payload sets");
+      const ImplicitGraph g(p->sets);
+      p->dsatur = dsatur_color(g);
+      p->coloring = plan_coloring(*t->tree, p->sets, p->dsatur, m);
+      p->graph.num_vertices = int(p->sets.size());
+      p->graph.edges.assign(p->sets.size(), {});
+    } else {
+      p->graph = pairwise_graph ? build_graph_pairwise(p->sets) : build_graph(p->sets);
+      p->dsatur = dsatur_color(p->graph);
+      p->coloring = plan_coloring(*t->tree, p->sets, p->graph, m);
+    }
     if (!p->sets.empty())
       p->mats = assemble_test_matrices(p->sets, p->coloring, *t->tree, level, width, seed, phase);
     *out = p.release();

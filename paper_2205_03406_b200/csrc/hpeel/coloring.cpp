@@ -263,8 +263,8 @@ class KeyHeap {
 
 }  // namespace
 
-Coloring dsatur_color(const IncompatibilityGraph& graph) {
-  const int n = graph.num_vertices;
+template <class Degree, class Sweep>
+Coloring dsatur_impl(int n, Degree&& degree, Sweep&& sweep) {
   Coloring out;
   out.color.assign(size_t(n), -1);
   if (n == 0) return out;
@@ -295,7 +295,7 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
   std::vector<KeyHeap> bucket(1);
   bucket[0].reserve(size_t(n));
   for (int v = 0; v < n; ++v) {
-    const int d = int(graph.edges[size_t(v)].size());
+    const int d = degree(v);
     st[size_t(v)] = VState{-1, 0, d, 0};
     bucket[0].push(key(d, v));
   }
@@ -337,17 +337,9 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
     ++done;
     const size_t cw = size_t(c) >> 6;
     const std::uint64_t cb = std::uint64_t(1) << (c & 63);
-    const std::vector<int>& nb = graph.edges[size_t(v)];
-    const size_t m = nb.size();
-    for (size_t i = 0; i < m; ++i) {
-      if (i + kAhead < m) {
-        const size_t u = size_t(nb[i + kAhead]);
-        __builtin_prefetch(&st[u], 1, 1);
-        __builtin_prefetch(&seen[u * words + cw], 1, 1);
-      }
-      const int w = nb[i];
+    auto visit = [&](int w) {
       VState& sw = st[size_t(w)];
-      if (sw.color != -1) continue;
+      if (sw.color != -1) return;
       --sw.udeg;
       std::uint64_t& word = seen[size_t(w) * words + cw];
       if (!(word & cb)) {
@@ -358,14 +350,111 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
         if (ns > top) top = ns;
         ++out.queue_ops;
       }
-    }
+    };
+    sweep(v, visit, st, seen, words, cw);
   }
   return out;
 }
 
+Coloring dsatur_color(const IncompatibilityGraph& graph) {
+  return dsatur_impl(
+      graph.num_vertices, [&](int v) { return int(graph.edges[size_t(v)].size()); },
+      [&](int v, auto&& visit, auto& st, auto& seen, size_t words, size_t cw) {
+        constexpr int kAhead = 12;
+        const std::vector<int>& nb = graph.edges[size_t(v)];
+        const size_t m = nb.size();
+        for (size_t i = 0; i < m; ++i) {
+          if (i + kAhead < m) {
+            const size_t u = size_t(nb[i + kAhead]);
+            __builtin_prefetch(&st[u], 1, 1);
+            __builtin_prefetch(&seen[u * words + cw], 1, 1);
+          }
+          visit(nb[i]);
+        }
+      });
+}
+
+Coloring dsatur_color(const ImplicitGraph& graph) {
+  std::vector<int> stamp(size_t(graph.num_vertices()), -1);
+  return dsatur_impl(graph.num_vertices(), [&](int v) { return graph.degree(v); },
+                     [&](int v, auto&& visit, auto&, auto&, size_t, size_t) {
+                       graph.for_each_neighbor(v, stamp, v, visit);
+                     });
+}
+
+bool ImplicitGraph::applicable(const std::vector<ConstraintSet>& sets) {
+  if (sets.empty()) return true;
+  const PayloadTag t0 = sets[0].payload.empty() ? PayloadTag::kGaussian : sets[0].payload[0].second;
+  for (const auto& s : sets)
+    if (s.payload.size() != 1 || s.payload[0].second != t0) return false;
+  return true;
+}
+
+ImplicitGraph::ImplicitGraph(const std::vector<ConstraintSet>& sets) : sets_(&sets) {
+  n_ = int(sets.size());
+  int max_box = -1;
+  payload_.resize(sets.size());
+  for (size_t i = 0; i < sets.size(); ++i) {
+    payload_[i] = sets[i].payload[0].first;
+    max_box = std::max(max_box, payload_[i]);
+    for (int z : sets[i].zero) max_box = std::max(max_box, z);
+  }
+  const size_t nb = size_t(max_box + 1);
+  zoff_.assign(nb + 1, 0);
+  poff_.assign(nb + 1, 0);
+  for (size_t i = 0; i < sets.size(); ++i) {
+    for (int z : sets[i].zero) ++zoff_[size_t(z) + 1];
+    ++poff_[size_t(payload_[i]) + 1];
+  }
+  for (size_t b = 0; b < nb; ++b) {
+    zoff_[b + 1] += zoff_[b];
+    poff_[b + 1] += poff_[b];
+  }
+  zsets_.resize(size_t(zoff_[nb]));
+  psets_.resize(size_t(poff_[nb]));
+  {
+    std::vector<int> zc(zoff_.begin(), zoff_.end() - 1), pc(poff_.begin(), poff_.end() - 1);
+    for (size_t i = 0; i < sets.size(); ++i) {
+      for (int z : sets[i].zero) zsets_[size_t(zc[size_t(z)]++)] = int(i);
+      psets_[size_t(pc[size_t(payload_[i])]++)] = int(i);
+    }
+  }
+  // degrees: threads over vertices, each with its own stamp array
+  deg_.assign(sets.size(), 0);
+  const size_t n = sets.size();
+  const unsigned nt = n < 4096 ? 1u : std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::atomic<size_t> next{0};
+  std::atomic<std::size_t> total{0};
+  auto work = [&] {
+    std::vector<int> stamp(n, -1);
+    std::size_t local = 0;
+    for (;;) {
+      const size_t b = next.fetch_add(256);
+      if (b >= n) break;
+      for (size_t i = b; i < std::min(n, b + 256); ++i) {
+        int d = 0;
+        for_each_neighbor(int(i), stamp, int(i), [&](int) { ++d; });
+        deg_[i] = d;
+        local += size_t(d);
+      }
+    }
+    total += local;
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  edges2_ = total.load();
+}
+
 Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets,
                        const IncompatibilityGraph& graph, SampleMode mode) {
-  Coloring best = dsatur_color(graph);
+  return plan_coloring(tree, sets, dsatur_color(graph), mode);
+}
+
+Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets, Coloring dsatur,
+                       SampleMode mode) {
+  Coloring best = std::move(dsatur);
   if (mode == SampleMode::kUnifStage2 || !tree.is_fully_populated()) return best;
   const int mod = mode == SampleMode::kH1 ? 6 : mode == SampleMode::kUnifStage1 ? 5 : 3;
   std::vector<int> tile(sets.size());
@@ -488,12 +577,20 @@ SamplingPlan make_plan(const BoxTree& tree, const AdjacencyInfo& adj, int level,
   const auto sets = build_constraints(tree, adj, level, mode);
   lap("constraints");
   if (sets.empty()) return plan;
-  const auto graph = build_graph(sets);
-  lap("graph");
-  const auto coloring = plan_coloring(tree, sets, graph, mode);
+  Coloring coloring;
+  if (ImplicitGraph::applicable(sets)) {
+    const ImplicitGraph graph(sets);
+    lap("graph (implicit: degrees)");
+    coloring = plan_coloring(tree, sets, dsatur_color(graph), mode);
+    plan.n_edges = graph.num_edges();
+  } else {
+    const auto graph = build_graph(sets);
+    lap("graph");
+    coloring = plan_coloring(tree, sets, graph, mode);
+    plan.n_edges = graph.num_edges();
+  }
   lap("coloring");
   plan.n_vertices = sets.size();
-  plan.n_edges = graph.num_edges();
   plan.matrices = assemble_test_matrices(sets, coloring, tree, level, width, seed, phase);
   lap("matrices");
   for (size_t i = 0; i < sets.size(); ++i)

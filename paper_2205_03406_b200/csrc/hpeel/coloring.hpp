@@ -62,6 +62,53 @@ struct Coloring {
 /// smallest free color; same lazy max-heap, so queue_ops match.
 Coloring dsatur_color(const IncompatibilityGraph& graph);
 
+/// The same incompatibility graph without materializing it, for sets with
+/// one payload box each and a single payload tag (the H1 and leaf modes):
+/// N(v) = {sets whose zero set holds v's payload box} U {sets whose payload
+/// box is in v's zero set}, enumerated from two box -> set indexes with a
+/// stamp array. Degrees are counted in parallel; DSatur walks the same
+/// neighbor sets, so colorings equal dsatur_color(build_graph(sets)).
+class ImplicitGraph {
+ public:
+  static bool applicable(const std::vector<ConstraintSet>& sets);
+  explicit ImplicitGraph(const std::vector<ConstraintSet>& sets);
+  int num_vertices() const { return n_; }
+  std::size_t num_edges() const { return edges2_ / 2; }
+  int degree(int v) const { return deg_[size_t(v)]; }
+  /// f(w) once per neighbor w of v; stamp (size n, caller-owned) tags
+  /// visited vertices with `tag`, which must differ between calls.
+  template <class F>
+  void for_each_neighbor(int v, std::vector<int>& stamp, int tag, F&& f) const {
+    stamp[size_t(v)] = tag;
+    const int pb = payload_[size_t(v)];
+    for (int k = zoff_[size_t(pb)]; k < zoff_[size_t(pb) + 1]; ++k) {
+      const int w = zsets_[size_t(k)];
+      if (stamp[size_t(w)] != tag) {
+        stamp[size_t(w)] = tag;
+        f(w);
+      }
+    }
+    for (const int z : (*sets_)[size_t(v)].zero)
+      for (int k = poff_[size_t(z)]; k < poff_[size_t(z) + 1]; ++k) {
+        const int w = psets_[size_t(k)];
+        if (stamp[size_t(w)] != tag) {
+          stamp[size_t(w)] = tag;
+          f(w);
+        }
+      }
+  }
+
+ private:
+  const std::vector<ConstraintSet>* sets_;
+  int n_ = 0;
+  std::vector<int> payload_, zoff_, zsets_, poff_, psets_, deg_;
+  std::size_t edges2_ = 0;
+};
+Coloring dsatur_color(const ImplicitGraph& graph);
+
+/// proj/src/coloring.cpp:218-250 (DSatur result given).
+Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets, Coloring dsatur,
+                       SampleMode mode);
 /// proj/src/coloring.cpp:218-250.
 Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets,
                        const IncompatibilityGraph& graph, SampleMode mode);

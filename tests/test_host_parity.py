@@ -169,3 +169,20 @@ def test_export_sizes_match_layout(hp):
     w = max(len(ot.box(v).points) for v in range(len(ot.boxes)) if not ot.box(v).children)
     want_d = sum(len(ot.box(lam).points) * w for lam, _ in tree.dense_pairs())
     assert hp.export_sizes(tree, k) == (want_f, want_d)
+
+
+@pytest.mark.parametrize("name,pts,leaf", GEOMS, ids=[g[0] for g in GEOMS])
+def test_implicit_graph_dsatur_equals_explicit(hp, name, pts, leaf):
+    """compress() colors single-payload constraint sets (H1 and leaf modes)
+    without materializing the graph; its DSatur coloring, color count and
+    plan coloring equal the explicit graph's."""
+    t = hp.build_tree(pts, leaf)
+    modes = [("leaf", t.depth)] + [("h1", l) for l in range(2, t.depth + 1)]
+    for mode, level in modes:
+        a = hp.plan(t, level, mode, 8, 7, 0)
+        b = hp.plan(t, level, mode, 8, 7, 0, implicit=True)
+        if a.n_vertices == 0:
+            continue
+        assert a.dsatur_color == b.dsatur_color, (name, mode, level)
+        assert a.dsatur_colors == b.dsatur_colors and a.n_colors == b.n_colors
+        assert a.color == b.color and a.color_payload == b.color_payload, (name, mode, level)
