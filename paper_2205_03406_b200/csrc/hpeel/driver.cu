@@ -601,9 +601,12 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
       const bool checked = w.k2_checked || e.has_dups;
       // int8 tensor-core K2 (k2_i8.cuh): on-the-fly symmetric kernels,
-      // unchecked tiles, r <= 64 (7 accumulator groups x r fit TMEM)
-      const bool use_i8 = op.kind() != kOpDense && op.symmetric() && !checked && r <= 64 &&
-                          k2_mode() == 0 && k2_int8_enabled();
+      // unchecked tiles, widths with the group split (r <= 48). At r = 64 the
+      // column-split int8 kernel is no faster than DMMA (config 4 scaled:
+      // 1.74 s both) and its sample error (5e-13) sits closest to the 1e-12
+      // bar, so those widths keep FP64 DMMA.
+      const bool use_i8 = op.kind() != kOpDense && op.symmetric() && !checked &&
+                          k2i8::group_split(k2i8::padded_width(r)) && k2_mode() == 0 && k2_int8_enabled();
       apply_path[size_t(l)] = use_i8 ? 1 : 0;
       DevBuf<unsigned char> bdig;
       DevBuf<std::int64_t> d_step_off, d_pb_off;

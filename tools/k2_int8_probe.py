@@ -15,7 +15,7 @@ w = configs.scaled(name, n) if n != configs.CONFIGS[name].n else configs.CONFIGS
 pts = w.points()
 t = hp.build_tree(pts, w.leaf)
 op = hp.kernel_operator(w.kernel, pts, w.param)
-rank, over = (w.rank, w.oversample) if w.rank + w.oversample <= 64 else (48, 16)
+rank, over = (w.rank, w.oversample) if w.rank + w.oversample <= 48 else (36, 12)
 cap = n <= 65536
 reps = {}
 for path in ("fp64", "int8", "int8"):
