@@ -6,9 +6,11 @@
 // pseudo-inverse tolerances, and the same error behaviour. What changes is
 // where the work runs: every level's host plan (coloring, task lists, QR
 // and peeling structure) is built on host threads up front, and the device
-// executes the levels back to back on one stream -- K1 payload, K2 apply on
-// the sample rows the extraction reads, K3 peeling restricted to nonzero
-// payload rows, batched K4 QR and K5 B-solves -- with no host round trip.
+// executes the levels with no host round trip: K1 payload and K2 apply on
+// the sample rows the extraction reads (apply stream, one level ahead), then
+// K3 peeling restricted to nonzero payload rows, batched K4 QR and K5
+// B-solves (main stream), so level l + 1's apply overlaps level l's
+// factorization.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -332,6 +334,43 @@ struct LevelTimers {
   Events apply, peel, mid, qr, bsolve;
 };
 
+/// One level's sampling stage (K1 payload + K2 apply), issued on the apply
+/// stream one level ahead of the level's peel / QR / B work on the main
+/// stream: K2 of level l + 1 depends only on its host plan, so it overlaps
+/// the factorization of level l. Every buffer is allocated and freed on the
+/// main stream `s`; the apply stream starts after `ready` (recorded on `s`
+/// after the uploads) and the frees wait for `done`.
+struct ApplyStage {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ready = nullptr, done = nullptr;
+  LevelWork w;
+  std::unique_ptr<LevelTimers> tm;
+  bool use_i8 = false;
+  DevBuf<int> d_pos_box, d_local;
+  DevBuf<K2Row> d_rowtab;
+  DevBuf<std::int64_t> d_pay_off;
+  DevBuf<int> d_pay_pos;
+  DevBuf<double> samples, gcol, xcol;
+  DevBuf<unsigned char> bdig;
+  DevBuf<std::int64_t> d_step_off, d_pb_off;
+  DevBuf<double> xstep;
+  DevBuf<int> d_step_color, d_pb_box;
+  std::vector<DevBuf<K2Task>> d_tasks;
+
+  explicit ApplyStage(cudaStream_t st) : s(st) {
+    HP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    HP_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  }
+  ApplyStage(const ApplyStage&) = delete;
+  ApplyStage& operator=(const ApplyStage&) = delete;
+  ~ApplyStage() {
+    cudaStreamWaitEvent(s, done, 0);  // the members' frees (on s) follow the apply stream's use
+    cudaEventDestroy(ready);
+    cudaEventDestroy(done);
+    reap_async(std::move(w));
+  }
+};
+
 }  // namespace
 
 void PeelConfig::validate() const {
@@ -457,8 +496,15 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
   auto adj = std::make_shared<const AdjacencyInfo>(adjacency(*tree));
   auto lay = std::make_shared<const TreeLayout>(tree_layout(*tree));
 
-  cudaStream_t s;
-  HP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // s: uploads, peel / QR / B and the leaf phase (high priority: it gates the
+  // next level's stage); sa: K1 + K2 of the level ahead (ApplyStage)
+  cudaStream_t s, sa;
+  {
+    int least = 0, greatest = 0;
+    HP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    HP_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, greatest));
+    HP_CUDA(cudaStreamCreateWithPriority(&sa, cudaStreamNonBlocking, least));
+  }
   PeelResult result;
   auto rep = std::make_shared<H1Rep>();
   rep->tree = tree;
@@ -533,7 +579,9 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     };
 
     const int gld = 2 * r;
-    DevBuf<double> g(size_t(n) * size_t(gld), s);
+    // payload Gaussians of two levels: K1 of level l + 1 (apply stream) runs
+    // while level l's peel and B solve (main stream) still read its payloads
+    DevBuf<double> gbuf[2] = {DevBuf<double>(size_t(n) * size_t(gld), s), DevBuf<double>(size_t(n) * size_t(gld), s)};
     std::vector<std::unique_ptr<LevelTimers>> timers(size_t(tree->depth()) + 1);
     std::vector<std::int64_t> rank_off(size_t(tree->depth()) + 1, 0);
     std::vector<double> evals(size_t(tree->depth()) + 1, 0.0), peel_flops(size_t(tree->depth()) + 1, 0.0);
@@ -544,61 +592,35 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
 
     std::vector<double> wait_ms(size_t(tree->depth()) + 1, 0.0);
     report.setup_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_begin).count();
-    for (int l = 2; l <= tree->depth(); ++l) {
+
+    // K1 + K2 of level l: uploads on s, launches on sa after `ready`
+    auto issue_apply = [&](int l) {
+      auto st = std::make_unique<ApplyStage>(s);
       const auto t_wait = Clock::now();
-      LevelWork w = futs[size_t(l)].get();
-      const auto t_got = Clock::now();
-      wait_ms[size_t(l)] = std::chrono::duration<double, std::milli>(t_got - t_wait).count();
-      struct IterTimer {  // HP_DRIVER_TIMING: host time spent issuing this level
-        int level;
-        Clock::time_point t0;
-        ~IterTimer() {
-          static const bool on = std::getenv("HP_DRIVER_TIMING") != nullptr;
-          if (on)
-            std::fprintf(stderr, "[driver] level %d issue %.1f ms\n", level,
-                         std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
-        }
-      } iter_timer{l, t_got};
-      struct Reap {  // this level's plan is released off the driver thread
-        LevelWork* w;
-        ~Reap() { reap_async(std::move(*w)); }
-      } reap_level{&w};
-      if (w.empty) continue;  // proj/src/peeling.cpp:221 (built_level not advanced)
+      st->w = futs[size_t(l)].get();
+      wait_ms[size_t(l)] = std::chrono::duration<double, std::milli>(Clock::now() - t_wait).count();
+      LevelWork& w = st->w;
+      if (w.empty) return st;  // proj/src/peeling.cpp:221 (built_level not advanced)
       if (!w.symmetric) throw std::logic_error("asymmetric admissibility structure");
-      if (l - 1 >= 2 && l - 1 > built)
-        throw std::runtime_error("h1 apply: representation incomplete for level " + std::to_string(l - 1));
-      auto& ld = rep->levels[size_t(l)];
       const size_t np = w.np;
-      auto tm = std::make_unique<LevelTimers>();
+      st->tm = std::make_unique<LevelTimers>();
+      LevelTimers* tm = st->tm.get();
       colors[size_t(l)] = w.nc;
       fcols[size_t(l)] = w.fwd_cols;
       evals[size_t(l)] = w.evals;
       peel_flops[size_t(l)] = w.peel.coeff_flops + w.peel.apply_flops;
+      double* g = gbuf[l & 1].get();
 
-      // K1 payload
-      DevBuf<int> d_pos_box, d_local;
-      d_pos_box.upload(w.pos_box, s);
-      d_local.upload(w.local, s);
-      launch_payload_gaussian(g.get(), gld, r, n, d_pos_box.get(), d_local.get(), config.seed, l, s);
-
-      // K2 apply (forward + adjoint samples of every pair's row block); each
-      // shard launches its own tiles, then the shards' rows are broadcast
-      const std::vector<std::int64_t>& seg = w.seg;
-      DevBuf<K2Row> d_rowtab;
-      d_rowtab.upload(w.rowtab, s);
-      DevBuf<std::int64_t> d_pay_off;
-      d_pay_off.upload(w.pay_off, s);
-      DevBuf<int> d_pay_pos;
-      d_pay_pos.upload(w.pay_pos, s);
-      DevBuf<double> samples(size_t(w.soff[np]), s);
+      st->d_pos_box.upload(w.pos_box, s);
+      st->d_local.upload(w.local, s);
+      st->d_rowtab.upload(w.rowtab, s);
+      st->d_pay_off.upload(w.pay_off, s);
+      st->d_pay_pos.upload(w.pay_pos, s);
+      st->samples.alloc(size_t(w.soff[np]), s);
       // payload rows and coordinates in color order (contiguous K2 chunks)
       const std::int64_t nnz = std::int64_t(w.pay_pos.size());
-      DevBuf<double> gcol(size_t(nnz) * size_t(gld), s);
-      DevBuf<double> xcol(op.kind() == kOpDense ? 1 : size_t(nnz) * size_t(op.dim()), s);
-      HP_CUDA(cudaEventRecord(tm->apply.a, s));
-      launch_permute_rows(g.get(), gld, 1, d_pay_pos.get(), nnz, gld, gcol.get(), gld, 1, s);
-      if (op.kind() != kOpDense)
-        launch_permute_rows(e.dop.x, 1, n, d_pay_pos.get(), nnz, op.dim(), xcol.get(), 1, nnz, s);
+      st->gcol.alloc(size_t(nnz) * size_t(gld), s);
+      st->xcol.alloc(op.kind() == kOpDense ? 1 : size_t(nnz) * size_t(op.dim()), s);
       const bool checked = w.k2_checked || e.has_dups;
       // int8 tensor-core K2 (k2_i8.cuh): on-the-fly symmetric kernels,
       // unchecked tiles, widths with the group split (r <= 48). At r = 64 the
@@ -607,125 +629,161 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       // bar, so those widths keep FP64 DMMA.
       const bool use_i8 = op.kind() != kOpDense && op.symmetric() && !checked &&
                           k2i8::group_split(k2i8::padded_width(r)) && k2_mode() == 0 && k2_int8_enabled();
+      st->use_i8 = use_i8;
       apply_path[size_t(l)] = use_i8 ? 1 : 0;
-      DevBuf<unsigned char> bdig;
-      DevBuf<std::int64_t> d_step_off, d_pb_off;
-      DevBuf<double> xstep;
-      DevBuf<int> d_step_color, d_pb_box;
-      std::int64_t half_stride = 0;
+      std::int64_t half_stride = 0, tsteps = 0;
       if (use_i8) {
-        const std::int64_t tsteps = w.step_off.back();
+        tsteps = w.step_off.back();
         half_stride = tsteps * k2i8::b_step_bytes(k2i8::padded_width(r));
-        bdig.alloc(size_t(std::max<std::int64_t>(2 * half_stride, 16)), s);  // same size in both layouts
+        st->bdig.alloc(size_t(std::max<std::int64_t>(2 * half_stride, 16)), s);  // same size in both layouts
+        st->d_step_off.upload(w.step_off, s);
+        st->d_step_color.upload(w.step_color, s);
+        st->d_pb_off.upload(w.pb_off, s);
+        st->d_pb_box.upload(w.pb_box, s);
+        st->xstep.alloc(size_t(std::max<std::int64_t>(tsteps, 1)) * 32 * size_t(op.dim()), s);
+        e.ensure_box_bbox();  // on s, before `ready`
+      }
+      st->d_tasks.reserve(w.k2.size());
+      for (int sr = 0; sr < int(w.k2.size()); ++sr) {
+        st->d_tasks.emplace_back();
+        if (my_rank >= 0 && sr != my_rank) continue;
+        st->d_tasks.back().upload(w.k2[size_t(sr)], s);
+      }
+      HP_CUDA(cudaEventRecord(st->ready, s));
+      HP_CUDA(cudaStreamWaitEvent(sa, st->ready, 0));
+
+      // K1 payload
+      launch_payload_gaussian(g, gld, r, n, st->d_pos_box.get(), st->d_local.get(), config.seed, l, sa);
+      // K2 apply (forward + adjoint samples of every pair's row block); each
+      // shard launches its own tiles, then the shards' rows are broadcast
+      HP_CUDA(cudaEventRecord(tm->apply.a, sa));
+      launch_permute_rows(g, gld, 1, st->d_pay_pos.get(), nnz, gld, st->gcol.get(), gld, 1, sa);
+      if (op.kind() != kOpDense)
+        launch_permute_rows(e.dop.x, 1, n, st->d_pay_pos.get(), nnz, op.dim(), st->xcol.get(), 1, nnz, sa);
+      if (use_i8) {
         // group split: the CTA pair adds two partial sums per sample element
-        if (k2i8::group_split(k2i8::padded_width(r)))
-          HP_CUDA(cudaMemsetAsync(samples.get(), 0, size_t(w.soff[np]) * sizeof(double), s));
-        d_step_off.upload(w.step_off, s);
-        d_step_color.upload(w.step_color, s);
-        d_pb_off.upload(w.pb_off, s);
-        d_pb_box.upload(w.pb_box, s);
-        k2i8::launch_payload_digits(gcol.get(), gld, r, d_pay_off.get(), d_step_off.get(), d_step_color.get(),
-                                    tsteps, bdig.get(), half_stride, s);
-        xstep.alloc(size_t(std::max<std::int64_t>(tsteps, 1)) * 32 * size_t(op.dim()), s);
-        k2i8::launch_step_coords(xcol.get(), nnz, op.dim(), d_pay_off.get(), d_step_off.get(), d_step_color.get(),
-                                 tsteps, xstep.get(), s);
-        e.ensure_box_bbox();
+        HP_CUDA(cudaMemsetAsync(st->samples.get(), 0, size_t(w.soff[np]) * sizeof(double), sa));
+        k2i8::launch_payload_digits(st->gcol.get(), gld, r, st->d_pay_off.get(), st->d_step_off.get(),
+                                    st->d_step_color.get(), tsteps, st->bdig.get(), half_stride, sa);
+        k2i8::launch_step_coords(st->xcol.get(), nnz, op.dim(), st->d_pay_off.get(), st->d_step_off.get(),
+                                 st->d_step_color.get(), tsteps, st->xstep.get(), sa);
       }
       for (int sr = 0; sr < int(w.k2.size()); ++sr) {
         if (my_rank >= 0 && sr != my_rank) continue;
-        const auto& tl = w.k2[size_t(sr)];
-        DevBuf<K2Task> d_tasks;
-        d_tasks.upload(tl, s);
-        const int nt = int(tl.size());
+        const K2Task* tasks = st->d_tasks[size_t(sr)].get();
+        const int nt = int(w.k2[size_t(sr)].size());
         if (use_i8) {
-          k2i8::launch_sample_apply_i8(e.dop, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(), d_step_off.get(),
-                                       xstep.get(), d_pb_off.get(), d_pb_box.get(), e.d_box_bbox.get(),
-                                       bdig.get(), half_stride, r, samples.get(), s);
+          k2i8::launch_sample_apply_i8(e.dop, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                                       st->d_step_off.get(), st->xstep.get(), st->d_pb_off.get(),
+                                       st->d_pb_box.get(), e.d_box_bbox.get(), st->bdig.get(), half_stride, r,
+                                       st->samples.get(), sa);
         } else if (op.symmetric()) {
-          launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
-                              d_pay_pos.get(), gcol.get(), gld, 0, 2 * r, xcol.get(), nnz,
-                              samples.get(), 0, checked, s);
+          launch_sample_apply(e.dop, false, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                              st->d_pay_pos.get(), st->gcol.get(), gld, 0, 2 * r, st->xcol.get(), nnz,
+                              st->samples.get(), 0, checked, sa);
         } else {
-          launch_sample_apply(e.dop, false, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
-                              d_pay_pos.get(), gcol.get(), gld, 0, r, xcol.get(), nnz, samples.get(), 0,
-                              checked, s);
-          launch_sample_apply(e.dop, true, d_tasks.get(), d_rowtab.get(), nt, d_pay_off.get(),
-                              d_pay_pos.get(), gcol.get(), gld, r, r, xcol.get(), nnz, samples.get(), r,
-                              checked, s);
+          launch_sample_apply(e.dop, false, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                              st->d_pay_pos.get(), st->gcol.get(), gld, 0, r, st->xcol.get(), nnz,
+                              st->samples.get(), 0, checked, sa);
+          launch_sample_apply(e.dop, true, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                              st->d_pay_pos.get(), st->gcol.get(), gld, r, r, st->xcol.get(), nnz,
+                              st->samples.get(), r, checked, sa);
         }
       }
-      if (config.comm) config.comm->broadcast_segments(samples.get(), seg, s);
-      HP_CUDA(cudaEventRecord(tm->apply.b, s));
+      HP_CUDA(cudaEventRecord(tm->apply.b, sa));
+      HP_CUDA(cudaEventRecord(st->done, sa));
+      return st;
+    };
+    std::unique_ptr<ApplyStage> next;
+    if (tree->depth() >= 2) next = issue_apply(2);
+    for (int l = 2; l <= tree->depth(); ++l) {
+      std::unique_ptr<ApplyStage> cur = std::move(next);
+      // issue the next level's sampling ahead of this level's factorization
+      // (waiting for its host plan here is fine: the host runs far ahead of
+      // the device, and H1 level plans take <= 1.5 s even at config 4 full)
+      if (l + 1 <= tree->depth()) next = issue_apply(l + 1);
+      LevelWork& w = cur->w;
+      if (!w.empty) {
+        if (l - 1 >= 2 && l - 1 > built)
+          throw std::runtime_error("h1 apply: representation incomplete for level " + std::to_string(l - 1));
+        auto& ld = rep->levels[size_t(l)];
+        const size_t np = w.np;
+        LevelTimers* tm = cur->tm.get();
+        double* g = gbuf[l & 1].get();
+        double* samples = cur->samples.get();
+        HP_CUDA(cudaStreamWaitEvent(s, cur->done, 0));
+        if (config.comm) config.comm->broadcast_segments(samples, w.seg, s);
 
-      // K3 peel
-      HP_CUDA(cudaEventRecord(tm->peel.a, s));
-      if (w.has_peel) run_peel(w.peel, e, *rep, g.get(), gld, r, false, samples.get(), r, s);
-      HP_CUDA(cudaEventRecord(tm->peel.b, s));
+        // K3 peel
+        HP_CUDA(cudaEventRecord(tm->peel.a, s));
+        if (w.has_peel) run_peel(w.peel, e, *rep, g, gld, r, false, samples, r, s);
+        HP_CUDA(cudaEventRecord(tm->peel.b, s));
 
-      if (config.capture_samples) {
-        HP_CUDA(cudaStreamSynchronize(s));
-        std::vector<Matrix> cap;
-        for (size_t p = 0; p < np; ++p) {
-          const int rows = e.count(ld.pairs[p].first);
-          Matrix m(rows, 2 * r);
-          HP_CUDA(cudaMemcpy(m.data(), samples.get() + w.soff[p], size_t(rows) * 2 * r * 8,
-                             cudaMemcpyDeviceToHost));
-          cap.push_back(std::move(m));
+        if (config.capture_samples) {
+          HP_CUDA(cudaStreamSynchronize(s));
+          std::vector<Matrix> cap;
+          for (size_t p = 0; p < np; ++p) {
+            const int rows = e.count(ld.pairs[p].first);
+            Matrix m(rows, 2 * r);
+            HP_CUDA(cudaMemcpy(m.data(), samples + w.soff[p], size_t(rows) * 2 * r * 8,
+                               cudaMemcpyDeviceToHost));
+            cap.push_back(std::move(m));
+          }
+          rep->captured[l] = std::move(cap);
         }
-        rep->captured[l] = std::move(cap);
-      }
 
-      // K5a: middle = G'_a^T Y_p before the QR overwrites Y; K4 QR; K5b grams
-      // and B -- each shard on its own pairs, then the shards' factor and
-      // rank segments are broadcast
-      DevBuf<double> middle(np * size_t(r) * size_t(r), s), gpu(np * size_t(r) * size_t(k), s),
-          vg(np * size_t(k) * size_t(r), s);
-      DevBuf<int> d_ranks(2 * np, s);
-      DevBuf<std::int64_t> d_boff;
-      d_boff.upload(ld.boff, s);
-      auto mine = [&](int sr) { return my_rank < 0 || sr == my_rank; };
-      HP_CUDA(cudaEventRecord(tm->mid.a, s));
-      for (int sr = 0; sr < int(w.s45.size()); ++sr)
-        if (mine(sr))
-          run_gram(w.s45[size_t(sr)].g_mid, g.get(), samples.get(),
-                   middle.get() + w.s45[size_t(sr)].p0 * r * r, s);
-      HP_CUDA(cudaEventRecord(tm->mid.b, s));
-      HP_CUDA(cudaEventRecord(tm->qr.a, s));
-      for (int sr = 0; sr < int(w.s45.size()); ++sr)
-        if (mine(sr)) run_qr(w.s45[size_t(sr)].qr, samples.get(), rep->d_factors, d_ranks.get(), r, k, s);
-      HP_CUDA(cudaEventRecord(tm->qr.b, s));
-      HP_CUDA(cudaEventRecord(tm->bsolve.a, s));
-      for (int sr = 0; sr < int(w.s45.size()); ++sr) {
-        if (!mine(sr)) continue;
-        const LevelWork::Shard45& sh = w.s45[size_t(sr)];
-        run_gram(sh.g_gpu, g.get(), rep->d_factors, gpu.get() + sh.p0 * r * k, s);
-        run_gram(sh.g_vg, rep->d_factors, g.get(), vg.get() + sh.p0 * k * r, s);
-        launch_bsolve(int(sh.p1 - sh.p0), gpu.get() + sh.p0 * r * k, middle.get() + sh.p0 * r * r,
-                      vg.get() + sh.p0 * k * r, r, k, kPinvCutoff, d_boff.get() + sh.p0, rep->d_factors, s);
-      }
-      if (config.comm && np > 0) {
-        const std::int64_t fend = ld.boff[np - 1] + std::int64_t(k) * k;
-        std::vector<std::int64_t> fseg(w.fb.size()), useg(w.fb.size()), vseg(w.fb.size());
-        for (size_t q = 0; q < w.fb.size(); ++q) {
-          const std::int64_t p = w.fb[q];
-          fseg[q] = p < std::int64_t(np) ? ld.uoff[size_t(p)] : fend;
-          useg[q] = p;
-          vseg[q] = std::int64_t(np) + p;
+        // K5a: middle = G'_a^T Y_p before the QR overwrites Y; K4 QR; K5b grams
+        // and B -- each shard on its own pairs, then the shards' factor and
+        // rank segments are broadcast
+        DevBuf<double> middle(np * size_t(r) * size_t(r), s), gpu(np * size_t(r) * size_t(k), s),
+            vg(np * size_t(k) * size_t(r), s);
+        DevBuf<int> d_ranks(2 * np, s);
+        DevBuf<std::int64_t> d_boff;
+        d_boff.upload(ld.boff, s);
+        auto mine = [&](int sr) { return my_rank < 0 || sr == my_rank; };
+        HP_CUDA(cudaEventRecord(tm->mid.a, s));
+        for (int sr = 0; sr < int(w.s45.size()); ++sr)
+          if (mine(sr))
+            run_gram(w.s45[size_t(sr)].g_mid, g, samples, middle.get() + w.s45[size_t(sr)].p0 * r * r, s);
+        HP_CUDA(cudaEventRecord(tm->mid.b, s));
+        HP_CUDA(cudaEventRecord(tm->qr.a, s));
+        for (int sr = 0; sr < int(w.s45.size()); ++sr)
+          if (mine(sr)) run_qr(w.s45[size_t(sr)].qr, samples, rep->d_factors, d_ranks.get(), r, k, s);
+        HP_CUDA(cudaEventRecord(tm->qr.b, s));
+        HP_CUDA(cudaEventRecord(tm->bsolve.a, s));
+        for (int sr = 0; sr < int(w.s45.size()); ++sr) {
+          if (!mine(sr)) continue;
+          const LevelWork::Shard45& sh = w.s45[size_t(sr)];
+          run_gram(sh.g_gpu, g, rep->d_factors, gpu.get() + sh.p0 * r * k, s);
+          run_gram(sh.g_vg, rep->d_factors, g, vg.get() + sh.p0 * k * r, s);
+          launch_bsolve(int(sh.p1 - sh.p0), gpu.get() + sh.p0 * r * k, middle.get() + sh.p0 * r * r,
+                        vg.get() + sh.p0 * k * r, r, k, kPinvCutoff, d_boff.get() + sh.p0, rep->d_factors, s);
         }
-        config.comm->broadcast_segments(rep->d_factors, fseg, s);
-        config.comm->broadcast_segments_i32(d_ranks.get(), useg, s);
-        config.comm->broadcast_segments_i32(d_ranks.get(), vseg, s);
+        if (config.comm && np > 0) {
+          const std::int64_t fend = ld.boff[np - 1] + std::int64_t(k) * k;
+          std::vector<std::int64_t> fseg(w.fb.size()), useg(w.fb.size()), vseg(w.fb.size());
+          for (size_t q = 0; q < w.fb.size(); ++q) {
+            const std::int64_t p = w.fb[q];
+            fseg[q] = p < std::int64_t(np) ? ld.uoff[size_t(p)] : fend;
+            useg[q] = p;
+            vseg[q] = std::int64_t(np) + p;
+          }
+          config.comm->broadcast_segments(rep->d_factors, fseg, s);
+          config.comm->broadcast_segments_i32(d_ranks.get(), useg, s);
+          config.comm->broadcast_segments_i32(d_ranks.get(), vseg, s);
+        }
+        HP_CUDA(cudaEventRecord(tm->bsolve.b, s));
+        HP_CUDA(cudaMemcpyAsync(h_ranks + roff, d_ranks.get(), 2 * np * sizeof(int), cudaMemcpyDeviceToHost, s));
+        rank_off[size_t(l)] = roff;
+        roff += 2 * std::int64_t(np);
+        timers[size_t(l)] = std::move(cur->tm);
+        if (exporter.active() && np > 0) {  // this level's U, V, B are final
+          const std::int64_t f0 = ld.uoff[0], f1 = ld.boff[np - 1] + std::int64_t(k) * k;
+          exporter.copy(exporter.factors() ? exporter.factors() + f0 : nullptr, rep->d_factors + f0, f1 - f0, s);
+        }
+        built = l;
       }
-      HP_CUDA(cudaEventRecord(tm->bsolve.b, s));
-      HP_CUDA(cudaMemcpyAsync(h_ranks + roff, d_ranks.get(), 2 * np * sizeof(int), cudaMemcpyDeviceToHost, s));
-      rank_off[size_t(l)] = roff;
-      roff += 2 * std::int64_t(np);
-      timers[size_t(l)] = std::move(tm);
-      if (exporter.active() && np > 0) {  // this level's U, V, B are final
-        const std::int64_t f0 = ld.uoff[0], f1 = ld.boff[np - 1] + std::int64_t(k) * k;
-        exporter.copy(exporter.factors() ? exporter.factors() + f0 : nullptr, rep->d_factors + f0, f1 - f0, s);
-      }
-      built = l;
+      cur.reset();  // frees (on s) after the apply stream's use of its buffers
     }
     rep->built_level = tree->depth();
 
@@ -877,11 +935,14 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     // planning threads' pages) had put 0-0.6 s of host time on the return path
     reap_async(std::move(lw));
   } catch (...) {
+    cudaStreamSynchronize(sa);
     cudaStreamSynchronize(s);
+    cudaStreamDestroy(sa);
     cudaStreamDestroy(s);
     throw;
   }
   HP_CUDA(cudaStreamSynchronize(s));
+  cudaStreamDestroy(sa);
   cudaStreamDestroy(s);
   result.rep = rep;
   return result;
