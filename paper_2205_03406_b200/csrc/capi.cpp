@@ -548,6 +548,8 @@ int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times)
       times[7] = ph.kernel_evals;
       times[8] = ph.host_wait_ms;
       times[9] = ph.start_ms;
+      times[10] = ph.peel_flops;
+      times[11] = ph.qr_flops;
     }
   });
 }

@@ -502,8 +502,9 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
   {
     int least = 0, greatest = 0;
     HP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    HP_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, greatest));
-    HP_CUDA(cudaStreamCreateWithPriority(&sa, cudaStreamNonBlocking, least));
+    static const int flip = std::getenv("HP_APPLY_PRIORITY") ? std::atoi(std::getenv("HP_APPLY_PRIORITY")) : 0;
+    HP_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, flip == 1 ? least : greatest));
+    HP_CUDA(cudaStreamCreateWithPriority(&sa, cudaStreamNonBlocking, flip == 1 ? greatest : least));
   }
   PeelResult result;
   auto rep = std::make_shared<H1Rep>();
@@ -694,6 +695,10 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       HP_CUDA(cudaEventRecord(st->done, sa));
       return st;
     };
+    // HP_SERIAL_LEVELS=1: no overlap (each level's apply after the previous
+    // level's factorization), so K2 can be timed alone (bench.py)
+    const char* serial_env = std::getenv("HP_SERIAL_LEVELS");
+    const bool serial = serial_env && std::atoi(serial_env) != 0;
     std::unique_ptr<ApplyStage> next;
     if (tree->depth() >= 2) next = issue_apply(2);
     for (int l = 2; l <= tree->depth(); ++l) {
@@ -701,7 +706,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       // issue the next level's sampling ahead of this level's factorization
       // (waiting for its host plan here is fine: the host runs far ahead of
       // the device, and H1 level plans take <= 1.5 s even at config 4 full)
-      if (l + 1 <= tree->depth()) next = issue_apply(l + 1);
+      if (!serial && l + 1 <= tree->depth()) next = issue_apply(l + 1);
       LevelWork& w = cur->w;
       if (!w.empty) {
         if (l - 1 >= 2 && l - 1 > built)
@@ -784,6 +789,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         built = l;
       }
       cur.reset();  // frees (on s) after the apply stream's use of its buffers
+      if (serial && l + 1 <= tree->depth()) next = issue_apply(l + 1);  // waits for this level on s
     }
     rep->built_level = tree->depth();
 
@@ -892,6 +898,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         const std::int64_t ma = e.count(ld.pairs[p].first), mb = e.count(ld.pairs[p].second);
         const std::int64_t ku = ld.ku[p], kv = ld.kv[p];
         ph.net_flops += 2 * ma * r * r + 2 * mb * r * r;
+        ph.qr_flops += 2.0 * double(ma) * r * r + 2.0 * double(mb) * r * r;
         ph.net_flops += gemm_flops(r, r, ma) + gemm_flops(r, ku, ma) + gemm_flops(kv, r, mb);
         if (ku > 0) ph.net_flops += svd_flops(r, ku) + gemm_flops(ku, r, r);
         if (kv > 0) ph.net_flops += svd_flops(r, kv) + gemm_flops(kv, ku, r);

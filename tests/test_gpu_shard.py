@@ -28,3 +28,24 @@ def test_emulated_shards_bit_identical(hp, gpu_available, name, n, shards):
                 assert np.array_equal(a, b)
     for i in range(len(t.dense_pairs())):
         assert np.array_equal(one.dense_block(i), many.dense_block(i))
+
+
+@pytest.mark.parametrize("name,n", [("c3", 32768), ("c5", 16384)])
+def test_level_overlap_bit_identical(hp, gpu_available, name, n, monkeypatch):
+    """Level l+1's K1/K2 run on the apply stream while level l peels, factors
+    and solves on the main stream (driver.cu ApplyStage); the overlapped run
+    and the serialized one (HP_SERIAL_LEVELS=1) give identical factors and
+    dense blocks (no capture: capture synchronizes inside each level)."""
+    w = configs.scaled(name, n)
+    pts = w.points()
+    t = hp.build_tree(pts, w.leaf)
+    op = hp.kernel_operator(w.kernel, pts, w.param)
+    over = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
+    monkeypatch.setenv("HP_SERIAL_LEVELS", "1")
+    ser = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
+    for l in range(2, t.depth + 1):
+        for i in range(len(t.admissible_pairs(l))):
+            for a, b in zip(over.block(l, i), ser.block(l, i)):
+                assert np.array_equal(a, b)
+    for i in range(len(t.dense_pairs())):
+        assert np.array_equal(over.dense_block(i), ser.dense_block(i))
