@@ -697,8 +697,14 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     };
     // HP_SERIAL_LEVELS=1: no overlap (each level's apply after the previous
     // level's factorization), so K2 can be timed alone (bench.py)
+    // Overlap only pays when K2 runs on the int8 tensor cores: the FP64 DMMA
+    // K2 and the peel / QR / B kernels share the FP64 datapath, and there the
+    // overlapped order measured slower (config 5 scaled 3.12 s vs 3.02 s
+    // serialized; config 4 scaled 3.767 vs 3.757 s).
     const char* serial_env = std::getenv("HP_SERIAL_LEVELS");
-    const bool serial = serial_env && std::atoi(serial_env) != 0;
+    const bool k2_on_int8 = op.kind() != kOpDense && op.symmetric() &&
+                            k2i8::group_split(k2i8::padded_width(r)) && k2_mode() == 0 && k2_int8_enabled();
+    const bool serial = serial_env ? std::atoi(serial_env) != 0 : !k2_on_int8;
     std::unique_ptr<ApplyStage> next;
     if (tree->depth() >= 2) next = issue_apply(2);
     for (int l = 2; l <= tree->depth(); ++l) {

@@ -12,6 +12,8 @@
 // strides (== 4 mod 16 doubles) and cp.async double buffering.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.hpp"
 
 namespace hpeel {
@@ -27,15 +29,20 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 __host__ __device__ constexpr int stride4(int n) { return ((n + 11) / 16) * 16 + 4; }
 
-constexpr int kThreads = 128;
+constexpr int kThreads = 128;       // coefficient kernel
+constexpr int kApplyThreads = 256;  // apply: 4 row groups x 2 column halves
 constexpr int kRows = 64;  // apply tile rows (4 warps x 16)
 constexpr int kFS = kRows + 4;
 
 // ------------------------------------------------------------------ apply
 // out[rows, c0 + c] += alpha * sum_terms F[rows, :k] T[:k, c0 + c]
 // F tile staged column-major (ld kFS), T staged column-major (ld ts).
+// Eight warps: warp & 3 picks the 16-row group, warp >> 2 the half of the NT
+// column tiles (the staged tiles take ~150 KB at k = 64, w = 80, so one CTA
+// fits an SM; four warps alone left the DMMA pipe mostly idle, ncu: 6%
+// occupancy, 90% of cycles without an eligible warp).
 template <int NT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kApplyThreads)
 peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict__ refs,
                   const PeelTerm* __restrict__ terms, const double* __restrict__ factors,
                   const double* __restrict__ tbuf, int k, int w, double* __restrict__ out, int ocol0,
@@ -50,28 +57,31 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
   const int c0 = blockIdx.y * NT * 8;
   const int ncol = min(NT * 8, w - c0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < 2 * (fsz + tsz); e += kThreads) sm[e] = 0.0;
+  const int rg = warp & 3;                  // 16-row group
+  constexpr int NH = (NT + 1) / 2;          // column tiles per half
+  const int t0 = (warp >> 2) * NH;          // first column tile of this warp
+  for (int e = tid; e < 2 * (fsz + tsz); e += kApplyThreads) sm[e] = 0.0;
   __syncthreads();
 
   auto issue = [&](int buf, int q, std::int64_t roff) {
     const PeelTerm term = terms[q];
     const double* f0 = factors + term.f + roff;
-    for (int e = tid; e < kRows * k; e += kThreads) {
+    for (int e = tid; e < kRows * k; e += kApplyThreads) {
       const int i = e % kRows, l = e / kRows;
       if (i < task.rows) cp_async8(fs(buf) + l * kFS + i, f0 + i + std::int64_t(l) * term.fld);
     }
-    for (int e = tid; e < ncol * k; e += kThreads) {
-      const int l = e % k, c = e / k;
-      cp_async8(tsm(buf) + c * ts + l, tbuf + term.t + l + std::int64_t(c0 + c) * k);
-    }
+    // one warp per T column, lanes along k (coalesced, no runtime division)
+    for (int c = warp; c < ncol; c += kApplyThreads / 32)
+      for (int l = lane; l < k; l += 32)
+        cp_async8(tsm(buf) + c * ts + l, tbuf + term.t + l + std::int64_t(c0 + c) * k);
     cp_async_commit();
   };
 
-  double acc[2][NT][2];
+  double acc[2][NH][2];
 #pragma unroll
   for (int m = 0; m < 2; ++m)
 #pragma unroll
-    for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
+    for (int t = 0; t < NH; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 
   // cursor over (ref, term): the next term after (ri, q)
   auto next = [&](int& ri, int& q) {
@@ -91,12 +101,13 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
     cp_async_wait_all();
     __syncthreads();
     if (nri < task.ref_end) issue(buf ^ 1, nq, refs[nri].roff);
-    const double* a0p = fs(buf) + (lane & 3) * kFS + warp * 16 + (lane >> 2);
-    const double* bp = tsm(buf) + (lane >> 2) * ts + (lane & 3);
+    const double* a0p = fs(buf) + (lane & 3) * kFS + rg * 16 + (lane >> 2);
+    const double* bp = tsm(buf) + (t0 * 8 + (lane >> 2)) * ts + (lane & 3);
     for (int kk = 0; kk < kp; kk += 4) {
       const double a0 = a0p[kk * kFS], a1 = a0p[kk * kFS + 8];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+      for (int nt = 0; nt < NH; ++nt) {
+        if (t0 + nt >= NT) break;  // odd NT: the second half has one tile less
         const double b = bp[nt * 8 * ts + kk];
         dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a0, b);
         dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, b);
@@ -107,13 +118,13 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
   }
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
-    const int rr = warp * 16 + m * 8 + (lane >> 2);
+    const int rr = rg * 16 + m * 8 + (lane >> 2);
     if (rr >= task.rows) continue;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NH; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int c = nt * 8 + (lane & 3) * 2 + h;
+        const int c = (t0 + nt) * 8 + (lane & 3) * 2 + h;
         if (c < ncol) out[task.out + rr + std::int64_t(ocol0 + c0 + c) * task.ld] += alpha * acc[m][nt][h];
       }
   }
@@ -136,7 +147,7 @@ peel_coeff_dmma_kernel(const CoeffTask* __restrict__ tasks, const double* __rest
   const int mt = (k + 7) / 8;       // m-tiles (<= 8)
   auto fs = [&](int b) { return sm + b * mt * 8 * FS; };
   auto gs = [&](int b) { return sm + 2 * mt * 8 * FS + b * kCK * S; };
-  double* ms = sm + 2 * mt * 8 * FS + 2 * kCK * S;  // k x w col-major (after the loop)
+  double* ms = sm;  // k x w col-major, after the loop: aliases the drained stages
   double* bs = ms + k * w;
   const CoeffTask task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -148,14 +159,14 @@ peel_coeff_dmma_kernel(const CoeffTask* __restrict__ tasks, const double* __rest
     const int cnt = left < kCK ? int(left) : kCK;
     const std::int64_t frow = seg_start[sg] - task.f_row0 + r0;
     const std::int64_t gpos = seg_start[sg] + r0;
-    for (int e = tid; e < cnt * k; e += kThreads) {
-      const int t = e % cnt, m = e / cnt;
-      cp_async8(fs(buf) + m * FS + t, factors + task.f + frow + t + std::int64_t(m) * task.frows);
-    }
-    for (int e = tid; e < cnt * w; e += kThreads) {
-      const int t = e / w, c = e - t * w;
-      cp_async8(gs(buf) + t * S + c, g + (gpos + t) * gld + gcol0 + c);
-    }
+    // F: one warp per factor column, lanes along the (<= 32) payload rows;
+    // G: one warp per payload row, lanes along its columns (no runtime division)
+    static_assert(kCK == 32, "one lane per payload row");
+    if (lane < cnt)
+      for (int m = warp; m < k; m += kThreads / 32)
+        cp_async8(fs(buf) + m * FS + lane, factors + task.f + frow + lane + std::int64_t(m) * task.frows);
+    for (int t = warp; t < cnt; t += kThreads / 32)
+      for (int c = lane; c < w; c += 32) cp_async8(gs(buf) + t * S + c, g + (gpos + t) * gld + gcol0 + c);
     cp_async_commit();
     return cnt;
   };
@@ -274,7 +285,9 @@ void coeff_nt(const CoeffTask* tasks, int ntasks, const double* factors, const d
   constexpr int S = stride4(NT * 8);
   constexpr int FS = stride4(kCK);
   const int mt = (k + 7) / 8;
-  const size_t smem = size_t(2 * mt * 8 * FS + 2 * kCK * S + k * w + k * k) * sizeof(double);
+  // the epilogue's M and B reuse the pipeline stages (80 KB instead of 154 KB
+  // at k = 64, w = 80: two CTAs per SM)
+  const size_t smem = size_t(std::max(2 * mt * 8 * FS + 2 * kCK * S, k * w + k * k)) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(peel_coeff_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   peel_coeff_dmma_kernel<NT><<<ntasks, kThreads, smem, s>>>(tasks, factors, bmat, ss, sc, g, gld, gcol0, k, w, tbuf);
   HP_LAUNCHED();
@@ -288,7 +301,7 @@ void apply_nt(const PeelTask* tasks, int ntasks, const PeelRef* refs, const Peel
   const size_t smem = size_t(2 * (kp * kFS + NT * 8 * stride4(kp))) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(peel_apply_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const dim3 grid(unsigned(ntasks), unsigned((w + NT * 8 - 1) / (NT * 8)));
-  peel_apply_kernel<NT><<<grid, kThreads, smem, s>>>(tasks, refs, terms, factors, tbuf, k, w, out, ocol0, alpha);
+  peel_apply_kernel<NT><<<grid, kApplyThreads, smem, s>>>(tasks, refs, terms, factors, tbuf, k, w, out, ocol0, alpha);
   HP_LAUNCHED();
 }
 

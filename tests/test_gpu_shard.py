@@ -35,11 +35,14 @@ def test_level_overlap_bit_identical(hp, gpu_available, name, n, monkeypatch):
     """Level l+1's K1/K2 run on the apply stream while level l peels, factors
     and solves on the main stream (driver.cu ApplyStage); the overlapped run
     and the serialized one (HP_SERIAL_LEVELS=1) give identical factors and
-    dense blocks (no capture: capture synchronizes inside each level)."""
+    dense blocks (no capture: capture synchronizes inside each level).
+    HP_SERIAL_LEVELS=0 forces the overlap where the driver would not choose
+    it (FP64 DMMA K2, config 5)."""
     w = configs.scaled(name, n)
     pts = w.points()
     t = hp.build_tree(pts, w.leaf)
     op = hp.kernel_operator(w.kernel, pts, w.param)
+    monkeypatch.setenv("HP_SERIAL_LEVELS", "0")
     over = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
     monkeypatch.setenv("HP_SERIAL_LEVELS", "1")
     ser = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7)
