@@ -36,11 +36,13 @@ constexpr int kFS = kRows + 4;
 
 // ------------------------------------------------------------------ apply
 // out[rows, c0 + c] += alpha * sum_terms F[rows, :k] T[:k, c0 + c]
-// F tile staged column-major (ld kFS), T staged column-major (ld ts).
-// Eight warps: warp & 3 picks the 16-row group, warp >> 2 the half of the NT
-// column tiles (the staged tiles take ~150 KB at k = 64, w = 80, so one CTA
-// fits an SM; four warps alone left the DMMA pipe mostly idle, ncu: 6%
-// occupancy, 90% of cycles without an eligible warp).
+// Staged in units of (term, 32-wide slice of k): F slice column-major (ld
+// kFS), T slice column-major (ld stride4(32)), double-buffered -- 80 KB at
+// w = 80, so two CTAs (16 warps) share an SM. Eight warps: warp & 3 picks the
+// 16-row group, warp >> 2 the half of the NT column tiles. (Whole-k stages
+// took ~150 KB at k = 64, w = 80: one CTA of four warps per SM left the DMMA
+// pipe mostly idle, ncu: 6% occupancy, 90% of cycles without an eligible warp.)
+constexpr int kKC = 32;
 template <int NT>
 __global__ void __launch_bounds__(kApplyThreads)
 peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict__ refs,
@@ -48,9 +50,10 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
                   const double* __restrict__ tbuf, int k, int w, double* __restrict__ out, int ocol0,
                   double alpha) {
   extern __shared__ __align__(16) double sm[];
+  constexpr int ts = stride4(kKC);
+  constexpr int fsz = kKC * kFS, tsz = NT * 8 * ts;
   const int kp = (k + 3) & ~3;
-  const int ts = stride4(kp);
-  const int fsz = kp * kFS, tsz = NT * 8 * ts;
+  const int nkc = (kp + kKC - 1) / kKC;
   auto fs = [&](int b) { return sm + b * (fsz + tsz); };
   auto tsm = [&](int b) { return sm + b * (fsz + tsz) + fsz; };
   const PeelTask task = tasks[blockIdx.x];
@@ -63,17 +66,30 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
   for (int e = tid; e < 2 * (fsz + tsz); e += kApplyThreads) sm[e] = 0.0;
   __syncthreads();
 
-  auto issue = [&](int buf, int q, std::int64_t roff) {
+  // slice kc of term q: columns / rows [kc * 32, kc * 32 + 32) of F / T; the
+  // padding k .. kp (k % 4 != 0) is stored as zeros
+  auto issue = [&](int buf, int q, std::int64_t roff, int kc) {
     const PeelTerm term = terms[q];
+    const int l0 = kc * kKC;
+    const int lend = min(kp, l0 + kKC) - l0;
     const double* f0 = factors + term.f + roff;
-    for (int e = tid; e < kRows * k; e += kApplyThreads) {
+    for (int e = tid; e < kRows * lend; e += kApplyThreads) {
       const int i = e % kRows, l = e / kRows;
-      if (i < task.rows) cp_async8(fs(buf) + l * kFS + i, f0 + i + std::int64_t(l) * term.fld);
+      if (i < task.rows) {
+        if (l0 + l < k)
+          cp_async8(fs(buf) + l * kFS + i, f0 + i + std::int64_t(l0 + l) * term.fld);
+        else
+          fs(buf)[l * kFS + i] = 0.0;
+      }
     }
-    // one warp per T column, lanes along k (coalesced, no runtime division)
+    // one warp per T column, lanes along the slice (coalesced, no runtime division)
     for (int c = warp; c < ncol; c += kApplyThreads / 32)
-      for (int l = lane; l < k; l += 32)
-        cp_async8(tsm(buf) + c * ts + l, tbuf + term.t + l + std::int64_t(c0 + c) * k);
+      if (lane < lend) {
+        if (l0 + lane < k)
+          cp_async8(tsm(buf) + c * ts + lane, tbuf + term.t + l0 + lane + std::int64_t(c0 + c) * k);
+        else
+          tsm(buf)[c * ts + lane] = 0.0;
+      }
     cp_async_commit();
   };
 
@@ -83,27 +99,30 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
 #pragma unroll
     for (int t = 0; t < NH; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 
-  // cursor over (ref, term): the next term after (ri, q)
-  auto next = [&](int& ri, int& q) {
+  // cursor over (ref, term, slice): the unit after (ri, q, kc)
+  auto next = [&](int& ri, int& q, int& kc) {
+    if (++kc < nkc) return;
+    kc = 0;
     ++q;
     while (ri < task.ref_end && q >= refs[ri].term_end) {
       ++ri;
       if (ri < task.ref_end) q = refs[ri].term_begin;
     }
   };
-  int ri = task.ref_begin, q = ri < task.ref_end ? refs[ri].term_begin - 1 : 0;
-  next(ri, q);
-  if (ri < task.ref_end) issue(0, q, refs[ri].roff);
+  int ri = task.ref_begin, q = ri < task.ref_end ? refs[ri].term_begin - 1 : 0, kc = nkc - 1;
+  next(ri, q, kc);
+  if (ri < task.ref_end) issue(0, q, refs[ri].roff, kc);
   int buf = 0;
   for (; ri < task.ref_end; buf ^= 1) {
-    int nri = ri, nq = q;
-    next(nri, nq);
+    int nri = ri, nq = q, nkc_ = kc;
+    next(nri, nq, nkc_);
     cp_async_wait_all();
     __syncthreads();
-    if (nri < task.ref_end) issue(buf ^ 1, nq, refs[nri].roff);
+    if (nri < task.ref_end) issue(buf ^ 1, nq, refs[nri].roff, nkc_);
+    const int kn = min(kKC, kp - kc * kKC);
     const double* a0p = fs(buf) + (lane & 3) * kFS + rg * 16 + (lane >> 2);
     const double* bp = tsm(buf) + (t0 * 8 + (lane >> 2)) * ts + (lane & 3);
-    for (int kk = 0; kk < kp; kk += 4) {
+    for (int kk = 0; kk < kn; kk += 4) {
       const double a0 = a0p[kk * kFS], a1 = a0p[kk * kFS + 8];
 #pragma unroll
       for (int nt = 0; nt < NH; ++nt) {
@@ -115,6 +134,7 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
     }
     ri = nri;
     q = nq;
+    kc = nkc_;
   }
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
@@ -297,8 +317,7 @@ template <int NT>
 void apply_nt(const PeelTask* tasks, int ntasks, const PeelRef* refs, const PeelTerm* terms,
               const double* factors, const double* tbuf, int k, int w, double* out, int ocol0, double alpha,
               cudaStream_t s) {
-  const int kp = (k + 3) & ~3;
-  const size_t smem = size_t(2 * (kp * kFS + NT * 8 * stride4(kp))) * sizeof(double);
+  const size_t smem = size_t(2 * (kKC * kFS + NT * 8 * stride4(kKC))) * sizeof(double);
   HP_CUDA(cudaFuncSetAttribute(peel_apply_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const dim3 grid(unsigned(ntasks), unsigned((w + NT * 8 - 1) / (NT * 8)));
   peel_apply_kernel<NT><<<grid, kApplyThreads, smem, s>>>(tasks, refs, terms, factors, tbuf, k, w, out, ocol0, alpha);
