@@ -167,8 +167,10 @@ peel_coeff_dmma_kernel(const CoeffTask* __restrict__ tasks, const double* __rest
   const int mt = (k + 7) / 8;       // m-tiles (<= 8)
   auto fs = [&](int b) { return sm + b * mt * 8 * FS; };
   auto gs = [&](int b) { return sm + 2 * mt * 8 * FS + b * kCK * S; };
-  double* ms = sm;  // k x w col-major, after the loop: aliases the drained stages
-  double* bs = ms + k * w;
+  // after the loop, aliasing the drained stages: M (k x w, ld MS) and B (k x k, ld MS)
+  const int MS = stride4(k);
+  double* ms = sm;
+  double* bs = ms + MS * w;
   const CoeffTask task = tasks[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int e = tid; e < 2 * (mt * 8 * FS + kCK * S); e += kThreads) sm[e] = 0.0;
@@ -248,20 +250,41 @@ peel_coeff_dmma_kernel(const CoeffTask* __restrict__ tasks, const double* __rest
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = nt * 8 + (lane & 3) * 2 + h;
-        if (m < k && c < w) ms[m + c * k] = acc[mm][nt][h];
+        if (m < k && c < w) ms[m + c * MS] = acc[mm][nt][h];
       }
   }
-  for (int e = tid; e < k * k; e += kThreads) bs[e] = bmat[task.b + e];
+  for (int l = warp; l < k; l += kThreads / 32)
+    for (int i = lane; i < k; i += 32) bs[i + l * MS] = bmat[task.b + i + l * k];
   __syncthreads();
-  for (int e = tid; e < k * w; e += kThreads) {
-    const int i = e % k, c = e / k;
-    double t = 0.0;
-    if (task.btrans) {
-      for (int l = 0; l < k; ++l) t = fma(bs[l + i * k], ms[l + c * k], t);
-    } else {
-      for (int l = 0; l < k; ++l) t = fma(bs[i + l * k], ms[l + c * k], t);
+  if ((k & 3) == 0) {
+    // T = op(B) M on DMMA: 8 x 8 output tiles over the warps; rows >= k and
+    // columns >= w of a tile read stale shared memory and are not stored
+    for (int tt = warp; tt < mt * NT; tt += kThreads / 32) {
+      const int mtile = tt / NT, nt = tt - mtile * NT;
+      const int am = mtile * 8 + (lane >> 2), bn = nt * 8 + (lane >> 2);
+      double c0 = 0.0, c1 = 0.0;
+      for (int kk = 0; kk < k; kk += 4) {
+        const int l = kk + (lane & 3);
+        const double a = task.btrans ? bs[l + am * MS] : bs[am + l * MS];
+        dmma8x8x4(c0, c1, a, ms[l + bn * MS]);
+      }
+      const int m = mtile * 8 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
+      if (m < k) {
+        if (c < w) tbuf[task.t_out + m + std::int64_t(c) * k] = c0;
+        if (c + 1 < w) tbuf[task.t_out + m + std::int64_t(c + 1) * k] = c1;
+      }
     }
-    tbuf[task.t_out + e] = t;
+  } else {
+    for (int e = tid; e < k * w; e += kThreads) {
+      const int i = e % k, c = e / k;
+      double t = 0.0;
+      if (task.btrans) {
+        for (int l = 0; l < k; ++l) t = fma(bs[l + i * MS], ms[l + c * MS], t);
+      } else {
+        for (int l = 0; l < k; ++l) t = fma(bs[i + l * MS], ms[l + c * MS], t);
+      }
+      tbuf[task.t_out + e] = t;
+    }
   }
 }
 
@@ -307,7 +330,7 @@ void coeff_nt(const CoeffTask* tasks, int ntasks, const double* factors, const d
   const int mt = (k + 7) / 8;
   // the epilogue's M and B reuse the pipeline stages (80 KB instead of 154 KB
   // at k = 64, w = 80: two CTAs per SM)
-  const size_t smem = size_t(std::max(2 * mt * 8 * FS + 2 * kCK * S, k * w + k * k)) * sizeof(double);
+  const size_t smem = size_t(std::max(2 * mt * 8 * FS + 2 * kCK * S, stride4(k) * (w + k + 8))) * sizeof(double);  // + 8: rows >= k of a DMMA tile
   HP_CUDA(cudaFuncSetAttribute(peel_coeff_dmma_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   peel_coeff_dmma_kernel<NT><<<ntasks, kThreads, smem, s>>>(tasks, factors, bmat, ss, sc, g, gld, gcol0, k, w, tbuf);
   HP_LAUNCHED();
