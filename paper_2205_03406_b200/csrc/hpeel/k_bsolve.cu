@@ -20,55 +20,73 @@ namespace {
 constexpr int kGramThreads = 256;
 constexpr int kGramRows = 32;
 
-template <int E>
+// Row stride of a staged operand: >= the 8-padded width and == 8 mod 16
+// doubles, so a DMMA fragment read (4 rows x 8 columns) hits each bank pair
+// at most twice.
+__host__ __device__ constexpr int gram_stride(int n) { return ((n + 7) / 16) * 16 + 8; }
+
+// out (nx x ny, col-major) = X^T Y over t.rows rows, on FP64 DMMA (m8n8k4):
+// 32-row chunks of X and Y staged row-major in shared memory (rows past the
+// end zeroed), 8 x 8 output tiles spread over the warps, TPW tiles per warp.
+// (Was one scalar FMA chain per output element with two shared loads per
+// FMA.)
+template <int TPW>
 __global__ void __launch_bounds__(kGramThreads)
 gram_kernel(const GramTask* __restrict__ tasks, const double* __restrict__ xb,
             const double* __restrict__ yb, int nx, int ny, double* __restrict__ out) {
   extern __shared__ double sm[];
-  double* xs = sm;                    // kGramRows x nx (row-major)
-  double* ys = sm + kGramRows * nx;   // kGramRows x ny (row-major)
+  const int XS = gram_stride(nx), YS = gram_stride(ny);
+  double* xs = sm;                    // kGramRows x XS (row-major)
+  double* ys = sm + kGramRows * XS;   // kGramRows x YS (row-major)
   const GramTask t = tasks[blockIdx.x];
-  const int tid = threadIdx.x;
-  double acc[E];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kGramThreads / 32;
+  const int ntl = (ny + 7) / 8, ntiles = ((nx + 7) / 8) * ntl;
+  int ao[TPW], bo[TPW];
+  double acc[TPW][2];
 #pragma unroll
-  for (int u = 0; u < E; ++u) acc[u] = 0.0;
+  for (int u = 0; u < TPW; ++u) {
+    const int tile = warp + u * kWarps;
+    const int mi = tile / ntl, ni = tile - mi * ntl;
+    ao[u] = mi * 8 + (lane >> 2);
+    bo[u] = ni * 8 + (lane >> 2);
+    acc[u][0] = acc[u][1] = 0.0;
+  }
+  auto stage = [&](double* dst, int ld, int n, const double* src, std::int64_t off, std::int64_t lsrc,
+                   bool rowmajor, int r0, int cnt) {
+    static_assert(kGramRows == 32, "one lane per chunk row");
+    if (rowmajor) {
+      for (int i = warp; i < kGramRows; i += kWarps)
+        for (int a = lane; a < n; a += 32)
+          dst[i * ld + a] = i < cnt ? src[off + std::int64_t(r0 + i) * lsrc + a] : 0.0;
+    } else {
+      for (int a = warp; a < n; a += kWarps)
+        dst[lane * ld + a] = lane < cnt ? src[off + r0 + lane + std::int64_t(a) * lsrc] : 0.0;
+    }
+  };
   for (int r0 = 0; r0 < t.rows; r0 += kGramRows) {
     const int cnt = t.rows - r0 < kGramRows ? t.rows - r0 : kGramRows;
     __syncthreads();
-    for (int e = tid; e < kGramRows * nx; e += kGramThreads) {
-      const int i = e / nx, a = e - i * nx;
-      double v = 0.0;
-      if (i < cnt) {
-        const std::int64_t row = r0 + i;
-        v = t.x_rowmajor ? xb[t.x + row * t.lx + a] : xb[t.x + row + std::int64_t(a) * t.lx];
-      }
-      xs[e] = v;
-    }
-    for (int e = tid; e < kGramRows * ny; e += kGramThreads) {
-      const int i = e / ny, b = e - i * ny;
-      double v = 0.0;
-      if (i < cnt) {
-        const std::int64_t row = r0 + i;
-        v = t.y_rowmajor ? yb[t.y + row * t.ly + b] : yb[t.y + row + std::int64_t(b) * t.ly];
-      }
-      ys[e] = v;
-    }
+    stage(xs, XS, nx, xb, t.x, t.lx, t.x_rowmajor, r0, cnt);
+    stage(ys, YS, ny, yb, t.y, t.ly, t.y_rowmajor, r0, cnt);
     __syncthreads();
+    const int kend = (cnt + 3) & ~3;
 #pragma unroll
-    for (int u = 0; u < E; ++u) {
-      const int e = tid + u * kGramThreads;
-      if (e < nx * ny) {
-        const int a = e % nx, b = e / nx;
-        double s = acc[u];
-        for (int i = 0; i < cnt; ++i) s = fma(xs[i * nx + a], ys[i * ny + b], s);
-        acc[u] = s;
-      }
+    for (int u = 0; u < TPW; ++u) {
+      if (warp + u * kWarps >= ntiles) break;
+      const double* ap = xs + (lane & 3) * XS + ao[u];
+      const double* bp = ys + (lane & 3) * YS + bo[u];
+      for (int kk = 0; kk < kend; kk += 4) dmma8x8x4(acc[u][0], acc[u][1], ap[kk * XS], bp[kk * YS]);
     }
   }
 #pragma unroll
-  for (int u = 0; u < E; ++u) {
-    const int e = tid + u * kGramThreads;
-    if (e < nx * ny) out[t.out + e] = acc[u];
+  for (int u = 0; u < TPW; ++u) {
+    if (warp + u * kWarps >= ntiles) break;
+    const int m = ao[u], n = bo[u] - (lane >> 2) + (lane & 3) * 2;
+    if (m < nx) {
+      if (n < ny) out[t.out + m + std::int64_t(n) * nx] = acc[u][0];
+      if (n + 1 < ny) out[t.out + m + std::int64_t(n + 1) * nx] = acc[u][1];
+    }
   }
 }
 
@@ -386,8 +404,8 @@ bsolve_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle
 void launch_gram(const GramTask* tasks, int ntasks, const double* xbase, const double* ybase,
                  int nx, int ny, double* out, cudaStream_t s) {
   if (ntasks == 0) return;
-  const int e = (nx * ny + kGramThreads - 1) / kGramThreads;
-  const size_t smem = size_t(kGramRows) * size_t(nx + ny) * sizeof(double);
+  const int e = (((nx + 7) / 8) * ((ny + 7) / 8) + kGramThreads / 32 - 1) / (kGramThreads / 32);  // tiles per warp
+  const size_t smem = size_t(kGramRows) * size_t(gram_stride(nx) + gram_stride(ny)) * sizeof(double);
 #define HP_G(EE)                                                                            \
   if (e <= EE) {                                                                            \
     HP_CUDA(cudaFuncSetAttribute(gram_kernel<EE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -396,9 +414,9 @@ void launch_gram(const GramTask* tasks, int ntasks, const double* xbase, const d
     HP_LAUNCHED();                                                            \
     return;                                                                                 \
   }
-  HP_G(2) HP_G(4) HP_G(8) HP_G(12) HP_G(16) HP_G(20) HP_G(25) HP_G(32)
+  HP_G(1) HP_G(2) HP_G(4) HP_G(8) HP_G(13) HP_G(18) HP_G(25) HP_G(32)
 #undef HP_G
-  throw std::invalid_argument("gram block too large (nx * ny > 8192)");
+  throw std::invalid_argument("gram block too large (more than 256 output tiles)");
 }
 
 void launch_sum_partials(const std::int64_t* off, int ndst, const double* src, int len,
