@@ -150,6 +150,45 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
   }
 }
 
+// T (k x w, col-major, ld k) = op(B) M from shared B (k x k) and M (k x w),
+// both with leading dimension ms_ld. With k % 4 == 0 on DMMA: 8 x 8 output
+// tiles over the warps (rows >= k / columns >= w of a tile read stale shared
+// memory -- callers allocate 8 spare rows -- and are not stored); otherwise
+// one scalar FMA chain per output.
+__device__ __forceinline__ void coeff_epilogue(const double* bs, const double* ms, int ms_ld, int k, int w,
+                                               bool btrans, double* __restrict__ t_out, int nthreads) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if ((k & 3) == 0) {
+    const int mt = (k + 7) / 8, ntl = (w + 7) / 8;
+    for (int tt = warp; tt < mt * ntl; tt += nthreads / 32) {
+      const int mtile = tt / ntl, nt = tt - mtile * ntl;
+      const int am = mtile * 8 + (lane >> 2), bn = nt * 8 + (lane >> 2);
+      double c0 = 0.0, c1 = 0.0;
+      for (int kk = 0; kk < k; kk += 4) {
+        const int l = kk + (lane & 3);
+        const double a = btrans ? bs[l + am * ms_ld] : bs[am + l * ms_ld];
+        dmma8x8x4(c0, c1, a, ms[l + bn * ms_ld]);
+      }
+      const int c = nt * 8 + (lane & 3) * 2;
+      if (am < k) {
+        if (c < w) t_out[am + std::int64_t(c) * k] = c0;
+        if (c + 1 < w) t_out[am + std::int64_t(c + 1) * k] = c1;
+      }
+    }
+  } else {
+    for (int e = tid; e < k * w; e += nthreads) {
+      const int i = e % k, c = e / k;
+      double t = 0.0;
+      if (btrans) {
+        for (int l = 0; l < k; ++l) t = fma(bs[l + i * ms_ld], ms[l + c * ms_ld], t);
+      } else {
+        for (int l = 0; l < k; ++l) t = fma(bs[i + l * ms_ld], ms[l + c * ms_ld], t);
+      }
+      t_out[e] = t;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ coeff
 // Gaussian payloads: M (k x w) = sum_v F[v rows]^T G[v rows, gcol0 : gcol0 + w]
 // on DMMA (A = F^T staged [m][t], B = G staged [t][c]), then T = op(B) M.
@@ -256,36 +295,7 @@ peel_coeff_dmma_kernel(const CoeffTask* __restrict__ tasks, const double* __rest
   for (int l = warp; l < k; l += kThreads / 32)
     for (int i = lane; i < k; i += 32) bs[i + l * MS] = bmat[task.b + i + l * k];
   __syncthreads();
-  if ((k & 3) == 0) {
-    // T = op(B) M on DMMA: 8 x 8 output tiles over the warps; rows >= k and
-    // columns >= w of a tile read stale shared memory and are not stored
-    for (int tt = warp; tt < mt * NT; tt += kThreads / 32) {
-      const int mtile = tt / NT, nt = tt - mtile * NT;
-      const int am = mtile * 8 + (lane >> 2), bn = nt * 8 + (lane >> 2);
-      double c0 = 0.0, c1 = 0.0;
-      for (int kk = 0; kk < k; kk += 4) {
-        const int l = kk + (lane & 3);
-        const double a = task.btrans ? bs[l + am * MS] : bs[am + l * MS];
-        dmma8x8x4(c0, c1, a, ms[l + bn * MS]);
-      }
-      const int m = mtile * 8 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
-      if (m < k) {
-        if (c < w) tbuf[task.t_out + m + std::int64_t(c) * k] = c0;
-        if (c + 1 < w) tbuf[task.t_out + m + std::int64_t(c + 1) * k] = c1;
-      }
-    }
-  } else {
-    for (int e = tid; e < k * w; e += kThreads) {
-      const int i = e % k, c = e / k;
-      double t = 0.0;
-      if (task.btrans) {
-        for (int l = 0; l < k; ++l) t = fma(bs[l + i * MS], ms[l + c * MS], t);
-      } else {
-        for (int l = 0; l < k; ++l) t = fma(bs[i + l * MS], ms[l + c * MS], t);
-      }
-      tbuf[task.t_out + e] = t;
-    }
-  }
+  coeff_epilogue(bs, ms, MS, k, w, task.btrans, tbuf + task.t_out, kThreads);
 }
 
 // Identity payloads [I | 0] (leaf phase): M[:, t] = sum_v F[row v_t, :]^T for
@@ -296,29 +306,25 @@ peel_coeff_identity_kernel(const CoeffTask* __restrict__ tasks, const double* __
                            const std::int64_t* __restrict__ seg_count, int k, int w,
                            double* __restrict__ tbuf) {
   extern __shared__ __align__(16) double sm[];
+  const int MS = stride4(k);
   double* ms = sm;
-  double* bs = sm + k * w;
+  double* bs = sm + MS * w;
   const CoeffTask task = tasks[blockIdx.x];
   const double* f = factors + task.f;
-  for (int e = threadIdx.x; e < k * w; e += blockDim.x) {
-    const int i = e % k, c = e / k;
-    double acc = 0.0;
-    for (int sg = task.seg_begin; sg < task.seg_end; ++sg)
-      if (c < seg_count[sg]) acc += f[seg_start[sg] - task.f_row0 + c + std::int64_t(i) * task.frows];
-    ms[e] = acc;
-  }
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) bs[e] = bmat[task.b + e];
-  __syncthreads();
-  for (int e = threadIdx.x; e < k * w; e += blockDim.x) {
-    const int i = e % k, c = e / k;
-    double t = 0.0;
-    if (task.btrans) {
-      for (int l = 0; l < k; ++l) t = fma(bs[l + i * k], ms[l + c * k], t);
-    } else {
-      for (int l = 0; l < k; ++l) t = fma(bs[i + l * k], ms[l + c * k], t);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // M[i, c] = sum over segments of F[row c of the segment, i]: one warp per
+  // factor column i, lanes along c (coalesced rows of the column-major F)
+  for (int i = warp; i < k; i += nw)
+    for (int c = lane; c < w; c += 32) {
+      double acc = 0.0;
+      for (int sg = task.seg_begin; sg < task.seg_end; ++sg)
+        if (c < seg_count[sg]) acc += f[seg_start[sg] - task.f_row0 + c + std::int64_t(i) * task.frows];
+      ms[i + c * MS] = acc;
     }
-    tbuf[task.t_out + e] = t;
-  }
+  for (int l = warp; l < k; l += nw)
+    for (int i = lane; i < k; i += 32) bs[i + l * MS] = bmat[task.b + i + l * k];
+  __syncthreads();
+  coeff_epilogue(bs, ms, MS, k, w, task.btrans, tbuf + task.t_out, blockDim.x);
 }
 
 template <int NT>
@@ -356,7 +362,7 @@ void launch_peel_coeff(const CoeffTask* tasks, int ntasks, const double* factors
   if (ntasks == 0) return;
   if (k > 64) throw std::invalid_argument("peel: rank k > 64 is not supported");
   if (gcol0 < 0) {
-    const size_t smem = size_t(k * w + k * k) * sizeof(double);
+    const size_t smem = size_t(stride4(k) * (w + k + 8)) * sizeof(double);  // + 8: rows >= k of a DMMA tile
     HP_CUDA(cudaFuncSetAttribute(peel_coeff_identity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     peel_coeff_identity_kernel<<<ntasks, 256, smem, s>>>(tasks, factors, bmat, seg_start, seg_count, k, w, tbuf);
     HP_LAUNCHED();
