@@ -29,41 +29,62 @@ namespace {
 constexpr int kBsThreads = 256;
 constexpr double kCholFlag = 1e-2;  // min L_jj / max L_jj before falling back
 
+constexpr int kAtbTiles = 16;  // 8 x 8 output tiles per warp held in registers
+
+// C(c, d) = sum_{i < r} P(i, c) Q(i, d), c < m, d < nn, on FP64 DMMA (m8n8k4):
+// 8 x 8 tiles over the warps, accumulated in registers, then handed to
+// store(c, d, v) after a barrier (so C may overwrite P or Q). P(i, c) =
+// P[i * ps_i + c * ps_c], Q likewise. Needs ceil(m/8) ceil(nn/8) <= 8 *
+// kAtbTiles (launch_bsolve_reg checks). (Was one scalar FMA chain per output
+// with two shared loads per FMA: bound by shared-memory bandwidth.)
+template <class Store>
+__device__ __forceinline__ void atb_dmma(const double* P, int ps_i, int ps_c, const double* Q, int qs_i, int qs_d,
+                                         int r, int m, int nn, Store store) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kBsThreads / 32;
+  const int ntl = (nn + 7) / 8, ntiles = ((m + 7) / 8) * ntl;
+  double acc[kAtbTiles][2];
+#pragma unroll
+  for (int u = 0; u < kAtbTiles; ++u) {
+    acc[u][0] = acc[u][1] = 0.0;
+    const int tile = warp + u * kWarps;
+    if (tile < ntiles) {
+      const int mi = tile / ntl, ni = tile - mi * ntl;
+      const int c = mi * 8 + (lane >> 2), d = ni * 8 + (lane >> 2);
+      const double* pc = P + c * ps_c;
+      const double* qd = Q + d * qs_d;
+      for (int kk = 0; kk < r; kk += 4) {
+        const int i = kk + (lane & 3);
+        const double av = (i < r && c < m) ? pc[i * ps_i] : 0.0;
+        const double bv = (i < r && d < nn) ? qd[i * qs_i] : 0.0;
+        dmma8x8x4(acc[u][0], acc[u][1], av, bv);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kAtbTiles; ++u) {
+    const int tile = warp + u * kWarps;
+    if (tile < ntiles) {
+      const int mi = tile / ntl, ni = tile - mi * ntl;
+      const int c = mi * 8 + (lane >> 2), d = ni * 8 + (lane & 3) * 2;
+      if (c < m) {
+        if (d < nn) store(c, d, acc[u][0]);
+        if (d + 1 < nn) store(c, d + 1, acc[u][1]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // N = A^T A (lower, k x k, ld ldn) and Y = A^T X (k x nr), Y written over X
 // with ld k + 1 once every thread has read X. A: r x k (ld lda), X: r x nr.
 __device__ void gram_pair(const double* a, double* x, double* n, int r, int k, int nr, int lda, int ldx,
                           int ldn) {
-  constexpr int kMaxY = 24;  // Y outputs per thread (k * nr <= 256 * 24)
-  double acc[kMaxY];
-#pragma unroll
-  for (int u = 0; u < kMaxY; ++u) {
-    const int e = threadIdx.x + u * kBsThreads;
-    acc[u] = 0.0;
-    if (e < k * nr) {
-      const int i = e % k, c = e / k;
-      const double* ai = a + i * lda;
-      const double* xc = x + c * ldx;
-      double s = 0.0;
-      for (int l = 0; l < r; ++l) s = fma(ai[l], xc[l], s);
-      acc[u] = s;
-    }
-  }
-  for (int e = threadIdx.x; e < k * k; e += kBsThreads) {
-    const int i = e % k, j = e / k;
-    if (i < j) continue;
-    const double* ai = a + i * lda;
-    const double* aj = a + j * lda;
-    double s = 0.0;
-    for (int l = 0; l < r; ++l) s = fma(ai[l], aj[l], s);
-    n[i + j * ldn] = s;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kMaxY; ++u) {
-    const int e = threadIdx.x + u * kBsThreads;
-    if (e < k * nr) x[e % k + (e / k) * (k + 1)] = acc[u];
-  }
-  __syncthreads();
+  atb_dmma(a, 1, lda, x, 1, ldx, r, k, nr, [&](int c, int d, double v) { x[c + d * (k + 1)] = v; });
+  atb_dmma(a, 1, lda, a, 1, lda, r, k, k, [&](int c, int d, double v) {
+    if (c >= d) n[c + d * ldn] = v;
+  });
 }
 
 // In-place lower Cholesky of n (k x k, ld ldn). Exactly zero diagonals mark
@@ -165,39 +186,12 @@ bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ m
     a[i + c * lda] = vg[p * k * r + c + std::int64_t(i) * k];
   }
   __syncthreads();
-  {
-    // Y2 = M2^T left^T (k x k): Y2(c, d) = sum_i M2(i, c) left(d, i)
-    constexpr int kMaxY = 16;
-    double acc[kMaxY];
-#pragma unroll
-    for (int u = 0; u < kMaxY; ++u) {
-      const int e = t + u * kBsThreads;
-      acc[u] = 0.0;
-      if (e < k * k) {
-        const int c = e % k, d = e / k;
-        const double* ac = a + c * lda;
-        double s = 0.0;
-        for (int i = 0; i < r; ++i) s = fma(ac[i], x[d + i * (k + 1)], s);
-        acc[u] = s;
-      }
-    }
-    for (int e = t; e < k * k; e += kBsThreads) {
-      const int i = e % k, j = e / k;
-      if (i < j) continue;
-      const double* ai = a + i * lda;
-      const double* aj = a + j * lda;
-      double s = 0.0;
-      for (int l = 0; l < r; ++l) s = fma(ai[l], aj[l], s);
-      n[i + j * ldn] = s;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < kMaxY; ++u) {
-      const int e = t + u * kBsThreads;
-      if (e < k * k) x[e % k + (e / k) * (k + 1)] = acc[u];
-    }
-    __syncthreads();
-  }
+  // Y2 = M2^T left^T (k x k): Y2(c, d) = sum_i M2(i, c) left(d, i), over x;
+  // N2 = M2^T M2 (lower)
+  atb_dmma(a, 1, lda, x, k + 1, 1, r, k, k, [&](int c, int d, double v) { x[c + d * (k + 1)] = v; });
+  atb_dmma(a, 1, lda, a, 1, lda, r, k, k, [&](int c, int d, double v) {
+    if (c >= d) n[c + d * ldn] = v;
+  });
   const bool ok2 = cholesky(n, k, ldn, null_col);
   chol_solve(n, k, ldn, null_col, x, k, k + 1);  // out2 (k x k, ld k + 1)
   const bool ok = ok1 && ok2;
@@ -214,6 +208,7 @@ bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ m
 bool launch_bsolve_reg(int npairs, const double* gpu_, const double* middle, const double* vg, int r, int k,
                        const std::int64_t* boff, double* b, int* flags, cudaStream_t s) {
   if (k > 64 || k > r || k * r > kBsThreads * 24 || k * k > kBsThreads * 16) return false;
+  if (((k + 7) / 8) * ((r + 7) / 8) > (kBsThreads / 32) * kAtbTiles) return false;
   const int mx = r > k ? r : k;
   const size_t smem = size_t((r + 1) * k + (r + 1) * mx + (k + 1) * k) * sizeof(double);
   if (smem > 220 * 1024) return false;
