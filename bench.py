@@ -286,8 +286,9 @@ def run_ours(args, ws, rank, local):
     op = make_operator(hp, w, pts, local)
     kw = dict(rank=w.rank, oversample=w.oversample, seed=7)
     if ws > 1:
-        # one process per GPU: the black-box apply and leaf probes are split
-        # over the ranks and their rows broadcast with NCCL
+        # one process per GPU, owner-computes: each rank samples,
+        # peels and factors the pairs of its boxes; crossing pairs' factors
+        # move point-to-point over NCCL
         import torch.distributed as dist
         uid = [hp.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -341,7 +342,7 @@ def run_ours(args, ws, rank, local):
     if not args.no_e2e:
         # the caller's result arrays: page-locked host memory, allocated once
         # outside the timed region (as the contract's pinned input buffers)
-        nf, nd = hp.export_sizes(tree, w.rank)
+        nf, nd = hp.export_sizes(tree, w.rank, ws, rank)
         hf = hp.pinned_empty(nf)
         hd = hp.pinned_empty(max(nd, 1))
         host_pts_src = hp.pinned_empty(pts.size).reshape(pts.shape)
@@ -388,7 +389,7 @@ def run_ours(args, ws, rank, local):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "n": w.n, "description": w.description, "rank": w.rank,
-                   "oversample": w.oversample, "leaf": w.leaf, "parallelism": f"sharded-apply x{ws}" if ws > 1 else "single",
+                   "oversample": w.oversample, "leaf": w.leaf, "parallelism": f"owner-computes x{ws}" if ws > 1 else "single",
                    "l2": "flushed (512 MiB write) before every timed step"},
         "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -55,12 +55,6 @@ const char* hp_last_error(void);
 int hp_device_count(int* count);
 /* kernels launched by this library so far (bench.py gpu_launches) */
 int64_t hp_launch_count(void);
-/* profiling only: 1 = K2 skips kernel evaluation, 2 = K2 skips DMMA, 0 = normal */
-void hp_debug_set_k2_mode(int mode);
-/* K2 arithmetic path: 0 = int8 tensor-core digit products (exact fixed-point
- * emulation of the FP64 contraction, k2_i8.cuh) wherever eligible (default),
- * 1 = FP64 DMMA for every apply (A/B tests) */
-void hp_debug_set_k2_path(int path);
 int hp_device_synchronize(void);
 
 /* ---- RNG: proj/include/hpeel/rng.hpp:37-50, proj/src/rng.cpp:31-59 ---- */
@@ -123,6 +117,18 @@ int hp_op_dense(const double* a, int64_t n, int device, hp_op** out);
 /* points: raw coordinates, n x dim column-major, input order */
 int hp_op_kernel(int kind, const double* points, int64_t n, int dim, double param, int device,
                  hp_op** out);
+/* Caller-supplied black box: the reference's virtual LinearOperator::apply /
+ * apply_adjoint (proj/include/hpeel/linear_operator.hpp:19-20), called once
+ * per color and side as residual_samples does (proj/src/peeling.cpp:165-177)
+ * and once per color of the leaf probes (:490-524). fn computes
+ * y = A x (adjoint = 0) or A^T x (adjoint = 1) for an n x w column-major x in
+ * the caller's point order and returns 0 (nonzero = failure: compress fails
+ * with HP_ERR_RUNTIME). device_pointers = 0: x and y are host arrays and
+ * stream is NULL; 1: they are device pointers on `device` and the work must be
+ * ordered on `stream` (a cudaStream_t). ctx is passed through. */
+typedef int (*hp_apply_fn)(void* ctx, int adjoint, const double* x, int64_t w, double* y, void* stream);
+int hp_op_callback(int64_t n, int symmetric, int device_pointers, hp_apply_fn fn, void* ctx, int device,
+                   hp_op** out);
 void hp_op_free(hp_op* op);
 int hp_op_apply(const hp_op* op, int adjoint, const double* x, int64_t w, double* y);
 
@@ -134,22 +140,45 @@ int hp_compress(const hp_op* op, const hp_tree* tree, int rank, int oversample, 
                 int format, int strategy, int capture, hp_rep** out);
 void hp_rep_free(hp_rep* rep);
 
-/* ---- multi-GPU (one process per GPU): NCCL communicator.
- *      Rank 0 calls hp_comm_unique_id and distributes the 128 bytes. ---- */
+/* ---- multi-GPU (one process per GPU, owner-computes): NCCL
+ *      communicator. Rank 0 calls hp_comm_unique_id and distributes the 128
+ *      bytes. Each rank's representation holds the factors of the pairs that
+ *      touch its boxes and the dense blocks of its leaves. ---- */
 typedef struct hp_comm hp_comm;
 int hp_comm_unique_id(unsigned char* id128);
 int hp_comm_create(const unsigned char* id128, int rank, int world, int device, hp_comm** out);
 void hp_comm_free(hp_comm* comm);
-/* compress with the black-box apply and leaf probes sharded over `comm`
- * (NULL: single GPU); emulate_shards > 1 splits the launches as that many
- * ranks would, in this process (tests) */
+/* compress on this rank of `comm` (NULL: single GPU) */
 int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
-                   int format, int strategy, int capture, hp_comm* comm, int emulate_shards,
-                   hp_rep** out);
+                   int format, int strategy, int capture, hp_comm* comm, hp_rep** out);
+/* compress on `world` ranks emulated by threads of this process on the
+ * operator's device (the same sharded path, device copies instead of NCCL);
+ * outs[g] = rank g's representation */
+int hp_compress_group(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
+                      int format, int strategy, int capture, int world, hp_rep** outs);
+/* box ownership for `world` ranks: owner per box (-1 above the cut), the cut
+ * level (levels below it are replicated) and the world + 1 tree-position
+ * bounds of the ranks' point ranges; any output may be NULL */
+int hp_shard_owners(const hp_tree* tree, int world, int* owner, int* cut, int64_t* point_bounds);
+/* per-rank device memory plan in bytes: out[g * 4 + 0..3] = factors held,
+ * dense blocks, largest level's samples + apply buffers, total estimate */
+int hp_shard_memory_plan(const hp_tree* tree, int rank, int oversample, int world, double* out);
+/* doubles shard `shard` sends to / receives from each of the `world` ranks
+ * (send[world], recv[world]) in level `level`'s crossing-pair exchange
+ * `phase` (1: V to the row owner, 2: U and B to the column owner) */
+int hp_shard_exchange_counts(const hp_tree* tree, int rank, int world, int shard, int level, int phase,
+                             int64_t* send, int64_t* recv);
+/* hp_export_sizes for shard `shard` of `world` */
+int hp_export_sizes_shard(const hp_tree* tree, int rank, int world, int shard, int64_t* factor_doubles,
+                          int64_t* dense_doubles);
+/* world and rank of a representation; *held = whether it holds block `pair`
+ * of `level` (level < 0: dense block `pair`); outputs may be NULL */
+int hp_rep_shard(const hp_rep* rep, int level, int64_t pair, int* world, int* shard, int* held);
 /* the work partition every rank computes: world + 1 boundaries */
 int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bounds);
-/* totals[0..6] = forward_cols, adjoint_cols, max_sampling_colors,
- * wall_s_total, wall_s_net, net_flops, setup_ms; *nphases = phase count */
+/* totals[0..8] = forward_cols, adjoint_cols, max_sampling_colors,
+ * wall_s_total, wall_s_net, net_flops, setup_ms, peak device bytes of this
+ * compress, bytes this rank sent in sharded exchanges; *nphases = phase count */
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases);
 /* per phase: ints[7] = is_leaf, level, colors, forward_cols, adjoint_cols, net_flops,
  * apply_path (K2: 0 FP64 DMMA, 1 int8 tensor cores) and
@@ -204,20 +233,6 @@ int hp_rep_captured(const hp_rep* rep, int level, int64_t pair, int64_t* rows, i
 /* rel_error_power_method (proj/src/linalg.cpp:206-218; binding module.cpp:219-229) */
 int hp_rel_error_power_method(const hp_rep* rep, const hp_op* op, int iters, uint64_t seed,
                               double* out);
-
-/* ---- K1 parity probe: payload rows of every level-`level` box for width r,
- *      both phases, on the device; out = n x 2r column-major in input order
- *      (columns [0, r) phase 0, [r, 2r) phase 1; rows not in a level box = 0). */
-int hp_debug_payload(const hp_tree* tree, int level, int r, uint64_t seed, int device,
-                     double* out);
-/* K4 probe: the batched range finder on nb blocks stacked column-major (block
- * i is rows[i] x cols); q gets Q(:, :kmax) of each block stacked the same way
- * (zero columns beyond the kept rank), ranks the kept ranks, *ms the device
- * time of the QR stage. */
-int hp_debug_qr(const double* blocks, const int* rows, int nb, int cols, int kmax, int device,
-                double* q, int* ranks, double* ms);
-/* device natural log used by the log-kernel black box, for accuracy tests */
-int hp_debug_log(const double* x, int64_t n, int device, double* out);
 
 #ifdef __cplusplus
 }

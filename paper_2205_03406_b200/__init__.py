@@ -19,7 +19,8 @@ from ._lib import check, dptr, fmat, iptr, lptr, lib
 __all__ = [
     "gaussian_matrix", "mix_seed", "random_cloud", "equispaced_1d", "uniform_grid_points",
     "BoxTree", "build_tree", "Plan", "plan", "level_coloring", "dsatur",
-    "Operator", "dense_operator", "kernel_operator", "CompressedRep", "compress",
+    "Operator", "dense_operator", "kernel_operator", "callback_operator", "CompressedRep", "compress",
+    "compress_group", "shard_owners", "shard_memory_plan",
     "rel_error_power_method", "device_count", "debug_payload", "export_sizes", "pinned_empty",
     "load_rep", "save_dense_matrix", "load_dense_matrix",
 ]
@@ -320,6 +321,46 @@ def dense_operator(a, device: int = 0) -> Operator:
     return Operator(h.value, a.shape[0])
 
 
+class CallbackOperator(Operator):
+    """A Python black box behind the C ABI's callback boundary (hp_op_callback:
+    the reference's virtual LinearOperator::apply / apply_adjoint,
+    proj/include/hpeel/linear_operator.hpp:19-20). `apply(x, adjoint)` gets an
+    n x w float64 array in the caller's point order and returns A x (A^T x).
+    Exceptions raised inside are re-raised by the next compress()."""
+
+    def __init__(self, n: int, apply, symmetric: bool = True, device: int = 0):
+        self._fn = apply
+        self.error = None
+        self.calls = 0
+        self.columns = [0, 0]
+
+        def trampoline(ctx, adjoint, x, w, y, stream):
+            try:
+                xa = np.ctypeslib.as_array(x, shape=(int(n) * int(w),)).reshape((n, w), order="F")
+                out = np.asarray(self._fn(xa, bool(adjoint)), dtype=np.float64)
+                if out.shape != (n, w):
+                    raise ValueError(f"black box returned shape {out.shape}, expected {(n, w)}")
+                ya = np.ctypeslib.as_array(y, shape=(int(n) * int(w),)).reshape((n, w), order="F")
+                ya[...] = out
+                self.calls += 1
+                self.columns[int(bool(adjoint))] += int(w)
+                return 0
+            except BaseException as e:  # noqa: BLE001 -- reported through compress()
+                self.error = e
+                return 1
+
+        self._cb = _lib.APPLY_FN(trampoline)  # kept alive with the operator
+        h = C.c_void_p()
+        check(lib().hp_op_callback(int(n), int(bool(symmetric)), 0, C.cast(self._cb, C.c_void_p), None, device,
+                                   C.byref(h)))
+        super().__init__(h.value, n)
+
+
+def callback_operator(n: int, apply, symmetric: bool = True, device: int = 0) -> CallbackOperator:
+    """Black box from a Python function apply(x, adjoint) -> y (host arrays)."""
+    return CallbackOperator(n, apply, symmetric, device)
+
+
 def kernel_operator(kind: str, points, param: float = 1.0, device: int = 0) -> Operator:
     """On-the-fly kernel black box over raw coordinates (BASELINE.json configs)."""
     pts = fmat(points)
@@ -337,7 +378,7 @@ class CompressedRep:
         self.rank = rank
         self.width = rank + oversample
         self.format = "h1"
-        totals = np.zeros(7)
+        totals = np.zeros(9)
         nph = C.c_int64(0)
         check(lib().hp_rep_report(self._h, dptr(totals), C.byref(nph)))
         ln = C.c_int64(0)
@@ -362,6 +403,7 @@ class CompressedRep:
             "forward_cols": int(totals[0]), "adjoint_cols": int(totals[1]),
             "max_sampling_colors": int(totals[2]), "wall_s_total": totals[3],
             "wall_s_net": totals[4], "net_flops": int(totals[5]), "setup_ms": totals[6],
+            "peak_device_bytes": totals[7], "exchange_bytes": totals[8],
             "csv": buf.value.decode(),
             "phases": phases,
         }
@@ -415,6 +457,18 @@ class CompressedRep:
         check(lib().hp_rep_captured(self._h, level, pair, C.byref(rows), C.byref(cols), dptr(out)))
         return out
 
+    def shard(self):
+        """(world, rank) of the group that built this representation."""
+        w, r = C.c_int(0), C.c_int(0)
+        check(lib().hp_rep_shard(self._h, 0, 0, C.byref(w), C.byref(r), None))
+        return w.value, r.value
+
+    def holds(self, level: int, pair: int) -> bool:
+        """Whether this rank holds block `pair` of `level` (level < 0: dense block)."""
+        h = C.c_int(0)
+        check(lib().hp_rep_shard(self._h, int(level), int(pair), None, None, C.byref(h)))
+        return bool(h.value)
+
     def storage(self) -> dict:
         t = C.c_int64(0)
         check(lib().hp_rep_storage(self._h, C.byref(t)))
@@ -466,11 +520,21 @@ def partition_ranges(work, world: int):
     return [int(v) for v in out]
 
 
+def _raise_callback(op, exc):
+    err = getattr(op, "error", None)
+    if err is not None:
+        op.error = None
+        raise err from exc
+    raise exc
+
+
 def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, oversample: int = 10,
              tol: float = 0.0, seed: int = 0, strategy: str = "graph", capture: bool = False,
-             comm: "Comm | None" = None, emulate_shards: int = 0, export_to=None) -> CompressedRep:
+             comm: "Comm | None" = None, export_to=None) -> CompressedRep:
     """compress_py (module.cpp:65-93) on the device; fixed-rank H1 only.
-    `comm`: shard the black-box apply over the ranks of an NCCL group.
+    `comm`: this process's rank of an NCCL group (owner-computes sharding:
+    the representation holds the factors of the pairs touching this rank's
+    boxes).
     `export_to=(host_factors, host_dense)`: float64 arrays of export_sizes()
     filled with the representation while it is built (each level as soon as
     it is final; asynchronous when they come from pinned_empty())."""
@@ -482,20 +546,66 @@ def compress(op: Operator, tree: BoxTree, format: str = "h1", rank: int = 10, ov
         raise ValueError("relative-tolerance truncation is outside the H1 fixed-rank hot path")
     h = C.c_void_p()
     if export_to is not None:
-        if capture or emulate_shards:
-            raise ValueError("export_to cannot be combined with capture or emulate_shards")
+        if capture:
+            raise ValueError("export_to cannot be combined with capture")
         hf, hd = export_to
         for a in (hf, hd):
             if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
                 raise ValueError("export arrays must be contiguous float64")
-        check(lib().hp_compress_export(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
-                                       STRATEGIES[strategy], comm._h if comm else None, dptr(hf), hf.size,
-                                       dptr(hd), hd.size, C.byref(h)))
+        try:
+            check(lib().hp_compress_export(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
+                                           STRATEGIES[strategy], comm._h if comm else None, dptr(hf), hf.size,
+                                           dptr(hd), hd.size, C.byref(h)))
+        except (RuntimeError, ValueError, AssertionError) as e:
+            _raise_callback(op, e)
         return CompressedRep(h.value, tree, rank, oversample)
-    check(lib().hp_compress_ex(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
-                               STRATEGIES[strategy], int(capture), comm._h if comm else None,
-                               int(emulate_shards), C.byref(h)))
+    try:
+        check(lib().hp_compress_ex(op._h, tree._h, int(rank), int(oversample), int(seed), FORMATS[format],
+                                   STRATEGIES[strategy], int(capture), comm._h if comm else None, C.byref(h)))
+    except (RuntimeError, ValueError, AssertionError) as e:
+        _raise_callback(op, e)
     return CompressedRep(h.value, tree, rank, oversample)
+
+
+def compress_group(op: Operator, tree: BoxTree, world: int, rank: int = 10, oversample: int = 10, seed: int = 0,
+                   capture: bool = False) -> list:
+    """compress() on `world` ranks emulated by threads of this process on the
+    operator's device: the owner-computes sharded path with device copies in
+    place of NCCL. Returns one representation per rank."""
+    hs = (C.c_void_p * int(world))()
+    try:
+        check(lib().hp_compress_group(op._h, tree._h, int(rank), int(oversample), int(seed), 0, 0, int(capture),
+                                      int(world), hs))
+    except (RuntimeError, ValueError, AssertionError) as e:
+        _raise_callback(op, e)
+    return [CompressedRep(hs[g], tree, rank, oversample) for g in range(int(world))]
+
+
+def shard_owners(tree: BoxTree, world: int):
+    """(owner per box (-1 above the cut), cut level, rank point bounds)."""
+    owner = np.zeros(tree.num_boxes, dtype=np.int32)
+    cut = C.c_int(0)
+    bounds = np.zeros(int(world) + 1, dtype=np.int64)
+    check(lib().hp_shard_owners(tree._h, int(world), iptr(owner), C.byref(cut), lptr(bounds)))
+    return owner, cut.value, bounds
+
+
+def shard_exchange_counts(tree: BoxTree, rank: int, world: int, shard: int, level: int, phase: int):
+    """(send[world], recv[world]) doubles of shard `shard`'s crossing-pair
+    exchange `phase` (1: V, 2: U and B) at `level`."""
+    send = np.zeros(int(world), dtype=np.int64)
+    recv = np.zeros(int(world), dtype=np.int64)
+    check(lib().hp_shard_exchange_counts(tree._h, int(rank), int(world), int(shard), int(level), int(phase),
+                                         lptr(send), lptr(recv)))
+    return send, recv
+
+
+def shard_memory_plan(tree: BoxTree, rank: int, oversample: int, world: int) -> np.ndarray:
+    """Per-rank device bytes (world x 4): factors held, dense blocks, largest
+    level's samples + apply buffers, total estimate."""
+    out = np.zeros(int(world) * 4)
+    check(lib().hp_shard_memory_plan(tree._h, int(rank), int(oversample), int(world), dptr(out)))
+    return out.reshape(int(world), 4)
 
 
 def load_rep(path: str, device: int = 0) -> "CompressedRep":
@@ -524,11 +634,15 @@ def load_dense_matrix(path: str) -> np.ndarray:
     return out
 
 
-def export_sizes(tree: BoxTree, rank: int):
+def export_sizes(tree: BoxTree, rank: int, world: int = 1, shard: int = 0):
     """(factor doubles, dense doubles) of the host arrays ``compress(...,
-    export_to=...)`` and ``CompressedRep.export`` fill for this tree and rank."""
+    export_to=...)`` and ``CompressedRep.export`` fill for this tree and rank
+    (of shard `shard` of a `world`-rank group)."""
     f, d = C.c_int64(0), C.c_int64(0)
-    check(lib().hp_export_sizes(tree._h, int(rank), C.byref(f), C.byref(d)))
+    if world == 1:
+        check(lib().hp_export_sizes(tree._h, int(rank), C.byref(f), C.byref(d)))
+    else:
+        check(lib().hp_export_sizes_shard(tree._h, int(rank), int(world), int(shard), C.byref(f), C.byref(d)))
     return f.value, d.value
 
 
@@ -557,7 +671,10 @@ def pinned_empty(n: int) -> np.ndarray:
 def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, seed: int = 0) -> float:
     """proj/src/linalg.cpp:206-218 (module.cpp:219-229)."""
     out = C.c_double(0.0)
-    check(lib().hp_rel_error_power_method(rep._h, ref._h, int(iters), int(seed), C.byref(out)))
+    try:
+        check(lib().hp_rel_error_power_method(rep._h, ref._h, int(iters), int(seed), C.byref(out)))
+    except (RuntimeError, ValueError, AssertionError) as e:
+        _raise_callback(ref, e)
     return out.value
 
 

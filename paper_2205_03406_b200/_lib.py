@@ -29,8 +29,6 @@ _SIGNATURES = {
     "hp_last_error": (C.c_char_p, []),
     "hp_device_count": (C.c_int, [ip]),
     "hp_launch_count": (i64, []),
-    "hp_debug_set_k2_mode": (None, [C.c_int]),
-    "hp_debug_set_k2_path": (None, [C.c_int]),
     "hp_device_synchronize": (C.c_int, []),
     "hp_mix_seed": (u64, [u64, u64]),
     "hp_gaussian_matrix": (C.c_int, [i64, i64, u64, dp]),
@@ -54,6 +52,7 @@ _SIGNATURES = {
     "hp_dsatur": (C.c_int, [C.c_int, lp, ip, ip, ip, lp]),
     "hp_op_dense": (C.c_int, [dp, i64, C.c_int, C.POINTER(P)]),
     "hp_op_kernel": (C.c_int, [C.c_int, dp, i64, C.c_int, C.c_double, C.c_int, C.POINTER(P)]),
+    "hp_op_callback": (C.c_int, [i64, C.c_int, C.c_int, P, P, C.c_int, C.POINTER(P)]),
     "hp_op_free": (None, [P]),
     "hp_op_apply": (C.c_int, [P, C.c_int, dp, i64, dp]),
     "hp_compress": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
@@ -61,8 +60,14 @@ _SIGNATURES = {
     "hp_comm_unique_id": (C.c_int, [C.c_char_p]),
     "hp_comm_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
     "hp_comm_free": (None, [P]),
-    "hp_compress_ex": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, P, C.c_int,
-                                 C.POINTER(P)]),
+    "hp_compress_ex": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, P, C.POINTER(P)]),
+    "hp_compress_group": (C.c_int, [P, P, C.c_int, C.c_int, u64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(P)]),
+    "hp_shard_owners": (C.c_int, [P, C.c_int, ip, ip, lp]),
+    "hp_shard_memory_plan": (C.c_int, [P, C.c_int, C.c_int, C.c_int, dp]),
+    "hp_shard_exchange_counts": (C.c_int, [P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, lp, lp]),
+    "hp_export_sizes_shard": (C.c_int, [P, C.c_int, C.c_int, C.c_int, lp, lp]),
+    "hp_rep_shard": (C.c_int, [P, C.c_int, i64, ip, ip, ip]),
     "hp_partition_ranges": (C.c_int, [dp, i64, C.c_int, lp]),
     "hp_rep_report": (C.c_int, [P, dp, lp]),
     "hp_rep_phase": (C.c_int, [P, i64, lp, dp]),
@@ -85,10 +90,21 @@ _SIGNATURES = {
     "hp_load_dense_matrix": (C.c_int, [C.c_char_p, lp, lp, dp, i64]),
     "hp_rep_captured": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
     "hp_rel_error_power_method": (C.c_int, [P, P, C.c_int, u64, dp]),
+}
+
+# probe entry points (paper_2205_03406_b200/csrc/hpeel_probe.h): tests and
+# profiling tools only, not part of the drop-in boundary
+_PROBE_SIGNATURES = {
+    "hp_debug_set_k2_mode": (None, [C.c_int]),
+    "hp_debug_set_k2_path": (None, [C.c_int]),
     "hp_debug_payload": (C.c_int, [P, C.c_int, C.c_int, u64, C.c_int, dp]),
     "hp_debug_qr": (C.c_int, [dp, ip, C.c_int, C.c_int, C.c_int, C.c_int, dp, ip, dp]),
     "hp_debug_log": (C.c_int, [dp, i64, C.c_int, dp]),
 }
+
+# hp_apply_fn (include/hpeel_b200.h): ctx, adjoint, x, w, y, stream
+APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double),
+                       C.c_void_p)
 
 
 def lib():
@@ -100,7 +116,7 @@ def lib():
                 f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
                 "(there is no CPU fallback for the hpeel_b200 path)")
         handle = C.CDLL(LIB_PATH)
-        for name, (res, args) in _SIGNATURES.items():
+        for name, (res, args) in list(_SIGNATURES.items()) + list(_PROBE_SIGNATURES.items()):
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
@@ -110,6 +126,10 @@ def lib():
 
 def exported_symbols():
     return list(_SIGNATURES)
+
+
+def probe_symbols():
+    return list(_PROBE_SIGNATURES)
 
 
 def check(rc):

@@ -1,5 +1,6 @@
 // C ABI over the hpeel host layer and device engine (include/hpeel_b200.h).
 #include "../../include/hpeel_b200.h"
+#include "hpeel_probe.h"
 
 #include <cuda_runtime.h>
 
@@ -414,6 +415,17 @@ int hp_op_kernel(int kind, const double* points, int64_t n, int dim, double para
 
 void hp_op_free(hp_op* op) { delete op; }
 
+int hp_op_callback(int64_t n, int symmetric, int device_pointers, hp_apply_fn fn, void* ctx, int device,
+                   hp_op** out) {
+  return guard([&] {
+    need(out, "out");
+    need(reinterpret_cast<const void*>(fn), "apply function");
+    auto o = std::make_unique<hp_op>();
+    o->op = DeviceOperator::callback(n, symmetric != 0, device_pointers != 0, fn, ctx, device);
+    *out = o.release();
+  });
+}
+
 int hp_op_apply(const hp_op* op, int adjoint, const double* x, int64_t w, double* y) {
   return guard([&] {
     need(op, "op");
@@ -449,7 +461,7 @@ void hp_rep_free(hp_rep* rep) { delete rep; }
 int hp_comm_unique_id(unsigned char* id128) {
   return guard([&] {
     need(id128, "id");
-    Comm::unique_id(id128);
+    NcclComm::unique_id(id128);
   });
 }
 
@@ -458,35 +470,38 @@ int hp_comm_create(const unsigned char* id128, int rank, int world, int device, 
     need(out, "out");
     if (world > 1) need(id128, "id");
     auto c = std::make_unique<hp_comm>();
-    c->comm = std::make_unique<Comm>(id128, rank, world, device);
+    c->comm = std::make_unique<NcclComm>(id128, rank, world, device);
     *out = c.release();
   });
 }
 
 void hp_comm_free(hp_comm* comm) { delete comm; }
 
+namespace {
+PeelConfig make_config(const hp_tree* tree, int rank, int oversample, uint64_t seed, int format, int strategy,
+                       int capture) {
+  if (format < 0 || format > 3) throw std::invalid_argument("unknown format");
+  PeelConfig cfg;
+  cfg.rank = rank;
+  cfg.oversample = oversample;
+  cfg.leaf_capacity = tree->tree->leaf_capacity();
+  cfg.seed = seed;
+  cfg.format = PeelFormat(format);
+  cfg.strategy = strategy == HP_STRATEGY_FALLBACK_PATTERN ? ColoringStrategy::kFallbackPattern
+                                                          : ColoringStrategy::kGraph;
+  cfg.capture_samples = capture != 0;
+  return cfg;
+}
+}  // namespace
+
 int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
-                   int format, int strategy, int capture, hp_comm* comm, int emulate_shards,
-                   hp_rep** out) {
+                   int format, int strategy, int capture, hp_comm* comm, hp_rep** out) {
   return guard([&] {
     need(op, "op");
     need(tree, "tree");
     need(out, "out");
-    if (format < 0 || format > 3) throw std::invalid_argument("unknown format");
-    if (emulate_shards < 0) throw std::invalid_argument("negative shard count");
-    PeelConfig cfg;
-    cfg.rank = rank;
-    cfg.oversample = oversample;
-    cfg.leaf_capacity = tree->tree->leaf_capacity();
-    cfg.seed = seed;
-    cfg.format = PeelFormat(format);
-    cfg.strategy = strategy == HP_STRATEGY_FALLBACK_PATTERN ? ColoringStrategy::kFallbackPattern
-                                                            : ColoringStrategy::kGraph;
-    cfg.capture_samples = capture != 0;
+    PeelConfig cfg = make_config(tree, rank, oversample, seed, format, strategy, capture);
     cfg.comm = comm ? comm->comm.get() : nullptr;
-    cfg.emulate_shards = emulate_shards;
-    if (cfg.comm && cfg.comm->device() != op->op->device())
-      throw std::invalid_argument("communicator and operator on different devices");
     auto r = std::make_unique<hp_rep>();
     static const bool timing = std::getenv("HP_DRIVER_TIMING") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
@@ -495,6 +510,81 @@ int hp_compress_ex(const hp_op* op, const hp_tree* tree, int rank, int oversampl
       std::fprintf(stderr, "[capi] compress() returned after %.1f ms\n",
                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     *out = r.release();
+  });
+}
+
+int hp_compress_group(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
+                      int format, int strategy, int capture, int world, hp_rep** outs) {
+  return guard([&] {
+    need(op, "op");
+    need(tree, "tree");
+    need(outs, "outs");
+    if (world < 1) throw std::invalid_argument("world size must be >= 1");
+    const PeelConfig cfg = make_config(tree, rank, oversample, seed, format, strategy, capture);
+    auto results = compress_group(*op->op, tree->tree, cfg, world);
+    for (int g = 0; g < world; ++g) {
+      auto r = std::make_unique<hp_rep>();
+      r->result = std::move(results[size_t(g)]);
+      outs[g] = r.release();
+    }
+  });
+}
+
+int hp_shard_owners(const hp_tree* tree, int world, int* owner, int* cut, int64_t* point_bounds) {
+  return guard([&] {
+    need(tree, "tree");
+    const Ownership o = make_ownership(*tree->tree, *tree->layout, world, 0);
+    if (owner) std::memcpy(owner, o.owner.data(), o.owner.size() * sizeof(int));
+    if (cut) *cut = o.cut;
+    if (point_bounds) std::memcpy(point_bounds, o.point_bounds.data(), o.point_bounds.size() * sizeof(int64_t));
+  });
+}
+
+int hp_shard_memory_plan(const hp_tree* tree, int rank, int oversample, int world, double* out) {
+  return guard([&] {
+    need(tree, "tree");
+    need(out, "out");
+    if (rank < 1 || oversample < 0 || world < 1) throw std::invalid_argument("bad rank / oversampling / world");
+    shard_memory_plan(*tree->tree, rank, oversample, world, out);
+  });
+}
+
+int hp_shard_exchange_counts(const hp_tree* tree, int rank, int world, int shard, int level, int phase,
+                             int64_t* send, int64_t* recv) {
+  return guard([&] {
+    need(tree, "tree");
+    need(send, "send");
+    need(recv, "recv");
+    if (rank < 1 || world < 1 || shard < 0 || shard >= world || (phase != 1 && phase != 2))
+      throw std::invalid_argument("bad rank / shard / world / phase");
+    shard_exchange_counts(*tree->tree, rank, world, shard, level, phase, send, recv);
+  });
+}
+
+int hp_export_sizes_shard(const hp_tree* tree, int rank, int world, int shard, int64_t* factor_doubles,
+                          int64_t* dense_doubles) {
+  return guard([&] {
+    need(tree, "tree");
+    if (rank < 1) throw std::invalid_argument("fixed rank must be >= 1");
+    if (world < 1 || shard < 0 || shard >= world) throw std::invalid_argument("bad shard / world size");
+    export_sizes(*tree->tree, rank, factor_doubles, dense_doubles, world, shard);
+  });
+}
+
+int hp_rep_shard(const hp_rep* rep, int level, int64_t pair, int* world, int* shard, int* held) {
+  return guard([&] {
+    need(rep, "rep");
+    const H1Rep& h = *rep->result.rep;
+    if (world) *world = h.world;
+    if (shard) *shard = h.shard_rank;
+    if (held) {
+      if (level < 0) {
+        *held = pair >= 0 && size_t(pair) < h.dense.off.size() && h.dense.off[size_t(pair)] >= 0;
+      } else {
+        *held = size_t(level) < h.levels.size() && pair >= 0 && size_t(pair) < h.levels[size_t(level)].uoff.size() &&
+                h.levels[size_t(level)].uoff[size_t(pair)] >= 0;
+      }
+    }
   });
 }
 
@@ -518,6 +608,8 @@ int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases) {
       totals[3] = r.wall_s_total;
       totals[4] = r.wall_s_net;
       totals[5] = double(r.net_flops);
+      totals[7] = r.peak_device_bytes;
+      totals[8] = r.exchange_bytes;
       totals[6] = r.setup_ms;
     }
     if (nphases) *nphases = int64_t(r.phases.size());
@@ -673,7 +765,8 @@ int hp_compress_export(const hp_op* op, const hp_tree* tree, int rank, int overs
     need(host_dense, "host_dense");
     if (format < 0 || format > 3) throw std::invalid_argument("unknown format");
     std::int64_t nf = 0, nd = 0;
-    if (rank >= 1) export_sizes(*tree->tree, rank, &nf, &nd);
+    if (rank >= 1)
+      export_sizes(*tree->tree, rank, &nf, &nd, comm ? comm->comm->world() : 1, comm ? comm->comm->rank() : 0);
     if (factor_doubles < nf || dense_doubles < nd)
       throw std::invalid_argument("export arrays smaller than hp_export_sizes");
     PeelConfig cfg;
@@ -687,8 +780,6 @@ int hp_compress_export(const hp_op* op, const hp_tree* tree, int rank, int overs
     cfg.comm = comm ? comm->comm.get() : nullptr;
     cfg.export_factors = host_factors;
     cfg.export_dense = host_dense;
-    if (cfg.comm && cfg.comm->device() != op->op->device())
-      throw std::invalid_argument("communicator and operator on different devices");
     auto r = std::make_unique<hp_rep>();
     r->result = compress(*op->op, tree->tree, cfg);
     *out = r.release();

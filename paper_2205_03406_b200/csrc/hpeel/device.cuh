@@ -36,6 +36,7 @@ enum OpKind : int {
   kOpLog = 1,        // log|x - y|, A_ii = 0
   kOpInvDist4Pi = 2, // 1 / (4 pi |x - y|), A_ii = 0
   kOpExp = 3,        // exp(-|x - y| / ell), A_ii = 1
+  kOpCallback = 4,   // caller-supplied apply / apply_adjoint (no device kernel evaluates it)
 };
 
 struct DevOp {

@@ -11,11 +11,21 @@
 // K3 peeling restricted to nonzero payload rows, batched K4 QR and K5
 // B-solves (main stream), so level l + 1's apply overlaps level l's
 // factorization.
+//
+// Multi-GPU (shard.hpp): owner-computes. Each rank computes the
+// samples of the pairs whose row box it owns, peels them with the factors it
+// holds, and keeps only the factors of pairs touching its boxes; per level two
+// point-to-point exchanges ship V (to the row owner) and U, B (to the column
+// owner) of the cut-crossing pairs. The levels above the cut are replicated.
+// The black box itself may be the caller's callback (the reference's virtual
+// LinearOperator::apply): then each color's dense test matrix is realized on
+// the device, handed to the callback, and the sample rows read back.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <chrono>
 #include <future>
+#include <mutex>
 #include <memory>
 #include <cstdio>
 #include <cstdlib>
@@ -44,12 +54,13 @@ std::int64_t svd_flops(std::int64_t m, std::int64_t n) {
 }
 
 // Reference flop count of H1Rep::apply_truncated(level) for one width-w
-// product (proj/src/hmatrix.cpp:86-100).
+// product (proj/src/hmatrix.cpp:86-100), over the pairs this rank counts.
 std::int64_t truncated_apply_flops(const H1Rep& rep, int level, std::int64_t w, const Engine& e) {
   std::int64_t f = 0;
   for (int l = 2; l <= std::min<int>(level, int(rep.levels.size()) - 1); ++l) {
     const auto& ld = rep.levels[size_t(l)];
     for (size_t p = 0; p < ld.pairs.size(); ++p) {
+      if (!rep.counts_pair(l, int(p))) continue;
       const std::int64_t ma = e.count(ld.pairs[p].first), mb = e.count(ld.pairs[p].second);
       f += gemm_flops(ld.kv[p], w, mb) + gemm_flops(ld.ku[p], w, ld.kv[p]) + gemm_flops(ma, w, ld.ku[p]);
     }
@@ -65,15 +76,154 @@ void reap_async(T&& obj) {
   std::thread([p] { delete p; }).detach();
 }
 
+// ------------------------------------------------------------------ arena
+
+/// Factor-arena and dense-block layout of one rank: offsets of the pairs it
+/// holds (-1 elsewhere). Replicated levels come first and are laid out the
+/// same on every rank; dense blocks are compact |I_lam| x |I_mu|
+/// (D = Y(I_lam, 0:|I_mu|), proj/src/peeling.cpp:513-517).
+struct ArenaLayout {
+  std::vector<H1Rep::LevelData> levels;
+  std::int64_t factors = 0;
+  std::vector<std::pair<int, int>> dense_pairs;
+  std::vector<std::int64_t> dense_off;
+  std::int64_t dense = 0;
+};
+
+ArenaLayout arena_layout(const BoxTree& tree, const AdjacencyInfo& adj, const Ownership& o, int k) {
+  ArenaLayout L;
+  L.levels.resize(size_t(tree.depth()) + 1);
+  auto cnt = [&](int b) { return std::int64_t(tree.box(b).points.size()); };
+  for (int l = 2; l <= tree.depth(); ++l) {
+    auto& ld = L.levels[size_t(l)];
+    ld.pairs = admissible_pairs(tree, adj, l);
+    const size_t np = ld.pairs.size();
+    ld.uoff.assign(np, -1);
+    ld.voff.assign(np, -1);
+    ld.boff.assign(np, -1);
+    ld.ku.assign(np, 0);
+    ld.kv.assign(np, 0);
+    for (size_t p = 0; p < np; ++p) {
+      const auto [a, b] = ld.pairs[p];
+      if (!(o.replicated(l) || o.mine(a) || o.mine(b))) continue;
+      ld.uoff[p] = L.factors;
+      L.factors += cnt(a) * k;
+      ld.voff[p] = L.factors;
+      L.factors += cnt(b) * k;
+      ld.boff[p] = L.factors;
+      L.factors += std::int64_t(k) * k;
+    }
+  }
+  L.dense_pairs = dense_pairs(tree, adj);
+  L.dense_off.assign(L.dense_pairs.size(), -1);
+  for (size_t p = 0; p < L.dense_pairs.size(); ++p) {
+    const auto [lam, mu] = L.dense_pairs[p];
+    if (!o.mine(lam)) continue;
+    L.dense_off[p] = L.dense;
+    L.dense += cnt(lam) * cnt(mu);
+  }
+  return L;
+}
+
+// ------------------------------------------------------------------ exchanges
+
+/// One all-to-all-v of factor segments and rank slots between the owners of
+/// cut-crossing pairs. Phase 1: V_q (computed by the column owner) to the row
+/// owner; phase 2: U_q and B_q (row owner) to the column owner. Message i -> j
+/// carries the pairs q in ascending order, so both ends enumerate it alike.
+struct Exchange {
+  std::vector<CopySeg> pack, unpack;      // arena -> send buffer, recv buffer -> arena
+  std::vector<std::int64_t> soff, roff;   // world + 1 (doubles)
+  std::vector<int> rs_idx, rr_idx;        // rank slots gathered / scattered
+  std::vector<std::int64_t> rsoff, rroff; // world + 1 (ints)
+};
+
+Exchange make_exchange(const H1Rep::LevelData& ld, const Ownership& o, const BoxTree& tree, int k, bool phase1) {
+  Exchange X;
+  const int W = o.world, me = o.rank;
+  const size_t np = ld.pairs.size();
+  auto cnt = [&](int b) { return std::int64_t(tree.box(b).points.size()); };
+  auto ends = [&](size_t q, int& from, int& to) {
+    const int oa = o.of(ld.pairs[q].first), ob = o.of(ld.pairs[q].second);
+    from = phase1 ? ob : oa;
+    to = phase1 ? oa : ob;
+  };
+  auto parts = [&](size_t q, auto&& fn) {
+    if (phase1) {
+      fn(ld.voff[q], cnt(ld.pairs[q].second) * k);
+    } else {
+      fn(ld.uoff[q], cnt(ld.pairs[q].first) * k);
+      fn(ld.boff[q], std::int64_t(k) * k);
+    }
+  };
+  auto slot = [&](size_t q) { return int(phase1 ? np + q : q); };
+  X.soff.assign(size_t(W) + 1, 0);
+  X.roff.assign(size_t(W) + 1, 0);
+  X.rsoff.assign(size_t(W) + 1, 0);
+  X.rroff.assign(size_t(W) + 1, 0);
+  std::int64_t cur = 0, rcur = 0;
+  for (int j = 0; j < W; ++j) {
+    X.soff[size_t(j)] = cur;
+    X.rsoff[size_t(j)] = std::int64_t(X.rs_idx.size());
+    X.roff[size_t(j)] = rcur;
+    X.rroff[size_t(j)] = std::int64_t(X.rr_idx.size());
+    if (j == me) continue;
+    for (size_t q = 0; q < np; ++q) {
+      int from = 0, to = 0;
+      ends(q, from, to);
+      if (from == me && to == j) {
+        parts(q, [&](std::int64_t off, std::int64_t len) {
+          X.pack.push_back(CopySeg{off, cur, len});
+          cur += len;
+        });
+        X.rs_idx.push_back(slot(q));
+      } else if (from == j && to == me) {
+        parts(q, [&](std::int64_t off, std::int64_t len) {
+          X.unpack.push_back(CopySeg{rcur, off, len});
+          rcur += len;
+        });
+        X.rr_idx.push_back(slot(q));
+      }
+    }
+  }
+  X.soff[size_t(W)] = cur;
+  X.roff[size_t(W)] = rcur;
+  X.rsoff[size_t(W)] = std::int64_t(X.rs_idx.size());
+  X.rroff[size_t(W)] = std::int64_t(X.rr_idx.size());
+  return X;
+}
+
+double run_exchange(const Exchange& X, Comm& comm, double* arena, int* d_ranks, cudaStream_t s) {
+  DevBuf<double> send(size_t(X.soff.back()), s), recv(size_t(X.roff.back()), s);
+  DevBuf<CopySeg> dp, du;
+  dp.upload(X.pack, s);
+  du.upload(X.unpack, s);
+  launch_copy_segments(arena, dp.get(), int(X.pack.size()), send.get(), s);
+  comm.exchange(send.get(), X.soff, recv.get(), X.roff, s);
+  launch_copy_segments(recv.get(), du.get(), int(X.unpack.size()), arena, s);
+  DevBuf<int> si, ri, isend(X.rs_idx.size(), s), irecv(X.rr_idx.size(), s);
+  si.upload(X.rs_idx, s);
+  ri.upload(X.rr_idx, s);
+  launch_move_i32(d_ranks, si.get(), std::int64_t(X.rs_idx.size()), isend.get(), nullptr, s);
+  comm.exchange_i32(isend.get(), X.rsoff, irecv.get(), X.rroff, s);
+  launch_move_i32(irecv.get(), nullptr, std::int64_t(X.rr_idx.size()), d_ranks, ri.get(), s);
+  return double(X.soff.back()) * 8.0 + double(X.rs_idx.size()) * 4.0;
+}
+
+// ------------------------------------------------------------------ level plan
+
 struct LevelWork {
   int level = 0;
   bool empty = true;
   bool symmetric = true;
+  bool replicated = false;   // above the cut: every rank holds every pair
   int nc = 0;
   std::int64_t fwd_cols = 0;
   size_t np = 0;
-  std::vector<int> pcolor, swap;
-  std::vector<std::int64_t> soff;
+  std::vector<int> pcolor, swap;           // per pair
+  std::vector<int> own;                    // sample blocks on this rank (pair indices)
+  std::vector<int> own_idx;                // per pair: index in `own` or -1
+  std::vector<std::int64_t> soff;          // per own block (+ total)
   std::vector<std::int64_t> pay_off;
   std::vector<int> pay_pos;
   std::vector<std::int64_t> step_off;      // int8 K2: 32-row K-steps per color (prefix)
@@ -81,25 +231,28 @@ struct LevelWork {
   std::vector<std::int64_t> pb_off;        // payload boxes per color (prefix)
   std::vector<int> pb_box;
   std::vector<int> pos_box, local;
-  std::vector<K2Row> rowtab;               // K2 rows, grouped by shard and color
-  std::vector<std::vector<K2Task>> k2;     // K2 tiles per shard
-  std::vector<std::int64_t> seg;           // shard q owns samples [seg[q], seg[q+1])
+  std::vector<K2Row> rowtab;               // K2 rows of this rank's tiles
+  std::vector<K2Task> k2;                  // K2 tiles this rank launches
+  std::vector<std::int64_t> seg;           // replicated: rank q computes samples [seg[q], seg[q+1])
   bool k2_checked = false;                 // some row box is in its own color's payload
   double evals = 0;
   bool has_peel = false;
   PeelPlan peel;
-  // K4/K5 per shard: shard q owns pairs [fb[q], fb[q+1]) and
-  // computes their U, V (QR), grams and B; factor segments are then shared
-  struct Shard45 {
-    std::int64_t p0 = 0, p1 = 0;
-    QrPlan qr;
-    GramPlan g_mid, g_gpu, g_vg;
-  };
-  std::vector<Shard45> s45;
-  std::vector<std::int64_t> fb;
+  // callback black box: per color, the own sample rows it serves
+  std::vector<std::int64_t> cb_off;
+  std::vector<GatherRow> cb_rows;
+  // K4/K5 on this rank: QR requests (U and V), grams and B solves of `solve`
+  QrPlan qr;
+  GramPlan g_mid, g_gpu, g_vg;
+  std::vector<int> solve;
+  std::vector<std::int64_t> solve_boff;
+  // replicated: factor / rank broadcast segments (rank q solves pairs [fb[q], fb[q+1]))
+  std::vector<std::int64_t> fb, fseg, useg, vseg;
+  // owned: crossing-pair exchanges (V to the row owner, then U / B back)
+  Exchange x1, x2;
 };
 
-LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig& cfg) {
+LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig& cfg, const Ownership& o) {
   LevelWork w;
   w.level = l;
   const auto& ld = rep.levels[size_t(l)];
@@ -111,6 +264,8 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
       if (!all.count({b, a})) w.symmetric = false;
   }
   if (!w.symmetric) return w;
+  w.replicated = o.replicated(l);
+  const int world = o.world, me = o.rank;
   const int r = e.r, k = e.k;
   static const bool timing = std::getenv("HP_PLAN_TIMING") != nullptr;
   auto t0 = Clock::now();
@@ -147,13 +302,22 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
   const size_t np = ld.pairs.size();
   w.np = np;
   w.pcolor.resize(np);
-  w.soff.assign(np + 1, 0);
   w.swap.resize(np);
   for (size_t p = 0; p < np; ++p) {
     w.pcolor[p] = plan.block_to_matrix.at(ld.pairs[p]);
-    w.soff[p + 1] = w.soff[p] + std::int64_t(e.count(ld.pairs[p].first)) * 2 * r;
     w.swap[p] = pair_index(ld.pairs, ld.pairs[p].second, ld.pairs[p].first);
   }
+  // sample blocks computed here: every pair on a replicated level, else the
+  // pairs whose row box this rank owns
+  w.own_idx.assign(np, -1);
+  for (size_t p = 0; p < np; ++p)
+    if (w.replicated || o.mine(ld.pairs[p].first)) {
+      w.own_idx[p] = int(w.own.size());
+      w.own.push_back(int(p));
+    }
+  w.soff.assign(w.own.size() + 1, 0);
+  for (size_t i = 0; i < w.own.size(); ++i)
+    w.soff[i + 1] = w.soff[i] + std::int64_t(e.count(ld.pairs[size_t(w.own[i])].first)) * 2 * r;
   // K1: pos -> box, local rank
   w.pos_box.assign(size_t(e.n), -1);
   w.local.assign(size_t(e.n), 0);
@@ -164,15 +328,10 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
       w.local[size_t(e.start(b) + q)] = lr[q];
     }
   }
-  // K2: split the pairs into work-balanced contiguous ranges, one per shard
-  // (DESIGN.md §7); inside a shard, the target rows of all pairs served by
-  // one color are packed into full tiles, largest payload lists first.
-  const int world = cfg.comm ? cfg.comm->world() : std::max(1, cfg.emulate_shards);
   std::vector<double> pair_work(np);
   for (size_t p = 0; p < np; ++p) {
     const std::int64_t nnz = w.pay_off[size_t(w.pcolor[p]) + 1] - w.pay_off[size_t(w.pcolor[p])];
     pair_work[p] = double(e.count(ld.pairs[p].first)) * double(nnz);
-    w.evals += pair_work[p];
   }
   {
     // a valid H1 coloring never puts a row box into the payload serving it;
@@ -183,17 +342,42 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
     for (size_t p = 0; p < np; ++p)
       if (box_color.count({ld.pairs[p].first, w.pcolor[p]})) w.k2_checked = true;
   }
-  const auto bounds = partition_ranges(pair_work, world);
-  w.seg.resize(size_t(world) + 1);
-  for (int q = 0; q <= world; ++q) w.seg[size_t(q)] = w.soff[size_t(bounds[size_t(q)])];
-  const int tile = k2_tile_rows(e.dop.symmetric ? 2 * r : r);
-  w.k2.resize(size_t(world));
-  std::vector<std::vector<int>> by_color(size_t(w.nc));
-  for (int q = 0; q < world; ++q) {
-    for (auto& v : by_color) v.clear();
-    for (std::int64_t p = bounds[size_t(q)]; p < bounds[size_t(q) + 1]; ++p)
-      by_color[size_t(w.pcolor[size_t(p)])].push_back(int(p));
-    auto& tl = w.k2[size_t(q)];
+  // K2 pairs this rank applies: its own blocks, or on a replicated level its
+  // work-balanced contiguous range (the rows are then broadcast)
+  std::int64_t k2_p0 = 0, k2_p1 = std::int64_t(np);
+  if (w.replicated) {
+    const auto bounds = partition_ranges(pair_work, world);
+    w.seg.resize(size_t(world) + 1);
+    for (int q = 0; q <= world; ++q) w.seg[size_t(q)] = w.soff[size_t(bounds[size_t(q)])];
+    k2_p0 = bounds[size_t(me)];
+    k2_p1 = bounds[size_t(me) + 1];
+  }
+  for (size_t i = 0; i < w.own.size(); ++i) {
+    const int p = w.own[i];
+    if (p >= k2_p0 && p < k2_p1) w.evals += pair_work[size_t(p)];
+  }
+  if (e.op.is_callback()) {
+    // rows of the blocks each color serves, read back from the callback's Y
+    std::vector<std::vector<int>> by_color(size_t(w.nc));
+    for (std::int64_t p = k2_p0; p < k2_p1; ++p)
+      if (w.own_idx[size_t(p)] >= 0) by_color[size_t(w.pcolor[size_t(p)])].push_back(int(p));
+    w.cb_off.assign(size_t(w.nc) + 1, 0);
+    for (int c = 0; c < w.nc; ++c) {
+      for (int p : by_color[size_t(c)]) {
+        const int a = ld.pairs[size_t(p)].first, rows = e.count(a);
+        const std::int64_t base = w.soff[size_t(w.own_idx[size_t(p)])];
+        for (int i = 0; i < rows; ++i) w.cb_rows.push_back(GatherRow{base + i, int(e.start(a) + i), rows, r, 0});
+      }
+      w.cb_off[size_t(c) + 1] = std::int64_t(w.cb_rows.size());
+    }
+  } else {
+    // inside this rank's range, the target rows of all pairs served by one
+    // color are packed into full tiles, largest payload lists first
+    const int tile = k2_tile_rows(e.dop.symmetric ? 2 * r : r);
+    std::vector<std::vector<int>> by_color(size_t(w.nc));
+    for (std::int64_t p = k2_p0; p < k2_p1; ++p)
+      if (w.own_idx[size_t(p)] >= 0) by_color[size_t(w.pcolor[size_t(p)])].push_back(int(p));
+    auto& tl = w.k2;
     for (int c = 0; c < w.nc; ++c) {
       // whole tiles of big boxes run in place; their remainders and the small
       // boxes are packed through the row table
@@ -202,61 +386,87 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
         const int a = ld.pairs[size_t(p)].first;
         const int rows = e.count(a);
         const int full = rows / tile * tile;
-        for (int t0 = 0; t0 < full; t0 += tile)
-          tl.push_back(K2Task{w.soff[size_t(p)] + t0, tile, c, rows, int(e.start(a) + t0)});
-        for (int i = full; i < rows; ++i)
-          w.rowtab.push_back(K2Row{w.soff[size_t(p)] + i, int(e.start(a) + i), rows});
+        const std::int64_t base = w.soff[size_t(w.own_idx[size_t(p)])];
+        for (int t0r = 0; t0r < full; t0r += tile)
+          tl.push_back(K2Task{base + t0r, tile, c, rows, int(e.start(a) + t0r)});
+        for (int i = full; i < rows; ++i) w.rowtab.push_back(K2Row{base + i, int(e.start(a) + i), rows});
       }
       const std::int64_t last = std::int64_t(w.rowtab.size());
-      for (std::int64_t t0 = first; t0 < last; t0 += tile)
-        tl.push_back(K2Task{t0, int(std::min<std::int64_t>(tile, last - t0)), c, 0, 0});
+      for (std::int64_t t0r = first; t0r < last; t0r += tile)
+        tl.push_back(K2Task{t0r, int(std::min<std::int64_t>(tile, last - t0r)), c, 0, 0});
     }
     std::stable_sort(tl.begin(), tl.end(), [&](const K2Task& x, const K2Task& y) {
       return w.pay_off[size_t(x.color) + 1] - w.pay_off[size_t(x.color)] >
              w.pay_off[size_t(y.color) + 1] - w.pay_off[size_t(y.color)];
     });
   }
-  // K3 (prev_level = l - 1 >= 2)
+  lap("k2 tasks");
+  // K3 (prev_level = l - 1 >= 2) on this rank's blocks
   if (l - 1 >= 2) {
-    std::vector<SampleBlock> blocks(np);
-    for (size_t p = 0; p < np; ++p) blocks[p] = SampleBlock{ld.pairs[p].first, w.pcolor[p], w.soff[p]};
-    lap("k2 tasks");
+    std::vector<SampleBlock> blocks(w.own.size());
+    for (size_t i = 0; i < w.own.size(); ++i)
+      blocks[i] = SampleBlock{ld.pairs[size_t(w.own[i])].first, w.pcolor[size_t(w.own[i])], w.soff[i]};
     w.peel = plan_peel(e, rep, blocks, color_boxes, l - 1, r, true);
     lap("plan_peel");
     w.has_peel = true;
   }
-  // K5a middle = G'_a^T Y_p; K4 QR; K5b grams -- per shard, on the pairs it
-  // owns (outputs by pair: U_p from Y_p, V_p from Z of swap(p))
+  // K5a middle = G'_a^T Y_p; K4 QR; K5b grams -- on the pairs this rank
+  // solves (outputs by pair: U_p from Y_p, V from the adjoint columns)
   const int gld = 2 * r;
-  {
+  std::vector<GramReq> mid, gu, vg;
+  std::vector<QrRequest> qr;
+  if (w.replicated) {
     std::vector<double> w45(np);
     for (size_t p = 0; p < np; ++p)
       w45[p] = double(e.count(ld.pairs[p].first) + e.count(ld.pairs[p].second)) * double(r) * double(r);
     w.fb = partition_ranges(w45, world);
-  }
-  w.s45.resize(size_t(world));
-  for (int q = 0; q < world; ++q) {
-    LevelWork::Shard45& sh = w.s45[size_t(q)];
-    sh.p0 = w.fb[size_t(q)];
-    sh.p1 = w.fb[size_t(q) + 1];
-    std::vector<GramReq> mid, gu, vg;
-    std::vector<QrRequest> qr;
-    for (std::int64_t p = sh.p0; p < sh.p1; ++p) {
+    for (std::int64_t p = w.fb[size_t(me)]; p < w.fb[size_t(me) + 1]; ++p) w.solve.push_back(int(p));
+    for (int p : w.solve) {
       const auto [a, b] = ld.pairs[size_t(p)];
-      const int rows = e.count(a), rows_b = e.count(b);
+      const int rows_b = e.count(b);
       const std::int64_t sp = w.swap[size_t(p)];  // block (b, a): its adjoint columns give V_p
-      mid.push_back(GramReq{e.start(a) * gld + r, w.soff[size_t(p)], rows, gld, rows, 1, 0});
-      gu.push_back(GramReq{e.start(a) * gld + r, ld.uoff[size_t(p)], rows, gld, rows, 1, 0});
-      vg.push_back(GramReq{ld.voff[size_t(p)], e.start(b) * gld, rows_b, rows_b, gld, 0, 1});
-      qr.push_back(QrRequest{w.soff[size_t(p)], ld.uoff[size_t(p)], rows, rows, int(p)});
+      qr.push_back(QrRequest{w.soff[size_t(p)], ld.uoff[size_t(p)], e.count(a), e.count(a), p});
       qr.push_back(QrRequest{w.soff[size_t(sp)] + std::int64_t(rows_b) * r, ld.voff[size_t(p)], rows_b, rows_b,
-                             int(np + size_t(p))});
+                             int(np) + p});
     }
-    sh.g_mid = plan_gram(mid, r, r);
-    sh.g_gpu = plan_gram(gu, r, k);
-    sh.g_vg = plan_gram(vg, k, r);
-    sh.qr = plan_qr(qr, r, k);
+    const std::int64_t fend = ld.boff[np - 1] + std::int64_t(k) * k;
+    w.fseg.resize(size_t(world) + 1);
+    w.useg.resize(size_t(world) + 1);
+    w.vseg.resize(size_t(world) + 1);
+    for (int q = 0; q <= world; ++q) {
+      const std::int64_t p = w.fb[size_t(q)];
+      w.fseg[size_t(q)] = p < std::int64_t(np) ? ld.uoff[size_t(p)] : fend;
+      w.useg[size_t(q)] = p;
+      w.vseg[size_t(q)] = std::int64_t(np) + p;
+    }
+  } else {
+    w.solve = w.own;
+    for (size_t i = 0; i < w.own.size(); ++i) {
+      const int p = w.own[i];
+      const int a = ld.pairs[size_t(p)].first;
+      const int sp = w.swap[size_t(p)];  // pair (b, a): V of it comes from the adjoint columns of block p
+      qr.push_back(QrRequest{w.soff[i], ld.uoff[size_t(p)], e.count(a), e.count(a), p});
+      qr.push_back(QrRequest{w.soff[i] + std::int64_t(e.count(a)) * r, ld.voff[size_t(sp)], e.count(a), e.count(a),
+                             int(np) + sp});
+    }
+    if (world > 1) {
+      w.x1 = make_exchange(ld, o, e.tree, k, true);
+      w.x2 = make_exchange(ld, o, e.tree, k, false);
+    }
   }
+  for (int p : w.solve) {
+    const auto [a, b] = ld.pairs[size_t(p)];
+    const int rows = e.count(a), rows_b = e.count(b);
+    const std::int64_t so = w.soff[size_t(w.own_idx[size_t(p)])];
+    mid.push_back(GramReq{e.start(a) * gld + r, so, rows, gld, rows, 1, 0});
+    gu.push_back(GramReq{e.start(a) * gld + r, ld.uoff[size_t(p)], rows, gld, rows, 1, 0});
+    vg.push_back(GramReq{ld.voff[size_t(p)], e.start(b) * gld, rows_b, rows_b, gld, 0, 1});
+    w.solve_boff.push_back(ld.boff[size_t(p)]);
+  }
+  w.g_mid = plan_gram(mid, r, r);
+  w.g_gpu = plan_gram(gu, r, k);
+  w.g_vg = plan_gram(vg, k, r);
+  w.qr = plan_qr(qr, r, k);
   lap("plan_qr");
   return w;
 }
@@ -271,12 +481,11 @@ struct LeafWork {
   double evals = 0;
   bool has_peel = false;
   PeelPlan peel;
-  std::vector<std::pair<int, int>> pairs;
-  std::vector<std::int64_t> off;
-  std::int64_t total = 0;
+  std::vector<std::int64_t> cb_off;   // callback: per color, rows of this rank's dense blocks
+  std::vector<GatherRow> cb_rows;
 };
 
-LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg) {
+LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg, const Ownership& o) {
   LeafWork lw;
   const BoxTree& tree = e.tree;
   lw.w = tree.max_leaf_size();
@@ -303,24 +512,33 @@ LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg) {
     lw.pay_off[size_t(c) + 1] = std::int64_t(lw.pay_box.size());
     lw.fwd_cols += plan.matrices[size_t(c)].payload.empty() ? 0 : lw.w;
   }
-  lw.pairs = dense_pairs(tree, e.adj);
-  const size_t nd = lw.pairs.size();
-  lw.off.resize(nd);
-  std::vector<SampleBlock> blocks(nd);
-  for (size_t p = 0; p < nd; ++p) {
-    const auto [lam, mu] = lw.pairs[p];
-    const int c = plan.block_to_matrix.at(lw.pairs[p]);
-    const int rows = e.count(lam);
-    lw.off[p] = lw.total;
-    for (int t0 = 0; t0 < rows; t0 += kTile)
-      lw.tasks.push_back(SampleTask{e.start(lam) + t0, lw.total + t0, std::min(kTile, rows - t0), c, rows, 0});
-    blocks[p] = SampleBlock{lam, c, lw.total};
+  const auto& pairs = rep.dense.pairs;
+  std::vector<SampleBlock> blocks;
+  std::vector<std::vector<GatherRow>> cb(size_t(lw.nc));
+  for (size_t p = 0; p < pairs.size(); ++p) {
+    const std::int64_t off = rep.dense.off[p];
+    if (off < 0) continue;
+    const auto [lam, mu] = pairs[p];
+    const int c = plan.block_to_matrix.at(pairs[p]);
+    const int rows = e.count(lam), cols = e.count(mu);
+    for (int r0 = 0; r0 < rows; r0 += kTile)
+      lw.tasks.push_back(SampleTask{e.start(lam) + r0, off + r0, std::min(kTile, rows - r0), c, rows, cols});
+    blocks.push_back(SampleBlock{lam, c, off, cols});
+    if (e.op.is_callback())
+      for (int i = 0; i < rows; ++i) cb[size_t(c)].push_back(GatherRow{off + i, int(e.start(lam) + i), rows, cols, 0});
     std::int64_t nnz = 0;
     for (std::int64_t q = lw.pay_off[size_t(c)]; q < lw.pay_off[size_t(c) + 1]; ++q)
       nnz += e.count(lw.pay_box[size_t(q)]);
     lw.evals += double(rows) * double(nnz);
-    lw.total += std::int64_t(rows) * lw.w;
   }
+  if (e.op.is_callback()) {
+    lw.cb_off.assign(size_t(lw.nc) + 1, 0);
+    for (int c = 0; c < lw.nc; ++c) {
+      lw.cb_rows.insert(lw.cb_rows.end(), cb[size_t(c)].begin(), cb[size_t(c)].end());
+      lw.cb_off[size_t(c) + 1] = std::int64_t(lw.cb_rows.size());
+    }
+  }
+  (void)o;
   lap("tasks");
   if (tree.depth() >= 2) {
     lw.peel = plan_peel(e, rep, blocks, color_boxes, tree.depth(), lw.w, false);
@@ -355,7 +573,9 @@ struct ApplyStage {
   DevBuf<std::int64_t> d_step_off, d_pb_off;
   DevBuf<double> xstep;
   DevBuf<int> d_step_color, d_pb_box;
-  std::vector<DevBuf<K2Task>> d_tasks;
+  DevBuf<K2Task> d_tasks;
+  DevBuf<GatherRow> d_cb_rows;
+  DevBuf<double> omega, yprod;
 
   explicit ApplyStage(cudaStream_t st) : s(st) {
     HP_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -390,17 +610,68 @@ std::string RunReport::to_csv() const {
 }
 
 void export_sizes(const BoxTree& tree, int rank, std::int64_t* factor_doubles,
-                  std::int64_t* dense_doubles) {
+                  std::int64_t* dense_doubles, int world, int shard) {
   const AdjacencyInfo adj = adjacency(tree);
-  std::int64_t f = 0, d = 0;
-  for (int l = 2; l <= tree.depth(); ++l)
-    for (auto [a, b] : admissible_pairs(tree, adj, l))
-      f += std::int64_t(tree.box(a).points.size() + tree.box(b).points.size()) * rank +
-           std::int64_t(rank) * rank;
-  const std::int64_t w = tree.max_leaf_size();
-  for (auto [lam, mu] : dense_pairs(tree, adj)) d += std::int64_t(tree.box(lam).points.size()) * w;
-  if (factor_doubles) *factor_doubles = f;
-  if (dense_doubles) *dense_doubles = d;
+  const TreeLayout lay = tree_layout(tree);
+  const Ownership o = make_ownership(tree, lay, world, shard);
+  const ArenaLayout L = arena_layout(tree, adj, o, rank);
+  if (factor_doubles) *factor_doubles = L.factors;
+  if (dense_doubles) *dense_doubles = L.dense;
+}
+
+void shard_memory_plan(const BoxTree& tree, int rank, int oversample, int world, double* out) {
+  const AdjacencyInfo adj = adjacency(tree);
+  const TreeLayout lay = tree_layout(tree);
+  const std::int64_t n = tree.num_points();
+  const int r = rank + oversample;
+  for (int g = 0; g < world; ++g) {
+    const Ownership o = make_ownership(tree, lay, world, g);
+    const ArenaLayout L = arena_layout(tree, adj, o, rank);
+    // largest level: own sample blocks (|I_a| x 2r) + the apply stage's
+    // color-ordered payload / coordinate / digit copies (~ N rows each) and
+    // the two payload buffers (N x 2r)
+    double level_max = 0.0;
+    // levels overlap (two stages alive) only on the int8 K2 path (r <= 48)
+    const double stages = k2i8::group_split(k2i8::padded_width(r)) ? 2.0 : 1.0;
+    for (int l = 2; l <= tree.depth(); ++l) {
+      const auto& ld = L.levels[size_t(l)];
+      double rows = 0.0, solve = 0.0;
+      for (auto [a, b] : ld.pairs)
+        if (o.replicated(l) || o.mine(a)) {
+          rows += double(tree.box(a).points.size());
+          solve += 1.0;
+        }
+      if (o.replicated(l)) solve /= world;
+      const double samples = rows * 2 * r * 8.0;
+      const double stage = double(n) * (2 * r * 8.0 + 3 * 8.0 + 7.0 * k2i8::padded_width(r) / 2.0);
+      // grams (middle, G'^T U, V^T G) and their row-chunk partials
+      const double grams = solve * (double(r) * r + 2.0 * r * rank) * 8.0 * 2.0;
+      level_max = std::max(level_max, stages * (samples + stage) + grams);
+    }
+    const double factors = double(L.factors) * 8.0, dense = double(L.dense) * 8.0;
+    const double fixed = 2.0 * double(n) * 2 * r * 8.0 + double(n) * 4 * 8.0;  // payload buffers, coordinates
+    out[g * 4 + 0] = factors;
+    out[g * 4 + 1] = dense;
+    out[g * 4 + 2] = level_max;
+    out[g * 4 + 3] = factors + dense + level_max + fixed;
+  }
+}
+
+void shard_exchange_counts(const BoxTree& tree, int rank, int world, int shard, int level, int phase,
+                           std::int64_t* send, std::int64_t* recv) {
+  if (level < 2 || level > tree.depth()) throw std::invalid_argument("level out of range");
+  const AdjacencyInfo adj = adjacency(tree);
+  const TreeLayout lay = tree_layout(tree);
+  const Ownership o = make_ownership(tree, lay, world, shard);
+  const ArenaLayout L = arena_layout(tree, adj, o, rank);
+  const auto& ld = L.levels[size_t(level)];
+  for (int j = 0; j < world; ++j) send[j] = recv[j] = 0;
+  if (world == 1 || o.replicated(level) || ld.pairs.empty()) return;
+  const Exchange X = make_exchange(ld, o, tree, rank, phase == 1);
+  for (int j = 0; j < world; ++j) {
+    send[j] = X.soff[size_t(j) + 1] - X.soff[size_t(j)];
+    recv[j] = X.roff[size_t(j) + 1] - X.roff[size_t(j)];
+  }
 }
 
 namespace {
@@ -473,6 +744,18 @@ class Exporter {
   std::vector<Deferred> deferred_;
 };
 
+/// Memory high-water of this thread's compress (RunReport::peak_device_bytes).
+class TrackScope {
+ public:
+  TrackScope() : prev_(MemTracker::current()) { MemTracker::current() = &t_; }
+  ~TrackScope() { MemTracker::current() = prev_; }
+  MemTracker& get() { return t_; }
+
+ private:
+  MemTracker t_;
+  MemTracker* prev_;
+};
+
 }  // namespace
 
 PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tree,
@@ -485,16 +768,23 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     throw std::invalid_argument("only format h1 is on the device hot path");
   if (config.strategy != ColoringStrategy::kGraph)
     throw std::invalid_argument("only the graph coloring strategy is on the device hot path");
-  if (op.kind() != kOpDense && op.dim() != tree->dim())
+  if (op.kind() != kOpDense && !op.is_callback() && op.dim() != tree->dim())
     throw std::invalid_argument("operator and tree dimensions differ");
+  if (config.comm && config.comm->device() != op.device())
+    throw std::invalid_argument("communicator and operator on different devices");
   const int r = config.sample_width();
   const int k = config.rank;
   if (2 * r > 160) throw std::invalid_argument("sample width k + p > 80 is not supported");
+  if (k > 64) throw std::invalid_argument("rank k > 64 is not supported");
 
   DeviceGuard guard(op.device());
+  TrackScope track;
   const auto t_begin = Clock::now();
   auto adj = std::make_shared<const AdjacencyInfo>(adjacency(*tree));
   auto lay = std::make_shared<const TreeLayout>(tree_layout(*tree));
+  const int world = config.comm ? config.comm->world() : 1;
+  const int my_rank = config.comm ? config.comm->rank() : 0;
+  const Ownership own = make_ownership(*tree, *lay, world, my_rank);
 
   // s: uploads, peel / QR / B and the leaf phase (high priority: it gates the
   // next level's stage); sa: K1 + K2 of the level ahead (ApplyStage)
@@ -513,7 +803,9 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
   rep->layout = lay;
   rep->rank = k;
   rep->device = op.device();
-  rep->levels.resize(size_t(tree->depth()) + 1);
+  rep->world = world;
+  rep->shard_rank = my_rank;
+  if (world > 1) rep->box_owner = own.owner;
   RunReport& report = result.report;
   int* h_ranks = nullptr;
 
@@ -527,57 +819,30 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     e.k = k;
     const Index n = tree->num_points();
 
-    // Factor arena: U (|I_a| x k), V (|I_b| x k), B (k x k) per pair, all levels.
-    std::int64_t ftotal = 0, rank_total = 0;
-    for (int l = 2; l <= tree->depth(); ++l) {
-      auto& ld = rep->levels[size_t(l)];
-      ld.pairs = admissible_pairs(*tree, *adj, l);
-      const size_t np = ld.pairs.size();
-      ld.uoff.resize(np);
-      ld.voff.resize(np);
-      ld.boff.resize(np);
-      ld.ku.assign(np, 0);
-      ld.kv.assign(np, 0);
-      for (size_t p = 0; p < np; ++p) {
-        ld.uoff[p] = ftotal;
-        ftotal += std::int64_t(e.count(ld.pairs[p].first)) * k;
-        ld.voff[p] = ftotal;
-        ftotal += std::int64_t(e.count(ld.pairs[p].second)) * k;
-        ld.boff[p] = ftotal;
-        ftotal += std::int64_t(k) * k;
-      }
-      rank_total += 2 * std::int64_t(np);
+    // Factor arena: U (|I_a| x k), V (|I_b| x k), B (k x k) per held pair.
+    {
+      ArenaLayout L = arena_layout(*tree, *adj, own, k);
+      rep->levels = std::move(L.levels);
+      rep->factor_doubles = L.factors;
+      rep->dense.pairs = std::move(L.dense_pairs);
+      rep->dense.off = std::move(L.dense_off);
+      rep->dense_doubles = L.dense;
     }
-    rep->factor_doubles = ftotal;
+    std::int64_t rank_total = 0;
+    for (int l = 2; l <= tree->depth(); ++l) rank_total += 2 * std::int64_t(rep->levels[size_t(l)].pairs.size());
     // stream-ordered from the retained device pool: repeated compress() calls reuse the memory
-    HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_factors), size_t(std::max<std::int64_t>(ftotal, 1)) * 8, s));
+    HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_factors),
+                            size_t(std::max<std::int64_t>(rep->factor_doubles, 1)) * 8, s));
+    MemTracker::add(std::max<std::int64_t>(rep->factor_doubles, 1) * 8);
     h_ranks = static_cast<int*>(persistent_pinned(size_t(std::max<std::int64_t>(rank_total, 1)) * sizeof(int), 0));
 
     // Host plans of every level and of the leaf phase, built concurrently.
     std::vector<std::future<LevelWork>> futs(size_t(tree->depth()) + 1);
     for (int l = 2; l <= tree->depth(); ++l)
       futs[size_t(l)] = std::async(std::launch::async, build_level, std::cref(e), std::cref(*rep), l,
-                                   std::cref(config));
-    auto leaf_fut = std::async(std::launch::async, build_leaf, std::cref(e), std::cref(*rep),
-                               std::cref(config));
-
-    // Sharding: ranks launch K2/K6 for contiguous work-balanced
-    // ranges and broadcast their rows; emulate_shards splits the launches the
-    // same way inside one process (tests).
-    const int world = config.comm ? config.comm->world() : std::max(1, config.emulate_shards);
-    const int my_rank = config.comm ? config.comm->rank() : -1;
-    auto shard_tasks = [&](const std::vector<SampleTask>& tasks, const std::vector<double>& work,
-                           const std::vector<std::int64_t>& item_off, std::vector<std::int64_t>& seg) {
-      const auto b = partition_ranges(work, world);
-      seg.assign(size_t(world) + 1, 0);
-      for (int q = 0; q <= world; ++q) seg[size_t(q)] = item_off[size_t(b[size_t(q)])];
-      std::vector<std::vector<SampleTask>> lists(static_cast<size_t>(world));
-      for (const SampleTask& t : tasks) {
-        const int q = int(std::upper_bound(seg.begin(), seg.end(), t.out) - seg.begin()) - 1;
-        lists[size_t(std::min(std::max(q, 0), world - 1))].push_back(t);
-      }
-      return lists;
-    };
+                                   std::cref(config), std::cref(own));
+    auto leaf_fut = std::async(std::launch::async, build_leaf, std::cref(e), std::cref(*rep), std::cref(config),
+                               std::cref(own));
 
     const int gld = 2 * r;
     // payload Gaussians of two levels: K1 of level l + 1 (apply stream) runs
@@ -594,6 +859,9 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     std::vector<double> wait_ms(size_t(tree->depth()) + 1, 0.0);
     report.setup_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_begin).count();
 
+    const bool int8_ok = op.kind() != kOpDense && !op.is_callback() && op.symmetric() &&
+                         k2i8::group_split(k2i8::padded_width(r)) && k2_mode() == 0 && k2_int8_enabled();
+
     // K1 + K2 of level l: uploads on s, launches on sa after `ready`
     auto issue_apply = [&](int l) {
       auto st = std::make_unique<ApplyStage>(s);
@@ -603,7 +871,6 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       LevelWork& w = st->w;
       if (w.empty) return st;  // proj/src/peeling.cpp:221 (built_level not advanced)
       if (!w.symmetric) throw std::logic_error("asymmetric admissibility structure");
-      const size_t np = w.np;
       st->tm = std::make_unique<LevelTimers>();
       LevelTimers* tm = st->tm.get();
       colors[size_t(l)] = w.nc;
@@ -614,12 +881,39 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
 
       st->d_pos_box.upload(w.pos_box, s);
       st->d_local.upload(w.local, s);
-      st->d_rowtab.upload(w.rowtab, s);
       st->d_pay_off.upload(w.pay_off, s);
       st->d_pay_pos.upload(w.pay_pos, s);
-      st->samples.alloc(size_t(w.soff[np]), s);
-      // payload rows and coordinates in color order (contiguous K2 chunks)
+      st->samples.alloc(size_t(w.soff.back()), s);
       const std::int64_t nnz = std::int64_t(w.pay_pos.size());
+      if (op.is_callback()) {
+        st->d_cb_rows.upload(w.cb_rows, s);
+        st->omega.alloc(size_t(n) * size_t(r), s);
+        st->yprod.alloc(size_t(n) * size_t(r), s);
+        HP_CUDA(cudaEventRecord(st->ready, s));
+        HP_CUDA(cudaStreamWaitEvent(sa, st->ready, 0));
+        launch_payload_gaussian(g, gld, r, n, st->d_pos_box.get(), st->d_local.get(), config.seed, l, sa);
+        HP_CUDA(cudaEventRecord(tm->apply.a, sa));
+        // residual_samples (proj/src/peeling.cpp:165-177): per color, realize
+        // the dense test matrix, apply the black box, keep the rows read back
+        for (int side = 0; side < 2; ++side) {
+          for (int c = 0; c < w.nc; ++c) {
+            const std::int64_t q0 = w.pay_off[size_t(c)], q1 = w.pay_off[size_t(c) + 1];
+            if (q1 == q0) continue;  // empty payload: no apply (peeling.cpp:166)
+            HP_CUDA(cudaMemsetAsync(st->omega.get(), 0, size_t(n) * size_t(r) * 8, sa));
+            launch_scatter_payload(g, gld, side * r, r, st->d_pay_pos.get() + q0, q1 - q0, e.d_perm.get(),
+                                   st->omega.get(), n, sa);
+            op.call(side == 1, st->omega.get(), r, st->yprod.get(), sa);
+            launch_gather_sample_rows(st->yprod.get(), n, e.d_perm.get(), st->d_cb_rows.get() + w.cb_off[size_t(c)],
+                                      w.cb_off[size_t(c) + 1] - w.cb_off[size_t(c)], r, st->samples.get(),
+                                      side * r, sa);
+          }
+        }
+        HP_CUDA(cudaEventRecord(tm->apply.b, sa));
+        HP_CUDA(cudaEventRecord(st->done, sa));
+        return st;
+      }
+      st->d_rowtab.upload(w.rowtab, s);
+      // payload rows and coordinates in color order (contiguous K2 chunks)
       st->gcol.alloc(size_t(nnz) * size_t(gld), s);
       st->xcol.alloc(op.kind() == kOpDense ? 1 : size_t(nnz) * size_t(op.dim()), s);
       const bool checked = w.k2_checked || e.has_dups;
@@ -628,8 +922,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       // column-split int8 kernel is no faster than DMMA (config 4 scaled:
       // 1.74 s both) and its sample error (5e-13) sits closest to the 1e-12
       // bar, so those widths keep FP64 DMMA.
-      const bool use_i8 = op.kind() != kOpDense && op.symmetric() && !checked &&
-                          k2i8::group_split(k2i8::padded_width(r)) && k2_mode() == 0 && k2_int8_enabled();
+      const bool use_i8 = int8_ok && !checked;
       st->use_i8 = use_i8;
       apply_path[size_t(l)] = use_i8 ? 1 : 0;
       std::int64_t half_stride = 0, tsteps = 0;
@@ -644,52 +937,43 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         st->xstep.alloc(size_t(std::max<std::int64_t>(tsteps, 1)) * 32 * size_t(op.dim()), s);
         e.ensure_box_bbox();  // on s, before `ready`
       }
-      st->d_tasks.reserve(w.k2.size());
-      for (int sr = 0; sr < int(w.k2.size()); ++sr) {
-        st->d_tasks.emplace_back();
-        if (my_rank >= 0 && sr != my_rank) continue;
-        st->d_tasks.back().upload(w.k2[size_t(sr)], s);
-      }
+      st->d_tasks.upload(w.k2, s);
       HP_CUDA(cudaEventRecord(st->ready, s));
       HP_CUDA(cudaStreamWaitEvent(sa, st->ready, 0));
 
       // K1 payload
       launch_payload_gaussian(g, gld, r, n, st->d_pos_box.get(), st->d_local.get(), config.seed, l, sa);
-      // K2 apply (forward + adjoint samples of every pair's row block); each
-      // shard launches its own tiles, then the shards' rows are broadcast
+      // K2 apply (forward + adjoint samples of this rank's row blocks)
       HP_CUDA(cudaEventRecord(tm->apply.a, sa));
       launch_permute_rows(g, gld, 1, st->d_pay_pos.get(), nnz, gld, st->gcol.get(), gld, 1, sa);
       if (op.kind() != kOpDense)
         launch_permute_rows(e.dop.x, 1, n, st->d_pay_pos.get(), nnz, op.dim(), st->xcol.get(), 1, nnz, sa);
       if (use_i8) {
         // group split: the CTA pair adds two partial sums per sample element
-        HP_CUDA(cudaMemsetAsync(st->samples.get(), 0, size_t(w.soff[np]) * sizeof(double), sa));
+        HP_CUDA(cudaMemsetAsync(st->samples.get(), 0, size_t(w.soff.back()) * sizeof(double), sa));
         k2i8::launch_payload_digits(st->gcol.get(), gld, r, st->d_pay_off.get(), st->d_step_off.get(),
                                     st->d_step_color.get(), tsteps, st->bdig.get(), half_stride, sa);
         k2i8::launch_step_coords(st->xcol.get(), nnz, op.dim(), st->d_pay_off.get(), st->d_step_off.get(),
                                  st->d_step_color.get(), tsteps, st->xstep.get(), sa);
       }
-      for (int sr = 0; sr < int(w.k2.size()); ++sr) {
-        if (my_rank >= 0 && sr != my_rank) continue;
-        const K2Task* tasks = st->d_tasks[size_t(sr)].get();
-        const int nt = int(w.k2[size_t(sr)].size());
-        if (use_i8) {
-          k2i8::launch_sample_apply_i8(e.dop, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
-                                       st->d_step_off.get(), st->xstep.get(), st->d_pb_off.get(),
-                                       st->d_pb_box.get(), e.d_box_bbox.get(), st->bdig.get(), half_stride, r,
-                                       st->samples.get(), sa);
-        } else if (op.symmetric()) {
-          launch_sample_apply(e.dop, false, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
-                              st->d_pay_pos.get(), st->gcol.get(), gld, 0, 2 * r, st->xcol.get(), nnz,
-                              st->samples.get(), 0, checked, sa);
-        } else {
-          launch_sample_apply(e.dop, false, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
-                              st->d_pay_pos.get(), st->gcol.get(), gld, 0, r, st->xcol.get(), nnz,
-                              st->samples.get(), 0, checked, sa);
-          launch_sample_apply(e.dop, true, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
-                              st->d_pay_pos.get(), st->gcol.get(), gld, r, r, st->xcol.get(), nnz,
-                              st->samples.get(), r, checked, sa);
-        }
+      const K2Task* tasks = st->d_tasks.get();
+      const int nt = int(w.k2.size());
+      if (use_i8) {
+        k2i8::launch_sample_apply_i8(e.dop, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                                     st->d_step_off.get(), st->xstep.get(), st->d_pb_off.get(),
+                                     st->d_pb_box.get(), e.d_box_bbox.get(), st->bdig.get(), half_stride, r,
+                                     st->samples.get(), sa);
+      } else if (op.symmetric()) {
+        launch_sample_apply(e.dop, false, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                            st->d_pay_pos.get(), st->gcol.get(), gld, 0, 2 * r, st->xcol.get(), nnz,
+                            st->samples.get(), 0, checked, sa);
+      } else {
+        launch_sample_apply(e.dop, false, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                            st->d_pay_pos.get(), st->gcol.get(), gld, 0, r, st->xcol.get(), nnz,
+                            st->samples.get(), 0, checked, sa);
+        launch_sample_apply(e.dop, true, tasks, st->d_rowtab.get(), nt, st->d_pay_off.get(),
+                            st->d_pay_pos.get(), st->gcol.get(), gld, r, r, st->xcol.get(), nnz,
+                            st->samples.get(), r, checked, sa);
       }
       HP_CUDA(cudaEventRecord(tm->apply.b, sa));
       HP_CUDA(cudaEventRecord(st->done, sa));
@@ -700,11 +984,10 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     // Overlap only pays when K2 runs on the int8 tensor cores: the FP64 DMMA
     // K2 and the peel / QR / B kernels share the FP64 datapath, and there the
     // overlapped order measured slower (config 5 scaled 3.12 s vs 3.02 s
-    // serialized; config 4 scaled 3.767 vs 3.757 s).
+    // serialized; config 4 scaled 3.767 vs 3.757 s). A callback black box
+    // runs serialized (the caller's apply is synchronous).
     const char* serial_env = std::getenv("HP_SERIAL_LEVELS");
-    const bool k2_on_int8 = op.kind() != kOpDense && op.symmetric() &&
-                            k2i8::group_split(k2i8::padded_width(r)) && k2_mode() == 0 && k2_int8_enabled();
-    const bool serial = serial_env ? std::atoi(serial_env) != 0 : !k2_on_int8;
+    const bool serial = op.is_callback() || (serial_env ? std::atoi(serial_env) != 0 : !int8_ok);
     std::unique_ptr<ApplyStage> next;
     if (tree->depth() >= 2) next = issue_apply(2);
     for (int l = 2; l <= tree->depth(); ++l) {
@@ -723,7 +1006,10 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         double* g = gbuf[l & 1].get();
         double* samples = cur->samples.get();
         HP_CUDA(cudaStreamWaitEvent(s, cur->done, 0));
-        if (config.comm) config.comm->broadcast_segments(samples, w.seg, s);
+        if (w.replicated) {
+          config.comm->broadcast_segments(samples, w.seg, s);
+          report.exchange_bytes += double(w.seg[size_t(my_rank) + 1] - w.seg[size_t(my_rank)]) * 8.0 * (world - 1);
+        }
 
         // K3 peel
         HP_CUDA(cudaEventRecord(tm->peel.a, s));
@@ -732,65 +1018,59 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
 
         if (config.capture_samples) {
           HP_CUDA(cudaStreamSynchronize(s));
-          std::vector<Matrix> cap;
-          for (size_t p = 0; p < np; ++p) {
-            const int rows = e.count(ld.pairs[p].first);
+          std::vector<Matrix> cap(np);
+          for (size_t i = 0; i < w.own.size(); ++i) {
+            const int p = w.own[i];
+            const int rows = e.count(ld.pairs[size_t(p)].first);
             Matrix m(rows, 2 * r);
-            HP_CUDA(cudaMemcpy(m.data(), samples + w.soff[p], size_t(rows) * 2 * r * 8,
-                               cudaMemcpyDeviceToHost));
-            cap.push_back(std::move(m));
+            HP_CUDA(cudaMemcpy(m.data(), samples + w.soff[i], size_t(rows) * 2 * r * 8, cudaMemcpyDeviceToHost));
+            cap[size_t(p)] = std::move(m);
           }
           rep->captured[l] = std::move(cap);
         }
 
         // K5a: middle = G'_a^T Y_p before the QR overwrites Y; K4 QR; K5b grams
-        // and B -- each shard on its own pairs, then the shards' factor and
-        // rank segments are broadcast
-        DevBuf<double> middle(np * size_t(r) * size_t(r), s), gpu(np * size_t(r) * size_t(k), s),
-            vg(np * size_t(k) * size_t(r), s);
+        // and B (DESIGN.md §7 for the sharded variants)
+        const size_t ns = w.solve.size();
+        DevBuf<double> middle(ns * size_t(r) * size_t(r), s), gpu(ns * size_t(r) * size_t(k), s),
+            vg(ns * size_t(k) * size_t(r), s);
         DevBuf<int> d_ranks(2 * np, s);
         DevBuf<std::int64_t> d_boff;
-        d_boff.upload(ld.boff, s);
-        auto mine = [&](int sr) { return my_rank < 0 || sr == my_rank; };
+        d_boff.upload(w.solve_boff, s);
         HP_CUDA(cudaEventRecord(tm->mid.a, s));
-        for (int sr = 0; sr < int(w.s45.size()); ++sr)
-          if (mine(sr))
-            run_gram(w.s45[size_t(sr)].g_mid, g, samples, middle.get() + w.s45[size_t(sr)].p0 * r * r, s);
+        run_gram(w.g_mid, g, samples, middle.get(), s);
         HP_CUDA(cudaEventRecord(tm->mid.b, s));
         HP_CUDA(cudaEventRecord(tm->qr.a, s));
-        for (int sr = 0; sr < int(w.s45.size()); ++sr)
-          if (mine(sr)) run_qr(w.s45[size_t(sr)].qr, samples, rep->d_factors, d_ranks.get(), r, k, s);
+        run_qr(w.qr, samples, rep->d_factors, d_ranks.get(), r, k, s);
         HP_CUDA(cudaEventRecord(tm->qr.b, s));
         HP_CUDA(cudaEventRecord(tm->bsolve.a, s));
-        for (int sr = 0; sr < int(w.s45.size()); ++sr) {
-          if (!mine(sr)) continue;
-          const LevelWork::Shard45& sh = w.s45[size_t(sr)];
-          run_gram(sh.g_gpu, g, rep->d_factors, gpu.get() + sh.p0 * r * k, s);
-          run_gram(sh.g_vg, rep->d_factors, g, vg.get() + sh.p0 * k * r, s);
-          launch_bsolve(int(sh.p1 - sh.p0), gpu.get() + sh.p0 * r * k, middle.get() + sh.p0 * r * r,
-                        vg.get() + sh.p0 * k * r, r, k, kPinvCutoff, d_boff.get() + sh.p0, rep->d_factors, s);
-        }
-        if (config.comm && np > 0) {
-          const std::int64_t fend = ld.boff[np - 1] + std::int64_t(k) * k;
-          std::vector<std::int64_t> fseg(w.fb.size()), useg(w.fb.size()), vseg(w.fb.size());
-          for (size_t q = 0; q < w.fb.size(); ++q) {
-            const std::int64_t p = w.fb[q];
-            fseg[q] = p < std::int64_t(np) ? ld.uoff[size_t(p)] : fend;
-            useg[q] = p;
-            vseg[q] = std::int64_t(np) + p;
-          }
-          config.comm->broadcast_segments(rep->d_factors, fseg, s);
-          config.comm->broadcast_segments_i32(d_ranks.get(), useg, s);
-          config.comm->broadcast_segments_i32(d_ranks.get(), vseg, s);
+        if (!w.replicated && world > 1)  // V of crossing pairs to their row owner
+          report.exchange_bytes += run_exchange(w.x1, *config.comm, rep->d_factors, d_ranks.get(), s);
+        run_gram(w.g_gpu, g, rep->d_factors, gpu.get(), s);
+        run_gram(w.g_vg, rep->d_factors, g, vg.get(), s);
+        launch_bsolve(int(ns), gpu.get(), middle.get(), vg.get(), r, k, kPinvCutoff, d_boff.get(), rep->d_factors, s);
+        if (w.replicated) {
+          config.comm->broadcast_segments(rep->d_factors, w.fseg, s);
+          config.comm->broadcast_segments_i32(d_ranks.get(), w.useg, s);
+          config.comm->broadcast_segments_i32(d_ranks.get(), w.vseg, s);
+          report.exchange_bytes += double(w.fseg[size_t(my_rank) + 1] - w.fseg[size_t(my_rank)]) * 8.0 * (world - 1);
+        } else if (world > 1) {  // U and B of crossing pairs to their column owner
+          report.exchange_bytes += run_exchange(w.x2, *config.comm, rep->d_factors, d_ranks.get(), s);
         }
         HP_CUDA(cudaEventRecord(tm->bsolve.b, s));
         HP_CUDA(cudaMemcpyAsync(h_ranks + roff, d_ranks.get(), 2 * np * sizeof(int), cudaMemcpyDeviceToHost, s));
         rank_off[size_t(l)] = roff;
         roff += 2 * std::int64_t(np);
         timers[size_t(l)] = std::move(cur->tm);
-        if (exporter.active() && np > 0) {  // this level's U, V, B are final
-          const std::int64_t f0 = ld.uoff[0], f1 = ld.boff[np - 1] + std::int64_t(k) * k;
-          exporter.copy(exporter.factors() ? exporter.factors() + f0 : nullptr, rep->d_factors + f0, f1 - f0, s);
+        if (exporter.active()) {  // this level's U, V, B are final
+          std::int64_t f0 = -1, f1 = -1;
+          for (size_t p = 0; p < np; ++p)
+            if (ld.uoff[p] >= 0) {
+              if (f0 < 0) f0 = ld.uoff[p];
+              f1 = ld.boff[p] + std::int64_t(k) * k;
+            }
+          if (f0 >= 0)
+            exporter.copy(exporter.factors() ? exporter.factors() + f0 : nullptr, rep->d_factors + f0, f1 - f0, s);
         }
         built = l;
       }
@@ -803,59 +1083,54 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     const auto t_leaf_wait = Clock::now();
     LeafWork lw = leaf_fut.get();
     const double leaf_wait_ms = std::chrono::duration<double, std::milli>(Clock::now() - t_leaf_wait).count();
-    rep->dense.pairs = lw.pairs;
-    rep->dense.off = lw.off;
-    rep->dense_doubles = lw.total;
-    HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_dense), size_t(std::max<std::int64_t>(lw.total, 1)) * 8, s));
+    HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&rep->d_dense),
+                            size_t(std::max<std::int64_t>(rep->dense_doubles, 1)) * 8, s));
+    MemTracker::add(std::max<std::int64_t>(rep->dense_doubles, 1) * 8);
     Events leaf_apply, leaf_peel;
     {
-      std::vector<double> dwork(lw.pairs.size());
-      std::vector<std::int64_t> doff(lw.off);
-      doff.push_back(lw.total);
-      for (size_t p = 0; p < lw.pairs.size(); ++p)
-        dwork[p] = double(e.count(lw.pairs[p].first)) * double(lw.w);
-      std::vector<std::int64_t> seg;
-      const auto lists = shard_tasks(lw.tasks, dwork, doff, seg);
       DevBuf<std::int64_t> d_pay_off;
       d_pay_off.upload(lw.pay_off, s);
       DevBuf<int> d_pay_box;
       d_pay_box.upload(lw.pay_box, s);
+      DevBuf<SampleTask> d_tasks;
+      d_tasks.upload(lw.tasks, s);
       HP_CUDA(cudaEventRecord(leaf_apply.a, s));
-      for (int sr = 0; sr < int(lists.size()); ++sr) {
-        if (my_rank >= 0 && sr != my_rank) continue;
-        DevBuf<SampleTask> d_tasks;
-        d_tasks.upload(lists[size_t(sr)], s);
-        launch_identity_apply(e.dop, d_tasks.get(), int(lists[size_t(sr)].size()), d_pay_off.get(),
-                              d_pay_box.get(), e.d_box_start.get(), e.d_box_count.get(), lw.w,
-                              rep->d_dense, s);
+      if (op.is_callback()) {
+        // extract_leaf (proj/src/peeling.cpp:490-524): identity probes per color
+        DevBuf<GatherRow> d_rows;
+        d_rows.upload(lw.cb_rows, s);
+        DevBuf<double> om(size_t(n) * size_t(lw.w), s), yp(size_t(n) * size_t(lw.w), s);
+        for (int c = 0; c < lw.nc; ++c) {
+          const std::int64_t q0 = lw.pay_off[size_t(c)], q1 = lw.pay_off[size_t(c) + 1];
+          if (q1 == q0) continue;
+          HP_CUDA(cudaMemsetAsync(om.get(), 0, size_t(n) * size_t(lw.w) * 8, s));
+          launch_scatter_identity(d_pay_box.get() + q0, int(q1 - q0), e.d_box_start.get(), e.d_box_count.get(),
+                                  e.d_perm.get(), lw.w, om.get(), n, s);
+          op.call(false, om.get(), lw.w, yp.get(), s);
+          launch_gather_sample_rows(yp.get(), n, e.d_perm.get(), d_rows.get() + lw.cb_off[size_t(c)],
+                                    lw.cb_off[size_t(c) + 1] - lw.cb_off[size_t(c)], lw.w, rep->d_dense, 0, s);
+        }
+      } else {
+        launch_identity_apply(e.dop, d_tasks.get(), int(lw.tasks.size()), d_pay_off.get(), d_pay_box.get(),
+                              e.d_box_start.get(), e.d_box_count.get(), lw.w, rep->d_dense, s);
       }
       HP_CUDA(cudaEventRecord(leaf_apply.b, s));
       HP_CUDA(cudaEventRecord(leaf_peel.a, s));
-      if (lw.has_peel) {
-        if (my_rank >= 0) {
-          // peel this rank's dense blocks only, then share them
-          PeelPlan mine = lw.peel;
-          const std::int64_t lo = seg[size_t(my_rank)], hi = seg[size_t(my_rank) + 1];
-          mine.tasks_fwd.erase(std::remove_if(mine.tasks_fwd.begin(), mine.tasks_fwd.end(),
-                                              [&](const PeelTask& t) { return t.out < lo || t.out >= hi; }),
-                               mine.tasks_fwd.end());
-          run_peel(mine, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
-        } else {
-          run_peel(lw.peel, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
-        }
-      }
-      if (config.comm) config.comm->broadcast_segments(rep->d_dense, seg, s);
+      if (lw.has_peel) run_peel(lw.peel, e, *rep, nullptr, 0, lw.w, true, rep->d_dense, 0, s);
       HP_CUDA(cudaEventRecord(leaf_peel.b, s));
-      if (exporter.active()) exporter.copy(exporter.dense(), rep->d_dense, lw.total, s);
+      if (exporter.active()) exporter.copy(exporter.dense(), rep->d_dense, rep->dense_doubles, s);
     }
     exporter.finish(s);
     HP_CUDA(cudaStreamSynchronize(s));
     if (config.capture_samples) {
-      for (size_t p = 0; p < lw.pairs.size(); ++p) {
-        const int rows = e.count(lw.pairs[p].first);
-        Matrix m(rows, lw.w);
-        HP_CUDA(cudaMemcpy(m.data(), rep->d_dense + lw.off[p], size_t(rows) * lw.w * 8, cudaMemcpyDeviceToHost));
-        rep->captured_leaf.push_back(std::move(m));
+      rep->captured_leaf.assign(rep->dense.pairs.size(), Matrix());
+      for (size_t p = 0; p < rep->dense.pairs.size(); ++p) {
+        if (rep->dense.off[p] < 0) continue;
+        const int rows = e.count(rep->dense.pairs[p].first), cols = e.count(rep->dense.pairs[p].second);
+        Matrix m(rows, cols);
+        HP_CUDA(cudaMemcpy(m.data(), rep->d_dense + rep->dense.off[p], size_t(rows) * cols * 8,
+                           cudaMemcpyDeviceToHost));
+        rep->captured_leaf[p] = std::move(m);
       }
     }
     rep->dense_ready = true;
@@ -870,6 +1145,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       if (!timers[size_t(l)]) continue;
       const size_t np = ld.pairs.size();
       for (size_t p = 0; p < np; ++p) {
+        if (ld.uoff[p] < 0) continue;
         ld.ku[p] = h_ranks[rank_off[size_t(l)] + std::int64_t(p)];
         ld.kv[p] = h_ranks[rank_off[size_t(l)] + std::int64_t(np + p)];
       }
@@ -901,6 +1177,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
       if (l - 1 >= 2) ph.net_flops += 2 * std::int64_t(ph.colors) * truncated_apply_flops(*rep, l - 1, r, e);
       // QR (flops.hpp:18-20) and the B solve (peeling.cpp:262-268)
       for (size_t p = 0; p < ld.pairs.size(); ++p) {
+        if (!rep->counts_pair(l, int(p))) continue;
         const std::int64_t ma = e.count(ld.pairs[p].first), mb = e.count(ld.pairs[p].second);
         const std::int64_t ku = ld.ku[p], kv = ld.kv[p];
         ph.net_flops += 2 * ma * r * r + 2 * mb * r * r;
@@ -955,10 +1232,43 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     throw;
   }
   HP_CUDA(cudaStreamSynchronize(s));
+  report.peak_device_bytes = double(track.get().peak);
   cudaStreamDestroy(sa);
   cudaStreamDestroy(s);
   result.rep = rep;
   return result;
+}
+
+std::vector<PeelResult> compress_group(const DeviceOperator& op, std::shared_ptr<const BoxTree> tree,
+                                       const PeelConfig& config, int world) {
+  if (world < 1) throw std::invalid_argument("world size must be >= 1");
+  if (config.comm) throw std::invalid_argument("compress_group builds its own communicators");
+  auto group = std::make_shared<LocalGroup>(world);
+  std::vector<PeelResult> out(static_cast<size_t>(world));
+  std::exception_ptr first_err;
+  std::mutex err_mu;
+  std::vector<std::thread> threads;
+  for (int g = 0; g < world; ++g)
+    threads.emplace_back([&, g] {
+      try {
+        LocalComm comm(group, g, op.device());
+        PeelConfig cfg = config;
+        cfg.comm = &comm;
+        out[size_t(g)] = compress(op, tree, cfg);
+        // keep the communicator's events alive until every rank is done
+        group->barrier();
+      } catch (...) {
+        {
+          // the first failure is the cause; peers then fail in the aborted barrier
+          std::lock_guard<std::mutex> lock(err_mu);
+          if (!first_err) first_err = std::current_exception();
+        }
+        group->abort();
+      }
+    });
+  for (auto& t : threads) t.join();
+  if (first_err) std::rethrow_exception(first_err);
+  return out;
 }
 
 }  // namespace hpeel

@@ -104,8 +104,8 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
                const DeviceOperator& o, cudaStream_t st)
     : tree(t), adj(a), lay(l), op(o), s(st) {
   n = tree.num_points();
-  DevBuf<int> perm;
-  perm.upload(lay.perm, s);
+  d_perm.upload(lay.perm, s);
+  d_inv.upload(lay.inv, s);
   dop.kind = op.kind();
   dop.dim = op.dim();
   dop.n = n;
@@ -116,12 +116,12 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
     DevBuf<double> tmp(size_t(n) * size_t(n), s);
     at.alloc(size_t(n) * size_t(n), s);
     // rows then columns: at[s + t n] = a[perm[s] + perm[t] n]
-    launch_permute_rows(op.device_matrix(), 1, n, perm.get(), n, int(n), tmp.get(), 1, n, s);
-    launch_permute_rows(tmp.get(), n, 1, perm.get(), n, int(n), at.get(), n, 1, s);
+    launch_permute_rows(op.device_matrix(), 1, n, d_perm.get(), n, int(n), tmp.get(), 1, n, s);
+    launch_permute_rows(tmp.get(), n, 1, d_perm.get(), n, int(n), at.get(), n, 1, s);
     dop.a = at.get();
-  } else {
+  } else if (op.kind() != kOpCallback) {
     xt.alloc(size_t(op.dim()) * size_t(n), s);
-    launch_permute_rows(op.device_points(), 1, n, perm.get(), n, op.dim(), xt.get(), 1, n, s);
+    launch_permute_rows(op.device_points(), 1, n, d_perm.get(), n, op.dim(), xt.get(), 1, n, s);
     dop.x = xt.get();
   }
   d_box_start.upload(lay.start, s);
@@ -136,7 +136,7 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
   }
   int* h_flag = nullptr;
   DevBuf<int> d_flag;
-  if (op.kind() != kOpDense) {
+  if (op.kind() != kOpDense && op.kind() != kOpCallback) {
     // coincident points can only share a leaf
     std::vector<std::int64_t> ls, lc;
     for (const Box& b : tree.boxes())
@@ -158,6 +158,19 @@ Engine::Engine(const BoxTree& t, const AdjacencyInfo& a, const TreeLayout& l,
     has_dups = *h_flag != 0;
     // (persistent pinned buffer: not freed)
   }
+}
+
+void Engine::op_apply(bool adjoint, const double* x, int w, double* y) const {
+  if (w <= 0) return;
+  if (op.kind() != kOpCallback) {
+    launch_full_apply(dop, adjoint, x, w, y, s);
+    return;
+  }
+  // the caller's black box works in its own point order
+  DevBuf<double> xi(size_t(n) * size_t(w), s), yi(size_t(n) * size_t(w), s);
+  launch_permute_rows(x, 1, n, d_inv.get(), n, w, xi.get(), 1, n, s);
+  op.call(adjoint, xi.get(), w, yi.get(), s);
+  launch_permute_rows(yi.get(), 1, n, d_perm.get(), n, w, y, 1, n, s);
 }
 
 int pair_index(const std::vector<std::pair<int, int>>& pairs, int a, int b) {
@@ -379,6 +392,8 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
     const int src = side == 0 ? y : x;
     auto g = groups.find(Key{lp, src, c});
     if (g == groups.end()) return slot = -1;
+    if (ld.uoff[size_t(q)] < 0 || ld.voff[size_t(q)] < 0)
+      throw std::logic_error("peel: a coarse pair's factors are not held by this rank");
     CoeffTask t{};
     t.f = side == 0 ? ld.voff[size_t(q)] : ld.uoff[size_t(q)];
     t.btrans = side == 0 ? 0 : 1;
@@ -432,8 +447,9 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
     const int rows = e.count(a);
     for (int t0 = 0; t0 < rows; t0 += kTile) {
       const int trows = std::min(kTile, rows - t0);
-      PeelTask tf{sb.off + t0, trows, rows, int(pp.refs_fwd.size()), 0};
-      PeelTask ta{sb.off + t0, trows, rows, int(pp.refs_adj.size()), 0};
+      const int cols = std::min(sb.cols, w);
+      PeelTask tf{sb.off + t0, trows, rows, int(pp.refs_fwd.size()), 0, cols, 0};
+      PeelTask ta{sb.off + t0, trows, rows, int(pp.refs_adj.size()), 0, cols, 0};
       for (int lp = 2; lp <= std::min(la, top_level); ++lp) {
         const auto& ld = rep.levels[size_t(lp)];
         if (ld.pairs.empty()) continue;

@@ -57,6 +57,22 @@ class StagingScope {
   PinnedStaging staging_;
 };
 
+/// Device bytes held by the buffers of the calling thread's compress()
+/// (peak reported as RunReport::peak_device_bytes).
+struct MemTracker {
+  std::int64_t cur = 0, peak = 0;
+  static MemTracker*& current() {
+    thread_local MemTracker* t = nullptr;
+    return t;
+  }
+  static void add(std::int64_t b) {
+    if (MemTracker* t = current()) {
+      t->cur += b;
+      if (t->cur > t->peak) t->peak = t->cur;
+    }
+  }
+};
+
 template <class T>
 class DevBuf {
  public:
@@ -70,7 +86,10 @@ class DevBuf {
     release();
     n_ = n;
     s_ = s;
-    if (n) HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    if (n) {
+      HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+      MemTracker::add(std::int64_t(n * sizeof(T)));
+    }
   }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     alloc(v.size(), s);
@@ -85,7 +104,10 @@ class DevBuf {
     }
   }
   void release() {
-    if (p_) cudaFreeAsync(p_, s_);
+    if (p_) {
+      cudaFreeAsync(p_, s_);
+      MemTracker::add(-std::int64_t(n_ * sizeof(T)));
+    }
     p_ = nullptr;
     n_ = 0;
   }
@@ -149,6 +171,7 @@ struct Engine {
   DevBuf<double> at;  // tree-order dense matrix
   DevOp dop;
   DevBuf<std::int64_t> d_box_start, d_box_count;
+  DevBuf<int> d_perm, d_inv;  // tree position -> input index and back
   bool has_dups = false;  // kernel kinds: two distinct points share coordinates
   DevBuf<double> d_box_bbox;  // int8 K2: raw-coordinate bounding box per box (built on first use)
   std::vector<std::vector<int>> anc;  // anc[l][box] = ancestor at level l (or -1)
@@ -158,6 +181,9 @@ struct Engine {
   std::int64_t start(int b) const { return lay.start[size_t(b)]; }
   int count(int b) const { return int(lay.count[size_t(b)]); }
   void ensure_box_bbox();
+  /// y = A x (or A^T x) on tree-order col-major n x w device buffers, through
+  /// the black box: on-the-fly / dense kernels or the caller's callback.
+  void op_apply(bool adjoint, const double* x_tree, int w, double* y_tree) const;
 };
 
 int pair_index(const std::vector<std::pair<int, int>>& pairs, int a, int b);
@@ -208,6 +234,7 @@ struct SampleBlock {
   int box;
   int color;
   std::int64_t off;  // sample block offset (col-major, ld = |I_box|)
+  int cols = 1 << 30;  // columns kept (compact dense blocks: |I_mu|)
 };
 PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBlock>& blocks,
                    const std::vector<std::vector<int>>& payload_boxes, int top_level, int w,

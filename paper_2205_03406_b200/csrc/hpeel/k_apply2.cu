@@ -76,7 +76,8 @@ __global__ void identity_apply_kernel(DevOp op, const SampleTask* __restrict__ t
   }
   const double* tab = KIND == kOpLog ? s_tab : op.ltab;
   const std::int64_t q0 = pay_off[task.color], q1 = pay_off[task.color + 1];
-  const int nidx = task.rows * w;
+  // compact dense blocks: only the |I_mu| columns the block keeps (task.pad)
+  const int nidx = task.rows * (task.pad > 0 && task.pad < w ? task.pad : w);
   // per-thread accumulators for kPer (row, column) entries per pass
   constexpr int kPer = 16;
   for (int base = 0; base < nidx; base += kPer * int(blockDim.x)) {

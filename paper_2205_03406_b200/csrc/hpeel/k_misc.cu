@@ -3,6 +3,8 @@
 // (dense_contribution, proj/src/hmatrix.cpp:59-73), and small reductions.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.hpp"
 
 namespace hpeel {
@@ -137,4 +139,112 @@ const double* log_table_device(int device) {
   tabs[device] = d;
   return d;
 }
+}  // namespace hpeel
+
+// ------------------------------------------------------------------ sharding
+// Packing of the per-level factor exchanges and the callback
+// black box's dense test matrices / sample rows.
+namespace hpeel {
+
+namespace {
+
+// one CTA per segment, 16-byte vector copies when both ends are aligned
+__global__ void copy_segments_kernel(const double* __restrict__ src, const CopySeg* __restrict__ segs,
+                                     double* __restrict__ dst) {
+  const CopySeg sg = segs[blockIdx.x];
+  const double* a = src + sg.src;
+  double* b = dst + sg.dst;
+  if (((sg.src | sg.dst) & 1) == 0) {
+    const std::int64_t n2 = sg.len >> 1;
+    for (std::int64_t e = threadIdx.x; e < n2; e += blockDim.x)
+      reinterpret_cast<double2*>(b)[e] = reinterpret_cast<const double2*>(a)[e];
+    if ((sg.len & 1) && threadIdx.x == 0) b[sg.len - 1] = a[sg.len - 1];
+  } else {
+    for (std::int64_t e = threadIdx.x; e < sg.len; e += blockDim.x) b[e] = a[e];
+  }
+}
+
+__global__ void move_i32_kernel(const int* __restrict__ src, const int* __restrict__ sidx, std::int64_t n,
+                                int* __restrict__ dst, const int* __restrict__ didx) {
+  for (std::int64_t e = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; e < n;
+       e += std::int64_t(gridDim.x) * blockDim.x)
+    dst[didx ? didx[e] : e] = src[sidx ? sidx[e] : e];
+}
+
+__global__ void gather_sample_rows_kernel(const double* __restrict__ y, std::int64_t ldy,
+                                          const int* __restrict__ perm, const GatherRow* __restrict__ rows,
+                                          std::int64_t nrows, int w, double* __restrict__ out, int ocol0) {
+  const std::int64_t total = nrows * w;
+  for (std::int64_t e = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += std::int64_t(gridDim.x) * blockDim.x) {
+    const std::int64_t i = e % nrows;
+    const int c = int(e / nrows);
+    const GatherRow r = rows[i];
+    if (c < r.cols) out[r.out + std::int64_t(ocol0 + c) * r.ld] = y[perm[r.pos] + std::int64_t(c) * ldy];
+  }
+}
+
+__global__ void scatter_payload_kernel(const double* __restrict__ g, int gld, int gcol0, int w,
+                                       const int* __restrict__ pos, std::int64_t cnt,
+                                       const int* __restrict__ perm, double* __restrict__ omega,
+                                       std::int64_t ldo) {
+  const std::int64_t total = cnt * w;
+  for (std::int64_t e = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += std::int64_t(gridDim.x) * blockDim.x) {
+    const std::int64_t q = e % cnt;
+    const int c = int(e / cnt);
+    const int p = pos[q];
+    omega[perm[p] + std::int64_t(c) * ldo] = g[std::int64_t(p) * gld + gcol0 + c];
+  }
+}
+
+__global__ void scatter_identity_kernel(const int* __restrict__ boxes, const std::int64_t* __restrict__ box_start,
+                                        const std::int64_t* __restrict__ box_count, const int* __restrict__ perm,
+                                        int w, double* __restrict__ omega, std::int64_t ldo) {
+  const int b = boxes[blockIdx.x];
+  const std::int64_t st = box_start[b];
+  const int cnt = int(box_count[b] < w ? box_count[b] : w);
+  for (int t = threadIdx.x; t < cnt; t += blockDim.x) omega[perm[st + t] + std::int64_t(t) * ldo] = 1.0;
+}
+
+unsigned grid_for(std::int64_t total) {
+  return unsigned(std::max<std::int64_t>(1, std::min<std::int64_t>((total + 255) / 256, 148 * 16)));
+}
+
+}  // namespace
+
+void launch_copy_segments(const double* src, const CopySeg* segs, int nseg, double* dst, cudaStream_t s) {
+  if (nseg == 0) return;
+  copy_segments_kernel<<<nseg, 256, 0, s>>>(src, segs, dst);
+  HP_LAUNCHED();
+}
+
+void launch_move_i32(const int* src, const int* sidx, std::int64_t n, int* dst, const int* didx, cudaStream_t s) {
+  if (n == 0) return;
+  move_i32_kernel<<<grid_for(n), 256, 0, s>>>(src, sidx, n, dst, didx);
+  HP_LAUNCHED();
+}
+
+void launch_gather_sample_rows(const double* y, std::int64_t ldy, const int* perm, const GatherRow* rows,
+                               std::int64_t nrows, int w, double* out, int ocol0, cudaStream_t s) {
+  if (nrows == 0 || w == 0) return;
+  gather_sample_rows_kernel<<<grid_for(nrows * w), 256, 0, s>>>(y, ldy, perm, rows, nrows, w, out, ocol0);
+  HP_LAUNCHED();
+}
+
+void launch_scatter_payload(const double* g, int gld, int gcol0, int w, const int* pos, std::int64_t cnt,
+                            const int* perm, double* omega, std::int64_t ldo, cudaStream_t s) {
+  if (cnt == 0 || w == 0) return;
+  scatter_payload_kernel<<<grid_for(cnt * w), 256, 0, s>>>(g, gld, gcol0, w, pos, cnt, perm, omega, ldo);
+  HP_LAUNCHED();
+}
+
+void launch_scatter_identity(const int* boxes, int nbox, const std::int64_t* box_start,
+                             const std::int64_t* box_count, const int* perm, int w, double* omega,
+                             std::int64_t ldo, cudaStream_t s) {
+  if (nbox == 0) return;
+  scatter_identity_kernel<<<nbox, 128, 0, s>>>(boxes, box_start, box_count, perm, w, omega, ldo);
+  HP_LAUNCHED();
+}
+
 }  // namespace hpeel

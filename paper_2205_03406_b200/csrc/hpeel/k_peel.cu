@@ -58,7 +58,8 @@ peel_apply_kernel(const PeelTask* __restrict__ tasks, const PeelRef* __restrict_
   auto tsm = [&](int b) { return sm + b * (fsz + tsz) + fsz; };
   const PeelTask task = tasks[blockIdx.x];
   const int c0 = blockIdx.y * NT * 8;
-  const int ncol = min(NT * 8, w - c0);
+  const int ncol = min(NT * 8, min(task.cols, w) - c0);
+  if (ncol <= 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rg = warp & 3;                  // 16-row group
   constexpr int NH = (NT + 1) / 2;          // column tiles per half

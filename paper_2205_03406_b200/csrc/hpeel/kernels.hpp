@@ -28,7 +28,7 @@ struct SampleTask {
   int rows;
   int color;
   int ld;
-  int pad;
+  int pad;   // identity probes: columns written (|I_mu| of the compact dense block; 0 = w)
 };
 /// K2 row table entry: one output row of a sample block (element offset of
 /// its column 0 and the block's column stride) and its tree position.
@@ -131,6 +131,8 @@ struct PeelTask {
   int ld;
   int ref_begin;
   int ref_end;
+  int cols;  // columns of this output block (<= w; compact dense blocks keep |I_mu|)
+  int pad;
 };
 /// A shared term list [term_begin, term_end) read at row offset roff.
 struct PeelRef {
@@ -254,5 +256,37 @@ struct DenseTask {
 void launch_dense_apply(const DenseTask* tasks, const int* box_off, int nboxes,
                         const double* dense, const double* x, int w, bool adjoint, double* y,
                         std::int64_t ldy, cudaStream_t s);
+
+// ---------------------------------------------------------------- sharding / callback
+/// dst[s.dst + i] = src[s.src + i] for i < s.len, one CTA per segment.
+struct CopySeg {
+  std::int64_t src;
+  std::int64_t dst;
+  std::int64_t len;
+};
+void launch_copy_segments(const double* src, const CopySeg* segs, int nseg, double* dst, cudaStream_t s);
+/// dst[didx ? didx[e] : e] = src[sidx ? sidx[e] : e] for e < n.
+void launch_move_i32(const int* src, const int* sidx, std::int64_t n, int* dst, const int* didx, cudaStream_t s);
+/// One sample row read back from a black-box product Y (input order, column
+/// stride ldy): out[out + (ocol0 + c) * ld] = Y[perm[pos] + c * ldy], c < min(w, cols).
+struct GatherRow {
+  std::int64_t out;
+  int pos;
+  int ld;
+  int cols;
+  int pad;
+};
+void launch_gather_sample_rows(const double* y, std::int64_t ldy, const int* perm, const GatherRow* rows,
+                               std::int64_t nrows, int w, double* out, int ocol0, cudaStream_t s);
+/// Dense test matrix of one color for a callback black box
+/// (BlockTestMatrix::realize, proj/src/coloring.cpp:261-291), input order:
+/// omega[perm[pos[q]] + c * ldo] = g[pos[q] * gld + gcol0 + c], c < w
+/// (payload rows; the caller zero-fills the rest).
+void launch_scatter_payload(const double* g, int gld, int gcol0, int w, const int* pos, std::int64_t cnt,
+                            const int* perm, double* omega, std::int64_t ldo, cudaStream_t s);
+/// Identity payloads [I | 0] of the leaf phase: omega[perm[start_b + t] + t * ldo] = 1, t < min(|b|, w).
+void launch_scatter_identity(const int* boxes, int nbox, const std::int64_t* box_start,
+                             const std::int64_t* box_count, const int* perm, int w, double* omega,
+                             std::int64_t ldo, cudaStream_t s);
 
 }  // namespace hpeel

@@ -38,8 +38,7 @@ struct PeelConfig {
   PeelFormat format = PeelFormat::kH1;
   ColoringStrategy strategy = ColoringStrategy::kGraph;
   bool capture_samples = false;  // keep post-peel sample blocks on the host (tests)
-  Comm* comm = nullptr;          // multi-GPU: this process's rank in the NCCL group
-  int emulate_shards = 0;        // tests: split K2/K6 launches as `n` ranks would
+  Comm* comm = nullptr;          // multi-GPU: this rank's communicator (NCCL, or an emulated group)
   // Streamed export: when set, every level's factor slice and the dense leaf
   // blocks are copied to these host arrays (export_sizes() doubles each, the
   // H1Rep::export_all layout) on a second stream as soon as they are final,
@@ -83,8 +82,18 @@ struct RunReport {
   double wall_s_net = 0.0;
   std::int64_t net_flops = 0;
   double setup_ms = 0.0;  // adjacency, layout, device operator staging, plan launch
+  double peak_device_bytes = 0.0;  // high-water of the buffers compress() allocated (this rank)
+  double exchange_bytes = 0.0;     // bytes this rank sent in sharded exchanges / broadcasts
   std::string to_csv() const;  // proj/src/peeling.cpp:478-488 columns
 };
+
+/// Caller-supplied black box (the reference's virtual LinearOperator::apply /
+/// apply_adjoint, proj/include/hpeel/linear_operator.hpp:19-20): Y = A X or
+/// A^T X for an n x w column-major X in the caller's point order. Host
+/// variant: x / y are host arrays and stream is null; device variant: x / y
+/// are device pointers on the operator's device and the work must be ordered
+/// on `stream` (a cudaStream_t). Nonzero return = failure.
+using ApplyFn = int (*)(void* ctx, int adjoint, const double* x, std::int64_t w, double* y, void* stream);
 
 /// A black box behind the reference's LinearOperator plugin boundary
 /// (proj/include/hpeel/linear_operator.hpp:12-24), resident on the device.
@@ -93,6 +102,12 @@ class DeviceOperator {
   static std::shared_ptr<DeviceOperator> dense(const Matrix& a, int device);
   static std::shared_ptr<DeviceOperator> kernel(int kind, const Matrix& raw_points, double param,
                                                 int device);
+  static std::shared_ptr<DeviceOperator> callback(Index n, bool symmetric, bool device_pointers, ApplyFn fn,
+                                                  void* ctx, int device);
+  bool is_callback() const { return fn_ != nullptr; }
+  /// Callback black box on device buffers (input order, n x w col-major),
+  /// ordered on s; the host variant stages through pinned host memory.
+  void call(bool adjoint, const double* d_x, std::int64_t w, double* d_y, cudaStream_t s) const;
   ~DeviceOperator();
   Index rows() const { return n_; }
   Index cols() const { return n_; }
@@ -116,6 +131,9 @@ class DeviceOperator {
   int device_ = 0;
   double* d_x_ = nullptr;
   double* d_a_ = nullptr;
+  ApplyFn fn_ = nullptr;
+  void* ctx_ = nullptr;
+  bool device_pointers_ = false;
 };
 
 struct LowRankBlockHost {
@@ -144,6 +162,11 @@ class H1Rep {
   std::vector<LevelData> levels;  // indexed by level
   DenseData dense;
   int device = 0;
+  // owner-computes sharding (shard.hpp): this rank holds the factors of the
+  // pairs with uoff >= 0 and the dense blocks with off >= 0
+  int world = 1;
+  int shard_rank = 0;
+  std::vector<int> box_owner;   // per box (-1 above the cut); empty = unsharded
   double* d_factors = nullptr;  // U, V, B blocks of all levels
   double* d_dense = nullptr;
   std::int64_t factor_doubles = 0;
@@ -169,6 +192,17 @@ class H1Rep {
   std::int64_t storage_total() const;
   /// Copy every factor and dense block to pinned host memory (e2e export).
   std::int64_t export_all(double* host_factors, double* host_dense) const;
+  bool sharded() const { return world > 1; }
+  bool holds(int level, int pair) const { return levels.at(size_t(level)).uoff.at(size_t(pair)) >= 0; }
+  bool holds_dense(int pair) const { return dense.off.at(size_t(pair)) >= 0; }
+  /// the rank that computed U and B of the pair (its row box's owner) counts it
+  bool counts_pair(int level, int pair) const {
+    const auto& ld = levels[size_t(level)];
+    if (ld.uoff[size_t(pair)] < 0) return false;
+    if (box_owner.empty()) return true;
+    const int o = box_owner[size_t(ld.pairs[size_t(pair)].first)];
+    return o < 0 ? shard_rank == 0 : o == shard_rank;
+  }
 };
 
 struct PeelResult {
@@ -181,9 +215,26 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
                     const PeelConfig& config);
 
 /// Doubles of the factor arena and of the dense leaf blocks compress() will
-/// produce for this tree and rank (the export_all / export_* layout sizes).
+/// produce for this tree and rank (the export_all / export_* layout sizes);
+/// with world > 1, of shard `shard` (owner-computes layout, shard.hpp).
 void export_sizes(const BoxTree& tree, int rank, std::int64_t* factor_doubles,
-                  std::int64_t* dense_doubles);
+                  std::int64_t* dense_doubles, int world = 1, int shard = 0);
+
+/// compress() on `world` ranks emulated by threads of this process on the
+/// operator's device (LocalComm): one representation per rank.
+std::vector<PeelResult> compress_group(const DeviceOperator& op, std::shared_ptr<const BoxTree> tree,
+                                       const PeelConfig& config, int world);
+
+/// Per-rank device memory plan of an owner-computes compress (bytes):
+/// out[g * 4 + 0..3] = factors held, dense blocks, largest level's samples
+/// plus its apply buffers, total estimate.
+void shard_memory_plan(const BoxTree& tree, int rank, int oversample, int world, double* out);
+
+/// Doubles shard `shard` sends to / receives from each rank in the level's
+/// crossing-pair exchange `phase` (1: V to the row owner, 2: U and B to the
+/// column owner); zero on replicated levels.
+void shard_exchange_counts(const BoxTree& tree, int rank, int world, int shard, int level, int phase,
+                           std::int64_t* send, std::int64_t* recv);
 
 /// proj/src/linalg.cpp:206-218 with both operators applied on the device.
 double rel_error_power_method(const H1Rep& rep, const DeviceOperator& op, int iters,

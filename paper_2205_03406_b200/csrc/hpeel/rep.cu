@@ -57,6 +57,45 @@ std::shared_ptr<DeviceOperator> DeviceOperator::kernel(int kind, const Matrix& p
   return op;
 }
 
+std::shared_ptr<DeviceOperator> DeviceOperator::callback(Index n, bool symmetric, bool device_pointers,
+                                                         ApplyFn fn, void* ctx, int device) {
+  if (n < 1) throw std::invalid_argument("callback operator needs n >= 1");
+  if (!fn) throw std::invalid_argument("callback operator needs an apply function");
+  DeviceGuard g(device);
+  std::shared_ptr<DeviceOperator> op(new DeviceOperator());
+  op->kind_ = kOpCallback;
+  op->n_ = n;
+  op->symmetric_ = symmetric;
+  op->device_ = device;
+  op->fn_ = fn;
+  op->ctx_ = ctx;
+  op->device_pointers_ = device_pointers;
+  return op;
+}
+
+void DeviceOperator::call(bool adjoint, const double* d_x, std::int64_t w, double* d_y, cudaStream_t s) const {
+  if (!fn_) throw std::logic_error("not a callback operator");
+  int rc = 0;
+  if (device_pointers_) {
+    rc = fn_(ctx_, adjoint ? 1 : 0, d_x, w, d_y, s);
+  } else {
+    // the reference's call: host matrices in, host matrix out
+    const size_t bytes = size_t(n_) * size_t(w) * sizeof(double);
+    double* hx = static_cast<double*>(detail::persistent_pinned(bytes, 2));
+    double* hy = static_cast<double*>(detail::persistent_pinned(bytes, 3));
+    HP_CUDA(cudaMemcpyAsync(hx, d_x, bytes, cudaMemcpyDeviceToHost, s));
+    HP_CUDA(cudaStreamSynchronize(s));
+    rc = fn_(ctx_, adjoint ? 1 : 0, hx, w, hy, nullptr);
+    if (rc == 0) {
+      HP_CUDA(cudaMemcpyAsync(d_y, hy, bytes, cudaMemcpyHostToDevice, s));
+      HP_CUDA(cudaStreamSynchronize(s));  // hy is reused by the next call
+    }
+  }
+  if (rc != 0)
+    throw std::runtime_error("black-box apply" + std::string(adjoint ? "_adjoint" : "") + " failed (status " +
+                             std::to_string(rc) + ")");
+}
+
 DeviceOperator::~DeviceOperator() {
   if (d_x_) cudaFree(d_x_);
   if (d_a_) cudaFree(d_a_);
@@ -77,10 +116,17 @@ Matrix DeviceOperator::apply(const Matrix& x, bool adjoint) const {
   cudaStream_t s;
   HP_CUDA(cudaStreamCreate(&s));
   Matrix y(x.rows(), x.cols());
+  if (fn_ && !device_pointers_) {
+    cudaStreamDestroy(s);
+    if (x.cols() > 0 && fn_(ctx_, adjoint ? 1 : 0, x.data(), x.cols(), y.data(), nullptr) != 0)
+      throw std::runtime_error("black-box apply failed");
+    return y;
+  }
   {
     DevBuf<double> dx(size_t(x.size()), s), dy(size_t(x.size()), s);
     HP_CUDA(cudaMemcpyAsync(dx.get(), x.data(), size_t(x.size()) * 8, cudaMemcpyHostToDevice, s));
-    if (x.cols() > 0) launch_full_apply(d, adjoint, dx.get(), int(x.cols()), dy.get(), s);
+    if (x.cols() > 0 && fn_) call(adjoint, dx.get(), x.cols(), dy.get(), s);
+    else if (x.cols() > 0) launch_full_apply(d, adjoint, dx.get(), int(x.cols()), dy.get(), s);
     HP_CUDA(cudaMemcpyAsync(y.data(), dy.get(), size_t(x.size()) * 8, cudaMemcpyDeviceToHost, s));
     HP_CUDA(cudaStreamSynchronize(s));
   }
@@ -108,19 +154,25 @@ std::int64_t H1Rep::storage_total() const {
   for (size_t l = 0; l < levels.size(); ++l) {
     const auto& ld = levels[l];
     for (size_t p = 0; p < ld.pairs.size(); ++p) {
+      if (!counts_pair(int(l), int(p))) continue;
       t += std::int64_t(tree->box(ld.pairs[p].first).points.size()) * ld.ku[p];
       t += std::int64_t(tree->box(ld.pairs[p].second).points.size()) * ld.kv[p];
       t += std::int64_t(ld.ku[p]) * ld.kv[p];
     }
   }
-  for (auto [lam, mu] : dense.pairs)
-    t += std::int64_t(tree->box(lam).points.size()) * std::int64_t(tree->box(mu).points.size());
+  for (size_t p = 0; p < dense.pairs.size(); ++p)
+    if (dense.off[p] >= 0)
+      t += std::int64_t(tree->box(dense.pairs[p].first).points.size()) *
+           std::int64_t(tree->box(dense.pairs[p].second).points.size());
   return t;
 }
 
 LowRankBlockHost H1Rep::block(int level, int p) const {
   DeviceGuard g(device);
   const auto& ld = levels.at(size_t(level));
+  if (ld.uoff.at(size_t(p)) < 0)
+    throw std::invalid_argument("block (" + std::to_string(level) + ", " + std::to_string(p) +
+                                ") is not held by this rank of a sharded representation");
   const auto [a, b] = ld.pairs.at(size_t(p));
   const int ma = int(layout->count[size_t(a)]), mb = int(layout->count[size_t(b)]);
   std::vector<double> u(size_t(ma) * rank), v(size_t(mb) * rank), bb(size_t(rank) * rank);
@@ -148,6 +200,8 @@ LowRankBlockHost H1Rep::block(int level, int p) const {
 Matrix H1Rep::dense_block(int p) const {
   DeviceGuard g(device);
   const auto [lam, mu] = dense.pairs.at(size_t(p));
+  if (dense.off.at(size_t(p)) < 0)
+    throw std::invalid_argument("dense block " + std::to_string(p) + " is not held by this rank");
   const Index ml = Index(tree->box(lam).points.size()), mm = Index(tree->box(mu).points.size());
   Matrix d(ml, mm);
   HP_CUDA(cudaMemcpy(d.data(), d_dense + dense.off[size_t(p)], size_t(ml * mm) * 8, cudaMemcpyDeviceToHost));
@@ -201,7 +255,7 @@ void H1Rep::apply_device(const double* x, int w, bool adjoint, double* y, cudaSt
       const int te = int(terms.size());
       for (int t0 = 0; t0 < rows; t0 += kTile) {
         tasks.push_back(PeelTask{layout->start[size_t(box)] + t0, std::min(kTile, rows - t0),
-                                 int(tree->num_points()), int(refs.size()), int(refs.size()) + 1});
+                                 int(tree->num_points()), int(refs.size()), int(refs.size()) + 1, w, 0});
         refs.push_back(PeelRef{tb, te, t0});
       }
     }
@@ -249,6 +303,7 @@ void H1Rep::apply_device(const double* x, int w, bool adjoint, double* y, cudaSt
 
 Matrix H1Rep::apply(const Matrix& x, bool adjoint) const {
   if (!dense_ready) throw std::runtime_error("h1 apply: dense blocks missing");
+  if (sharded()) throw std::invalid_argument("h1 apply: this rank holds a shard of the representation");
   const Index n = tree->num_points();
   if (x.rows() != n) throw std::invalid_argument("rep apply: row mismatch");
   DeviceGuard g(device);
@@ -290,6 +345,7 @@ double rel_error_power_method(const H1Rep& rep, const DeviceOperator& op, int it
   const Index n = rep.tree->num_points();
   if (op.rows() != n) throw std::invalid_argument("operator dimension mismatch");
   if (!rep.dense_ready) throw std::runtime_error("h1 apply: dense blocks missing");
+  if (rep.sharded()) throw std::invalid_argument("power method: this rank holds a shard of the representation");
   DeviceGuard guard(rep.device);
   cudaStream_t s;
   HP_CUDA(cudaStreamCreate(&s));
@@ -323,7 +379,7 @@ double rel_error_power_method(const H1Rep& rep, const DeviceOperator& op, int it
       double estimate = 0.0;
       for (int it = 0; it < iters; ++it) {
         // y = A_rep x - A x   (or A x)
-        launch_full_apply(e.dop, false, x.get(), 1, y.get(), s);
+        e.op_apply(false, x.get(), 1, y.get());
         if (with_rep) {
           HP_CUDA(cudaMemsetAsync(t.get(), 0, size_t(n) * 8, s));
           rep.apply_device(x.get(), 1, false, t.get(), s);
@@ -334,7 +390,7 @@ double rel_error_power_method(const H1Rep& rep, const DeviceOperator& op, int it
           for (size_t i = 0; i < a.size(); ++i) a[i] -= b[i];
           HP_CUDA(cudaMemcpyAsync(y.get(), a.data(), a.size() * 8, cudaMemcpyHostToDevice, s));
         }
-        launch_full_apply(e.dop, true, y.get(), 1, z.get(), s);
+        e.op_apply(true, y.get(), 1, z.get());
         if (with_rep) {
           HP_CUDA(cudaMemsetAsync(t.get(), 0, size_t(n) * 8, s));
           rep.apply_device(y.get(), 1, true, t.get(), s);

@@ -121,6 +121,7 @@ std::vector<size_t> sorted_order(const std::vector<std::pair<int, int>>& pairs) 
 }  // namespace
 
 void save_rep(const std::string& path, const H1Rep& rep) {
+  if (rep.sharded()) throw std::invalid_argument("save_rep: this rank holds a shard of the representation");
   const BoxTree& tree = *rep.tree;
   const TreeLayout& lay = *rep.layout;
   const int k = rep.rank;

@@ -10,8 +10,8 @@ from paper_2205_03406_b200 import _lib
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_symbols():
-    text = open(os.path.join(ROOT, "include", "hpeel_b200.h")).read()
+def declared_symbols(path=os.path.join(ROOT, "include", "hpeel_b200.h")):
+    text = open(path).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(hp_[a-z0-9_]+)\s*\(", text)))
 
@@ -26,6 +26,18 @@ def test_header_symbols_exported():
 
 def test_python_binding_covers_header():
     assert set(declared_symbols()) == set(_lib.exported_symbols())
+
+
+def test_probe_entry_points_are_not_in_the_public_header():
+    """The K2 switches and parity probes live in the internal probe header
+    (csrc/hpeel_probe.h), not in the drop-in boundary."""
+    probe = declared_symbols(os.path.join(ROOT, "paper_2205_03406_b200", "csrc", "hpeel_probe.h"))
+    public = declared_symbols()
+    assert probe and not set(probe) & set(public)
+    assert not [n for n in public if n.startswith("hp_debug")]
+    assert set(probe) == set(_lib.probe_symbols())
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    assert all(hasattr(lib, n) for n in probe)
 
 
 def test_library_is_sm100a():

@@ -157,7 +157,8 @@ def test_error_behaviour(hp):
 
 def test_export_sizes_match_layout(hp):
     """hp_export_sizes: U, V, B per admissible pair of every level plus the
-    |I_lam| x max_leaf_size dense probe blocks (H1Rep::export_all layout)."""
+    compact |I_lam| x |I_mu| dense blocks (D = Y(I_lam, 0:|I_mu|),
+    proj/src/peeling.cpp:513-517; H1Rep::export_all layout)."""
     pts = O.random_cloud(3000, 2, O.mix_seed(7, 0xE3))
     tree = hp.build_tree(pts, 32)
     ot = O.BoxTree(O.PointCloud(pts), 32)
@@ -166,9 +167,49 @@ def test_export_sizes_match_layout(hp):
     for level in range(2, tree.depth + 1):
         for a, b in tree.admissible_pairs(level):
             want_f += (len(ot.box(a).points) + len(ot.box(b).points)) * k + k * k
-    w = max(len(ot.box(v).points) for v in range(len(ot.boxes)) if not ot.box(v).children)
-    want_d = sum(len(ot.box(lam).points) * w for lam, _ in tree.dense_pairs())
+    want_d = sum(len(ot.box(lam).points) * len(ot.box(mu).points) for lam, mu in tree.dense_pairs())
     assert hp.export_sizes(tree, k) == (want_f, want_d)
+    # sharded layouts: every dense block on exactly one rank, every pair on its
+    # owners (both for a cut-crossing pair), replicated levels on every rank
+    for world in (2, 3, 8):
+        owner, cut, bounds = hp.shard_owners(tree, world)
+        assert bounds[0] == 0 and bounds[-1] == tree.num_points and all(np.diff(bounds) >= 0)
+        f_tot = d_tot = 0
+        for g in range(world):
+            f, d = hp.export_sizes(tree, k, world, g)
+            f_tot += f
+            d_tot += d
+        assert d_tot == want_d
+        want_fw = 0
+        for level in range(2, tree.depth + 1):
+            for a, b in tree.admissible_pairs(level):
+                size = (len(ot.box(a).points) + len(ot.box(b).points)) * k + k * k
+                if level < cut:
+                    want_fw += world * size
+                else:
+                    assert owner[a] >= 0 and owner[b] >= 0
+                    want_fw += size * (1 if owner[a] == owner[b] else 2)
+        assert f_tot == want_fw
+
+
+def test_shard_ownership_is_a_contiguous_partition(hp):
+    """Boxes at or below the cut belong to exactly one rank, a box's rank owns
+    its whole tree-order range, and the ranks' point counts are balanced at
+    frontier-box granularity."""
+    w = configs.scaled("c3", 16384)
+    t = hp.build_tree(w.points(), w.leaf)
+    lvl, parent, _, off, _ = t._box_arrays()
+    for world in (2, 4, 8):
+        owner, cut, bounds = hp.shard_owners(t, world)
+        for b in range(t.num_boxes):
+            if lvl[b] >= cut or not t.children(b):
+                assert 0 <= owner[b] < world
+            else:
+                assert owner[b] == -1
+            if parent[b] >= 0 and owner[parent[b]] >= 0:
+                assert owner[b] == owner[parent[b]]
+        counts = np.diff(bounds)
+        assert counts.sum() == t.num_points and counts.min() > 0
 
 
 @pytest.mark.parametrize("name,pts,leaf", GEOMS, ids=[g[0] for g in GEOMS])

@@ -1,8 +1,10 @@
 """Multi-rank host logic on CPU (gloo, world_size 2): every rank computes the
 same work partition of every level's pairs and leaf blocks, the ranges tile
-the index space exactly once, and the per-rank work is balanced. The device
-side of the same split is checked on one GPU by emulation
-(tests/test_gpu_shard.py)."""
+the index space exactly once, and the per-rank work is balanced; each rank
+derives the same box ownership on its own, and the crossing-pair exchanges
+it plans (what it sends to / expects from every peer, per level and phase)
+match its peers' plans exactly. The device side of the same split is checked
+on one GPU by emulation (tests/test_gpu_shard.py)."""
 import os
 import socket
 
@@ -78,3 +80,49 @@ def test_partition_edge_cases(hp):
     assert b == [0, 4, 8]
     with pytest.raises(ValueError):
         hp.partition_ranges([1.0], 0)
+
+
+def _exchange_worker(rank, world, port, result):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2205_03406_b200 as hp
+    out = {}
+    for name, n in (("c3", 16384), ("c4", 16384), ("c2", 8192)):
+        w = configs.scaled(name, n)
+        tree = hp.build_tree(w.points(), w.leaf)
+        owner, cut, bounds = hp.shard_owners(tree, world)
+        plans = {}
+        for level in range(2, tree.depth + 1):
+            for phase in (1, 2):
+                send, recv = hp.shard_exchange_counts(tree, w.rank, world, rank, level, phase)
+                plans[(level, phase)] = (send.tolist(), recv.tolist())
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (owner.tolist(), cut, bounds.tolist(), plans))
+        out[name] = gathered
+    if rank == 0:
+        result["plans"] = out
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_plans_agree_across_ranks(world):
+    with mp.Manager() as mgr:
+        result = mgr.dict()
+        mp.spawn(_exchange_worker, args=(world, _free_port(), result), nprocs=world, join=True)
+        plans = dict(result["plans"])
+    for name, per_rank in plans.items():
+        owners = [p[0] for p in per_rank]
+        assert all(o == owners[0] for o in owners), name
+        assert all(p[1] == per_rank[0][1] and p[2] == per_rank[0][2] for p in per_rank), name
+        moved = 0
+        for key in per_rank[0][3]:
+            for i in range(world):
+                send_i = per_rank[i][3][key][0]
+                for j in range(world):
+                    recv_j = per_rank[j][3][key][1]
+                    assert send_i[j] == recv_j[i], (name, key, i, j)
+                    moved += send_i[j]
+                assert send_i[i] == 0
+        assert moved > 0, name  # some pairs cross the cut at every size tested
