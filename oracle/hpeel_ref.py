@@ -14,11 +14,11 @@ __all__ = [
     "GAMMA", "scramble", "mix_seed", "SplitMix64", "gaussian_matrix", "gaussian_matrix_libm",
     "random_cloud", "equispaced_1d", "uniform_grid_points", "PointCloud", "Box", "BoxTree",
     "Adjacency", "adjacency", "admissible_pairs", "dense_pairs", "ConstraintSet",
-    "build_constraints", "incompatible", "build_graph", "dsatur_color", "plan_coloring",
+    "build_constraints", "incompatible", "build_graph", "build_graph_literal", "dsatur_color", "plan_coloring",
     "BlockTestMatrix", "payload_gaussian", "assemble_test_matrices", "make_plan",
     "qr_orthonormal", "pinv_apply", "DenseOperator", "KernelOperator", "H1Rep", "run_h1",
     "extract_leaf", "compress", "rel_error_power_method", "synth_rank_structured",
-    "kernel_matrix", "H1", "LEAF", "UNIF1", "save_rep_bytes", "load_rep_bytes", "save_dense_matrix_bytes",
+    "kernel_matrix", "PhaseTimes", "H1", "LEAF", "UNIF1", "save_rep_bytes", "load_rep_bytes", "save_dense_matrix_bytes",
     "REP_MAGIC", "DENSE_MAGIC",
 ]
 
@@ -382,8 +382,10 @@ def incompatible(a: ConstraintSet, b: ConstraintSet) -> bool:
 
 
 def build_graph(sets):
-    """proj/src/coloring.cpp:154-167, the literal pairwise scan (vectorized
-    over j through Python sets; same edge set)."""
+    """proj/src/coloring.cpp:154-167: the pairwise `incompatible` scan,
+    vectorized with incidence matrices for up to 6000 sets and enumerated per
+    box above that (same edge set; build_graph_literal is the scan as
+    written, tests/test_oracle.py pins all three against each other)."""
     n = len(sets)
     if 0 < n <= 6000:
         # the same pairwise predicate, evaluated for all (i, j) at once with
@@ -408,27 +410,68 @@ def build_graph(sets):
                     inc |= (T[a] @ T[b].T) > 0
         np.fill_diagonal(inc, False)
         return [list(np.nonzero(inc[i])[0].astype(int)) for i in range(n)]
-    zeros = [set(s.zero) for s in sets]
-    pays = [dict(s.payload) for s in sets]
+    return _build_graph_indexed(sets)
+
+
+def build_graph_literal(sets):
+    """proj/src/coloring.cpp:154-167 as written: every pair (i < j) through
+    `incompatible` (O(V^2); small inputs, to pin the faster forms)."""
+    n = len(sets)
     edges = [[] for _ in range(n)]
     for i in range(n):
-        pi, zi = pays[i], zeros[i]
         for j in range(i + 1, n):
-            pj, zj = pays[j], zeros[j]
-            hit = False
-            for p in pi:
-                if p in zj or (p in pj and pj[p] != pi[p]):
-                    hit = True
-                    break
-            if not hit:
-                for p in pj:
-                    if p in zi:
-                        hit = True
-                        break
-            if hit:
+            if incompatible(sets[i], sets[j]):
                 edges[i].append(j)
                 edges[j].append(i)
-    return [sorted(e) for e in edges]
+    return edges
+
+
+def _build_graph_indexed(sets, chunk=1 << 24):
+    """The same edge set as the pairwise scan, enumerated per box: sets whose
+    payload holds box b clash with every set whose zero set holds b, and with
+    each other when their tags for b differ (`incompatible`'s three clauses).
+    Candidate pairs are encoded as i * n + j and de-duplicated with numpy."""
+    n = len(sets)
+    pay, zer = {}, {}
+    for i, s in enumerate(sets):
+        for b, t in s.payload:
+            pay.setdefault(b, []).append((i, t))
+        for z in s.zero:
+            zer.setdefault(z, []).append(i)
+    parts, pending, found = [], [], 0
+
+    def flush():
+        nonlocal pending, found
+        if pending:
+            parts.append(np.unique(np.concatenate(pending)))
+            pending, found = [], 0
+
+    for b, lst in pay.items():
+        pi = np.array([i for i, _ in lst], dtype=np.int64)
+        zs = zer.get(b)
+        if zs:
+            zi = np.array(zs, dtype=np.int64)
+            codes = (pi[:, None] * n + zi[None, :]).ravel()
+            pending += [codes, (zi[:, None] * n + pi[None, :]).ravel()]
+            found += 2 * codes.size
+        tags = np.array([t for _, t in lst])
+        if len(lst) > 1 and np.any(tags != tags[0]):
+            ii, jj = np.nonzero(tags[:, None] != tags[None, :])
+            pending.append(pi[ii] * n + pi[jj])
+            found += ii.size
+        if found > chunk:
+            flush()
+    flush()
+    if not parts:
+        return [[] for _ in range(n)]
+    codes = np.unique(np.concatenate(parts))
+    i, j = codes // n, codes % n
+    keep = i != j
+    i, j = i[keep], j[keep]
+    # codes are sorted by (i, j): split into per-vertex sorted lists
+    starts = np.searchsorted(i, np.arange(n + 1))
+    jl = j.tolist()
+    return [jl[starts[v]:starts[v + 1]] for v in range(n)]
 
 
 def dsatur_color(edges):
@@ -650,6 +693,10 @@ def kernel_matrix(kind, xi, xj, same=None, param=0.1):
     return k
 
 
+def _nonzero_rows(x):
+    return np.nonzero(np.any(x != 0.0, axis=1))[0]
+
+
 class DenseOperator:
     """proj/include/hpeel/operators.hpp:56-69."""
 
@@ -662,6 +709,12 @@ class DenseOperator:
 
     def apply_adjoint(self, x):
         return self.a.T @ x
+
+    def apply_rows(self, x, rows, adjoint=False):
+        """(A x)[rows] (or (A^T x)[rows]) over the nonzero rows of x only."""
+        nz = _nonzero_rows(x)
+        a = self.a.T if adjoint else self.a
+        return a[np.ix_(rows, nz)] @ x[nz]
 
 
 class KernelOperator:
@@ -694,6 +747,17 @@ class KernelOperator:
         return y
 
     apply_adjoint = apply  # symmetric kernels
+
+    def apply_rows(self, x, rows, adjoint=False):
+        """(K x)[rows] over the nonzero rows of x only (K symmetric)."""
+        nz = _nonzero_rows(x)
+        y = np.empty((len(rows), x.shape[1]))
+        xn = x[nz]
+        for i0 in range(0, len(rows), self.chunk):
+            r = rows[i0:i0 + self.chunk]
+            same = (r[:, None] == nz[None, :]) if self.kind != "exp" else None
+            y[i0:i0 + len(r)] = kernel_matrix(self.kind, self.x[r], self.x[nz], same, self.param) @ xn
+        return y
 
 
 # --------------------------------------------------------------------------- H1 rep
@@ -730,6 +794,44 @@ class H1Rep:
                 y[self.tree.box(b).points] += v @ (bb.T @ (u.T @ x[self.tree.box(a).points]))
         return y
 
+    def _box_at_level(self, l):
+        """point -> its box at level l (-1 if the point's leaf is coarser)."""
+        cache = self.__dict__.setdefault("_bal", {})
+        if l not in cache:
+            m = np.full(self.tree.num_points, -1, dtype=np.int64)
+            for b in self.tree.level_boxes(l):
+                m[self.tree.box(b).points] = b
+            cache[l] = m
+        return cache[l]
+
+    def apply_truncated_rows(self, level, x, mask, adjoint=False):
+        """Rows `mask` of apply_truncated(_adjoint)(level, x): only the pairs
+        whose column block of x is nonzero and whose row block meets the mask
+        contribute there (the same sums, in the same sorted pair order,
+        restricted to the rows the extraction reads)."""
+        self._check(level)
+        y = np.zeros_like(x)
+        nz = _nonzero_rows(x)
+        rows_all = np.nonzero(mask)[0]
+        for l in range(2, min(level, self.tree.depth) + 1):
+            bal = self._box_at_level(l)
+            srcs = set(np.unique(bal[nz]).tolist()) - {-1}
+            dsts = set(np.unique(bal[rows_all]).tolist()) - {-1}
+            if not srcs or not dsts:
+                continue
+            for (a, b), (u, bb, v) in sorted(self.levels[l].items()):
+                src, dst = (a, b) if adjoint else (b, a)
+                if src not in srcs or dst not in dsts:
+                    continue
+                rows = self.tree.box(dst).points
+                sel = mask[rows]
+                xs = x[self.tree.box(src).points]
+                if adjoint:
+                    y[rows[sel]] += v[sel] @ (bb.T @ (u.T @ xs))
+                else:
+                    y[rows[sel]] += u[sel] @ (bb @ (v.T @ xs))
+        return y
+
     def _dense(self, x, y, adjoint):
         """proj/src/hmatrix.cpp:59-73."""
         for (lam, mu), d in sorted(self.dense.items()):
@@ -764,27 +866,84 @@ class H1Rep:
 # --------------------------------------------------------------------------- driver
 # proj/src/peeling.cpp
 
-def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None):
-    """proj/src/peeling.cpp:158-178. Returns (samples, cols)."""
+class PhaseTimes(dict):
+    """Wall seconds per phase of the oracle's compress (bench.py reference
+    arm): plan, realize, apply (black box), peel (apply_truncated), qr, bsolve."""
+
+    def add(self, key, t0):
+        import time
+        self[key] = self.get(key, 0.0) + (time.perf_counter() - t0)
+
+
+def _small_blas():
+    """Per-pair QR / SVD / small GEMMs on one BLAS thread: a threaded BLAS is
+    ~50x slower on 64 x 48 matrices (thread start-up per call), and the
+    reference runs these serially anyway (proj/src/peeling.cpp:245-270)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=1)
+    except ImportError:  # pragma: no cover
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def _now():
+    import time
+    return time.perf_counter()
+
+
+def _served_rows(tree, plan, m_index):
+    """Tree points of the row boxes of the pairs a color serves (the rows the
+    extraction reads back from its sample)."""
+    pts = [tree.box(o[0]).points for i in plan.matrices[m_index].serves for o in plan.sets[i].owners]
+    return np.unique(np.concatenate(pts)) if pts else np.zeros(0, dtype=np.int64)
+
+
+def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None, restrict=False):
+    """proj/src/peeling.cpp:158-178. Returns (samples, cols). restrict=True
+    computes only the rows the extraction reads (value-identical on those
+    rows: the same products over the nonzero rows of Omega; other rows 0)."""
+    times = PhaseTimes() if times is None else times
     samples, cols = [], 0
-    for m in plan.matrices:
+    for ci, m in enumerate(plan.matrices):
         if not m.payload:
             samples.append(None)
             continue
         if phase is not None:
             m = BlockTestMatrix(m.rows, m.width, m.seed, m.level, phase, m.payload, m.zero, m.serves)
+        t0 = _now()
         omega = m.realize(rep.tree)
-        y = op.apply_adjoint(omega) if adjoint else op.apply(omega)
+        times.add("realize", t0)
         cols += omega.shape[1]
+        if restrict:
+            rows = _served_rows(rep.tree, plan, ci)
+            mask = np.zeros(omega.shape[0], dtype=bool)
+            mask[rows] = True
+            t0 = _now()
+            y = np.zeros_like(omega)
+            y[rows] = op.apply_rows(omega, rows, adjoint)
+            times.add("apply", t0)
+            if prev_level >= 2:
+                t0 = _now()
+                y[rows] -= rep.apply_truncated_rows(prev_level, omega, mask, adjoint)[rows]
+                times.add("peel", t0)
+            samples.append(y)
+            continue
+        t0 = _now()
+        y = op.apply_adjoint(omega) if adjoint else op.apply(omega)
+        times.add("apply", t0)
         if prev_level >= 2:
+            t0 = _now()
             y = y - (rep.apply_truncated_adjoint(prev_level, omega) if adjoint
                      else rep.apply_truncated(prev_level, omega))
+            times.add("peel", t0)
         samples.append(y)
     return samples, cols
 
 
-def run_h1(op, tree, adj, k, p, seed, report, capture=None):
+def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict=False):
     """proj/src/peeling.cpp:211-275 (Alg. 4.1)."""
+    times = PhaseTimes() if times is None else times
     rep = H1Rep(tree, adj)
     r = k + p
     for l in range(2, tree.depth + 1):
@@ -794,28 +953,38 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None):
         ps = set(pairs)
         if any((b, a) not in ps for a, b in pairs):
             raise AssertionError("asymmetric admissibility structure")
+        t0 = _now()
         plan = make_plan(tree, adj, l, H1, r, seed, 0)
-        ys, fcols = _residual_samples(op, rep, l - 1, plan, False)
+        times.add("plan", t0)
+        ys, fcols = _residual_samples(op, rep, l - 1, plan, False, times=times, restrict=restrict)
         u_bases = {}
-        for a, b in pairs:
-            y = ys[plan.block_to_matrix[(a, b)]]
-            u_bases[(a, b)] = qr_orthonormal(y[tree.box(a).points], k)
-        zs, acols = _residual_samples(op, rep, l - 1, plan, True, phase=1)
+        t0 = _now()
+        with _small_blas():
+            for a, b in pairs:
+                y = ys[plan.block_to_matrix[(a, b)]]
+                u_bases[(a, b)] = qr_orthonormal(y[tree.box(a).points], k)
+        times.add("qr", t0)
+        zs, acols = _residual_samples(op, rep, l - 1, plan, True, phase=1, times=times, restrict=restrict)
         if capture is not None:
             capture[l] = {(a, b): (ys[plan.block_to_matrix[(a, b)]][tree.box(a).points],
                                    zs[plan.block_to_matrix[(a, b)]][tree.box(a).points])
                           for a, b in pairs}
-        for a, b in pairs:
-            z = zs[plan.block_to_matrix[(b, a)]]
-            u = u_bases[(a, b)]
-            v = qr_orthonormal(z[tree.box(b).points], k)
-            g = payload_gaussian(tree, b, r, seed, l, 0)
-            gp = payload_gaussian(tree, a, r, seed, l, 1)
-            yb = ys[plan.block_to_matrix[(a, b)]][tree.box(a).points]
-            middle = gp.T @ yb
-            left = pinv_apply(gp.T @ u, middle)
-            bmat = pinv_apply((v.T @ g).T, left.T).T
-            rep.levels[l][(a, b)] = (u, bmat, v)
+        with _small_blas():
+            for a, b in pairs:
+                z = zs[plan.block_to_matrix[(b, a)]]
+                u = u_bases[(a, b)]
+                t0 = _now()
+                v = qr_orthonormal(z[tree.box(b).points], k)
+                times.add("qr", t0)
+                t0 = _now()
+                g = payload_gaussian(tree, b, r, seed, l, 0)
+                gp = payload_gaussian(tree, a, r, seed, l, 1)
+                yb = ys[plan.block_to_matrix[(a, b)]][tree.box(a).points]
+                middle = gp.T @ yb
+                left = pinv_apply(gp.T @ u, middle)
+                bmat = pinv_apply((v.T @ g).T, left.T).T
+                times.add("bsolve", t0)
+                rep.levels[l][(a, b)] = (u, bmat, v)
         rep.built_level = l
         report.append({"phase": "h1", "level": l, "colors": len(plan.matrices),
                        "forward_cols": fcols, "adjoint_cols": acols})
@@ -823,14 +992,20 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None):
     return rep
 
 
-def extract_leaf(op, rep, seed, report, capture=None):
+def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False):
     """proj/src/peeling.cpp:490-524."""
+    times = PhaseTimes() if times is None else times
     tree, adj = rep.tree, rep.adj
     if rep.built_level < tree.depth:
         raise RuntimeError("leaf extraction needs all admissible levels built")
     width = tree.max_leaf_size()
+    t0 = _now()
     plan = make_plan(tree, adj, tree.depth, LEAF, width, seed, 0)
-    ys, fcols = _residual_samples(op, rep, tree.depth, plan, False)
+    times.add("leaf_plan", t0)
+    leaf_times = PhaseTimes()
+    ys, fcols = _residual_samples(op, rep, tree.depth, plan, False, times=leaf_times, restrict=restrict)
+    for key, v in leaf_times.items():
+        times["leaf_" + key] = times.get("leaf_" + key, 0.0) + v
     for lam, mu in dense_pairs(tree, adj):
         y = ys[plan.block_to_matrix[(lam, mu)]]
         blk = y[tree.box(lam).points]
@@ -842,18 +1017,25 @@ def extract_leaf(op, rep, seed, report, capture=None):
                    "forward_cols": fcols, "adjoint_cols": 0})
 
 
-def compress(op, tree, k, p, seed, capture=None, leaf_capture=None):
-    """proj/src/peeling.cpp:576-639 for format h1. Returns (rep, report)."""
+def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, restrict=False):
+    """proj/src/peeling.cpp:576-639 for format h1. Returns (rep, report).
+    `times` (a PhaseTimes) collects wall seconds per phase. restrict=True
+    evaluates each color's black-box product and peeling only on the rows the
+    extraction reads and over Omega's nonzero rows (row-restricted oracle for
+    large N; the extracted samples are the same sums)."""
     if op.shape[0] != tree.num_points or op.shape[1] != tree.num_points:
         raise ValueError("operator and tree dimensions differ")
     if k < 1:
         raise ValueError("fixed rank must be >= 1")
     if p < 0:
         raise ValueError("negative oversampling")
+    t0 = _now()
     adj = adjacency(tree)
+    if times is not None:
+        times.add("adjacency", t0)
     report = []
-    rep = run_h1(op, tree, adj, k, p, seed, report, capture)
-    extract_leaf(op, rep, seed, report, leaf_capture)
+    rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict)
+    extract_leaf(op, rep, seed, report, leaf_capture, times, restrict)
     return rep, report
 
 

@@ -143,7 +143,7 @@ class BoxTree:
 
     def box_points(self, box: int):
         off, pts = self._box_arrays()[3:]
-        return [int(v) for v in pts[off[box]:off[box + 1]]]
+        return pts[off[box]:off[box + 1]].tolist()
 
     def children(self, box: int):
         return self._get(4, box)
@@ -165,11 +165,14 @@ class BoxTree:
         return int(lib().hp_tree_cross_level_adjacencies(self._h))
 
     def _pairs(self, level):
-        cnt = C.c_int64(0)
-        check(lib().hp_tree_pairs(self._h, level, C.byref(cnt), None))
-        arr = np.zeros(max(2 * cnt.value, 2), dtype=np.int32)
-        check(lib().hp_tree_pairs(self._h, level, C.byref(cnt), iptr(arr)))
-        return [(int(arr[2 * i]), int(arr[2 * i + 1])) for i in range(cnt.value)]
+        cache = self.__dict__.setdefault("_pair_cache", {})
+        if level not in cache:
+            cnt = C.c_int64(0)
+            check(lib().hp_tree_pairs(self._h, level, C.byref(cnt), None))
+            arr = np.zeros(max(2 * cnt.value, 2), dtype=np.int32)
+            check(lib().hp_tree_pairs(self._h, level, C.byref(cnt), iptr(arr)))
+            cache[level] = [(int(arr[2 * i]), int(arr[2 * i + 1])) for i in range(cnt.value)]
+        return cache[level]  # shared: callers must not mutate
 
     def admissible_pairs(self, level: int):
         return self._pairs(level)

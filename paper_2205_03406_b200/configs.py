@@ -12,9 +12,17 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import gaussian_matrix, mix_seed, random_cloud
-
 S0 = 7
+
+
+def _gen(gen):
+    """The point generators (random_cloud, gaussian_matrix, mix_seed): the
+    package's C ABI by default; bench.py's reference arm passes the oracle's
+    restatement so that arm never loads the product library."""
+    if gen is None:
+        import paper_2205_03406_b200 as pkg  # the C ABI loads on first call
+        return pkg
+    return gen
 
 
 @dataclass
@@ -30,15 +38,15 @@ class Workload:
     param: float = 1.0
     description: str = ""
 
-    def points(self) -> np.ndarray:
-        return make_points(self.name, self.n)
+    def points(self, gen=None) -> np.ndarray:
+        return make_points(self.name, self.n, gen)
 
 
-def starfish_points(n: int, seed: int) -> np.ndarray:
+def starfish_points(n: int, seed: int, gen=None) -> np.ndarray:
     """Config 3: r(t) = 1 + 0.3 cos 5t; half the parameters uniform on
     [0, 2 pi), half on [0, t*) where t* is the first grid point t_j = 2 pi j / 2^20
     whose trapezoid-rule arclength reaches 10% of the total."""
-    u = random_cloud(n, 1, seed)[:, 0]
+    u = _gen(gen).random_cloud(n, 1, seed)[:, 0]
     m = 1 << 20
     t = 2.0 * math.pi * np.arange(m + 1) / m
     r = 1.0 + 0.3 * np.cos(5.0 * t)
@@ -55,7 +63,7 @@ def starfish_points(n: int, seed: int) -> np.ndarray:
     return np.stack([rr * np.cos(tt), rr * np.sin(tt)], axis=1)
 
 
-def fibonacci_sphere(n: int, seed: int) -> np.ndarray:
+def fibonacci_sphere(n: int, seed: int, gen=None) -> np.ndarray:
     """Config 4: Fibonacci lattice plus 1e-3 seeded Gaussian jitter, projected
     back to the unit sphere."""
     i = np.arange(n, dtype=np.float64)
@@ -63,21 +71,22 @@ def fibonacci_sphere(n: int, seed: int) -> np.ndarray:
     phi = i * math.pi * (3.0 - math.sqrt(5.0))
     rho = np.sqrt(1.0 - z * z)
     f = np.stack([rho * np.cos(phi), rho * np.sin(phi), z], axis=1)
-    f = f + 1e-3 * gaussian_matrix(n, 3, seed)
+    f = f + 1e-3 * _gen(gen).gaussian_matrix(n, 3, seed)
     return f / np.linalg.norm(f, axis=1, keepdims=True)
 
 
-def make_points(name: str, n: int) -> np.ndarray:
+def make_points(name: str, n: int, gen=None) -> np.ndarray:
+    g = _gen(gen)
     if name == "c1":
-        return np.sort(random_cloud(n, 1, mix_seed(S0, 0xC1)), axis=0)
+        return np.sort(g.random_cloud(n, 1, g.mix_seed(S0, 0xC1)), axis=0)
     if name == "c2":
-        return np.sort(random_cloud(n, 1, mix_seed(S0, 0xC2)), axis=0)
+        return np.sort(g.random_cloud(n, 1, g.mix_seed(S0, 0xC2)), axis=0)
     if name == "c3":
-        return starfish_points(n, mix_seed(S0, 0xC3))
+        return starfish_points(n, g.mix_seed(S0, 0xC3), gen)
     if name == "c4":
-        return fibonacci_sphere(n, mix_seed(S0, 0xC4))
+        return fibonacci_sphere(n, g.mix_seed(S0, 0xC4), gen)
     if name == "c5":
-        return random_cloud(n, 3, mix_seed(S0, 0xC5))
+        return g.random_cloud(n, 3, g.mix_seed(S0, 0xC5))
     raise ValueError(name)
 
 
