@@ -5,6 +5,7 @@ TEST INFRASTRUCTURE ONLY: never imported by the product package.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -749,14 +750,28 @@ class KernelOperator:
     apply_adjoint = apply  # symmetric kernels
 
     def apply_rows(self, x, rows, adjoint=False):
-        """(K x)[rows] over the nonzero rows of x only (K symmetric)."""
+        """(K x)[rows] over the nonzero rows of x only (K symmetric); row
+        chunks on a thread pool (numpy releases the GIL in both steps)."""
         nz = _nonzero_rows(x)
         y = np.empty((len(rows), x.shape[1]))
         xn = x[nz]
-        for i0 in range(0, len(rows), self.chunk):
-            r = rows[i0:i0 + self.chunk]
+        xz = self.x[nz]
+        step = max(64, min(self.chunk, (1 << 22) // max(len(nz), 1)))
+
+        def work(i0):
+            r = rows[i0:i0 + step]
             same = (r[:, None] == nz[None, :]) if self.kind != "exp" else None
-            y[i0:i0 + len(r)] = kernel_matrix(self.kind, self.x[r], self.x[nz], same, self.param) @ xn
+            y[i0:i0 + len(r)] = kernel_matrix(self.kind, self.x[r], xz, same, self.param) @ xn
+
+        starts = list(range(0, len(rows), step))
+        threads = getattr(self, "threads", os.cpu_count() or 1)
+        if threads > 1 and len(starts) > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            with _small_blas(), ThreadPoolExecutor(threads) as ex:
+                list(ex.map(work, starts))
+        else:
+            for i0 in starts:
+                work(i0)
         return y
 
 
@@ -875,6 +890,18 @@ class PhaseTimes(dict):
         self[key] = self.get(key, 0.0) + (time.perf_counter() - t0)
 
 
+def _pair_map(fn, pairs):
+    """fn over the pairs in order; independent per-pair solves run on a
+    thread pool when there are many (LAPACK releases the GIL; the results and
+    their order are those of the serial loop, proj/src/peeling.cpp:245-270)."""
+    threads = os.cpu_count() or 1
+    if threads == 1 or len(pairs) < 256:
+        return [fn(ab) for ab in pairs]
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(fn, pairs, chunksize=64))
+
+
 def _small_blas():
     """Per-pair QR / SVD / small GEMMs on one BLAS thread: a threaded BLAS is
     ~50x slower on 64 x 48 matrices (thread start-up per call), and the
@@ -960,31 +987,35 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict
         u_bases = {}
         t0 = _now()
         with _small_blas():
-            for a, b in pairs:
-                y = ys[plan.block_to_matrix[(a, b)]]
-                u_bases[(a, b)] = qr_orthonormal(y[tree.box(a).points], k)
+            qs = _pair_map(lambda ab: qr_orthonormal(ys[plan.block_to_matrix[ab]][tree.box(ab[0]).points], k),
+                           pairs)
+            for ab, q in zip(pairs, qs):
+                u_bases[ab] = q
         times.add("qr", t0)
         zs, acols = _residual_samples(op, rep, l - 1, plan, True, phase=1, times=times, restrict=restrict)
         if capture is not None:
             capture[l] = {(a, b): (ys[plan.block_to_matrix[(a, b)]][tree.box(a).points],
                                    zs[plan.block_to_matrix[(a, b)]][tree.box(a).points])
                           for a, b in pairs}
+        def solve(ab):
+            a, b = ab
+            z = zs[plan.block_to_matrix[(b, a)]]
+            u = u_bases[(a, b)]
+            v = qr_orthonormal(z[tree.box(b).points], k)
+            g = payload_gaussian(tree, b, r, seed, l, 0)
+            gp = payload_gaussian(tree, a, r, seed, l, 1)
+            yb = ys[plan.block_to_matrix[(a, b)]][tree.box(a).points]
+            middle = gp.T @ yb
+            left = pinv_apply(gp.T @ u, middle)
+            bmat = pinv_apply((v.T @ g).T, left.T).T
+            return (u, bmat, v)
+
+        t0 = _now()
         with _small_blas():
-            for a, b in pairs:
-                z = zs[plan.block_to_matrix[(b, a)]]
-                u = u_bases[(a, b)]
-                t0 = _now()
-                v = qr_orthonormal(z[tree.box(b).points], k)
-                times.add("qr", t0)
-                t0 = _now()
-                g = payload_gaussian(tree, b, r, seed, l, 0)
-                gp = payload_gaussian(tree, a, r, seed, l, 1)
-                yb = ys[plan.block_to_matrix[(a, b)]][tree.box(a).points]
-                middle = gp.T @ yb
-                left = pinv_apply(gp.T @ u, middle)
-                bmat = pinv_apply((v.T @ g).T, left.T).T
-                times.add("bsolve", t0)
-                rep.levels[l][(a, b)] = (u, bmat, v)
+            blocks = _pair_map(solve, pairs)
+        times.add("bsolve", t0)  # the V QR included
+        for ab, blk in zip(pairs, blocks):
+            rep.levels[l][ab] = blk
         rep.built_level = l
         report.append({"phase": "h1", "level": l, "colors": len(plan.matrices),
                        "forward_cols": fcols, "adjoint_cols": acols})

@@ -75,11 +75,11 @@ def test_exact_recovery_adaptive_2d(hp, gpu_available):
 
 
 def _compare_with_oracle(hp, pts, leaf, op_dev, op_ref, k, p, seed, sample_tol=1e-12,
-                         exact_ranks=False):
+                         exact_ranks=False, restrict=False):
     t, ot = both_trees(hp, pts, leaf)
     rep = hp.compress(op_dev, t, rank=k, oversample=p, seed=seed, capture=True)
     cap, leaf_cap = {}, {}
-    orep, oreport = O.compress(op_ref, ot, k, p, seed, cap, leaf_cap)
+    orep, oreport = O.compress(op_ref, ot, k, p, seed, cap, leaf_cap, restrict=restrict)
     # report counts (proj/src/peeling.cpp:478-488)
     got_phases = [(ph["phase"], ph["level"], ph["colors"], ph["forward_cols"], ph["adjoint_cols"])
                   for ph in rep.report["phases"]]

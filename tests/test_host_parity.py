@@ -32,6 +32,10 @@ def test_tree_and_adjacency_bit_exact(hp, name, pts, leaf):
     t = hp.build_tree(pts, leaf)
     ot = O.BoxTree(O.PointCloud(pts), leaf)
     oadj = O.adjacency(ot)
+    _trees_equal(t, ot, oadj)
+
+
+def _trees_equal(t, ot, oadj):
     assert (t.depth, t.num_boxes, t.num_points) == (ot.depth, ot.num_boxes, ot.num_points)
     assert t.fully_populated == ot.is_fully_populated()
     assert t.max_leaf_size == ot.max_leaf_size()
@@ -59,7 +63,11 @@ def _compare_plan(hp, t, ot, oadj, level, mode, omode):
         assert tuple(tuple(x) for x in got["payload"]) == want.payload
         assert tuple(got["zero"]) == want.zero
         assert [tuple(o) for o in got["owners"]] == want.owners
-    if len(sets) <= 2500:  # literal O(V^2) oracle scan
+    if len(sets) <= 2500:  # the oracle's three graph builds agree with the literal O(V^2) scan
+        from oracle import hpeel_ref
+        lit = O.build_graph_literal(sets)
+        assert lit == O.build_graph(sets) == hpeel_ref._build_graph_indexed(sets)
+    if True:
         edges = O.build_graph(sets)
         assert p.edges == edges
         col, n = O.plan_coloring(ot, sets, edges, omode)
@@ -79,6 +87,50 @@ def test_h1_and_leaf_plans_bit_exact(hp, name, pts, leaf):
     for l in range(2, ot.depth + 1):
         _compare_plan(hp, t, ot, oadj, l, "h1", O.H1)
     _compare_plan(hp, t, ot, oadj, ot.depth, "leaf", O.LEAF)
+
+
+def _plans_equal_at_scale(hp, t, ot, oadj, levels, leaf=True):
+    """Constraint sets, DSatur / plan colorings and per-color payload lists of
+    the product (implicit graph, the path compress() takes) equal the
+    oracle's (indexed graph build, same edge set as the pairwise scan)."""
+    modes = [("h1", O.H1, l) for l in levels] + ([("leaf", O.LEAF, ot.depth)] if leaf else [])
+    for mode, omode, level in modes:
+        p = hp.plan(t, level, mode, 12, 7, 0, implicit=True)
+        op = O.make_plan(ot, oadj, level, omode, 12, 7, 0)
+        assert p.n_vertices == len(op.sets), (mode, level)
+        if not op.sets:
+            continue
+        for got, want in zip(p.sets, op.sets):
+            assert tuple(got["zero"]) == want.zero and got["payload"][0][0] == want.payload[0][0]
+        assert p.color == list(op.color), (mode, level)
+        assert p.n_colors == len(op.matrices)
+        assert p.color_payload == [[b for b, _ in m.payload] for m in op.matrices], (mode, level)
+
+
+def test_full_size_c3_planning_bit_exact(hp):
+    """Config 3 at its full N = 2^18 (the bench workload): tree, adjacency,
+    pair lists and every H1 level's and the leaf phase's coloring equal the
+    oracle's."""
+    pts = configs.make_points("c3", 262144)
+    t = hp.build_tree(pts, 128)
+    ot = O.BoxTree(O.PointCloud(pts), 128)
+    oadj = O.adjacency(ot)
+    _trees_equal(t, ot, oadj)
+    _plans_equal_at_scale(hp, t, ot, oadj, range(2, ot.depth + 1))
+
+
+@pytest.mark.gpu  # CPU-only but ~10 minutes of oracle planning: runs with the GPU-box suite
+@pytest.mark.timeout(3600)
+def test_full_size_c4_planning_bit_exact(hp):
+    """Config 4 at N = 2^20 (the north-star target): tree, adjacency, pair
+    lists and every H1 level's coloring equal the oracle's. (Its leaf
+    graph, 1.5e9 edges, is beyond the oracle's reach.)"""
+    pts = configs.make_points("c4", 1 << 20)
+    t = hp.build_tree(pts, 256)
+    ot = O.BoxTree(O.PointCloud(pts), 256)
+    oadj = O.adjacency(ot)
+    _trees_equal(t, ot, oadj)
+    _plans_equal_at_scale(hp, t, ot, oadj, range(2, ot.depth + 1), leaf=False)
 
 
 def test_inverted_index_graph_equals_pairwise_scan(hp):
