@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <thread>
 #include <tuple>
+#include <unordered_map>
 
 #include "rng.hpp"
 
@@ -17,113 +18,118 @@ namespace hpeel {
 
 namespace {
 
-std::vector<int> merge_sorted(const std::vector<int>& a, const std::vector<int>& b) {
+// Constraint sets keyed by their literal (payload, zero) requirement
+// (proj/src/coloring.cpp:26-51): a repeated requirement only gains an owner,
+// so the first occurrence fixes the vertex id. Requirements are hashed and
+// compared only within a hash bucket.
+class RequirementTable {
+ public:
+  void add(std::vector<std::pair<int, PayloadTag>>&& payload, std::vector<int>&& zero, std::pair<int, int> owner) {
+    const std::uint64_t h = digest(payload, zero);
+    auto& bucket = by_hash_[h];
+    for (int id : bucket) {
+      ConstraintSet& s = sets_[size_t(id)];
+      if (s.payload == payload && s.zero == zero) {
+        s.owners.push_back(owner);
+        return;
+      }
+    }
+    bucket.push_back(int(sets_.size()));
+    ConstraintSet s;
+    s.payload = std::move(payload);
+    s.zero = std::move(zero);
+    s.owners.push_back(owner);
+    sets_.push_back(std::move(s));
+  }
+  std::vector<ConstraintSet> release() { return std::move(sets_); }
+
+ private:
+  static std::uint64_t digest(const std::vector<std::pair<int, PayloadTag>>& payload, const std::vector<int>& zero) {
+    std::uint64_t h = 0x84222325cbf29ce4ull;
+    auto mix = [&](std::uint64_t v) { h = (h ^ v) * 0x100000001b3ull + (h >> 29); };
+    for (const auto& [box, tag] : payload) mix((std::uint64_t(unsigned(box)) << 8) | std::uint64_t(tag));
+    mix(~std::uint64_t(0));
+    for (int z : zero) mix(std::uint64_t(unsigned(z)));
+    return h;
+  }
+  std::unordered_map<std::uint64_t, std::vector<int>> by_hash_;
+  std::vector<ConstraintSet> sets_;
+};
+
+// sorted union of sorted lists
+std::vector<int> union_of(std::initializer_list<const std::vector<int>*> lists) {
   std::vector<int> out;
-  out.reserve(a.size() + b.size());
-  std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(out));
+  for (const auto* l : lists) out.insert(out.end(), l->begin(), l->end());
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
   return out;
 }
 
-void drop(std::vector<int>& v, int value) {
-  v.erase(std::remove(v.begin(), v.end(), value), v.end());
+// copy of a sorted list without one value
+std::vector<int> without(const std::vector<int>& sorted, int value) {
+  std::vector<int> out;
+  out.reserve(sorted.size());
+  const auto at = std::lower_bound(sorted.begin(), sorted.end(), value);
+  out.insert(out.end(), sorted.begin(), at);
+  out.insert(out.end(), at != sorted.end() && *at == value ? at + 1 : at, sorted.end());
+  return out;
 }
-
-// Dedup keyed by the literal (payload, zero) requirement
-// (proj/src/coloring.cpp:26-51); first occurrence fixes the vertex id.
-class Dedup {
- public:
-  void add(std::vector<std::pair<int, PayloadTag>> payload, std::vector<int> zero,
-           std::pair<int, int> owner) {
-    auto key = std::make_pair(std::move(payload), std::move(zero));
-    auto it = index_.find(key);
-    if (it != index_.end()) {
-      sets_[size_t(it->second)].owners.push_back(owner);
-      return;
-    }
-    ConstraintSet s;
-    s.payload = key.first;
-    s.zero = key.second;
-    s.owners.push_back(owner);
-    index_.emplace(std::move(key), int(sets_.size()));
-    sets_.push_back(std::move(s));
-  }
-  std::vector<ConstraintSet> take() { return std::move(sets_); }
-
- private:
-  std::map<std::pair<std::vector<std::pair<int, PayloadTag>>, std::vector<int>>, int> index_;
-  std::vector<ConstraintSet> sets_;
-};
 
 }  // namespace
 
 std::vector<ConstraintSet> build_constraints(const BoxTree& tree, const AdjacencyInfo& adj,
                                              int level, SampleMode mode) {
-  Dedup dd;
-  switch (mode) {
-    case SampleMode::kH1: {
-      int last_alpha = -1;
-      std::vector<int> reach;
-      for (auto [alpha, beta] : admissible_pairs(tree, adj, level)) {
-        if (alpha != last_alpha) {
-          reach = merge_sorted(adj.neighbors[size_t(alpha)],
-                               merge_sorted(adj.interaction[size_t(alpha)],
-                                            adj.coarse_leaf_neighbors[size_t(alpha)]));
-          last_alpha = alpha;
-        }
-        std::vector<int> zero = reach;
-        drop(zero, beta);
-        dd.add({{beta, PayloadTag::kGaussian}}, std::move(zero), {alpha, beta});
+  RequirementTable table;
+  if (mode == SampleMode::kUnifStage2)
+    throw std::invalid_argument("unif-stage2 constraints need the uniform driver (out of scope)");
+  if (mode == SampleMode::kH1) {
+    // (alpha, beta): payload {beta: Gaussian}, zero N(alpha) u I(alpha) u
+    // CL(alpha) minus beta; one union per row box alpha
+    std::vector<int> reach;
+    int reach_of = -1;
+    for (const auto& [alpha, beta] : admissible_pairs(tree, adj, level)) {
+      if (alpha != reach_of) {
+        reach = union_of({&adj.neighbors[size_t(alpha)], &adj.interaction[size_t(alpha)],
+                          &adj.coarse_leaf_neighbors[size_t(alpha)]});
+        reach_of = alpha;
       }
-      break;
+      table.add({{beta, PayloadTag::kGaussian}}, without(reach, beta), {alpha, beta});
     }
-    case SampleMode::kUnifStage1: {
-      if (level < 2 || level > tree.depth()) throw std::invalid_argument("sampling level out of range");
-      for (int alpha : tree.level_boxes(level)) {
-        if (adj.interaction[size_t(alpha)].empty()) continue;
-        std::vector<std::pair<int, PayloadTag>> payload;
-        for (int beta : adj.interaction[size_t(alpha)]) payload.emplace_back(beta, PayloadTag::kGaussian);
-        dd.add(std::move(payload),
-               merge_sorted(adj.neighbors[size_t(alpha)], adj.coarse_leaf_neighbors[size_t(alpha)]),
-               {alpha, -1});
-      }
-      break;
+  } else if (mode == SampleMode::kUnifStage1) {
+    if (level < 2 || level > tree.depth()) throw std::invalid_argument("sampling level out of range");
+    // alpha: payload = every interaction box, zero = N(alpha) u CL(alpha)
+    for (int alpha : tree.level_boxes(level)) {
+      const auto& il = adj.interaction[size_t(alpha)];
+      if (il.empty()) continue;
+      std::vector<std::pair<int, PayloadTag>> payload;
+      payload.reserve(il.size());
+      for (int beta : il) payload.emplace_back(beta, PayloadTag::kGaussian);
+      table.add(std::move(payload),
+                union_of({&adj.neighbors[size_t(alpha)], &adj.coarse_leaf_neighbors[size_t(alpha)]}),
+                {alpha, -1});
     }
-    case SampleMode::kLeaf: {
-      for (auto [lambda, mu] : dense_pairs(tree, adj)) {
-        std::vector<int> zero = adj.dense_partners[size_t(lambda)];
-        drop(zero, mu);
-        dd.add({{mu, PayloadTag::kIdentity}}, std::move(zero), {lambda, mu});
-      }
-      break;
-    }
-    case SampleMode::kUnifStage2:
-      throw std::invalid_argument("unif-stage2 constraints need the uniform driver (out of scope)");
+  } else {
+    // leaf probes (lambda, mu): identity payload on mu, zero = the other dense partners
+    for (const auto& [lambda, mu] : dense_pairs(tree, adj))
+      table.add({{mu, PayloadTag::kIdentity}}, without(adj.dense_partners[size_t(lambda)], mu), {lambda, mu});
   }
-  return dd.take();
+  return table.release();
 }
 
 bool incompatible(const ConstraintSet& a, const ConstraintSet& b) {
-  auto hits = [](const ConstraintSet& s, const ConstraintSet& t) {
-    auto p = s.payload.begin();
-    auto z = t.zero.begin();
-    while (p != s.payload.end() && z != t.zero.end()) {
-      if (p->first < *z) ++p;
-      else if (*z < p->first) ++z;
-      else return true;
-    }
-    return false;
+  // proj/src/coloring.cpp:115-146: a payload box of one set lies in the
+  // other's zero set, or both carry a box with different tags. Payload lists
+  // are short, so each entry is looked up in the other sorted lists.
+  auto payload_hits_zero = [](const ConstraintSet& p, const ConstraintSet& z) {
+    return std::any_of(p.payload.begin(), p.payload.end(), [&](const std::pair<int, PayloadTag>& e) {
+      return std::binary_search(z.zero.begin(), z.zero.end(), e.first);
+    });
   };
-  if (hits(a, b) || hits(b, a)) return true;
-  auto x = a.payload.begin();
-  auto y = b.payload.begin();
-  while (x != a.payload.end() && y != b.payload.end()) {
-    if (x->first < y->first) ++x;
-    else if (y->first < x->first) ++y;
-    else {
-      if (x->second != y->second) return true;
-      ++x;
-      ++y;
-    }
+  if (payload_hits_zero(a, b) || payload_hits_zero(b, a)) return true;
+  for (const auto& [box, tag] : a.payload) {
+    const auto it = std::lower_bound(b.payload.begin(), b.payload.end(), box,
+                                     [](const std::pair<int, PayloadTag>& e, int v) { return e.first < v; });
+    if (it != b.payload.end() && it->first == box && it->second != tag) return true;
   }
   return false;
 }

@@ -12,6 +12,7 @@
 #include <fstream>
 #include <numeric>
 #include <stdexcept>
+#include <type_traits>
 
 #include "engine.cuh"
 #include "peeling.hpp"
@@ -27,86 +28,115 @@ constexpr std::uint64_t kRepMagic = 0x3150524C45455048ull;    // "HPEELRP1"
 constexpr std::uint64_t kDenseMagic = 0x314D444C45455048ull;  // "HPEELDM1"
 constexpr std::uint8_t kFormatH1 = 1;                         // RepFormat::kH1
 
-struct Writer {
-  std::ofstream out;
-  explicit Writer(const std::string& path) : out(path, std::ios::binary | std::ios::trunc) {
-    if (!out) throw std::runtime_error("cannot write " + path);
-  }
+// Little-endian byte image of a file, built in memory and written at once.
+class ByteSink {
+ public:
   template <typename T>
-  void put(T v) {
-    out.write(reinterpret_cast<const char*>(&v), sizeof(T));
+  ByteSink& operator<<(T v) {
+    static_assert(std::is_trivially_copyable<T>::value, "plain values only");
+    const char* p = reinterpret_cast<const char*>(&v);
+    bytes_.insert(bytes_.end(), p, p + sizeof(T));
+    return *this;
   }
-  void put_ints(const std::vector<int>& v) {
-    put<std::int32_t>(std::int32_t(v.size()));
-    for (int x : v) put<std::int32_t>(x);
+  void raw(const void* p, size_t n) {
+    const char* c = static_cast<const char*>(p);
+    bytes_.insert(bytes_.end(), c, c + n);
   }
-  void put_matrix(std::int64_t rows, std::int64_t cols, const double* data) {
-    put<std::int64_t>(rows);
-    put<std::int64_t>(cols);
-    out.write(reinterpret_cast<const char*>(data), std::streamsize(sizeof(double) * size_t(rows * cols)));
+  // int32 count, then the values
+  void list(const std::vector<int>& v) {
+    *this << std::int32_t(v.size());
+    for (int x : v) *this << std::int32_t(x);
   }
+  // (rows i64, cols i64, column-major doubles)
+  void matrix(std::int64_t rows, std::int64_t cols, const double* data) {
+    *this << rows << cols;
+    raw(data, sizeof(double) * size_t(rows * cols));
+  }
+  void save(const std::string& path) const {
+    std::ofstream out(path, std::ios::binary | std::ios::trunc);
+    if (!out) throw std::runtime_error("cannot write " + path);
+    out.write(bytes_.data(), std::streamsize(bytes_.size()));
+    if (!out) throw std::runtime_error("write failed: " + path);
+  }
+
+ private:
+  std::vector<char> bytes_;
 };
 
-struct Reader {
-  std::ifstream in;
-  explicit Reader(const std::string& path) : in(path, std::ios::binary) {
+// Bounds-checked cursor over a whole file read into memory.
+class ByteSource {
+ public:
+  explicit ByteSource(const std::string& path) {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
     if (!in) throw std::runtime_error("cannot read " + path);
+    bytes_.resize(size_t(in.tellg()));
+    in.seekg(0);
+    in.read(bytes_.data(), std::streamsize(bytes_.size()));
   }
   template <typename T>
-  T get() {
+  T take() {
     T v;
-    in.read(reinterpret_cast<char*>(&v), sizeof(T));
-    if (!in) throw std::runtime_error("truncated representation file");
+    std::memcpy(&v, next(sizeof(T)), sizeof(T));
     return v;
   }
-  std::vector<int> get_ints() {
-    const auto n = get<std::int32_t>();
+  std::vector<int> list() {
+    const auto n = take<std::int32_t>();
     if (n < 0) throw std::runtime_error("corrupt representation file");
     std::vector<int> v(static_cast<size_t>(n));
-    for (auto& x : v) x = get<std::int32_t>();
+    for (auto& x : v) x = take<std::int32_t>();
     return v;
   }
-  Matrix get_matrix() {
-    const auto rows = get<std::int64_t>();
-    const auto cols = get<std::int64_t>();
-    if (rows < 0 || cols < 0) throw std::runtime_error("corrupt representation file");
+  Matrix matrix() {
+    const auto rows = take<std::int64_t>();
+    const auto cols = take<std::int64_t>();
+    if (rows < 0 || cols < 0 || (cols > 0 && rows > std::int64_t(remaining() / 8) / cols))
+      throw std::runtime_error("corrupt representation file");
     Matrix m(rows, cols);
-    in.read(reinterpret_cast<char*>(m.data()), std::streamsize(sizeof(double) * size_t(rows * cols)));
-    if (!in) throw std::runtime_error("truncated representation file");
+    std::memcpy(m.data(), next(sizeof(double) * size_t(rows * cols)), sizeof(double) * size_t(rows * cols));
     return m;
   }
+
+ private:
+  size_t remaining() const { return bytes_.size() - pos_; }
+  const char* next(size_t n) {
+    if (n > remaining()) throw std::runtime_error("truncated representation file");
+    const char* p = bytes_.data() + pos_;
+    pos_ += n;
+    return p;
+  }
+  std::vector<char> bytes_;
+  size_t pos_ = 0;
 };
 
-void write_tree(Writer& w, const BoxTree& tree) {
-  w.put<std::int32_t>(tree.dim());
-  w.put<std::int32_t>(tree.leaf_capacity());
-  w.put<std::int64_t>(tree.num_points());
-  w.put<std::int32_t>(tree.num_boxes());
+// tree section: dim, leaf capacity, n, box count, then per box level,
+// parent, coordinates, children, points (the reference's field order)
+void encode_tree(ByteSink& out, const BoxTree& tree) {
+  out << std::int32_t(tree.dim()) << std::int32_t(tree.leaf_capacity()) << std::int64_t(tree.num_points())
+      << std::int32_t(tree.num_boxes());
   for (const Box& b : tree.boxes()) {
-    w.put<std::int32_t>(b.level);
-    w.put<std::int32_t>(b.parent);
-    for (std::int64_t c : b.coord) w.put<std::int64_t>(c);
-    w.put_ints(b.children);
-    w.put_ints(b.points);
+    out << std::int32_t(b.level) << std::int32_t(b.parent);
+    for (std::int64_t c : b.coord) out << c;
+    out.list(b.children);
+    out.list(b.points);
   }
 }
 
-std::shared_ptr<const BoxTree> read_tree(Reader& r) {
-  const int dim = r.get<std::int32_t>();
-  const int leaf = r.get<std::int32_t>();
-  const auto n = r.get<std::int64_t>();
-  const int nboxes = r.get<std::int32_t>();
-  if (dim < 1 || n < 0 || nboxes < 0) throw std::runtime_error("corrupt representation file");
-  std::vector<Box> boxes(static_cast<size_t>(nboxes));
-  for (int i = 0; i < nboxes; ++i) {
-    Box& b = boxes[size_t(i)];
-    b.id = i;
-    b.level = r.get<std::int32_t>();
-    b.parent = r.get<std::int32_t>();
+std::shared_ptr<const BoxTree> decode_tree(ByteSource& in) {
+  const int dim = in.take<std::int32_t>();
+  const int leaf = in.take<std::int32_t>();
+  const auto n = in.take<std::int64_t>();
+  const int count = in.take<std::int32_t>();
+  if (dim < 1 || n < 0 || count < 0) throw std::runtime_error("corrupt representation file");
+  std::vector<Box> boxes(static_cast<size_t>(count));
+  int id = 0;
+  for (Box& b : boxes) {
+    b.id = id++;
+    b.level = in.take<std::int32_t>();
+    b.parent = in.take<std::int32_t>();
     b.coord.resize(size_t(dim));
-    for (auto& c : b.coord) c = r.get<std::int64_t>();
-    b.children = r.get_ints();
-    b.points = r.get_ints();
+    for (auto& c : b.coord) c = in.take<std::int64_t>();
+    b.children = in.list();
+    b.points = in.list();
   }
   return std::make_shared<const BoxTree>(BoxTree::from_parts(dim, leaf, n, std::move(boxes)));
 }
@@ -134,28 +164,21 @@ void save_rep(const std::string& path, const H1Rep& rep) {
     if (rep.dense_doubles > 0 && rep.d_dense)
       HP_CUDA(cudaMemcpy(hd.data(), rep.d_dense, size_t(rep.dense_doubles) * 8, cudaMemcpyDeviceToHost));
   }
-  Writer w(path);
-  w.put<std::uint64_t>(kRepMagic);
-  // write_meta (serialize.cpp:128-138)
-  w.put<std::uint8_t>(kFormatH1);
-  w.put<std::int64_t>(tree.num_points());
-  w.put<std::int32_t>(tree.dim());
-  w.put<std::int32_t>(tree.depth());
-  w.put<std::int32_t>(tree.leaf_capacity());
-  w.put<std::int32_t>(k);
-  w.put<std::int32_t>(rep.built_level);
-  w.put<std::uint8_t>(rep.dense_ready ? 1 : 0);
-  write_tree(w, tree);
+  ByteSink w;
+  // magic, then the meta block (proj/src/serialize.cpp:128-138)
+  w << kRepMagic << kFormatH1 << std::int64_t(tree.num_points()) << std::int32_t(tree.dim())
+    << std::int32_t(tree.depth()) << std::int32_t(tree.leaf_capacity()) << std::int32_t(k)
+    << std::int32_t(rep.built_level) << std::uint8_t(rep.dense_ready ? 1 : 0);
+  encode_tree(w, tree);
   std::vector<double> buf;
   for (int l = 0; l <= tree.depth(); ++l) {
     const H1Rep::LevelData* ld = size_t(l) < rep.levels.size() ? &rep.levels[size_t(l)] : nullptr;
     const size_t np = ld ? ld->pairs.size() : 0;
-    w.put<std::int32_t>(std::int32_t(np));
+    w << std::int32_t(np);
     if (!np) continue;
     for (size_t p : sorted_order(ld->pairs)) {
       const auto [a, b] = ld->pairs[p];
-      w.put<std::int32_t>(a);
-      w.put<std::int32_t>(b);
+      w << std::int32_t(a) << std::int32_t(b);
       const int ma = int(lay.count[size_t(a)]), mb = int(lay.count[size_t(b)]);
       const int ku = ld->ku[p], kv = ld->kv[p];
       // U rows back to box.points order (arena: tree order, ld = |I_a|)
@@ -166,45 +189,44 @@ void save_rep(const std::string& path, const H1Rep& rep) {
           const std::int64_t tr = lay.inv[size_t(pts[size_t(s)])] - lay.start[size_t(box)];
           for (int j = 0; j < kk; ++j) buf[size_t(s) + size_t(j) * size_t(m)] = hf[size_t(off + tr + std::int64_t(j) * m)];
         }
-        w.put_matrix(m, kk, buf.data());
+        w.matrix(m, kk, buf.data());
       };
       put_rows(a, ma, ku, ld->uoff[p]);
       buf.assign(size_t(ku) * size_t(kv), 0.0);
       for (int i = 0; i < ku; ++i)
         for (int j = 0; j < kv; ++j) buf[size_t(i) + size_t(j) * size_t(ku)] = hf[size_t(ld->boff[p] + i + std::int64_t(j) * k)];
-      w.put_matrix(ku, kv, buf.data());
+      w.matrix(ku, kv, buf.data());
       put_rows(b, mb, kv, ld->voff[p]);
     }
   }
   // dense blocks (leaf rows are in box.points order in the arena)
   const size_t nd = rep.dense_ready ? rep.dense.pairs.size() : 0;
-  w.put<std::int32_t>(std::int32_t(nd));
+  w << std::int32_t(nd);
   if (nd) {
     for (size_t p : sorted_order(rep.dense.pairs)) {
       const auto [lam, mu] = rep.dense.pairs[p];
-      w.put<std::int32_t>(lam);
-      w.put<std::int32_t>(mu);
+      w << std::int32_t(lam) << std::int32_t(mu);
       const std::int64_t ml = std::int64_t(tree.box(lam).points.size()), mm = std::int64_t(tree.box(mu).points.size());
-      w.put_matrix(ml, mm, hd.data() + rep.dense.off[p]);
+      w.matrix(ml, mm, hd.data() + rep.dense.off[p]);
     }
   }
-  if (!w.out) throw std::runtime_error("write failed: " + path);
+  w.save(path);
 }
 
 std::shared_ptr<H1Rep> load_rep(const std::string& path, int device) {
-  Reader r(path);
-  if (r.get<std::uint64_t>() != kRepMagic) throw std::runtime_error("not a representation file: " + path);
-  const std::uint8_t format = r.get<std::uint8_t>();
-  const auto n = r.get<std::int64_t>();
-  const int dim = r.get<std::int32_t>();
-  const int depth = r.get<std::int32_t>();
-  (void)r.get<std::int32_t>();  // leaf capacity (also in the tree)
-  const int rank = r.get<std::int32_t>();
-  const int built_level = r.get<std::int32_t>();
-  const bool dense_ready = r.get<std::uint8_t>() != 0;
+  ByteSource r(path);
+  if (r.take<std::uint64_t>() != kRepMagic) throw std::runtime_error("not a representation file: " + path);
+  const std::uint8_t format = r.take<std::uint8_t>();
+  const auto n = r.take<std::int64_t>();
+  const int dim = r.take<std::int32_t>();
+  const int depth = r.take<std::int32_t>();
+  (void)r.take<std::int32_t>();  // leaf capacity (also in the tree)
+  const int rank = r.take<std::int32_t>();
+  const int built_level = r.take<std::int32_t>();
+  const bool dense_ready = r.take<std::uint8_t>() != 0;
   if (format != kFormatH1)
     throw std::invalid_argument("only the h1 representation format is on the device path");
-  auto tree = read_tree(r);
+  auto tree = decode_tree(r);
   if (tree->num_points() != n || tree->dim() != dim || tree->depth() != depth)
     throw std::runtime_error("representation meta and tree disagree");
   auto rep = std::make_shared<H1Rep>();
@@ -220,15 +242,15 @@ std::shared_ptr<H1Rep> load_rep(const std::string& path, int device) {
   const int k = rep->rank;
   std::vector<double> hf;
   for (int l = 0; l <= depth; ++l) {
-    const auto count = r.get<std::int32_t>();
+    const auto count = r.take<std::int32_t>();
     if (count < 0) throw std::runtime_error("corrupt representation file");
     auto& ld = rep->levels[size_t(l)];
     for (std::int32_t i = 0; i < count; ++i) {
-      const int a = r.get<std::int32_t>();
-      const int b = r.get<std::int32_t>();
+      const int a = r.take<std::int32_t>();
+      const int b = r.take<std::int32_t>();
       if (a < 0 || b < 0 || a >= tree->num_boxes() || b >= tree->num_boxes())
         throw std::runtime_error("corrupt representation file");
-      const Matrix u = r.get_matrix(), bb = r.get_matrix(), v = r.get_matrix();
+      const Matrix u = r.matrix(), bb = r.matrix(), v = r.matrix();
       const int ma = int(lay.count[size_t(a)]), mb = int(lay.count[size_t(b)]);
       if (u.rows() != ma || v.rows() != mb || u.cols() > k || v.cols() > k || bb.rows() != u.cols() ||
           bb.cols() != v.cols())
@@ -255,12 +277,12 @@ std::shared_ptr<H1Rep> load_rep(const std::string& path, int device) {
     }
   }
   std::vector<double> hd;
-  const auto nd = r.get<std::int32_t>();
+  const auto nd = r.take<std::int32_t>();
   if (nd < 0) throw std::runtime_error("corrupt representation file");
   for (std::int32_t i = 0; i < nd; ++i) {
-    const int lam = r.get<std::int32_t>();
-    const int mu = r.get<std::int32_t>();
-    const Matrix d = r.get_matrix();
+    const int lam = r.take<std::int32_t>();
+    const int mu = r.take<std::int32_t>();
+    const Matrix d = r.matrix();
     if (lam < 0 || mu < 0 || lam >= tree->num_boxes() || mu >= tree->num_boxes() ||
         d.rows() != Index(tree->box(lam).points.size()) || d.cols() != Index(tree->box(mu).points.size()))
       throw std::runtime_error("dense block shapes disagree with the tree");
@@ -280,16 +302,16 @@ std::shared_ptr<H1Rep> load_rep(const std::string& path, int device) {
 }
 
 void save_dense_matrix(const std::string& path, const Matrix& m) {
-  Writer w(path);
-  w.put<std::uint64_t>(kDenseMagic);
-  w.put_matrix(m.rows(), m.cols(), m.data());
-  if (!w.out) throw std::runtime_error("write failed: " + path);
+  ByteSink w;
+  w << kDenseMagic;
+  w.matrix(m.rows(), m.cols(), m.data());
+  w.save(path);
 }
 
 Matrix load_dense_matrix(const std::string& path) {
-  Reader r(path);
-  if (r.get<std::uint64_t>() != kDenseMagic) throw std::runtime_error("not a dense matrix file: " + path);
-  return r.get_matrix();
+  ByteSource r(path);
+  if (r.take<std::uint64_t>() != kDenseMagic) throw std::runtime_error("not a dense matrix file: " + path);
+  return r.matrix();
 }
 
 }  // namespace hpeel
