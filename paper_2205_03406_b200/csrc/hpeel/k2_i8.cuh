@@ -5,12 +5,15 @@
 // Each operand entry is split into a 54-bit fixed-point integer relative to a
 // power-of-two scale (kernel rows: a per-row bound from the payload boxes'
 // bounding boxes; payload: 16 >= the Box-Muller maximum 8.6) and written as 7
-// balanced int8 digits (weights 2^48 .. 2^0). Digit products with a + b <= 6
-// are accumulated per group g = a + b in int32 TMEM columns (exact), and the
-// epilogue forms Y = sum_g 2^(w_g) P_g in FP64. Dropped groups (a + b >= 7)
-// and the two roundings give |error| <= ~2^-50 of scale x |Omega| per term,
-// i.e. ~1e-14 relative on the samples (tests/test_gpu_k2.py checks it
-// against the FP64 DMMA kernel and the oracle at 1e-12).
+// balanced int8 digits (weights 2^48 .. 2^0). Digit products with a + b <= 7
+// (group split; a + b <= 6 in the column-split layout) are accumulated per
+// group g = a + b in int32 TMEM columns (exact), and the epilogue forms
+// Y = sum_g 2^(w_g) P_g in FP64. The dropped groups and the two roundings give
+// |error| <= ~2^-58 of scale x |Omega| per term: the samples' error stays
+// ~1e-16 of the unpeeled product, so after peeling has cancelled most of it
+// (post-peel blocks are up to ~100x smaller at the deep levels of config 3)
+// they remain well inside 1e-12 (tests/test_gpu_fullsize.py; with a + b <= 6
+// those blocks reached 2.6e-12).
 //
 // One CTA = 128 packed output rows (the K2Task/K2Row tiles of k2_ws.cuh) x one
 // half of the sample columns (forward or adjoint, N = r padded to 16), so the
@@ -26,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.hpp"
@@ -48,12 +52,15 @@ constexpr int kAPlane = kRows * kStepK;  // bytes of one A digit plane per K-ste
 constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
 
 __host__ __device__ constexpr int padded_width(int r) { return (r + 15) / 16 * 16; }
-/// Group split (NP <= 48): CTA 0 of the pair accumulates digit-pair groups
-/// 0..kG0-1 and CTA 1 groups kG0..6, each for all 2 NP sample columns (one
-/// MMA of N = 2 NP per digit pair: 15 + 13 MMAs per K-step instead of 28 + 28
-/// of N = NP). Otherwise (NP = 64) CTA h owns column half h for all groups.
-constexpr int kG0 = 5;
-__host__ __device__ constexpr bool group_split(int np) { return kG0 * 2 * np <= 512 && (kGroups - kG0) * 2 * np <= 512; }
+/// Group split (NP <= 48): the CTA pair divides the digit-pair groups
+/// g = a + b <= 7 between its CTAs, each for all 2 NP sample columns (one MMA
+/// of N = 2 NP per digit pair): CTA 0 holds groups {0, 1, 2, 4, 7} and CTA 1
+/// {3, 5, 6}, 17 + 17 MMAs per K-step. Otherwise (NP = 64) CTA h owns column
+/// half h for the groups 0..6.
+constexpr int kGroupsGS = 8;
+__host__ __device__ constexpr unsigned gs_groups(int half) { return half == 0 ? 0x97u : 0x68u; }
+__host__ __device__ constexpr int gs_slots(int half) { return half == 0 ? 5 : 3; }
+__host__ __device__ constexpr bool group_split(int np) { return gs_slots(0) * 2 * np <= 512 && gs_slots(1) * 2 * np <= 512; }
 __host__ __device__ constexpr int mma_n(int np) { return group_split(np) ? 2 * np : np; }
 __host__ __device__ constexpr int b_step_bytes(int np) { return kPlanes * np * kStepK; }
 /// Pipeline depth: 4 digit-tile (A) stages and 4 payload digit + coordinate
@@ -291,9 +298,9 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
   const int nsteps = int((p1 - p0 + kStepK - 1) / kStepK);
   const std::int64_t step0 = step_off[task.color];
   const unsigned char* bsrc = bdig + (kGS ? 0 : half * half_stride) + step0 * kBStep;
-  // accumulator groups of this CTA
-  const int g_lo = kGS ? (half == 0 ? 0 : kG0) : 0;
-  const int g_hi = kGS ? (half == 0 ? kG0 : kGroups) : kGroups;
+  // accumulator groups of this CTA (group split: the gs_groups(half) mask,
+  // slot = rank of the group in the mask; column split: groups 0..6)
+  const unsigned gmask = kGS ? gs_groups(half) : (1u << kGroups) - 1u;
   const double* xsrc = xstep + step0 * (DIM * kStepK);
   const double* tab = kTab ? lts : op.ltab;
 
@@ -409,13 +416,33 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
                 }
               }
             }
+          } else if constexpr (kGS) {
+            // constant accumulator addresses per CTA half
+            auto issue = [&](auto mask_c) {
+              constexpr unsigned kMask = decltype(mask_c)::value;
+#pragma unroll
+              for (int g = 0; g < kGroupsGS; ++g) {
+                if (!((kMask >> g) & 1u)) continue;
+                const int slot = __popc(kMask & ((1u << g) - 1u));
+                const int a0 = g > kPlanes - 1 ? g - (kPlanes - 1) : 0;
+                const int a1 = g < kPlanes - 1 ? g : kPlanes - 1;
+#pragma unroll
+                for (int a = a0; a <= a1; ++a) {
+                  umma_i8(tmem + unsigned(slot * kN), ad0 + std::uint64_t((a * kAPlane) >> 4),
+                          bd0 + std::uint64_t(((g - a) * kN * kStepK) >> 4), kIdesc, (fresh && a == a0) ? 0u : 1u);
+                }
+              }
+            };
+            if (half == 0)
+              issue(std::integral_constant<unsigned, gs_groups(0)>{});
+            else
+              issue(std::integral_constant<unsigned, gs_groups(1)>{});
           } else {
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
-              if (g < g_lo || g >= g_hi) continue;
 #pragma unroll
               for (int a = 0; a <= g; ++a) {
-                umma_i8(tmem + unsigned((g - g_lo) * kN), ad0 + std::uint64_t((a * kAPlane) >> 4),
+                umma_i8(tmem + unsigned(g * kN), ad0 + std::uint64_t((a * kAPlane) >> 4),
                         bd0 + std::uint64_t(((g - a) * kN * kStepK) >> 4), kIdesc, (fresh && a == 0) ? 0u : 1u);
               }
             }
@@ -514,13 +541,14 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
         const int e = row_exp[orow];
         const unsigned lane_base = tmem + (unsigned((warp & 3) * 32) << 16) + unsigned(cq * kCq);
 #pragma unroll
-        for (int q = 0; q < kGroups; ++q) {
-          if (q < g_lo || q >= g_hi) continue;
+        for (int q = 0; q < kGroupsGS; ++q) {
+          if (!((gmask >> q) & 1u)) continue;
+          const int slot = __popc(gmask & ((1u << q) - 1u));
           const double wg = ldexp(1.0, e - 8 - 8 * q);
 #pragma unroll
           for (int c0 = 0; c0 < kCq; c0 += 4) {
             int v[4];
-            tmem_ld4(lane_base + unsigned((q - g_lo) * kN + c0), v);
+            tmem_ld4(lane_base + unsigned(slot * kN + c0), v);
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 4; ++c) y[c0 + c] = fma(double(v[c]), wg, y[c0 + c]);
