@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <functional>
+#include <memory>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -308,7 +310,6 @@ Coloring dsatur_impl(int n, Degree&& degree, Sweep&& sweep) {
   out.queue_ops += size_t(n);
   int top = 0;  // highest bucket that may be non-empty
   int done = 0;
-  constexpr int kAhead = 12;
   while (done < n) {
     while (bucket[size_t(top)].empty()) --top;
     KeyHeap& hb = bucket[size_t(top)];
@@ -380,12 +381,292 @@ Coloring dsatur_color(const IncompatibilityGraph& graph) {
       });
 }
 
-Coloring dsatur_color(const ImplicitGraph& graph) {
+namespace {
+
+// Max tournament tree over the vertices' packed DSatur keys
+// (saturation, uncolored degree, -v). Keys are lazy upper bounds: the
+// saturation part is exact, the degree part may be stale-high (degree
+// decrements are not propagated), so the selection re-keys a stale winner and
+// looks again -- a winner whose stored key is exact beats every true key.
+// Saturation increases only raise a key: `raise` is safe from several
+// threads (compare-and-swap maximum up the path, stopping where an ancestor
+// already dominates); `set` is single-threaded.
+class KeyTree {
+ public:
+  explicit KeyTree(int n) {
+    while (size_ < size_t(std::max(n, 1))) size_ <<= 1;
+    node_ = std::vector<std::atomic<std::uint64_t>>(2 * size_);
+    for (auto& x : node_) x.store(0, std::memory_order_relaxed);
+  }
+  void init(int v, std::uint64_t k) { node_[size_ + size_t(v)].store(k, std::memory_order_relaxed); }
+  void build() {
+    for (size_t i = size_ - 1; i >= 1; --i) node_[i].store(std::max(get(2 * i), get(2 * i + 1)), std::memory_order_relaxed);
+  }
+  std::uint64_t leaf(int v) const { return get(size_ + size_t(v)); }
+  void raise(int v, std::uint64_t k) {
+    size_t i = size_ + size_t(v);
+    node_[i].store(k, std::memory_order_relaxed);
+    for (i >>= 1; i >= 1; i >>= 1) {
+      std::uint64_t cur = node_[i].load(std::memory_order_relaxed);
+      bool raised = false;
+      while (cur < k)
+        if (node_[i].compare_exchange_weak(cur, k, std::memory_order_relaxed)) {
+          raised = true;
+          break;
+        }
+      if (!raised) return;
+    }
+  }
+  // raise from one thread only (no other thread touches the tree)
+  void raise_serial(int v, std::uint64_t k) {
+    size_t i = size_ + size_t(v);
+    node_[i].store(k, std::memory_order_relaxed);
+    for (i >>= 1; i >= 1 && get(i) < k; i >>= 1) node_[i].store(k, std::memory_order_relaxed);
+  }
+  void set(int v, std::uint64_t k) {
+    size_t i = size_ + size_t(v);
+    node_[i].store(k, std::memory_order_relaxed);
+    for (i >>= 1; i >= 1; i >>= 1) node_[i].store(std::max(get(2 * i), get(2 * i + 1)), std::memory_order_relaxed);
+  }
+  int argmax() const {
+    size_t i = 1;
+    while (i < size_) i = get(2 * i) >= get(2 * i + 1) ? 2 * i : 2 * i + 1;
+    return int(i - size_);
+  }
+
+ private:
+  std::uint64_t get(size_t i) const { return node_[i].load(std::memory_order_relaxed); }
+  size_t size_ = 1;
+  std::vector<std::atomic<std::uint64_t>> node_;
+};
+
+// Spinning worker team for the neighbor sweeps (a sweep is ~10 us of work:
+// thread start-up or a condition variable per sweep would cost more).
+class SpinTeam {
+ public:
+  explicit SpinTeam(int workers) {
+    for (int t = 0; t < workers; ++t) threads_.emplace_back([this, t] { loop(t + 1); });
+  }
+  ~SpinTeam() {
+    stop_.store(true, std::memory_order_release);
+    epoch_.fetch_add(1, std::memory_order_acq_rel);
+    for (auto& th : threads_) th.join();
+  }
+  int size() const { return int(threads_.size()) + 1; }
+  // run job(t) on every member t (0 = the caller) and wait for all
+  template <class F>
+  void run(F&& job) {
+    job_ = [&](int t) { job(t); };
+    pending_.store(int(threads_.size()), std::memory_order_relaxed);
+    epoch_.fetch_add(1, std::memory_order_acq_rel);
+    job(0);
+    while (pending_.load(std::memory_order_acquire) != 0) pause();
+  }
+
+ private:
+  static void pause() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  void loop(int t) {
+    std::uint64_t seen = 0;
+    for (;;) {
+      std::uint64_t e;
+      while ((e = epoch_.load(std::memory_order_acquire)) == seen) pause();
+      seen = e;
+      if (stop_.load(std::memory_order_acquire)) return;
+      job_(t);
+      pending_.fetch_sub(1, std::memory_order_acq_rel);
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::function<void(int)> job_;
+  std::atomic<std::uint64_t> epoch_{0};
+  std::atomic<int> pending_{0};
+  std::atomic<bool> stop_{false};
+};
+
+}  // namespace
+
+// DSatur on the implicit graph (same selection rule and result as
+// dsatur_impl): the tournament tree replaces the per-saturation heaps, and
+// the sweeps of high-degree vertices run on a spinning thread team -- first
+// the sets whose zero set holds v's payload box (each once), then, after a
+// barrier, the sets carrying a box of v's zero set that the first part did
+// not reach; every neighbor is updated by exactly one thread.
+Coloring dsatur_color_threaded(const ImplicitGraph& graph, int threads) {
+  const int n = graph.num_vertices();
+  Coloring out;
+  out.color.assign(size_t(n), -1);
+  if (n == 0) return out;
+  constexpr int kSatBits = 14, kDegBits = 26, kVBits = 24;
+  int max_deg = 0;
+  for (int v = 0; v < n; ++v) max_deg = std::max(max_deg, graph.degree(v));
+  if (n >= (1 << kVBits) - 1 || max_deg >= (1 << kDegBits)) return dsatur_color(graph, 1);
+  auto key = [](int sat, int udeg, int v) {
+    return (std::uint64_t(unsigned(sat)) << (kDegBits + kVBits)) | (std::uint64_t(unsigned(udeg)) << kVBits) |
+           std::uint64_t((1u << kVBits) - 1u - unsigned(v));
+  };
+  auto key_deg = [](std::uint64_t k) { return int((k >> kVBits) & ((1u << kDegBits) - 1u)); };
+  struct VState {
+    int color, sat, udeg, stamp;
+  };
+  std::vector<VState> st(static_cast<size_t>(n));
+  // neighbor-color bits color-major: plane q holds colors [64 q, 64 q + 64)
+  // of every vertex, so a sweep (one color) touches one n-word plane
+  std::vector<std::vector<std::uint64_t>> seen;
+  seen.emplace_back(static_cast<size_t>(n), 0);
+  KeyTree tree(n);
+  for (int v = 0; v < n; ++v) {
+    st[size_t(v)] = VState{-1, 0, graph.degree(v), -1};
+    tree.init(v, key(0, graph.degree(v), v));
+  }
+  tree.build();
+  out.queue_ops += size_t(n);
+  std::unique_ptr<SpinTeam> team;
+  if (threads > 1) team = std::make_unique<SpinTeam>(threads - 1);
+  const int nt = team ? team->size() : 1;
+  std::atomic<int> zcursor{0};
+  bool sat_overflow = false;
+  static const bool prof = std::getenv("HP_DSATUR_PROFILE") != nullptr;
+  using PClock = std::chrono::steady_clock;
+  double t_sel = 0, t_sweep = 0;
+  std::size_t n_threaded = 0, rekeys = 0, cand1 = 0, cand2 = 0;
+  auto tp = PClock::now();
+  auto lapp = [&](double& acc) {
+    if (!prof) return;
+    const auto t1 = PClock::now();
+    acc += std::chrono::duration<double>(t1 - tp).count();
+    tp = t1;
+  };
+  for (int done = 0; done < n; ++done) {
+    lapp(t_sweep);
+    int v;
+    for (;;) {
+      v = tree.argmax();
+      const std::uint64_t k = tree.leaf(v);
+      if (key_deg(k) == st[size_t(v)].udeg) break;
+      tree.set(v, key(st[size_t(v)].sat, st[size_t(v)].udeg, v));  // stale degree: re-key, look again
+      ++out.queue_ops;
+      ++rekeys;
+    }
+    VState& sv = st[size_t(v)];
+    size_t wi = 0;
+    while (wi < seen.size() && seen[wi][size_t(v)] == ~std::uint64_t(0)) ++wi;
+    const int c = int(64 * wi) + (wi < seen.size() ? __builtin_ctzll(~seen[wi][size_t(v)]) : 0);
+    if (size_t(c >> 6) >= seen.size()) seen.emplace_back(static_cast<size_t>(n), 0);
+    if (c + 1 >= (1 << kSatBits)) sat_overflow = true;
+    sv.color = c;
+    out.color[size_t(v)] = c;
+    out.num_colors = std::max(out.num_colors, c + 1);
+    tree.set(v, 0);
+    lapp(t_sel);
+    std::uint64_t* plane = seen[size_t(c) >> 6].data();
+    const std::uint64_t cb = std::uint64_t(1) << (c & 63);
+    auto visit = [&](int w) {
+      VState& sw = st[size_t(w)];
+      if (sw.color != -1) return;
+      --sw.udeg;
+      std::uint64_t& word = plane[size_t(w)];
+      if (!(word & cb)) {
+        word |= cb;
+        ++sw.sat;
+        tree.raise(w, key(sw.sat, sw.udeg, w));  // concurrent-safe maximum up the path
+      }
+    };
+    const int pb = graph.payload_box(v);
+    const int* z0 = graph.zero_sets_begin(pb);
+    const int* z1 = graph.zero_sets_end(pb);
+    const auto& zero = graph.zero_of(v);
+    static const int sweep_min =
+        std::getenv("HP_DSATUR_SWEEP_MIN") ? std::atoi(std::getenv("HP_DSATUR_SWEEP_MIN")) : 4096;
+    if (!team || graph.degree(v) < sweep_min) {
+      // serial sweep
+      sv.stamp = v;
+      for (const int* q = z0; q < z1; ++q)
+        if (st[size_t(*q)].stamp != v) {
+          st[size_t(*q)].stamp = v;
+          visit(*q);
+        }
+      for (int z : zero)
+        for (const int* q = graph.payload_sets_begin(z); q < graph.payload_sets_end(z); ++q)
+          if (st[size_t(*q)].stamp != v) {
+            st[size_t(*q)].stamp = v;
+            visit(*q);
+          }
+      out.queue_ops += 1;
+      continue;
+    }
+    ++n_threaded;
+    if (prof) {
+      cand1 += std::size_t(z1 - z0);
+      for (int z : zero) cand2 += std::size_t(graph.payload_sets_end(z) - graph.payload_sets_begin(z));
+    }
+    // threaded sweep: part 1 (each set once) in static slices; part 2 over
+    // the zero boxes, skipping part 1's sets and v itself
+    sv.stamp = v;
+    const std::int64_t n1 = z1 - z0;
+    constexpr int kAhead = 16;  // prefetch distance: the visits are independent cache misses
+    auto prefetch = [&](int w) {
+      __builtin_prefetch(&st[size_t(w)], 1, 1);
+      __builtin_prefetch(&plane[size_t(w)], 1, 1);
+    };
+    team->run([&](int t) {
+      const std::int64_t a = n1 * t / nt, b = n1 * (t + 1) / nt;
+      for (std::int64_t q = a; q < b; ++q) {
+        if (q + kAhead < b) prefetch(z0[q + kAhead]);
+        const int w = z0[q];
+        if (w == v) continue;
+        st[size_t(w)].stamp = v;
+        visit(w);
+      }
+    });
+    zcursor.store(0, std::memory_order_relaxed);
+    const int nz = int(zero.size());
+    team->run([&](int) {
+      for (;;) {
+        const int i0 = zcursor.fetch_add(4, std::memory_order_relaxed);
+        if (i0 >= nz) return;
+        for (int i = i0; i < std::min(nz, i0 + 4); ++i) {
+          const int z = zero[size_t(i)];
+          const int* qe = graph.payload_sets_end(z);
+          for (const int* q = graph.payload_sets_begin(z); q < qe; ++q) {
+            if (q + kAhead < qe) prefetch(q[kAhead]);
+            if (st[size_t(*q)].stamp != v) visit(*q);
+          }
+        }
+      }
+    });
+    out.queue_ops += 1;
+  }
+  lapp(t_sweep);
+  if (prof)
+    std::fprintf(stderr,
+                 "[dsatur] n %d threads %d select %.2f s (re-keys %zu) sweeps %.2f s (threaded %zu, candidates %zu + %zu)\n",
+                 n, nt, t_sel, rekeys, t_sweep, n_threaded, cand1, cand2);
+  if (sat_overflow) return dsatur_color(graph, 1);
+  return out;
+}
+
+Coloring dsatur_color(const ImplicitGraph& graph, int threads) {
+  if (threads > 1) return dsatur_color_threaded(graph, threads);
   std::vector<int> stamp(size_t(graph.num_vertices()), -1);
   return dsatur_impl(graph.num_vertices(), [&](int v) { return graph.degree(v); },
                      [&](int v, auto&& visit, auto&, auto&, size_t, size_t) {
                        graph.for_each_neighbor(v, stamp, v, visit);
                      });
+}
+
+Coloring dsatur_color(const ImplicitGraph& graph) {
+  // large leaf graphs (config 4: 3.9e5 vertices, 1.5e9 edges) on a thread team
+  static const int env = std::getenv("HP_DSATUR_THREADS") ? std::atoi(std::getenv("HP_DSATUR_THREADS")) : -1;
+  int threads = env;
+  if (threads < 0) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    threads = graph.num_edges() > 20'000'000 ? int(std::min(16u, hw)) : 1;
+  }
+  return dsatur_color(graph, threads);
 }
 
 bool ImplicitGraph::applicable(const std::vector<ConstraintSet>& sets) {

@@ -77,6 +77,14 @@ class ImplicitGraph {
   int degree(int v) const { return deg_[size_t(v)]; }
   /// f(w) once per neighbor w of v; stamp (size n, caller-owned) tags
   /// visited vertices with `tag`, which must differ between calls.
+  // the two neighbor sources of v (DSatur's threaded sweep walks them directly)
+  int payload_box(int v) const { return payload_[size_t(v)]; }
+  const std::vector<int>& zero_of(int v) const { return (*sets_)[size_t(v)].zero; }
+  const int* zero_sets_begin(int box) const { return zsets_.data() + zoff_[size_t(box)]; }
+  const int* zero_sets_end(int box) const { return zsets_.data() + zoff_[size_t(box) + 1]; }
+  const int* payload_sets_begin(int box) const { return psets_.data() + poff_[size_t(box)]; }
+  const int* payload_sets_end(int box) const { return psets_.data() + poff_[size_t(box) + 1]; }
+  int num_boxes() const { return int(zoff_.size()) - 1; }
   template <class F>
   void for_each_neighbor(int v, std::vector<int>& stamp, int tag, F&& f) const {
     stamp[size_t(v)] = tag;
@@ -105,6 +113,9 @@ class ImplicitGraph {
   std::size_t edges2_ = 0;
 };
 Coloring dsatur_color(const ImplicitGraph& graph);
+/// The same coloring with `threads` sweep threads (1: the serial heap-based
+/// implementation; > 1: tournament-tree selection + threaded sweeps).
+Coloring dsatur_color(const ImplicitGraph& graph, int threads);
 
 /// proj/src/coloring.cpp:218-250 (DSatur result given).
 Coloring plan_coloring(const BoxTree& tree, const std::vector<ConstraintSet>& sets, Coloring dsatur,

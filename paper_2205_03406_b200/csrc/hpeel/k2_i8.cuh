@@ -2,18 +2,20 @@
 // accumulators): the FP64 contraction Y = K(rows, payload) * Omega is
 // computed exactly in fixed point and rounded once.
 //
-// Each operand entry is split into a 54-bit fixed-point integer relative to a
-// power-of-two scale (kernel rows: a per-row bound from the payload boxes'
-// bounding boxes; payload: 16 >= the Box-Muller maximum 8.6) and written as 7
-// balanced int8 digits (weights 2^48 .. 2^0). Digit products with a + b <= 7
+// Each operand entry is split into a fixed-point integer relative to a
+// power-of-two scale -- kernel entries: 62 bits against a per-row bound from
+// the payload boxes' bounding boxes, written as 8 balanced int8 digits
+// (weights 2^56 .. 2^0); payload: 54 bits against 16 >= the Box-Muller
+// maximum 8.6, 7 digits (2^48 .. 2^0). Digit products with a + b <= 7
 // (group split; a + b <= 6 in the column-split layout) are accumulated per
 // group g = a + b in int32 TMEM columns (exact), and the epilogue forms
-// Y = sum_g 2^(w_g) P_g in FP64. The dropped groups and the two roundings give
-// |error| <= ~2^-58 of scale x |Omega| per term: the samples' error stays
-// ~1e-16 of the unpeeled product, so after peeling has cancelled most of it
-// (post-peel blocks are up to ~100x smaller at the deep levels of config 3)
-// they remain well inside 1e-12 (tests/test_gpu_fullsize.py; with a + b <= 6
-// those blocks reached 2.6e-12).
+// Y = sum_g 2^(w_g) P_g in FP64. The kernel entries' rounding (2^-63 of the
+// row bound: entries far below the bound keep ~60 bits, where 54 bits had
+// left the log kernel's near-zero values with ~1e-14 relative error), the
+// payload's (2^-55 of 16) and the dropped groups give errors ~1e-16 of the
+// unpeeled product, so after peeling has cancelled most of it (post-peel
+// blocks are up to ~100x smaller at the deep levels of config 3) the samples
+// stay well inside 1e-12 of the FP64 apply (tests/test_gpu_fullsize.py).
 //
 // One CTA = 128 packed output rows (the K2Task/K2Row tiles of k2_ws.cuh) x one
 // half of the sample columns (forward or adjoint, N = r padded to 16), so the
@@ -37,7 +39,8 @@
 namespace hpeel {
 namespace k2i8 {
 
-constexpr int kPlanes = 7;
+constexpr int kPlanes = 7;   // payload (B) digit planes: 54-bit fixed point
+constexpr int kPlanesA = 8;  // kernel-entry (A) digit planes: 62-bit fixed point
 constexpr int kGroups = 7;
 constexpr int kStepK = 32;
 constexpr int kWindow = 512;
@@ -68,9 +71,9 @@ __host__ __device__ constexpr int b_step_bytes(int np) { return kPlanes * np * k
 constexpr int kAStages = 4;
 constexpr int kStaticSmem = 9216 + 1024;
 __host__ __device__ constexpr int b_ring_bytes(int np) { return b_step_bytes(np) + 3 * kStepK * 8; }
-__host__ __device__ constexpr int bstages_for(int np, bool tab) { return (void)np, (void)tab, 4; }
+__host__ __device__ constexpr int bstages_for(int np, bool tab) { return (void)np, (void)tab, 3; }
 __host__ __device__ constexpr size_t smem_bytes(int np, bool tab) {
-  return size_t(kAStages) * kPlanes * kAPlane + size_t(bstages_for(np, tab)) * b_ring_bytes(mma_n(np)) +
+  return size_t(kAStages) * kPlanesA * kAPlane + size_t(bstages_for(np, tab)) * b_ring_bytes(mma_n(np)) +
          (tab ? 2 * kLogTab * 8 : 0) + 1024;
 }
 
@@ -181,6 +184,16 @@ __device__ __forceinline__ void split_digits(double v, double c, unsigned& uh, u
   uh = unsigned(hi + 0x808080);
   ul = unsigned(lo + 0x8080);
 }
+// Kernel entry v * c (|v * c| < 2^62, c = 2^(62 - e) a power of two, so the
+// product is exact) -> X = round(v c) in one conversion (values >= 2^52 are
+// already integers), biased by 0x80 in the seven low bytes: X + B returned as
+// (low word, high word). Bytes 0..6 xor 0x80 are balanced digits, byte 7
+// (arithmetic) the signed top digit.
+__device__ __forceinline__ void split62(double v, double c, unsigned& xl, unsigned& xh) {
+  const long long x = __double2ll_rn(v * c) + 0x0080808080808080ll;
+  xl = unsigned(x);
+  xh = unsigned(x >> 32);
+}
 // byte `i` of four words, packed a..d into bytes 0..3
 __device__ __forceinline__ unsigned gather4(unsigned a, unsigned b, unsigned c, unsigned d, unsigned i) {
   const unsigned sel = i | ((i + 4) << 4);
@@ -195,6 +208,17 @@ __device__ __forceinline__ void pack_planes(const unsigned (&uh)[4], const unsig
   w[4] = gather4(ul[0], ul[1], ul[2], ul[3], 2);
   w[5] = gather4(ul[0], ul[1], ul[2], ul[3], 1) ^ 0x80808080u;
   w[6] = gather4(ul[0], ul[1], ul[2], ul[3], 0) ^ 0x80808080u;
+}
+
+// the 8 kernel-entry digit-plane words of 4 consecutive entries (plane 0 =
+// byte 7, most significant)
+__device__ __forceinline__ void pack_planes8(const unsigned (&xl)[4], const unsigned (&xh)[4],
+                                             unsigned (&w)[kPlanesA]) {
+  w[0] = gather4(xh[0], xh[1], xh[2], xh[3], 3);
+#pragma unroll
+  for (int b = 2; b >= 0; --b) w[3 - b] = gather4(xh[0], xh[1], xh[2], xh[3], unsigned(b)) ^ 0x80808080u;
+#pragma unroll
+  for (int b = 3; b >= 0; --b) w[7 - b] = gather4(xl[0], xl[1], xl[2], xl[3], unsigned(b)) ^ 0x80808080u;
 }
 
 /// Bound on |K(x, y)| for y in a box with bounding box [lo, hi]: per row,
@@ -271,13 +295,13 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
   constexpr bool kGS = group_split(NP);
   constexpr int kN = mma_n(NP);  // MMA N (and TMEM columns per accumulator group)
   constexpr int kAcol = kGroups * NP;
-  constexpr bool kTS = !kGS && kAcol + 2 * kPlanes * 8 <= 512 && kTSEnabled;
+  constexpr bool kTS = !kGS && kAcol + 2 * kPlanesA * 8 <= 512 && kTSEnabled;
   constexpr int kBStep = b_step_bytes(kN);
   constexpr int kXStep = DIM * kStepK * 8;  // coordinates of one K-step (dim-major)
   constexpr unsigned kIdesc = umma_idesc(kN);
   extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* sa = smem;                                   // [kStages][kPlanes][kAPlane]
-  unsigned char* sb = smem + kStages * kPlanes * kAPlane;     // [kBS][kBStep]
+  unsigned char* sa = smem;                                   // [kStages][kPlanesA][kAPlane]
+  unsigned char* sb = smem + kStages * kPlanesA * kAPlane;    // [kBS][kBStep]
   double* sx = reinterpret_cast<double*>(sb + kBS * kBStep);  // [kBS][DIM][32]
   double* lts = sx + kBS * DIM * kStepK;
   // full_a: the peer's half of the digit tile landed (1 expect_tx arrival + bytes);
@@ -388,16 +412,16 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
         if (!(dbg & 1)) {
           // descriptors of plane 0 of this stage; planes are constant
           // offsets (16-byte units in the start-address field)
-          const std::uint64_t ad0 = umma_desc(smem_addr(sa + st * kPlanes * kAPlane));
+          const std::uint64_t ad0 = umma_desc(smem_addr(sa + st * kPlanesA * kAPlane));
           const std::uint64_t bd0 = umma_desc(smem_addr(sb + bs * kBStep));
           if constexpr (kTS) {
             // digit planes -> TMEM once per K-step (the MMAs then read A
             // from TMEM instead of re-reading each plane from shared memory
             // for every digit pair); tcgen05.cp and tcgen05.mma execute in
             // issue order, and the two A buffers alternate by step
-            const unsigned abuf = tmem + unsigned(kAcol + (step & 1) * kPlanes * 8);
+            const unsigned abuf = tmem + unsigned(kAcol + (step & 1) * kPlanesA * 8);
 #pragma unroll
-            for (int a = 0; a < kPlanes; ++a) tmem_cp_128x256b(abuf + unsigned(a * 8), ad0 + std::uint64_t((a * kAPlane) >> 4));
+            for (int a = 0; a < kPlanesA; ++a) tmem_cp_128x256b(abuf + unsigned(a * 8), ad0 + std::uint64_t((a * kAPlane) >> 4));
 #pragma unroll
             for (int g = 0; g < kGroups; ++g) {
 #pragma unroll
@@ -424,8 +448,8 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
               for (int g = 0; g < kGroupsGS; ++g) {
                 if (!((kMask >> g) & 1u)) continue;
                 const int slot = __popc(kMask & ((1u << g) - 1u));
-                const int a0 = g > kPlanes - 1 ? g - (kPlanes - 1) : 0;
-                const int a1 = g < kPlanes - 1 ? g : kPlanes - 1;
+                const int a0 = g > kPlanes - 1 ? g - (kPlanes - 1) : 0;    // payload plane g - a <= 6
+                const int a1 = g < kPlanesA - 1 ? g : kPlanesA - 1;        // kernel plane a <= 7
 #pragma unroll
                 for (int a = a0; a <= a1; ++a) {
                   umma_i8(tmem + unsigned(slot * kN), ad0 + std::uint64_t((a * kAPlane) >> 4),
@@ -463,12 +487,12 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
         const int st = step % kStages;
         const unsigned ph = (step / kStages) & 1;
         if (step >= kStages) mbar_wait(&full_a[st], ph ^ 1);  // previous round of this stage is complete
-        mbar_expect_tx(&full_a[st], kPlanes * kAPlane / 2);  // the peer's half, inbound
+        mbar_expect_tx(&full_a[st], kPlanesA * kAPlane / 2);  // the peer's half, inbound
         mbar_wait(&done_a[st], ph);                           // our half is stored (and the peer's stage is free)
         const unsigned bar_peer = mapa(smem_addr(&full_a[st]), peer);
-        const unsigned off = unsigned(st * kPlanes * kAPlane + half * (kAPlane / 2));
+        const unsigned off = unsigned(st * kPlanesA * kAPlane + half * (kAPlane / 2));
 #pragma unroll
-        for (int a = 0; a < kPlanes; ++a)
+        for (int a = 0; a < kPlanesA; ++a)
           bulk_s2peer(sa_peer + off + unsigned(a * kAPlane), sa + off + a * kAPlane, kAPlane / 2, bar_peer);
       }
     }
@@ -497,7 +521,7 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
     double xi[DIM];
 #pragma unroll
     for (int d = 0; d < DIM; ++d) xi[d] = op.x[d * op.n + epos];
-    const double cK = ldexp(1.0, 30 - row_exp[erow]);
+    const double cK = ldexp(1.0, 62 - row_exp[erow]);
     unsigned char* a_dst = sa + (erow >> 3) * 256 + kh * 128 + (erow & 7) * 16 + k4 * 4;
     // epilogue: TMEM lanes (warp & 3) * 32 + lane = tile rows, column quarter (warp >> 2)
     const int orow = (warp & 3) * 32 + lane;
@@ -513,22 +537,22 @@ sample_apply_i8_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* 
       if (step >= kStages) mbar_wait(&empty[st], ph ^ 1);
       mbar_wait(&full_b[step % kBS], (step / kBS) & 1);  // coordinates of this step
       const double* xs = sx + (step % kBS) * DIM * kStepK + kh * 16 + k4 * 4;
-      unsigned w[kPlanes];
+      unsigned w[kPlanesA];
       {
-        unsigned uh[4], ul[4];
+        unsigned xl[4], xh[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           double xj[DIM];
 #pragma unroll
           for (int d = 0; d < DIM; ++d) xj[d] = xs[d * kStepK + u];
           const double v = (dbg & 2) ? xj[0] : kernel_value<KIND, DIM, false>(xi, xj, false, op.param, tab);
-          split_digits(v, cK, uh[u], ul[u]);
+          split62(v, cK, xl[u], xh[u]);
         }
-        pack_planes(uh, ul, w);
+        pack_planes8(xl, xh, w);
       }
-      unsigned char* dst = a_dst + st * kPlanes * kAPlane;
+      unsigned char* dst = a_dst + st * kPlanesA * kAPlane;
 #pragma unroll
-      for (int a = 0; a < kPlanes; ++a) *reinterpret_cast<unsigned*>(dst + a * kAPlane) = w[a];
+      for (int a = 0; a < kPlanesA; ++a) *reinterpret_cast<unsigned*>(dst + a * kAPlane) = w[a];
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&done_a[st]);

@@ -2,11 +2,16 @@
 ABI) with the oracle: trees, adjacency, admissible/dense pairs, constraint
 sets, incompatibility graphs, DSatur/tile colorings and per-color payload
 lists. Runs without a GPU."""
+import os
+
 import numpy as np
 import pytest
 
 import oracle as O
 from paper_2205_03406_b200 import configs
+
+
+ROOT_DIR = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def geometries():
@@ -279,3 +284,26 @@ def test_implicit_graph_dsatur_equals_explicit(hp, name, pts, leaf):
         assert a.dsatur_color == b.dsatur_color, (name, mode, level)
         assert a.dsatur_colors == b.dsatur_colors and a.n_colors == b.n_colors
         assert a.color == b.color and a.color_payload == b.color_payload, (name, mode, level)
+
+
+def test_threaded_dsatur_equals_serial():
+    """The tournament-tree DSatur with threaded neighbor sweeps (used for the
+    big leaf graphs, e.g. 1.5e9 edges at config 4) colors exactly like the
+    serial heap implementation and the explicit graph: forced on with every
+    sweep threaded (HP_DSATUR_SWEEP_MIN=0), in a fresh process."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_2205_03406_b200 as hp\n"
+        "from paper_2205_03406_b200 import configs\n"
+        "for name, n, leaf in [('c3', 16384, 128), ('c4', 16384, 256), ('c5', 8192, 256), ('c2', 8192, 64)]:\n"
+        "    t = hp.build_tree(configs.make_points(name, n), leaf)\n"
+        "    for mode, level in [('leaf', t.depth)] + [('h1', l) for l in range(2, t.depth + 1)]:\n"
+        "        a = hp.plan(t, level, mode, 8, 7, 0)\n"
+        "        b = hp.plan(t, level, mode, 8, 7, 0, implicit=True)\n"
+        "        assert a.dsatur_color == b.dsatur_color and a.color == b.color, (name, mode, level)\n"
+        "print('ok')\n" % ROOT_DIR)
+    env = dict(os.environ, HP_DSATUR_THREADS="4", HP_DSATUR_SWEEP_MIN="0")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
