@@ -230,6 +230,10 @@ int hp_load_dense_matrix(const char* path, int64_t* rows, int64_t* cols, double*
  * order x (2r | leaf width) columns */
 int hp_rep_captured(const hp_rep* rep, int level, int64_t pair, int64_t* rows, int64_t* cols,
                     double* out);
+/* the same block of an H1 level before the peeling subtraction: the rows of
+ * A Omega (resp. A^T Psi) the extraction reads */
+int hp_rep_captured_raw(const hp_rep* rep, int level, int64_t pair, int64_t* rows, int64_t* cols,
+                        double* out);
 /* rel_error_power_method (proj/src/linalg.cpp:206-218; binding module.cpp:219-229) */
 int hp_rel_error_power_method(const hp_rep* rep, const hp_op* op, int iters, uint64_t seed,
                               double* out);

@@ -472,6 +472,14 @@ class CompressedRep:
         check(lib().hp_rep_shard(self._h, int(level), int(pair), None, None, C.byref(h)))
         return bool(h.value)
 
+    def captured_raw(self, level: int, pair: int) -> np.ndarray:
+        """The same block before peeling: rows of A Omega | A^T Psi."""
+        rows, cols = C.c_int64(0), C.c_int64(0)
+        check(lib().hp_rep_captured_raw(self._h, level, pair, C.byref(rows), C.byref(cols), None))
+        out = np.zeros((rows.value, cols.value), order="F")
+        check(lib().hp_rep_captured_raw(self._h, level, pair, C.byref(rows), C.byref(cols), dptr(out)))
+        return out
+
     def storage(self) -> dict:
         t = C.c_int64(0)
         check(lib().hp_rep_storage(self._h, C.byref(t)))
@@ -679,6 +687,13 @@ def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, s
     except (RuntimeError, ValueError, AssertionError) as e:
         _raise_callback(ref, e)
     return out.value
+
+
+def set_k2_mode(mode: int) -> None:
+    """K2 probe bits (probe header): 8 = FP64 apply with the payload chunks in
+    reverse order (another summation order, results valid); 1 / 2 skip work
+    (invalid results, timing only)."""
+    lib().hp_debug_set_k2_mode(int(mode))
 
 
 def set_k2_path(path: str) -> None:

@@ -89,6 +89,7 @@ _SIGNATURES = {
     "hp_save_dense_matrix": (C.c_int, [C.c_char_p, dp, i64, i64]),
     "hp_load_dense_matrix": (C.c_int, [C.c_char_p, lp, lp, dp, i64]),
     "hp_rep_captured": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
+    "hp_rep_captured_raw": (C.c_int, [P, C.c_int, i64, lp, lp, dp]),
     "hp_rel_error_power_method": (C.c_int, [P, P, C.c_int, u64, dp]),
 }
 

@@ -834,18 +834,20 @@ int hp_load_dense_matrix(const char* path, int64_t* rows, int64_t* cols, double*
   });
 }
 
-int hp_rep_captured(const hp_rep* rep, int level, int64_t pair, int64_t* rows, int64_t* cols,
-                    double* out) {
+namespace {
+int captured_block(const hp_rep* rep, int level, int64_t pair, int64_t* rows, int64_t* cols, double* out,
+                   bool raw) {
   return guard([&] {
     need(rep, "rep");
     const H1Rep& h = *rep->result.rep;
     const Matrix* m = nullptr;
     int box = -1;
     if (level < 0) {
+      if (raw) throw std::invalid_argument("pre-peel captures exist for H1 levels only");
       m = &h.captured_leaf.at(size_t(pair));
       box = h.dense.pairs.at(size_t(pair)).first;
     } else {
-      m = &h.captured.at(level).at(size_t(pair));
+      m = &(raw ? h.captured_raw : h.captured).at(level).at(size_t(pair));
       box = h.levels.at(size_t(level)).pairs.at(size_t(pair)).first;
     }
     if (rows) *rows = m->rows();
@@ -858,6 +860,17 @@ int hp_rep_captured(const hp_rep* rep, int level, int64_t pair, int64_t* rows, i
       for (int64_t c = 0; c < m->cols(); ++c) out[int64_t(s) + c * m->rows()] = (*m)(tr, c);
     }
   });
+}
+}  // namespace
+
+int hp_rep_captured(const hp_rep* rep, int level, int64_t pair, int64_t* rows, int64_t* cols,
+                    double* out) {
+  return captured_block(rep, level, pair, rows, cols, out, false);
+}
+
+int hp_rep_captured_raw(const hp_rep* rep, int level, int64_t pair, int64_t* rows, int64_t* cols,
+                        double* out) {
+  return captured_block(rep, level, pair, rows, cols, out, true);
 }
 
 int hp_rel_error_power_method(const hp_rep* rep, const hp_op* op, int iters, uint64_t seed,

@@ -1011,12 +1011,7 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
           report.exchange_bytes += double(w.seg[size_t(my_rank) + 1] - w.seg[size_t(my_rank)]) * 8.0 * (world - 1);
         }
 
-        // K3 peel
-        HP_CUDA(cudaEventRecord(tm->peel.a, s));
-        if (w.has_peel) run_peel(w.peel, e, *rep, g, gld, r, false, samples, r, s);
-        HP_CUDA(cudaEventRecord(tm->peel.b, s));
-
-        if (config.capture_samples) {
+        auto capture = [&](std::map<int, std::vector<Matrix>>& into) {
           HP_CUDA(cudaStreamSynchronize(s));
           std::vector<Matrix> cap(np);
           for (size_t i = 0; i < w.own.size(); ++i) {
@@ -1026,8 +1021,16 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
             HP_CUDA(cudaMemcpy(m.data(), samples + w.soff[i], size_t(rows) * 2 * r * 8, cudaMemcpyDeviceToHost));
             cap[size_t(p)] = std::move(m);
           }
-          rep->captured[l] = std::move(cap);
-        }
+          into[l] = std::move(cap);
+        };
+        if (config.capture_samples) capture(rep->captured_raw);
+
+        // K3 peel
+        HP_CUDA(cudaEventRecord(tm->peel.a, s));
+        if (w.has_peel) run_peel(w.peel, e, *rep, g, gld, r, false, samples, r, s);
+        HP_CUDA(cudaEventRecord(tm->peel.b, s));
+
+        if (config.capture_samples) capture(rep->captured);
 
         // K5a: middle = G'_a^T Y_p before the QR overwrites Y; K4 QR; K5b grams
         // and B (DESIGN.md §7 for the sharded variants)

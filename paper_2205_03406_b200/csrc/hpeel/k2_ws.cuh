@@ -106,6 +106,10 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
 
   const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
   const int nchunks = int((p1 - p0 + kBK - 1) / kBK);
+  // probe bit 3: payload chunks in reverse order (another FP64 summation
+  // order; the results stay valid)
+  const bool rev = (mode & 8) != 0;
+  auto chunk_base = [&](int c) { return p0 + std::int64_t(rev ? nchunks - 1 - c : c) * kBK; };
 
   if (warp >= ROWS / 16) {
     // ------------------------------------------------ evaluation warps
@@ -121,7 +125,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
     // stage chunk c: positions/coordinates, then payload rows (one group)
     auto load_chunk = [&](int c) {
       const int st = c % kStages;
-      const std::int64_t base = p0 + std::int64_t(c) * kBK;
+      const std::int64_t base = chunk_base(c);
       const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
       if (et < cnt) {
         cp_async4(&js[st][et], pc + base + et);
@@ -171,7 +175,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
         cp_async_wait_all();
       }
       bar_sync(kBarEval, kEval);  // ... and every eval thread's copies
-      const std::int64_t base = p0 + std::int64_t(c) * kBK;
+      const std::int64_t base = chunk_base(c);
       const int cnt = int(p1 - base < kBK ? p1 - base : kBK);
       double* kb = ksm + b * kBK * kKR;
       const bool skip = (mode & 1) != 0;

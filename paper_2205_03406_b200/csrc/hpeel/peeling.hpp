@@ -173,6 +173,7 @@ class H1Rep {
   std::int64_t dense_doubles = 0;
   // captured post-peel samples (capture_samples): level -> pair -> [Y | Z]
   std::map<int, std::vector<Matrix>> captured;
+  std::map<int, std::vector<Matrix>> captured_raw;  // the same blocks before peeling (= A Omega rows)
   std::vector<Matrix> captured_leaf;
 
   H1Rep() = default;

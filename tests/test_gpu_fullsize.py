@@ -28,36 +28,59 @@ pytestmark = pytest.mark.gpu
 
 
 def test_full_c3_int8_samples_match_fp64_and_host(hp, gpu_available):
+    """Samples are the black box's output A Omega (what the reference's
+    `apply` returns): int8 vs FP64 within 1e-12 of it on every level, before
+    and after peeling. The post-peel residual is ~1e2 smaller than A Omega at
+    the deep levels (cancellation), so any two FP64 summation orders differ
+    there by ~1e-12 of the residual: the FP64 apply with its payload chunks
+    reversed is the yardstick, and int8 must sit inside that noise."""
     w = configs.CONFIGS["c3"]
     pts = w.points()
     t = hp.build_tree(pts, w.leaf)
     op = hp.kernel_operator(w.kernel, pts, w.param)
     reps = {}
-    for path in ("fp64", "int8"):
-        hp.set_k2_path(path)
+    for path, mode in (("fp64", 0), ("fp64-reversed", 8), ("int8", 0)):
+        hp.set_k2_path("fp64" if path.startswith("fp64") else "int8")
+        hp.set_k2_mode(mode)
         try:
             reps[path] = hp.compress(op, t, rank=w.rank, oversample=w.oversample, seed=7, capture=True)
         finally:
             hp.set_k2_path("int8")
+            hp.set_k2_mode(0)
     assert {p["apply_path"] for p in reps["int8"].report["phases"] if p["phase"] == "h1"} == {"int8"}
-    worst, per_level = 0.0, {}
+    assert {p["apply_path"] for p in reps["fp64-reversed"].report["phases"] if p["phase"] == "h1"} == {"fp64"}
+    stats = {}
     for level in range(2, t.depth + 1):
-        lw = 0.0
+        raw_i8 = raw_rev = post_i8 = post_rev = post_rel_i8 = post_rel_rev = 0.0
         for i in range(len(t.admissible_pairs(level))):
-            lw = max(lw, rel(reps["int8"].captured(level, i), reps["fp64"].captured(level, i)))
-        per_level[level] = lw
-        worst = max(worst, lw)
-    print("int8 vs FP64 worst sample block per level", {k: f"{v:.2e}" for k, v in per_level.items()})
-    assert worst <= 1e-12, per_level
+            ref_raw = reps["fp64"].captured_raw(level, i)
+            scale = max(np.linalg.norm(ref_raw), 1e-300)
+            ref_post = reps["fp64"].captured(level, i)
+            raw_i8 = max(raw_i8, np.linalg.norm(reps["int8"].captured_raw(level, i) - ref_raw) / scale)
+            raw_rev = max(raw_rev, np.linalg.norm(reps["fp64-reversed"].captured_raw(level, i) - ref_raw) / scale)
+            d_i8 = np.linalg.norm(reps["int8"].captured(level, i) - ref_post)
+            d_rev = np.linalg.norm(reps["fp64-reversed"].captured(level, i) - ref_post)
+            post_i8, post_rev = max(post_i8, d_i8 / scale), max(post_rev, d_rev / scale)
+            pn = max(np.linalg.norm(ref_post), 1e-300)
+            post_rel_i8, post_rel_rev = max(post_rel_i8, d_i8 / pn), max(post_rel_rev, d_rev / pn)
+        stats[level] = (raw_i8, raw_rev, post_i8, post_rev, post_rel_i8, post_rel_rev)
+    print("level: raw int8 / raw fp64-rev / post int8 / post fp64-rev (all vs |A Omega|) ; "
+          "post int8 / post fp64-rev vs |residual|")
+    for level, v in stats.items():
+        print(level, " ".join(f"{x:.2e}" for x in v))
+    for level, (raw_i8, raw_rev, post_i8, post_rev, rel_i8, rel_rev) in stats.items():
+        assert raw_i8 <= 1e-12 and post_i8 <= 1e-12, (level, stats[level])
+        # int8 is within the FP64 summation-order noise of the residuals
+        assert rel_i8 <= max(4.0 * rel_rev, 1e-12), (level, stats[level])
     # level-2 rows against the host: Y(i, :) = sum_beta K(x_i, x_beta) G_beta
     r = w.rank + w.oversample
     ot = O.BoxTree(O.PointCloud(pts), w.leaf)
     plan = O.make_plan(ot, O.adjacency(ot), 2, O.H1, r, 7, 0)
     pairs = t.admissible_pairs(2)
     rng = np.random.default_rng(2)
-    picks = [(int(rng.integers(len(pairs))), None) for _ in range(256)]
-    worst_host = 0.0
-    for pi, _ in picks:
+    worst_host = {"int8": 0.0, "fp64": 0.0}
+    for _ in range(256):
+        pi = int(rng.integers(len(pairs)))
         a, b = pairs[pi]
         rows = ot.box(a).points
         j = int(rng.integers(len(rows)))
@@ -70,11 +93,10 @@ def test_full_c3_int8_samples_match_fp64_and_host(hp, gpu_available):
             yf += (kv @ O.payload_gaussian(ot, box, r, 7, 2, 0))[0]
             yb += (kv @ O.payload_gaussian(ot, box, r, 7, 2, 1))[0]
         want = np.concatenate([yf, yb])
-        for path in ("int8", "fp64"):
-            got = reps[path].captured(2, pi)[j]
-            worst_host = max(worst_host, rel(got, want))
-    print(f"level-2 rows vs host FP64: {worst_host:.2e}")
-    assert worst_host <= 1e-12, worst_host
+        for path in worst_host:
+            worst_host[path] = max(worst_host[path], rel(reps[path].captured(2, pi)[j], want))
+    print("level-2 rows vs host FP64:", {k: f"{v:.2e}" for k, v in worst_host.items()})
+    assert max(worst_host.values()) <= 1e-12, worst_host
 
 
 @pytest.mark.parametrize("name,n,depth", [("c4", 32768, 3), ("c5", 16384, 3), ("c4", 65536, 4)])
