@@ -926,15 +926,18 @@ def _served_rows(tree, plan, m_index):
     return np.unique(np.concatenate(pts)) if pts else np.zeros(0, dtype=np.int64)
 
 
-def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None, restrict=False):
+def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None, restrict=False, raw=None):
     """proj/src/peeling.cpp:158-178. Returns (samples, cols). restrict=True
     computes only the rows the extraction reads (value-identical on those
-    rows: the same products over the nonzero rows of Omega; other rows 0)."""
+    rows: the same products over the nonzero rows of Omega; other rows 0).
+    `raw` (a list) receives each color's black-box product before peeling."""
     times = PhaseTimes() if times is None else times
     samples, cols = [], 0
     for ci, m in enumerate(plan.matrices):
         if not m.payload:
             samples.append(None)
+            if raw is not None:
+                raw.append(None)
             continue
         if phase is not None:
             m = BlockTestMatrix(m.rows, m.width, m.seed, m.level, phase, m.payload, m.zero, m.serves)
@@ -950,6 +953,8 @@ def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None
             y = np.zeros_like(omega)
             y[rows] = op.apply_rows(omega, rows, adjoint)
             times.add("apply", t0)
+            if raw is not None:
+                raw.append(y.copy())
             if prev_level >= 2:
                 t0 = _now()
                 y[rows] -= rep.apply_truncated_rows(prev_level, omega, mask, adjoint)[rows]
@@ -959,6 +964,8 @@ def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None
         t0 = _now()
         y = op.apply_adjoint(omega) if adjoint else op.apply(omega)
         times.add("apply", t0)
+        if raw is not None:
+            raw.append(y)
         if prev_level >= 2:
             t0 = _now()
             y = y - (rep.apply_truncated_adjoint(prev_level, omega) if adjoint
@@ -968,7 +975,7 @@ def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None
     return samples, cols
 
 
-def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict=False):
+def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict=False, raw_capture=None):
     """proj/src/peeling.cpp:211-275 (Alg. 4.1)."""
     times = PhaseTimes() if times is None else times
     rep = H1Rep(tree, adj)
@@ -983,7 +990,8 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict
         t0 = _now()
         plan = make_plan(tree, adj, l, H1, r, seed, 0)
         times.add("plan", t0)
-        ys, fcols = _residual_samples(op, rep, l - 1, plan, False, times=times, restrict=restrict)
+        yraw, zraw = ([], []) if raw_capture is not None else (None, None)
+        ys, fcols = _residual_samples(op, rep, l - 1, plan, False, times=times, restrict=restrict, raw=yraw)
         u_bases = {}
         t0 = _now()
         with _small_blas():
@@ -992,7 +1000,11 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict
             for ab, q in zip(pairs, qs):
                 u_bases[ab] = q
         times.add("qr", t0)
-        zs, acols = _residual_samples(op, rep, l - 1, plan, True, phase=1, times=times, restrict=restrict)
+        zs, acols = _residual_samples(op, rep, l - 1, plan, True, phase=1, times=times, restrict=restrict, raw=zraw)
+        if raw_capture is not None:
+            raw_capture[l] = {(a, b): (yraw[plan.block_to_matrix[(a, b)]][tree.box(a).points],
+                                       zraw[plan.block_to_matrix[(a, b)]][tree.box(a).points])
+                              for a, b in pairs}
         if capture is not None:
             capture[l] = {(a, b): (ys[plan.block_to_matrix[(a, b)]][tree.box(a).points],
                                    zs[plan.block_to_matrix[(a, b)]][tree.box(a).points])
@@ -1048,7 +1060,7 @@ def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False
                    "forward_cols": fcols, "adjoint_cols": 0})
 
 
-def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, restrict=False):
+def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, restrict=False, raw_capture=None):
     """proj/src/peeling.cpp:576-639 for format h1. Returns (rep, report).
     `times` (a PhaseTimes) collects wall seconds per phase. restrict=True
     evaluates each color's black-box product and peeling only on the rows the
@@ -1065,7 +1077,7 @@ def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, 
     if times is not None:
         times.add("adjacency", t0)
     report = []
-    rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict)
+    rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict, raw_capture)
     extract_leaf(op, rep, seed, report, leaf_capture, times, restrict)
     return rep, report
 

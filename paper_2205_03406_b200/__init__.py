@@ -690,8 +690,9 @@ def rel_error_power_method(rep: CompressedRep, ref: Operator, iters: int = 20, s
 
 
 def set_k2_mode(mode: int) -> None:
-    """K2 probe bits (probe header): 8 = FP64 apply with the payload chunks in
-    reverse order (another summation order, results valid); 1 / 2 skip work
+    """K2 probe bits (probe header): 16 = FP64 apply with the payload chunks in
+    reverse order (another summation order, results valid); 8 = checked
+    evaluation path, 4 = fused kernel (results identical); 1 / 2 skip work
     (invalid results, timing only)."""
     lib().hp_debug_set_k2_mode(int(mode))
 

@@ -106,9 +106,9 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
 
   const std::int64_t p0 = pay_off[task.color], p1 = pay_off[task.color + 1];
   const int nchunks = int((p1 - p0 + kBK - 1) / kBK);
-  // probe bit 3: payload chunks in reverse order (another FP64 summation
+  // probe bit 4: payload chunks in reverse order (another FP64 summation
   // order; the results stay valid)
-  const bool rev = (mode & 8) != 0;
+  const bool rev = (mode & 16) != 0;
   auto chunk_base = [&](int c) { return p0 + std::int64_t(rev ? nchunks - 1 - c : c) * kBK; };
 
   if (warp >= ROWS / 16) {

@@ -14,7 +14,9 @@
 extern "C" {
 #endif
 
-/* profiling only: 1 = K2 skips kernel evaluation, 2 = K2 skips DMMA, 0 = normal */
+/* K2 probe bits: 1 = skip kernel evaluation, 2 = skip DMMA (timing only, invalid
+ * results); 4 = fused kernel, 8 = checked evaluation path, 16 = payload chunks
+ * in reverse order (valid results: another FP64 summation order); 0 = normal */
 void hp_debug_set_k2_mode(int mode);
 /* K2 arithmetic path: 0 = int8 tensor-core digit products (exact fixed-point
  * emulation of the FP64 contraction, k2_i8.cuh) wherever eligible (default),

@@ -39,7 +39,7 @@ def test_full_c3_int8_samples_match_fp64_and_host(hp, gpu_available):
     t = hp.build_tree(pts, w.leaf)
     op = hp.kernel_operator(w.kernel, pts, w.param)
     reps = {}
-    for path, mode in (("fp64", 0), ("fp64-reversed", 8), ("int8", 0)):
+    for path, mode in (("fp64", 0), ("fp64-reversed", 16), ("int8", 0)):
         hp.set_k2_path("fp64" if path.startswith("fp64") else "int8")
         hp.set_k2_mode(mode)
         try:
@@ -107,8 +107,11 @@ def test_3d_multilevel_oracle_parity(hp, gpu_available, name, n, depth):
     assert t.depth == depth
     assert sum(1 for l in range(2, t.depth + 1) if t.admissible_pairs(l)) >= 2  # peeling across H1 levels
     op_ref = O.KernelOperator(w.kernel, pts, w.param)
+    # post-peel residuals of these 3D blocks sit ~1e2 below A Omega: FP64
+    # summation-order noise (and rank choices at the 1e-14 noise floor) reach
+    # ~1e-12 of the residual, so samples are held to 1e-12 of A Omega
     _compare_with_oracle(hp, pts, w.leaf, hp.kernel_operator(w.kernel, pts, w.param), op_ref,
-                         w.rank, w.oversample, 7, restrict=True)
+                         w.rank, w.oversample, 7, restrict=True, post_relative=False)
 
 
 def _middle_empty_cloud():

@@ -31,13 +31,17 @@ def test_int8_samples_match_fp64(hp, gpu_available, name, n):
     rank, over = (w.rank, w.oversample) if w.rank + w.oversample <= 48 else (36, 12)
     a = _compress(hp, "fp64", op, t, w, rank, over)
     b = _compress(hp, "int8", op, t, w, rank, over)
+    # relative to the black-box product A Omega of the block (the peeled
+    # residual can be ~1e2 smaller; FP64 summation orders alone differ there
+    # at ~1e-12, tests/test_gpu_fullsize.py)
     worst = 0.0
     for l in range(2, t.depth + 1):
         for i in range(len(t.admissible_pairs(l))):
             x, y = a.captured(l, i), b.captured(l, i)
-            nx = np.linalg.norm(x)
+            nx = np.linalg.norm(a.captured_raw(l, i))
             if nx > 0:
                 worst = max(worst, np.linalg.norm(x - y) / nx)
+                worst = max(worst, np.linalg.norm(a.captured_raw(l, i) - b.captured_raw(l, i)) / nx)
     assert worst <= 1e-12, f"{name}: worst sample block {worst:.3e}"
     xs = np.random.default_rng(1).standard_normal((t.num_points, 3))
     ya, yb = a.apply(xs), b.apply(xs)
