@@ -160,7 +160,7 @@ def k2_roofline(report, w):
     """Dominant kernel K2 (black-box apply). achieved = useful FP64 flops of
     the rows read back (2 * rows * payload rows * 2r) / K2 device time,
     against the measured FP64 DMMA peak; the int8 path computes those flops
-    exactly as 28 int8 digit-pair products per entry and column (padded to
+    exactly as 35 int8 digit-pair products per entry and column (padded to
     16), reported against the INT8 tensor peak in `int8`."""
     flops = sum(ph["apply_flops"] for ph in report["phases"] if ph["phase"] == "h1")
     ms = sum(ph["apply_ms"] for ph in report["phases"] if ph["phase"] == "h1")
@@ -168,7 +168,7 @@ def k2_roofline(report, w):
     ach = flops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
     r = w.rank + w.oversample
     np_pad = (r + 15) // 16 * 16
-    int8_ops = flops / (4.0 * r) * 28 * 2 * (2 * np_pad)
+    int8_ops = flops / (4.0 * r) * 35 * 2 * (2 * np_pad)  # 35 digit pairs (a + b <= 7, 8 x 7 planes)
     int8_tops = int8_ops / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
     int8_path = any(ph.get("apply_path") == "int8" for ph in report["phases"] if ph["phase"] == "h1")
     out = {"bound": "tensor", "achieved": round(ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

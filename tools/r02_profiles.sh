@@ -12,8 +12,8 @@ timeout 900 $N --metrics gpu__time_duration.sum --clock-control none -c 3000 --c
   python tools/one_compress.py c5 131072 > $O/launches_c5s.log 2>&1
 timeout 900 $N --set full --clock-control none --import-source on -k regex:sample_apply_i8 --launch-skip 5 -c 1 \
   -o $O/k2i8_c3 python tools/one_compress.py c3 262144 > $O/k2i8.log 2>&1
-for k in peel_apply_kernel peel_coeff_dmma_kernel qr_reg_kernel bsolve_chol_kernel gram_kernel; do
-  timeout 900 $N --set full --clock-control none --import-source on -k regex:$k --launch-skip 3 -c 1 \
+for k in bsolve_chol_kernel qr_reg_backprop_kernel; do
+  timeout 900 $N --set full --clock-control none --import-source on -k regex:$k --launch-skip 1 -c 1 \
     -o $O/${k}_c5s python tools/one_compress.py c5 131072 > $O/$k.log 2>&1
 done
 for f in $O/*.ncu-rep; do $N -i $f --page raw --csv > ${f%.ncu-rep}_raw.csv 2>/dev/null; done
