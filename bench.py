@@ -151,8 +151,8 @@ def make_operator(hp, w, pts, device=0):
 
 # DRAM bytes (read + write) of one K2 launch from `ncu --set full` (config 3,
 # level 7; profiles/r01_k2_int8_ncu.txt), per launch like `achieved`.
-K2_NCU_TRAFFIC = 1621484800
-K2_NCU_SOURCE = "profiles/r01_k2_int8_ncu.txt: dram__bytes_read.sum + dram__bytes_write.sum of the level-7 launch (config 3)"
+K2_NCU_TRAFFIC = 943549952 + 677325824
+K2_NCU_SOURCE = "profiles/r02_k2_int8_ncu.txt: dram__bytes_read.sum + dram__bytes_write.sum of one level launch (config 3)"
 INT8_PEAK_TOPS = 4500.0   # B200 dense INT8 tensor peak (datasheet; MEASURED_PEAKS.json has no INT8 entry)
 
 
