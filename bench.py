@@ -36,7 +36,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA.8x8x4 peak on this pool's B200 (profiles/r01_fp64_peaks.txt)
-FP64_PEAK_SOURCE = "measured DMMA m8n8k4 peak, profiles/r01_fp64_peaks.txt (MEASURED_PEAKS.json has no FP64 entry)"
+FP64_PEAK_SOURCE = ("measured DMMA m8n8k4 peak, profiles/r02_fp64_peaks.txt (37.14 TF/s at 1965 MHz, clock record "
+                    "included; MEASURED_PEAKS.json has no FP64 entry)")
 METRIC = "H-matrix compression time (s)"
 
 
@@ -50,6 +51,8 @@ def parse():
     ap.add_argument("--n", type=int, default=0, help="override N (scaled workload)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--full-reference", action="store_true",
+                    help="reference arm: compress the whole workload in the oracle (no extrapolation)")
     ap.add_argument("--clock-ms", type=int, default=200, help="nvidia-smi sampling period (0: off)")
     return ap.parse_args()
 
@@ -182,7 +185,9 @@ def k2_roofline(report, w):
     # the batched reconstruction kernels, same FP64 peak (spans on the main stream)
     others = {}
     for key, fk, tk, what in (("K3_peel", "peel_flops", "peel_ms", "peel_coeff_dmma + peel_apply (all phases)"),
-                              ("K4_qr", "qr_flops", "qr_ms", "pivoted Householder QR, 2 m r^2 per U / V block")):
+                              ("K4_qr", "qr_flops", "qr_ms", "pivoted Householder QR, 2 m r^2 per U / V block"),
+                              ("K5_bsolve", "bsolve_flops", "bsolve_ms",
+                               "grams + Cholesky B solve, the reference's flop formulas")):
         f = sum(ph.get(fk, 0.0) for ph in report["phases"])
         t = sum(ph[tk] for ph in report["phases"])
         if t > 0 and f > 0:
@@ -204,7 +209,7 @@ def flush_l2(torch):
     del buf
 
 
-def reference_measure(w, steps, warmup, budget_s=10.0):
+def reference_measure(w, steps, warmup, budget_s=10.0, full=False):
     """The reference's CPU path, timed through the oracle (oracle/cpu_model.py):
     never loads libhpeel_b200.so. Config 1 (and any N <= 8192) is compressed
     in full and measured per phase, on all host threads and on one; larger
@@ -220,17 +225,18 @@ def reference_measure(w, steps, warmup, budget_s=10.0):
     if pts.ndim == 1:
         pts = pts[:, None]
     vals, phases = [], None
-    if w.dense or w.n <= 8192:
+    if full or w.dense or w.n <= 8192:
         for i in range(warmup + steps):
             total, times, _, _ = M.timed_compress(w, pts, threads)
             if i >= warmup:
                 vals.append(total)
                 phases = times
-        one, one_times, _, _ = M.timed_compress(w, pts, 1)
-        sample = (f"full oracle compress of the whole workload (N = {w.n}), measured per step on {threads} threads; "
-                  f"also measured once on 1 thread ({one:.2f} s)")
-        extra = {"kind_of_value": "measured", "phases_s": {k: round(v, 4) for k, v in phases.items()},
-                 "one_core": {"value": round(one, 4), "phases_s": {k: round(v, 4) for k, v in one_times.items()}}}
+        extra = {"kind_of_value": "measured", "phases_s": {k: round(v, 4) for k, v in phases.items()}}
+        sample = (f"full oracle compress of the whole workload (N = {w.n}), measured per step on {threads} threads")
+        if w.dense or w.n <= 8192:
+            one, one_times, _, _ = M.timed_compress(w, pts, 1)
+            sample += f"; also measured once on 1 thread ({one:.2f} s)"
+            extra["one_core"] = {"value": round(one, 4), "phases_s": {k: round(v, 4) for k, v in one_times.items()}}
         return float(np.median(vals)), threads, sample, extra
     from paper_2205_03406_b200 import configs as cfg
     ws = cfg.scaled(w.name, 4096)
@@ -266,7 +272,7 @@ def run_reference(args, ws, rank):
     if rank != 0:
         return
     w = cfg.CONFIGS[args.config] if not args.n else cfg.scaled(args.config, args.n)
-    value, threads, sample, extra = reference_measure(w, args.steps, args.warmup)
+    value, threads, sample, extra = reference_measure(w, args.steps, args.warmup, full=args.full_reference)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3,

@@ -182,10 +182,11 @@ int hp_partition_ranges(const double* work, int64_t n, int world, int64_t* bound
 int hp_rep_report(const hp_rep* rep, double* totals, int64_t* nphases);
 /* per phase: ints[7] = is_leaf, level, colors, forward_cols, adjoint_cols, net_flops,
  * apply_path (K2: 0 FP64 DMMA, 1 int8 tensor cores) and
- * times[12] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
+ * times[13] = wall_ms_total, wall_ms_net, apply_ms, peel_ms, qr_ms, bsolve_ms,
  * apply_flops, kernel_evals, host_wait_ms, start_ms (device time from the
  * first device work of compress to the phase start), peel_flops (K3),
- * qr_flops (K4, 2 m r^2 per U / V block) */
+ * qr_flops (K4, 2 m r^2 per U / V block), bsolve_flops (K5, the reference's
+ * B-solve flop formulas) */
 int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times);
 /* RunReport::to_csv (proj/src/peeling.cpp:478-488) */
 int hp_rep_csv(const hp_rep* rep, char* buf, int64_t cap, int64_t* len);

@@ -391,7 +391,7 @@ class CompressedRep:
         phases = []
         for i in range(nph.value):
             ints = np.zeros(7, dtype=np.int64)
-            times = np.zeros(12)
+            times = np.zeros(13)
             check(lib().hp_rep_phase(self._h, i, lptr(ints), dptr(times)))
             phases.append({
                 "phase": "leaf" if ints[0] else "h1", "level": int(ints[1]), "colors": int(ints[2]),
@@ -400,7 +400,7 @@ class CompressedRep:
                 "wall_ms_total": times[0], "wall_ms_net": times[1], "apply_ms": times[2],
                 "peel_ms": times[3], "qr_ms": times[4], "bsolve_ms": times[5],
                 "apply_flops": times[6], "kernel_evals": times[7], "host_wait_ms": times[8],
-                "start_ms": times[9], "peel_flops": times[10], "qr_flops": times[11],
+                "start_ms": times[9], "peel_flops": times[10], "qr_flops": times[11], "bsolve_flops": times[12],
             })
         self.report = {
             "forward_cols": int(totals[0]), "adjoint_cols": int(totals[1]),

@@ -642,6 +642,7 @@ int hp_rep_phase(const hp_rep* rep, int64_t phase, int64_t* ints, double* times)
       times[9] = ph.start_ms;
       times[10] = ph.peel_flops;
       times[11] = ph.qr_flops;
+      times[12] = ph.bsolve_flops;
     }
   });
 }

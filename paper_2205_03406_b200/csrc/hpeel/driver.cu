@@ -1185,9 +1185,11 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         const std::int64_t ku = ld.ku[p], kv = ld.kv[p];
         ph.net_flops += 2 * ma * r * r + 2 * mb * r * r;
         ph.qr_flops += 2.0 * double(ma) * r * r + 2.0 * double(mb) * r * r;
-        ph.net_flops += gemm_flops(r, r, ma) + gemm_flops(r, ku, ma) + gemm_flops(kv, r, mb);
-        if (ku > 0) ph.net_flops += svd_flops(r, ku) + gemm_flops(ku, r, r);
-        if (kv > 0) ph.net_flops += svd_flops(r, kv) + gemm_flops(kv, ku, r);
+        std::int64_t bf = gemm_flops(r, r, ma) + gemm_flops(r, ku, ma) + gemm_flops(kv, r, mb);
+        if (ku > 0) bf += svd_flops(r, ku) + gemm_flops(ku, r, r);
+        if (kv > 0) bf += svd_flops(r, kv) + gemm_flops(kv, ku, r);
+        ph.net_flops += bf;
+        ph.bsolve_flops += double(bf);
       }
       report.phases.push_back(ph);
     }

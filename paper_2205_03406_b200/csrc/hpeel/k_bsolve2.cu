@@ -90,42 +90,51 @@ __device__ void gram_pair(const double* a, double* x, double* n, int r, int k, i
 // In-place lower Cholesky of n (k x k, ld ldn). Exactly zero diagonals mark
 // null columns (zero rows in the solution). Returns false when a nonzero
 // pivot is small relative to the largest (or the matrix is not positive).
+// Per column: warp 0 takes the pivot and scales the column (shuffle
+// broadcast, no block barrier), then all warps update the trailing triangle
+// with columns on warps and rows on lanes (no index division): two block
+// barriers per column.
 __device__ bool cholesky(double* n, int k, int ldn, int* null_col) {
   __shared__ int bad;
   __shared__ double dmax;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kWarps = kBsThreads / 32;
   if (threadIdx.x == 0) {
     bad = 0;
     dmax = 0.0;
   }
   __syncthreads();
   for (int j = 0; j < k; ++j) {
-    if (threadIdx.x == 0) {
-      const double d = n[j + j * ldn];
-      if (d == 0.0) {
-        null_col[j] = 1;
-      } else if (!(d > 0.0)) {
-        bad = 1;
-        null_col[j] = 1;
-        n[j + j * ldn] = 0.0;
-      } else {
-        null_col[j] = 0;
-        const double l = sqrt(d);
-        n[j + j * ldn] = l;
-        dmax = fmax(dmax, l);
+    if (warp == 0) {
+      int nul = 0;
+      double l = 0.0;
+      if (lane == 0) {
+        const double d = n[j + j * ldn];
+        if (d == 0.0) {
+          nul = 1;
+        } else if (!(d > 0.0)) {
+          bad = 1;
+          nul = 1;
+          n[j + j * ldn] = 0.0;
+        } else {
+          l = sqrt(d);
+          n[j + j * ldn] = l;
+          dmax = fmax(dmax, l);
+        }
+        null_col[j] = nul;
+      }
+      nul = __shfl_sync(0xffffffffu, nul, 0);
+      l = __shfl_sync(0xffffffffu, l, 0);
+      if (!nul) {
+        const double inv = 1.0 / l;
+        for (int i = j + 1 + lane; i < k; i += 32) n[i + j * ldn] *= inv;
       }
     }
     __syncthreads();
-    const bool nul = null_col[j] != 0;
-    if (!nul) {
-      const double ljj = n[j + j * ldn];
-      for (int i = j + 1 + threadIdx.x; i < k; i += kBsThreads) n[i + j * ldn] /= ljj;
-    }
-    __syncthreads();
-    if (!nul) {
-      const int m = k - j - 1;
-      for (int e = threadIdx.x; e < m * m; e += kBsThreads) {
-        const int i = j + 1 + e % m, l = j + 1 + e / m;
-        if (i >= l) n[i + l * ldn] = fma(-n[i + j * ldn], n[l + j * ldn], n[i + l * ldn]);
+    if (!null_col[j]) {
+      for (int c = j + 1 + warp; c < k; c += kWarps) {
+        const double lc = n[c + j * ldn];
+        for (int i = c + lane; i < k; i += 32) n[i + c * ldn] = fma(-n[i + j * ldn], lc, n[i + c * ldn]);
       }
     }
     __syncthreads();
@@ -139,6 +148,8 @@ __device__ bool cholesky(double* n, int k, int ldn, int* null_col) {
 }
 
 // y (k x nr, ld ldy) <- N^{-1} y with N = L L^T; null columns give zero rows.
+// One thread per right-hand side; each substitution sum runs as four
+// independent partial sums (a quarter of the dependent FMA chain).
 __device__ void chol_solve(const double* n, int k, int ldn, const int* null_col, double* y, int nr, int ldy) {
   for (int c = threadIdx.x; c < nr; c += kBsThreads) {
     double* yc = y + c * ldy;
@@ -147,15 +158,29 @@ __device__ void chol_solve(const double* n, int k, int ldn, const int* null_col,
         yc[i] = 0.0;
         continue;
       }
-      double s = yc[i];
-      for (int l = 0; l < i; ++l) s = fma(-n[i + l * ldn], yc[l], s);
-      yc[i] = s / n[i + i * ldn];
+      double s0 = yc[i], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int l = 0;
+      for (; l + 4 <= i; l += 4) {
+        s0 = fma(-n[i + l * ldn], yc[l], s0);
+        s1 = fma(-n[i + (l + 1) * ldn], yc[l + 1], s1);
+        s2 = fma(-n[i + (l + 2) * ldn], yc[l + 2], s2);
+        s3 = fma(-n[i + (l + 3) * ldn], yc[l + 3], s3);
+      }
+      for (; l < i; ++l) s0 = fma(-n[i + l * ldn], yc[l], s0);
+      yc[i] = ((s0 + s1) + (s2 + s3)) / n[i + i * ldn];
     }
     for (int i = k - 1; i >= 0; --i) {
       if (null_col[i]) continue;
-      double s = yc[i];
-      for (int l = i + 1; l < k; ++l) s = fma(-n[l + i * ldn], yc[l], s);
-      yc[i] = s / n[i + i * ldn];
+      double s0 = yc[i], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int l = i + 1;
+      for (; l + 4 <= k; l += 4) {
+        s0 = fma(-n[l + i * ldn], yc[l], s0);
+        s1 = fma(-n[l + 1 + i * ldn], yc[l + 1], s1);
+        s2 = fma(-n[l + 2 + i * ldn], yc[l + 2], s2);
+        s3 = fma(-n[l + 3 + i * ldn], yc[l + 3], s3);
+      }
+      for (; l < k; ++l) s0 = fma(-n[l + i * ldn], yc[l], s0);
+      yc[i] = ((s0 + s1) + (s2 + s3)) / n[i + i * ldn];
     }
   }
   __syncthreads();

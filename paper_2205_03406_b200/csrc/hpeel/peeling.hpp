@@ -67,6 +67,7 @@ struct PhaseReport {
   double apply_flops = 0.0;      // FMAs*2 executed by K2 on needed rows
   double peel_flops = 0.0;       // FMAs*2 executed by K3 (coefficients + subtraction)
   double qr_flops = 0.0;         // K4: 2 m r^2 per U and per V block (flops.hpp:18-20)
+  double bsolve_flops = 0.0;     // K5: reference B-solve formulas (peeling.cpp:262-264, linalg.cpp:116-117)
   double kernel_evals = 0.0;
   double host_wait_ms = 0.0;      // driver thread blocked on this phase's host plan
   double start_ms = 0.0;          // device time from the first device work of compress to this phase
