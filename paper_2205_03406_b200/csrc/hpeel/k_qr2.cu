@@ -129,10 +129,11 @@ __device__ __forceinline__ double reflect(double (&x)[RPT], const double* v, dou
 
 // MODE 0: pivoted top (keep rule, Q(:, :keep) in place, Q to out).
 // MODE 1: unpivoted TSQR chunk (reflectors back in place, tau, R stacked).
-// Each step j: the pivot column's four threads build the reflector from the
-// tail norm and pivot-row value they computed in step j - 1 and publish it;
-// one barrier; every column applies it, then computes its exact remaining
-// norm (rows >= j + 1) and the warp-local argmax for step j + 1; one barrier.
+// Each step j: the pivot column's threads build the reflector from the tail
+// norm and pivot-row value they computed in step j - 1 and publish it; one
+// barrier; every column applies it, then computes its exact remaining norm
+// (rows >= j + 1) and the warp-local argmax for step j + 1; a second barrier
+// in MODE 0 only.
 // CTAs per SM the register budget allows (x[RPT] doubles + ~48 registers)
 __host__ __device__ constexpr int qr_min_blocks(int threads, int rpt) {
   return threads * (rpt * 2 + 48) <= 32768 ? 2 : 1;
@@ -236,7 +237,11 @@ qr_reg_kernel(const QrBlock* __restrict__ blocks, double* data, double* out, dou
     const double tau = sm.tau[j];
     if (tau != 0.0) reflect<TPC>(x, vj[g], done ? 0.0 : tau);
     if (j + 1 < steps) stats(j + 1, (j + 1) & 1);
-    __syncthreads();
+    // MODE 0: every thread reads the next pivot from the warps' argmax.
+    // MODE 1 needs no second barrier: the next reflector goes to the other
+    // buffer (its previous readers all passed this step's barrier), and the
+    // next pivot column's tail norm is reduced inside its own warp.
+    if (MODE == 0) __syncthreads();
   }
 
   if (MODE == 1) {
