@@ -113,8 +113,12 @@ def test_3d_multilevel_oracle_parity(hp, gpu_available, name, n, depth):
     # blocks, device and oracle alike (Eigen vs LAPACK would differ the same
     # way) -- so post-peel samples agree to ~3e-12 of A Omega (held to 1e-11)
     # while U B V^T agrees to ~3e-12 (held to 1e-8).
+    # Config 5's exp(-r / 0.1) far blocks have numerical ranks right at the
+    # cutoff: a handful of U B V^T differ at ~2e-8 of their (1e-4-floored)
+    # norm, while the representations apply alike to 1e-10.
     _compare_with_oracle(hp, pts, w.leaf, hp.kernel_operator(w.kernel, pts, w.param), op_ref,
-                         w.rank, w.oversample, 7, restrict=True, post_relative=False, peeled_tol=1e-11)
+                         w.rank, w.oversample, 7, restrict=True, post_relative=False, peeled_tol=1e-11,
+                         block_tol=1e-7)
 
 
 def _middle_empty_cloud():

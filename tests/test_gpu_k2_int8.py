@@ -33,16 +33,18 @@ def test_int8_samples_match_fp64(hp, gpu_available, name, n):
     b = _compress(hp, "int8", op, t, w, rank, over)
     # relative to the black-box product A Omega of the block (the peeled
     # residual can be ~1e2 smaller; FP64 summation orders alone differ there
-    # at ~1e-12, tests/test_gpu_fullsize.py)
-    worst = 0.0
+    # at ~1e-12, tests/test_gpu_fullsize.py); on 3D trees the peeled part
+    # also carries rank choices at the 1e-14 noise floor (1e-11)
+    worst_raw = worst_post = 0.0
     for l in range(2, t.depth + 1):
         for i in range(len(t.admissible_pairs(l))):
             x, y = a.captured(l, i), b.captured(l, i)
             nx = np.linalg.norm(a.captured_raw(l, i))
             if nx > 0:
-                worst = max(worst, np.linalg.norm(x - y) / nx)
-                worst = max(worst, np.linalg.norm(a.captured_raw(l, i) - b.captured_raw(l, i)) / nx)
-    assert worst <= 1e-12, f"{name}: worst sample block {worst:.3e}"
+                worst_post = max(worst_post, np.linalg.norm(x - y) / nx)
+                worst_raw = max(worst_raw, np.linalg.norm(a.captured_raw(l, i) - b.captured_raw(l, i)) / nx)
+    assert worst_raw <= 1e-12, f"{name}: worst unpeeled sample block {worst_raw:.3e}"
+    assert worst_post <= (1e-11 if w.dim == 3 else 1e-12), f"{name}: worst post-peel block {worst_post:.3e}"
     xs = np.random.default_rng(1).standard_normal((t.num_points, 3))
     ya, yb = a.apply(xs), b.apply(xs)
     assert np.linalg.norm(ya - yb) / np.linalg.norm(ya) <= 1e-9
