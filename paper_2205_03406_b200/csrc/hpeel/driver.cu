@@ -541,7 +541,10 @@ LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg, co
   (void)o;
   lap("tasks");
   if (tree.depth() >= 2) {
-    lw.peel = plan_peel(e, rep, blocks, color_boxes, tree.depth(), lw.w, false);
+    // the leaf plan is the last one the device needs but the largest one:
+    // its peel plan runs on several threads
+    const int threads = int(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+    lw.peel = plan_peel_parallel(e, rep, blocks, color_boxes, tree.depth(), lw.w, false, threads);
     lw.has_peel = true;
   }
   lap("plan_peel");

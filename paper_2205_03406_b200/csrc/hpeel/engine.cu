@@ -3,6 +3,9 @@
 #include "k2_i8.cuh"
 
 #include <mutex>
+#include <thread>
+
+#include "shard.hpp"
 
 #include <algorithm>
 #include <map>
@@ -474,6 +477,71 @@ PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBl
     }
   }
   return pp;
+}
+
+PeelPlan plan_peel_parallel(const Engine& e, const H1Rep& rep, const std::vector<SampleBlock>& blocks,
+                            const std::vector<std::vector<int>>& payload_boxes, int top_level, int w,
+                            bool with_adjoint, int threads) {
+  const int nc = int(payload_boxes.size());
+  if (threads <= 1 || nc < 2 || blocks.size() < 2048)
+    return plan_peel(e, rep, blocks, payload_boxes, top_level, w, with_adjoint);
+  // colors partitioned over the threads (balanced by block rows): coefficient
+  // tasks (q, c) and term lists (side, level, ancestor, c) never straddle two
+  // parts, so the merged plan is the serial one up to the order of its tasks
+  std::vector<double> rows_of_color(static_cast<size_t>(nc), 0.0);
+  for (const SampleBlock& b : blocks) rows_of_color[size_t(b.color)] += double(e.count(b.box));
+  const auto cuts = partition_ranges(rows_of_color, threads);
+  std::vector<std::vector<SampleBlock>> part(static_cast<size_t>(threads));
+  std::vector<int> part_of(static_cast<size_t>(nc), 0);
+  for (int t = 0; t < threads; ++t)
+    for (std::int64_t c = cuts[size_t(t)]; c < cuts[size_t(t) + 1]; ++c) part_of[size_t(c)] = t;
+  for (const SampleBlock& b : blocks) part[size_t(part_of[size_t(b.color)])].push_back(b);
+  std::vector<PeelPlan> plans(static_cast<size_t>(threads));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] { plans[size_t(t)] = plan_peel(e, rep, part[size_t(t)], payload_boxes, top_level, w, with_adjoint); });
+  for (auto& th : pool) th.join();
+  PeelPlan out;
+  const std::int64_t kw = std::int64_t(e.k) * w;
+  for (PeelPlan& pl : plans) {
+    const int seg0 = int(out.seg_start.size());
+    out.seg_start.insert(out.seg_start.end(), pl.seg_start.begin(), pl.seg_start.end());
+    out.seg_count.insert(out.seg_count.end(), pl.seg_count.begin(), pl.seg_count.end());
+    auto merge_side = [&](std::vector<CoeffTask>& coeff_out, std::vector<CoeffTask>& coeff,
+                          std::vector<PeelTask>& tasks_out, std::vector<PeelTask>& tasks,
+                          std::vector<PeelRef>& refs_out, std::vector<PeelRef>& refs,
+                          std::vector<PeelTerm>& terms_out, std::vector<PeelTerm>& terms) {
+      const std::int64_t c0 = std::int64_t(coeff_out.size()) * kw;
+      const int t0 = int(terms_out.size()), r0 = int(refs_out.size());
+      for (CoeffTask c : coeff) {
+        c.seg_begin += seg0;
+        c.seg_end += seg0;
+        c.t_out += c0;
+        coeff_out.push_back(c);
+      }
+      for (PeelTerm tm : terms) {
+        tm.t += c0;
+        terms_out.push_back(tm);
+      }
+      for (PeelRef rf : refs) {
+        rf.term_begin += t0;
+        rf.term_end += t0;
+        refs_out.push_back(rf);
+      }
+      for (PeelTask tk : tasks) {
+        tk.ref_begin += r0;
+        tk.ref_end += r0;
+        tasks_out.push_back(tk);
+      }
+    };
+    merge_side(out.coeff_fwd, pl.coeff_fwd, out.tasks_fwd, pl.tasks_fwd, out.refs_fwd, pl.refs_fwd, out.terms_fwd,
+               pl.terms_fwd);
+    merge_side(out.coeff_adj, pl.coeff_adj, out.tasks_adj, pl.tasks_adj, out.refs_adj, pl.refs_adj, out.terms_adj,
+               pl.terms_adj);
+    out.coeff_flops += pl.coeff_flops;
+    out.apply_flops += pl.apply_flops;
+  }
+  return out;
 }
 
 void run_peel(const PeelPlan& pp, const Engine& e, const H1Rep& rep, const double* g, int gld,

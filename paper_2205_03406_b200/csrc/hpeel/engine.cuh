@@ -239,6 +239,11 @@ struct SampleBlock {
 PeelPlan plan_peel(const Engine& e, const H1Rep& rep, const std::vector<SampleBlock>& blocks,
                    const std::vector<std::vector<int>>& payload_boxes, int top_level, int w,
                    bool with_adjoint);
+/// plan_peel with the colors split over `threads` host threads (same tasks,
+/// coefficients and term order per output tile; used for the leaf phase).
+PeelPlan plan_peel_parallel(const Engine& e, const H1Rep& rep, const std::vector<SampleBlock>& blocks,
+                            const std::vector<std::vector<int>>& payload_boxes, int top_level, int w,
+                            bool with_adjoint, int threads);
 void run_peel(const PeelPlan& pp, const Engine& e, const H1Rep& rep, const double* g, int gld,
               int w, bool identity, double* samples, int adj_col, cudaStream_t s);
 
