@@ -360,12 +360,17 @@ int qr_reg_cols(int cols) { return cols <= 32 ? 32 : cols <= 48 ? 48 : cols <= 6
 #ifndef HP_QR_TPC
 #define HP_QR_TPC 8
 #endif
-constexpr int tpc_for(int nc) { return nc <= 64 ? HP_QR_TPC : 4; }
+// 80 columns (config 5) take 8 threads per column too, with at most 24 rows
+// per thread (640 threads; 192-row blocks as before): the 4-thread layout
+// held 168 registers and one 320-thread CTA per SM, half of the stall
+// samples at the step barriers (profiles/r02_ncu_kernels.txt).
+constexpr int tpc_for(int nc) { return nc <= 80 ? HP_QR_TPC : 4; }
+constexpr int rpt_cap8(int nc) { return nc <= 64 ? 32 : 24; }
 
 int qr_reg_rows_max(int cols) {
   const int nc = qr_reg_cols(cols);
   if (nc == 0) return 0;
-  if (tpc_for(nc) == 8) return 8 * 32;
+  if (tpc_for(nc) == 8) return 8 * rpt_cap8(nc);
   return nc <= 64 ? 4 * 64 : 4 * 48;  // RPT cap: 64 (<= 256 threads) or 48 (register budget)
 }
 
@@ -373,7 +378,7 @@ namespace {
 int rpt_for(int nc, int max_rows) {
   const int tpc = tpc_for(nc);
   const int need = (max_rows + tpc - 1) / tpc;
-  if (tpc == 8) return need <= 8 ? 8 : need <= 16 ? 16 : 32;
+  if (tpc == 8) return need <= 8 ? 8 : need <= 16 ? 16 : need <= 24 && nc > 64 ? 24 : 32;
   const int cap = nc <= 64 ? 64 : 48;
   const int r = need <= 16 ? 16 : need <= 32 ? 32 : need <= 48 ? 48 : 64;
   return std::min(r, cap);
@@ -396,7 +401,12 @@ void launch_reg_nc(int mode, int rpt, const QrBlock* blocks, int nb, double* dat
     switch (rpt) {
       case 8: return launch_reg<NC, 8>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
       case 16: return launch_reg<NC, 16>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-      default: return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+      case 24:
+        if constexpr (NC > 64) return launch_reg<NC, 24>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+        break;
+      default:
+        if constexpr (NC <= 64) return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+        break;
     }
   } else {
     switch (rpt) {
@@ -423,7 +433,12 @@ void launch_bp_nc(int rpt, const QrBlock* blocks, int nb, const double* data, co
     switch (rpt) {
       case 8: return launch_bp<NC, 8>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
       case 16: return launch_bp<NC, 16>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-      default: return launch_bp<NC, 32>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+      case 24:
+        if constexpr (NC > 64) return launch_bp<NC, 24>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+        break;
+      default:
+        if constexpr (NC <= 64) return launch_bp<NC, 32>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+        break;
     }
   } else {
     switch (rpt) {
