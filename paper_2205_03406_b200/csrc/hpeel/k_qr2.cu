@@ -352,120 +352,109 @@ qr_reg_backprop_kernel(const QrBlock* __restrict__ blocks, const double* data,
 
 int qr_reg_cols(int cols) { return cols <= 32 ? 32 : cols <= 48 ? 48 : cols <= 64 ? 64 : cols <= 80 ? 80 : cols <= 96 ? 96 : 0; }
 
-// threads per column: 8 (a column's rows split over 8 threads: half the
-// dependent FMA chain of every Householder step and 1/2 the registers of the
-// 4-thread layout); HP_QR_TPC=4 selects the earlier layout for A/B runs
-// (NC <= 64; wider blocks keep 4 threads per column so a block still holds
-// 2r rows for TSQR within the register budget)
-#ifndef HP_QR_TPC
-#define HP_QR_TPC 8
-#endif
-// 80 columns (config 5) take 8 threads per column too, with at most 24 rows
-// per thread (640 threads; 192-row blocks as before): the 4-thread layout
-// held 168 registers and one 320-thread CTA per SM, half of the stall
-// samples at the step barriers (profiles/r02_ncu_kernels.txt).
-constexpr int tpc_for(int nc) { return nc <= 80 ? HP_QR_TPC : 4; }
-constexpr int rpt_cap8(int nc) { return nc <= 64 ? 32 : 24; }
+// Layout per block-size class, code = threads per column * 100 + rows per
+// thread (a block's arithmetic depends only on its class, so batches are
+// launched per class and sharded runs reproduce the unsharded factors):
+//  - up to 64 columns: 8 threads per column for <= 128 rows (8 or 16 rows
+//    each), 16 threads per column for 129..256 rows (16 rows each: half the
+//    dependent chain of a Householder step; for <= 128 rows the wider layout
+//    measured 1.6-2.3x slower, its threads mostly idle);
+//  - 80 columns (config 5): 8 threads per column, <= 24 rows each (640
+//    threads, 96 registers; the 4-thread layout held 168 registers, one
+//    320-thread CTA per SM and half of its stall samples at the step
+//    barriers, profiles/r02_ncu_kernels.txt);
+//  - 96 columns: 4 threads per column, <= 48 rows each.
+namespace {
+int variant_for(int nc, int max_rows) {
+  if (nc <= 64) {
+    const int need = (max_rows + 7) / 8;
+    return need <= 8 ? 808 : need <= 16 ? 816 : 1616;
+  }
+  if (nc <= 80) {
+    const int need = (max_rows + 7) / 8;
+    return need <= 8 ? 808 : need <= 16 ? 816 : 824;
+  }
+  const int need = (max_rows + 3) / 4;
+  return need <= 16 ? 416 : need <= 32 ? 432 : 448;
+}
+constexpr int vt(int v) { return v / 100; }
+constexpr int vr(int v) { return v % 100; }
+}  // namespace
 
 int qr_reg_rows_max(int cols) {
   const int nc = qr_reg_cols(cols);
   if (nc == 0) return 0;
-  if (tpc_for(nc) == 8) return 8 * rpt_cap8(nc);
-  return nc <= 64 ? 4 * 64 : 4 * 48;  // RPT cap: 64 (<= 256 threads) or 48 (register budget)
+  return nc <= 64 ? 256 : 192;
 }
 
 namespace {
-int rpt_for(int nc, int max_rows) {
-  const int tpc = tpc_for(nc);
-  const int need = (max_rows + tpc - 1) / tpc;
-  if (tpc == 8) return need <= 8 ? 8 : need <= 16 ? 16 : need <= 24 && nc > 64 ? 24 : 32;
-  const int cap = nc <= 64 ? 64 : 48;
-  const int r = need <= 16 ? 16 : need <= 32 ? 32 : need <= 48 ? 48 : 64;
-  return std::min(r, cap);
-}
 
-template <int NC, int RPT>
+template <int NC, int V>
 void launch_reg(int mode, const QrBlock* blocks, int nb, double* data, double* out, double* tau, int* ranks,
                 int cols, int kmax, double tol, cudaStream_t s) {
-  constexpr int T = tpc_for(NC);
+  constexpr int T = vt(V), R = vr(V);
   if (mode == 0)
-    qr_reg_kernel<NC, RPT, 0, T><<<nb, NC * T, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
+    qr_reg_kernel<NC, R, 0, T><<<nb, NC * T, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
   else
-    qr_reg_kernel<NC, RPT, 1, T><<<nb, NC * T, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
+    qr_reg_kernel<NC, R, 1, T><<<nb, NC * T, 0, s>>>(blocks, data, out, tau, ranks, cols, kmax, tol);
 }
 
 template <int NC>
-void launch_reg_nc(int mode, int rpt, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
+void launch_reg_nc(int mode, int v, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
                    int* ranks, int cols, int kmax, double tol, cudaStream_t s) {
-  if constexpr (tpc_for(NC) == 8) {
-    switch (rpt) {
-      case 8: return launch_reg<NC, 8>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-      case 16: return launch_reg<NC, 16>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-      case 24:
-        if constexpr (NC > 64) return launch_reg<NC, 24>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-        break;
-      default:
-        if constexpr (NC <= 64) return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-        break;
-    }
+#define HP_V(V)                                                                  \
+  case V:                                                                        \
+    return launch_reg<NC, V>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
+  if constexpr (NC <= 64) {
+    switch (v) { HP_V(808) HP_V(816) HP_V(1616) default: break; }
+  } else if constexpr (NC <= 80) {
+    switch (v) { HP_V(808) HP_V(816) HP_V(824) default: break; }
   } else {
-    switch (rpt) {
-      case 16: return launch_reg<NC, 16>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-      case 32: return launch_reg<NC, 32>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-      case 48: return launch_reg<NC, 48>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-      default:
-        if constexpr (NC <= 64) return launch_reg<NC, 64>(mode, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s);
-    }
+    switch (v) { HP_V(416) HP_V(432) HP_V(448) default: break; }
   }
+#undef HP_V
+  throw std::logic_error("qr_reg: no kernel for this block class");
 }
 
-template <int NC, int RPT>
+template <int NC, int V>
 void launch_bp(const QrBlock* blocks, int nb, const double* data, const double* tau, const double* parent,
                double* outbuf, int cols, int kmax, cudaStream_t s) {
-  constexpr int T = tpc_for(NC);
-  qr_reg_backprop_kernel<NC, RPT, T><<<nb, NC * T, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax);
+  constexpr int T = vt(V), R = vr(V);
+  qr_reg_backprop_kernel<NC, R, T><<<nb, NC * T, 0, s>>>(blocks, data, tau, parent, outbuf, cols, kmax);
 }
 
 template <int NC>
-void launch_bp_nc(int rpt, const QrBlock* blocks, int nb, const double* data, const double* tau,
+void launch_bp_nc(int v, const QrBlock* blocks, int nb, const double* data, const double* tau,
                   const double* parent, double* outbuf, int cols, int kmax, cudaStream_t s) {
-  if constexpr (tpc_for(NC) == 8) {
-    switch (rpt) {
-      case 8: return launch_bp<NC, 8>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-      case 16: return launch_bp<NC, 16>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-      case 24:
-        if constexpr (NC > 64) return launch_bp<NC, 24>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-        break;
-      default:
-        if constexpr (NC <= 64) return launch_bp<NC, 32>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-        break;
-    }
+#define HP_V(V)    \
+  case V:          \
+    return launch_bp<NC, V>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
+  if constexpr (NC <= 64) {
+    switch (v) { HP_V(808) HP_V(816) HP_V(1616) default: break; }
+  } else if constexpr (NC <= 80) {
+    switch (v) { HP_V(808) HP_V(816) HP_V(824) default: break; }
   } else {
-    switch (rpt) {
-      case 16: return launch_bp<NC, 16>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-      case 32: return launch_bp<NC, 32>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-      case 48: return launch_bp<NC, 48>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-      default:
-        if constexpr (NC <= 64) return launch_bp<NC, 64>(blocks, nb, data, tau, parent, outbuf, cols, kmax, s);
-    }
+    switch (v) { HP_V(416) HP_V(432) HP_V(448) default: break; }
   }
+#undef HP_V
+  throw std::logic_error("qr_reg backprop: no kernel for this block class");
 }
 }  // namespace
 
-int qr_reg_rpt(int cols, int rows) { return rpt_for(qr_reg_cols(cols), rows); }
+int qr_reg_rpt(int cols, int rows) { return variant_for(qr_reg_cols(cols), rows); }
 
 void launch_qr_reg(int mode, const QrBlock* blocks, int nb, double* data, double* out, double* tau,
                    int* ranks, int cols, int kmax, double tol, int max_rows, cudaStream_t s) {
   if (nb == 0) return;
   const int nc = qr_reg_cols(cols);
-  const int rpt = rpt_for(nc, max_rows);
-  if (nc == 0 || max_rows > tpc_for(nc) * rpt) throw std::invalid_argument("qr_reg: block too large");
+  const int v = variant_for(nc, max_rows);
+  if (nc == 0 || max_rows > vt(v) * vr(v)) throw std::invalid_argument("qr_reg: block too large");
   switch (nc) {
-    case 32: launch_reg_nc<32>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
-    case 48: launch_reg_nc<48>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
-    case 64: launch_reg_nc<64>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
-    case 80: launch_reg_nc<80>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
-    default: launch_reg_nc<96>(mode, rpt, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
+    case 32: launch_reg_nc<32>(mode, v, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
+    case 48: launch_reg_nc<48>(mode, v, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
+    case 64: launch_reg_nc<64>(mode, v, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
+    case 80: launch_reg_nc<80>(mode, v, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
+    default: launch_reg_nc<96>(mode, v, blocks, nb, data, out, tau, ranks, cols, kmax, tol, s); break;
   }
   HP_LAUNCHED();
 }
@@ -475,14 +464,14 @@ void launch_qr_reg_backprop(const QrBlock* blocks, int nb, const double* data, c
                             cudaStream_t s) {
   if (nb == 0) return;
   const int nc = qr_reg_cols(kmax);
-  const int rpt = rpt_for(nc, max_rows);
-  if (nc == 0 || max_rows > tpc_for(nc) * rpt) throw std::invalid_argument("qr_reg backprop: block too large");
+  const int v = variant_for(nc, max_rows);
+  if (nc == 0 || max_rows > vt(v) * vr(v)) throw std::invalid_argument("qr_reg backprop: block too large");
   switch (nc) {
-    case 32: launch_bp_nc<32>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
-    case 48: launch_bp_nc<48>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
-    case 64: launch_bp_nc<64>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
-    case 80: launch_bp_nc<80>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
-    default: launch_bp_nc<96>(rpt, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
+    case 32: launch_bp_nc<32>(v, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
+    case 48: launch_bp_nc<48>(v, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
+    case 64: launch_bp_nc<64>(v, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
+    case 80: launch_bp_nc<80>(v, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
+    default: launch_bp_nc<96>(v, blocks, nb, data, tau, parent, outbuf, cols, kmax, s); break;
   }
   HP_LAUNCHED();
 }

@@ -4,6 +4,7 @@ O=gpurun_out/${1:-r02k}
 mkdir -p $O
 python tools/qr_bench.py 80 64 192:4000 150:6000 100:10000 48:20000 > $O/qr_bench80.txt 2>&1
 python tools/qr_bench.py 42 32 256:3000 128:8000 64:16000 > $O/qr_bench42.txt 2>&1
+python tools/qr_bench.py 64 48 256:4000 128:8000 64:16000 > $O/qr_bench64.txt 2>&1
 timeout 900 python bench.py --config c5 --n 131072 --steps 3 --warmup 2 --no-cpu --no-e2e > $O/bench_c5s.json 2> $O/bench_c5s.err
 timeout 900 python bench.py --config c4 --n 262144 --steps 3 --warmup 2 --no-cpu --no-e2e > $O/bench_c4s.json 2> $O/bench_c4s.err
 timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e > $O/bench_c3.json 2> $O/bench_c3.err
