@@ -19,14 +19,14 @@ __all__ = [
     "BlockTestMatrix", "payload_gaussian", "assemble_test_matrices", "make_plan",
     "qr_orthonormal", "pinv_apply", "DenseOperator", "KernelOperator", "H1Rep", "run_h1",
     "extract_leaf", "compress", "rel_error_power_method", "synth_rank_structured",
-    "kernel_matrix", "PhaseTimes", "H1", "LEAF", "UNIF1", "save_rep_bytes", "load_rep_bytes", "save_dense_matrix_bytes",
+    "kernel_matrix", "PhaseTimes", "H1", "LEAF", "UNIF2", "BASIS", "UnifH1Rep", "run_uniform", "UNIF1", "save_rep_bytes", "load_rep_bytes", "save_dense_matrix_bytes",
     "REP_MAGIC", "DENSE_MAGIC",
 ]
 
 M64 = (1 << 64) - 1
 GAMMA = 0x9E3779B97F4A7C15
 H1, UNIF1, UNIF2, LEAF = 0, 1, 2, 3
-GAUSSIAN, IDENTITY = 0, 1
+GAUSSIAN, IDENTITY, BASIS = 0, 1, 2
 
 
 # --------------------------------------------------------------------------- RNG
@@ -338,7 +338,7 @@ class ConstraintSet:
 
 
 def build_constraints(tree, adj, level, mode):
-    """proj/src/coloring.cpp:55-113 (kH1, kUnifStage1, kLeaf)."""
+    """proj/src/coloring.cpp:55-113 (kH1, kUnifStage1, kUnifStage2, kLeaf)."""
     index = {}
     sets = []
 
@@ -355,6 +355,12 @@ def build_constraints(tree, adj, level, mode):
             z = set(adj.neighbors[a]) | set(adj.interaction[a]) | set(adj.coarse_leaf_neighbors[a])
             z.discard(b)
             add(((b, GAUSSIAN),), tuple(sorted(z)), (a, b))
+    elif mode == UNIF2:
+        # adjoint-side probe carrying the alpha basis, observed at I_beta
+        for a, b in admissible_pairs(tree, adj, level):
+            z = set(adj.neighbors[b]) | set(adj.interaction[b]) | set(adj.coarse_leaf_neighbors[b])
+            z.discard(a)
+            add(((a, BASIS),), tuple(sorted(z)), (a, b))
     elif mode == UNIF1:
         if level < 2 or level > tree.depth:
             raise ValueError("sampling level out of range")
@@ -540,7 +546,7 @@ def dsatur_color(edges):
 def plan_coloring(tree, sets, edges, mode):
     """proj/src/coloring.cpp:218-250."""
     color, ncol = dsatur_color(edges)
-    if not tree.is_fully_populated():
+    if mode == UNIF2 or not tree.is_fully_populated():
         return color, ncol
     mod = {H1: 6, UNIF1: 5, LEAF: 3}[mode]
     relabel = {}
@@ -575,13 +581,19 @@ class BlockTestMatrix:
     zero: list
     serves: list
 
-    def realize(self, tree):
+    def realize(self, tree, basis_table=None):
         """proj/src/coloring.cpp:261-291."""
         out = np.zeros((self.rows, self.width))
         for box, tag in self.payload:
             pts = tree.box(box).points
             if tag == GAUSSIAN:
                 blk = payload_gaussian(tree, box, self.width, self.seed, self.level, self.phase)
+            elif tag == BASIS:
+                if basis_table is None or box not in basis_table:
+                    raise RuntimeError("missing basis for payload box")
+                basis = basis_table[box]
+                blk = np.zeros((len(pts), self.width))
+                blk[:, :basis.shape[1]] = basis
             else:
                 blk = np.zeros((len(pts), self.width))
                 k = min(len(pts), self.width)
@@ -590,8 +602,9 @@ class BlockTestMatrix:
         return out
 
 
-def assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase):
-    """proj/src/coloring.cpp:293-332."""
+def assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase, basis_table=None):
+    """proj/src/coloring.cpp:293-332 (basis payloads: width = the widest
+    basis of the color)."""
     mats = [BlockTestMatrix(tree.num_points, width, seed, level, phase, [], [], []) for _ in range(ncol)]
     merged = [dict() for _ in range(ncol)]
     zeros = [set() for _ in range(ncol)]
@@ -606,6 +619,11 @@ def assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase):
     for c in range(ncol):
         mats[c].payload = sorted(merged[c].items())
         mats[c].zero = sorted(zeros[c])
+        bases = [b for b, t in mats[c].payload if t == BASIS]
+        if bases:
+            if basis_table is None or any(b not in basis_table for b in bases):
+                raise RuntimeError("missing basis for payload box")
+            mats[c].width = max([1] + [basis_table[b].shape[1] for b in bases])
     return mats
 
 
@@ -616,21 +634,25 @@ class Plan:
     color: list
     matrices: list
     block_to_matrix: dict
+    box_to_matrix: dict = field(default_factory=dict)
 
 
-def make_plan(tree, adj, level, mode, width, seed, phase):
+def make_plan(tree, adj, level, mode, width, seed, phase, basis_table=None):
     """proj/src/peeling.cpp:98-154 (graph strategy)."""
     sets = build_constraints(tree, adj, level, mode)
     if not sets:
         return Plan([], [], [], [], {})
     edges = build_graph(sets)
     color, ncol = plan_coloring(tree, sets, edges, mode)
-    mats = assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase)
-    b2m = {}
+    mats = assemble_test_matrices(sets, color, ncol, tree, level, width, seed, phase, basis_table)
+    b2m, box2m = {}, {}
     for i, s in enumerate(sets):
         for o in s.owners:
-            b2m[o] = color[i]
-    return Plan(sets, edges, color, mats, b2m)
+            if mode == UNIF1:
+                box2m[o[0]] = color[i]
+            else:
+                b2m[o] = color[i]
+    return Plan(sets, edges, color, mats, b2m, box2m)
 
 
 # --------------------------------------------------------------------------- linalg
@@ -878,6 +900,69 @@ class H1Rep:
         return t
 
 
+class UnifH1Rep:
+    """Uniform H1 (proj/include/hpeel/hmatrix.hpp:73-97, proj/src/hmatrix.cpp:152-250):
+    one row basis U_a and one column basis V_b per box, a coupling B_ab per
+    admissible pair."""
+
+    def __init__(self, tree, adj):
+        self.tree = tree
+        self.adj = adj
+        self.built_level = 1
+        self.dense_ready = False
+        self.box_u = {}
+        self.box_v = {}
+        self.level_b = [dict() for _ in range(tree.depth + 1)]
+        self.dense = {}
+
+    def _check(self, level):
+        if level > self.built_level:
+            raise RuntimeError(f"unif-h1 apply: representation incomplete for level {level}")
+
+    def apply_truncated(self, level, x):
+        """proj/src/hmatrix.cpp:165-189."""
+        self._check(level)
+        y = np.zeros_like(x)
+        for l in range(2, min(level, self.tree.depth) + 1):
+            qhat, uhat = {}, {}
+            for (a, b), bb in sorted(self.level_b[l].items()):
+                if b not in qhat:
+                    qhat[b] = self.box_v[b].T @ x[self.tree.box(b).points]
+                uhat[a] = uhat.get(a, 0) + bb @ qhat[b]
+            for a in sorted(uhat):
+                y[self.tree.box(a).points] += self.box_u[a] @ uhat[a]
+        return y
+
+    def apply_truncated_adjoint(self, level, x):
+        """proj/src/hmatrix.cpp:191-215."""
+        self._check(level)
+        y = np.zeros_like(x)
+        for l in range(2, min(level, self.tree.depth) + 1):
+            qhat, vhat = {}, {}
+            for (a, b), bb in sorted(self.level_b[l].items()):
+                if a not in qhat:
+                    qhat[a] = self.box_u[a].T @ x[self.tree.box(a).points]
+                vhat[b] = vhat.get(b, 0) + bb.T @ qhat[a]
+            for b in sorted(vhat):
+                y[self.tree.box(b).points] += self.box_v[b] @ vhat[b]
+        return y
+
+    def apply_truncated_rows(self, level, x, mask, adjoint=False):
+        out = self.apply_truncated_adjoint(level, x) if adjoint else self.apply_truncated(level, x)
+        out[~mask] = 0.0
+        return out
+
+    _dense = H1Rep._dense
+    apply = H1Rep.apply
+    apply_adjoint = H1Rep.apply_adjoint
+
+    def storage(self):
+        t = sum(u.size for u in self.box_u.values()) + sum(v.size for v in self.box_v.values())
+        t += sum(b.size for lv in self.level_b for b in lv.values())
+        t += sum(d.size for d in self.dense.values())
+        return t
+
+
 # --------------------------------------------------------------------------- driver
 # proj/src/peeling.cpp
 
@@ -919,14 +1004,16 @@ def _now():
     return time.perf_counter()
 
 
-def _served_rows(tree, plan, m_index):
+def _served_rows(tree, plan, m_index, owner_row=0):
     """Tree points of the row boxes of the pairs a color serves (the rows the
-    extraction reads back from its sample)."""
-    pts = [tree.box(o[0]).points for i in plan.matrices[m_index].serves for o in plan.sets[i].owners]
+    extraction reads back from its sample; owner_row 1: the column box, for
+    the uniform driver's adjoint basis probes)."""
+    pts = [tree.box(o[owner_row]).points for i in plan.matrices[m_index].serves for o in plan.sets[i].owners]
     return np.unique(np.concatenate(pts)) if pts else np.zeros(0, dtype=np.int64)
 
 
-def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None, restrict=False, raw=None):
+def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None, restrict=False, raw=None,
+                      basis_table=None, owner_row=0):
     """proj/src/peeling.cpp:158-178. Returns (samples, cols). restrict=True
     computes only the rows the extraction reads (value-identical on those
     rows: the same products over the nonzero rows of Omega; other rows 0).
@@ -942,11 +1029,11 @@ def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None
         if phase is not None:
             m = BlockTestMatrix(m.rows, m.width, m.seed, m.level, phase, m.payload, m.zero, m.serves)
         t0 = _now()
-        omega = m.realize(rep.tree)
+        omega = m.realize(rep.tree, basis_table)
         times.add("realize", t0)
         cols += omega.shape[1]
         if restrict:
-            rows = _served_rows(rep.tree, plan, ci)
+            rows = _served_rows(rep.tree, plan, ci, owner_row)
             mask = np.zeros(omega.shape[0], dtype=bool)
             mask[rows] = True
             t0 = _now()
@@ -1035,6 +1122,63 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict
     return rep
 
 
+def run_uniform(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict=False):
+    """proj/src/peeling.cpp:291-454 for the uniform-H1 target (no nesting):
+    stage 1 samples each box against its whole interaction list and takes the
+    row basis U_a from them; stage 2 loads U_a into adjoint probes, reads
+    S_ab = A_ab^T U_a at I_b, takes the column basis V_b from sum_a S_ab and
+    the couplings B_ab = S_ab^T V_b."""
+    times = PhaseTimes() if times is None else times
+    rep = UnifH1Rep(tree, adj)
+    r = k + p
+    for l in range(2, tree.depth + 1):
+        pairs = admissible_pairs(tree, adj, l)
+        if not pairs:
+            continue
+        ps = set(pairs)
+        if any((b, a) not in ps for a, b in pairs):
+            raise AssertionError("asymmetric admissibility structure")
+        # stage 1 (forward phase, Gaussian payloads on the interaction lists)
+        plan1 = make_plan(tree, adj, l, UNIF1, r, seed, 0)
+        ys, fcols = _residual_samples(op, rep, l - 1, plan1, False, times=times, restrict=restrict)
+        for a in tree.level_boxes(l):
+            if a not in plan1.box_to_matrix:
+                continue
+            sample = ys[plan1.box_to_matrix[a]][tree.box(a).points]
+            with _small_blas():
+                rep.box_u[a] = qr_orthonormal(sample, k)
+        report.append({"phase": "unif-stage1", "level": l, "colors": len(plan1.matrices),
+                       "forward_cols": fcols, "adjoint_cols": 0})
+        # stage 2 (adjoint probes carrying the stage-1 bases)
+        basis_table = {a: rep.box_u[a] for a in tree.level_boxes(l) if adj.interaction[a]}
+        plan2 = make_plan(tree, adj, l, UNIF2, r, seed, 1, basis_table)
+        zs, acols = _residual_samples(op, rep, l - 1, plan2, True, times=times, restrict=restrict,
+                                      basis_table=basis_table, owner_row=1)
+        projected = {}
+        for a, b in pairs:
+            z = zs[plan2.block_to_matrix[(a, b)]]
+            projected[(a, b)] = z[tree.box(b).points][:, :rep.box_u[a].shape[1]]
+        if capture is not None:
+            capture[l] = {"u": {a: rep.box_u[a] for a in basis_table}, "s": dict(projected)}
+        for b in tree.level_boxes(l):
+            width = max([0] + [projected[(a, b)].shape[1] for a in adj.interaction[b]])
+            if width == 0:
+                continue
+            acc = np.zeros((len(tree.box(b).points), width))
+            for a in adj.interaction[b]:
+                sab = projected[(a, b)]
+                acc[:, :sab.shape[1]] += sab
+            with _small_blas():
+                rep.box_v[b] = qr_orthonormal(acc, k)
+        for a, b in pairs:
+            rep.level_b[l][(a, b)] = projected[(a, b)].T @ rep.box_v[b]
+        rep.built_level = l
+        report.append({"phase": "unif-stage2", "level": l, "colors": len(plan2.matrices),
+                       "forward_cols": 0, "adjoint_cols": acols})
+    rep.built_level = tree.depth
+    return rep
+
+
 def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False):
     """proj/src/peeling.cpp:490-524."""
     times = PhaseTimes() if times is None else times
@@ -1060,7 +1204,8 @@ def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False
                    "forward_cols": fcols, "adjoint_cols": 0})
 
 
-def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, restrict=False, raw_capture=None):
+def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, restrict=False, raw_capture=None,
+             fmt="h1"):
     """proj/src/peeling.cpp:576-639 for format h1. Returns (rep, report).
     `times` (a PhaseTimes) collects wall seconds per phase. restrict=True
     evaluates each color's black-box product and peeling only on the rows the
@@ -1077,7 +1222,12 @@ def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, 
     if times is not None:
         times.add("adjacency", t0)
     report = []
-    rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict, raw_capture)
+    if fmt == "unif-h1":
+        rep = run_uniform(op, tree, adj, k, p, seed, report, capture, times, restrict)
+    elif fmt == "h1":
+        rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict, raw_capture)
+    else:
+        raise ValueError("unsupported format: " + fmt)
     extract_leaf(op, rep, seed, report, leaf_capture, times, restrict)
     return rep, report
 
@@ -1112,19 +1262,39 @@ def rel_error_power_method(approx, ref, iters, seed):
     return err / base
 
 
-def synth_rank_structured(tree, adj, k, seed):
-    """proj/src/operators.cpp:375-448, H1 format: per-pair rank-k blocks and
-    Gaussian dense leaf blocks."""
+def _orth_gaussian(rows, cols, seed):
+    """proj/src/operators.cpp:368-371: orthonormal basis of a Gaussian block."""
+    return qr_orthonormal(gaussian_matrix(rows, cols, seed))
+
+
+def synth_rank_structured(tree, adj, k, seed, fmt="h1"):
+    """proj/src/operators.cpp:375-448 (H1 and uniform-H1 formats): per-pair
+    rank-k blocks (H1: independent Gaussian factors; uniform: shared
+    orthonormal bases per box with a Gaussian core) and Gaussian dense leaf
+    blocks."""
     n = tree.num_points
     if n > 4096:
         raise ValueError("synthetic dense capped at 4096")
     a = np.zeros((n, n))
+    bu, bv = {}, {}
+    if fmt == "unif-h1":
+        for l in range(tree.depth, 0, -1):
+            for b in tree.level_boxes(l):
+                rows = len(tree.box(b).points)
+                bu[b] = _orth_gaussian(rows, k, mix_seed(seed, 101, b))
+                bv[b] = _orth_gaussian(rows, k, mix_seed(seed, 102, b))
+    elif fmt != "h1":
+        raise ValueError("unsupported synthetic format: " + fmt)
     for l in range(2, tree.depth + 1):
         for al, be in admissible_pairs(tree, adj, l):
             rows, cols = tree.box(al).points, tree.box(be).points
-            gu = gaussian_matrix(len(rows), k, mix_seed(seed, 201, al, be))
-            gv = gaussian_matrix(k, len(cols), mix_seed(seed, 202, al, be))
-            a[np.ix_(rows, cols)] = gu @ gv / math.sqrt(k)
+            if fmt == "h1":
+                gu = gaussian_matrix(len(rows), k, mix_seed(seed, 201, al, be))
+                gv = gaussian_matrix(k, len(cols), mix_seed(seed, 202, al, be))
+                a[np.ix_(rows, cols)] = gu @ gv / math.sqrt(k)
+            else:
+                core = gaussian_matrix(bu[al].shape[1], bv[be].shape[1], mix_seed(seed, 203, al, be))
+                a[np.ix_(rows, cols)] = bu[al] @ core @ bv[be].T
     for lam, mu in dense_pairs(tree, adj):
         rows, cols = tree.box(lam).points, tree.box(mu).points
         a[np.ix_(rows, cols)] = gaussian_matrix(len(rows), len(cols), mix_seed(seed, 204, lam, mu))

@@ -82,9 +82,16 @@ std::vector<int> without(const std::vector<int>& sorted, int value) {
 std::vector<ConstraintSet> build_constraints(const BoxTree& tree, const AdjacencyInfo& adj,
                                              int level, SampleMode mode) {
   RequirementTable table;
-  if (mode == SampleMode::kUnifStage2)
-    throw std::invalid_argument("unif-stage2 constraints need the uniform driver (out of scope)");
-  if (mode == SampleMode::kH1) {
+  if (mode == SampleMode::kUnifStage2) {
+    // (alpha, beta): adjoint-side probe carrying the alpha basis, observed at
+    // I_beta; zero N(beta) u I(beta) u CL(beta) minus alpha
+    std::vector<int> reach;
+    for (const auto& [alpha, beta] : admissible_pairs(tree, adj, level)) {
+      reach = union_of({&adj.neighbors[size_t(beta)], &adj.interaction[size_t(beta)],
+                        &adj.coarse_leaf_neighbors[size_t(beta)]});
+      table.add({{alpha, PayloadTag::kBasis}}, without(reach, alpha), {alpha, beta});
+    }
+  } else if (mode == SampleMode::kH1) {
     // (alpha, beta): payload {beta: Gaussian}, zero N(alpha) u I(alpha) u
     // CL(alpha) minus beta; one union per row box alpha
     std::vector<int> reach;
@@ -839,7 +846,6 @@ std::vector<BlockTestMatrix> assemble_test_matrices(const std::vector<Constraint
       if (!ins.second && ins.first->second != tag) {
         throw std::logic_error("conflicting payload tags within a color");
       }
-      if (tag == PayloadTag::kBasis) throw std::runtime_error("missing basis for payload box");
     }
     zeros[size_t(c)].insert(zeros[size_t(c)].end(), sets[i].zero.begin(), sets[i].zero.end());
   }

@@ -31,9 +31,8 @@ struct ConstraintSet {
   }
 };
 
-/// proj/src/coloring.cpp:55-113. Modes kH1 and kLeaf (the hot path) and
-/// kUnifStage1 (used by the known-answer tests); kUnifStage2 needs per-box
-/// bases of the uniform driver and throws std::invalid_argument here.
+/// proj/src/coloring.cpp:55-113: kH1, kUnifStage1, kUnifStage2 (basis
+/// payloads: the uniform driver supplies the bases) and kLeaf.
 std::vector<ConstraintSet> build_constraints(const BoxTree& tree, const AdjacencyInfo& adj,
                                              int level, SampleMode mode);
 

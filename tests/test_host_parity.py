@@ -79,18 +79,21 @@ def _compare_plan(hp, t, ot, oadj, level, mode, omode):
         assert p.color == col and p.n_colors == n
         dcol, dn = O.dsatur_color(edges)
         assert p.dsatur_color == dcol and p.dsatur_colors == dn
-        mats = O.assemble_test_matrices(sets, col, n, ot, level, 12, 7, 0)
+        basis = {b.id: np.zeros((0, 12)) for b in ot.boxes} if omode == O.UNIF2 else None
+        mats = O.assemble_test_matrices(sets, col, n, ot, level, 12, 7, 0, basis)
         assert p.color_payload == [[b for b, _ in m.payload] for m in mats]
     return p
 
 
 @pytest.mark.parametrize("name,pts,leaf", GEOMS, ids=[g[0] for g in GEOMS])
-def test_h1_and_leaf_plans_bit_exact(hp, name, pts, leaf):
+def test_level_and_leaf_plans_bit_exact(hp, name, pts, leaf):
     t = hp.build_tree(pts, leaf)
     ot = O.BoxTree(O.PointCloud(pts), leaf)
     oadj = O.adjacency(ot)
     for l in range(2, ot.depth + 1):
         _compare_plan(hp, t, ot, oadj, l, "h1", O.H1)
+        _compare_plan(hp, t, ot, oadj, l, "unif-stage1", O.UNIF1)
+        _compare_plan(hp, t, ot, oadj, l, "unif-stage2", O.UNIF2)
     _compare_plan(hp, t, ot, oadj, ot.depth, "leaf", O.LEAF)
 
 
