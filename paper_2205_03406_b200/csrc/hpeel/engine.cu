@@ -8,6 +8,8 @@
 #include "shard.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <map>
 #include <limits>
 #include <unordered_map>
@@ -191,8 +193,42 @@ std::pair<int, int> first_range(const std::vector<std::pair<int, int>>& pairs, i
 
 // ---------------------------------------------------------------- K4
 
+// HP_QR=householder selects the register-resident Householder kernels
+// (k_qr2.cu) instead of the Gram-based range finder (k_gqr.cu).
+static bool qr_use_gram(int r, int kmax) {
+  const char* e = std::getenv("HP_QR");
+  if (e && std::string(e) == "householder") return false;
+  return gqr_supported(r, kmax);
+}
+
 QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
   QrPlan pl;
+  if (qr_use_gram(r, kmax)) {
+    pl.gram = true;
+    pl.gblocks.reserve(reqs.size());
+    for (const QrRequest& q : reqs) {
+      GqrBlock b{};
+      b.a = q.a;
+      b.out = q.out;
+      b.lda = q.rows;
+      b.ldo = q.ldo;
+      b.rows = q.rows;
+      b.rank_slot = q.rank_slot;
+      b.task0 = int(pl.gtasks.size());
+      // row tasks of equal size (<= kGqrTaskRows)
+      const int nt = std::max(1, (q.rows + kGqrTaskRows - 1) / kGqrTaskRows);
+      const int base = q.rows / nt, extra = q.rows % nt;
+      int row = 0;
+      for (int i = 0; i < nt; ++i) {
+        const int rr = base + (i < extra ? 1 : 0);
+        pl.gtasks.push_back(GqrTask{int(pl.gblocks.size()), row, rr});
+        row += rr;
+      }
+      b.ntasks = nt;
+      pl.gblocks.push_back(b);
+    }
+    return pl;
+  }
   // register-resident kernels when the widths allow, else shared-memory ones
   // (chunks must hold more than r rows or TSQR cannot shrink the stack)
   pl.reg = qr_reg_cols(r) != 0 && qr_reg_cols(kmax) != 0 &&
@@ -255,8 +291,43 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
   return pl;
 }
 
+// Batches of whole blocks bounded by the workspace they need (Gram partials
+// per row task, transforms and state per block).
+static void run_gqr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, int kmax,
+                    cudaStream_t s) {
+  const std::int64_t psz = gqr_part_doubles(r, kmax), wsz = gqr_w_doubles(r, kmax);
+  constexpr std::int64_t kBudget = std::int64_t(3) << 27;  // doubles (3 GiB)
+  const size_t nb = pl.gblocks.size();
+  size_t b0 = 0;
+  while (b0 < nb) {
+    size_t b1 = b0;
+    std::int64_t need = 0;
+    while (b1 < nb) {
+      const std::int64_t add = std::int64_t(pl.gblocks[b1].ntasks) * psz + wsz;
+      if (b1 > b0 && need + add > kBudget) break;
+      need += add;
+      ++b1;
+    }
+    std::vector<GqrBlock> blocks(pl.gblocks.begin() + std::ptrdiff_t(b0), pl.gblocks.begin() + std::ptrdiff_t(b1));
+    const int t0 = blocks.front().task0, t1 = blocks.back().task0 + blocks.back().ntasks;
+    std::vector<GqrTask> tasks(pl.gtasks.begin() + t0, pl.gtasks.begin() + t1);
+    for (GqrBlock& b : blocks) b.task0 -= t0;
+    for (GqrTask& t : tasks) t.block -= int(b0);
+    DevBuf<GqrBlock> d_blocks;
+    d_blocks.upload(blocks, s);
+    DevBuf<GqrTask> d_tasks;
+    d_tasks.upload(tasks, s);
+    DevBuf<GqrState> d_state(blocks.size(), s);
+    DevBuf<double> part(size_t(tasks.size()) * size_t(psz), s), wbuf(blocks.size() * size_t(wsz), s);
+    launch_gqr(d_blocks.get(), int(blocks.size()), d_tasks.get(), int(tasks.size()), d_state.get(), data, out,
+               part.get(), wbuf.get(), d_ranks, r, kmax, kQrRankDropTol, s);
+    b0 = b1;
+  }
+}
+
 void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, int kmax,
             cudaStream_t s) {
+  if (pl.gram) return run_gqr(pl, data, out, d_ranks, r, kmax, s);
   auto max_rows = [](const std::vector<QrBlock>& v) {
     int m = 1;
     for (const QrBlock& b : v) m = std::max(m, b.rows);

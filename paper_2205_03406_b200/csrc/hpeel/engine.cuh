@@ -202,6 +202,10 @@ struct QrPlan {
   std::vector<std::vector<QrBlock>> chunk_rounds, back_rounds;
   std::int64_t wsize = 0, tausize = 0;
   bool reg = false;  // register-resident kernels (k_qr2.cu)
+  // Gram-based range finder (k_gqr.cu): when set, the lists above stay empty
+  bool gram = false;
+  std::vector<GqrBlock> gblocks;
+  std::vector<GqrTask> gtasks;
 };
 QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax);
 void run_qr(const QrPlan& plan, double* data, double* out, int* d_ranks, int r, int kmax,

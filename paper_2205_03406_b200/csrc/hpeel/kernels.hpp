@@ -201,6 +201,38 @@ void launch_qr_reg_backprop(const QrBlock* blocks, int nb, const double* data, c
                             const double* parent, double* outbuf, int cols, int kmax, int max_rows,
                             cudaStream_t s);
 
+/// Gram-based range finder (k_gqr.cu): staged pivoted Cholesky-QR on DMMA,
+/// the same pivots / kept rank / span as launch_qr_top's pivoted Householder
+/// QR (proj/src/linalg.cpp:53-78), blocks of any height. The input block is
+/// destroyed (deflated in place).
+struct GqrBlock {
+  std::int64_t a;    // input block (col-major, ld lda)
+  std::int64_t out;  // Q output (ld ldo, kmax columns, zero beyond the kept rank)
+  int lda;
+  int ldo;
+  int rows;
+  int rank_slot;     // index into ranks (or -1)
+  int task0;         // first row task of this block
+  int ntasks;
+};
+struct GqrTask {
+  int block;
+  int row0;
+  int rows;
+};
+struct GqrState {    // per block, device-only
+  int done, last, kq, j, keep, pad;
+  double d00;
+  unsigned char used[96];
+};
+constexpr int kGqrTaskRows = 256;
+bool gqr_supported(int r, int kmax);
+std::int64_t gqr_part_doubles(int r, int kmax);  // Gram workspace per row task
+std::int64_t gqr_w_doubles(int r, int kmax);     // transform workspace per block
+void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
+                double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
+                cudaStream_t s);
+
 // ---------------------------------------------------------------- K5 B
 /// Register-resident pivoted-QR B solve (k_bsolve2.cu, k <= 64, r <= 80):
 /// bsolve_qr_kernel's contract; false when the widths are unsupported.
