@@ -13,13 +13,16 @@
 // ~1e2 or worse) is flagged and solved by the Jacobi-SVD kernel instead,
 // which implements pinv_apply itself.
 //
-// One CTA per pair: M and the right-hand side in shared memory (odd leading
-// dimensions, conflict-free column reads), Gram products accumulated in
-// registers, a right-looking Cholesky and column-per-thread triangular solves.
+// One CTA per pair: M and the right-hand side in shared memory (leading
+// dimensions == 4 mod 16: conflict-free DMMA fragments), Gram products on
+// DMMA tiles, a left-looking Cholesky that builds X = L^-T alongside
+// (chol.cuh) and the solves as N^-1 Y = X (X^T Y) on DMMA tiles (were
+// column-per-thread triangular substitutions: a 2 k^2-long dependent chain).
 #include <cuda_runtime.h>
 
 #include <cmath>
 
+#include "chol.cuh"
 #include "kernels.hpp"
 
 namespace hpeel {
@@ -78,112 +81,42 @@ __device__ __forceinline__ void atb_dmma(const double* P, int ps_i, int ps_c, co
 }
 
 // N = A^T A (lower, k x k, ld ldn) and Y = A^T X (k x nr), Y written over X
-// with ld k + 1 once every thread has read X. A: r x k (ld lda), X: r x nr.
+// with ld ldn once every thread has read X. A: r x k (ld lda), X: r x nr.
 __device__ void gram_pair(const double* a, double* x, double* n, int r, int k, int nr, int lda, int ldx,
                           int ldn) {
-  atb_dmma(a, 1, lda, x, 1, ldx, r, k, nr, [&](int c, int d, double v) { x[c + d * (k + 1)] = v; });
+  atb_dmma(a, 1, lda, x, 1, ldx, r, k, nr, [&](int c, int d, double v) { x[c + d * ldn] = v; });
   atb_dmma(a, 1, lda, a, 1, lda, r, k, k, [&](int c, int d, double v) {
     if (c >= d) n[c + d * ldn] = v;
   });
 }
 
-// In-place lower Cholesky of n (k x k, ld ldn). Exactly zero diagonals mark
-// null columns (zero rows in the solution). Returns false when a nonzero
-// pivot is small relative to the largest (or the matrix is not positive).
-// Per column: warp 0 takes the pivot and scales the column (shuffle
-// broadcast, no block barrier), then all warps update the trailing triangle
-// with columns on warps and rows on lanes (no index division): two block
-// barriers per column.
-__device__ bool cholesky(double* n, int k, int ldn, int* null_col) {
+// N = L L^T in place (lower, ld ldn) with X = L^-T (upper, k x k, ld ldx)
+// built alongside (chol.cuh: one barrier pair per column, rows on threads).
+// Exactly zero diagonals mark null columns (zero rows in the solution).
+// Returns false when a pivot is negative or small relative to the largest.
+__device__ bool cholesky_inv(double* n, int k, int ldn, double* xinv, int ldx, int* status, CholShared& cs) {
   __shared__ int bad;
-  __shared__ double dmax;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kWarps = kBsThreads / 32;
+  double d00 = 0.0;
+  int last = 0;
+  bool used = false;
+  const CholStops stops{0, 0.0, 0.0, 0.0};
+  lazy_chol<false>(n, ldn, n, ldn, xinv, ldx, k, 0, k, stops, d00, last, used, cs, status);
   if (threadIdx.x == 0) {
-    bad = 0;
-    dmax = 0.0;
-  }
-  __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    if (warp == 0) {
-      int nul = 0;
-      double l = 0.0;
-      if (lane == 0) {
-        const double d = n[j + j * ldn];
-        if (d == 0.0) {
-          nul = 1;
-        } else if (!(d > 0.0)) {
-          bad = 1;
-          nul = 1;
-          n[j + j * ldn] = 0.0;
-        } else {
-          l = sqrt(d);
-          n[j + j * ldn] = l;
-          dmax = fmax(dmax, l);
-        }
-        null_col[j] = nul;
-      }
-      nul = __shfl_sync(0xffffffffu, nul, 0);
-      l = __shfl_sync(0xffffffffu, l, 0);
-      if (!nul) {
-        const double inv = 1.0 / l;
-        for (int i = j + 1 + lane; i < k; i += 32) n[i + j * ldn] *= inv;
-      }
-    }
-    __syncthreads();
-    if (!null_col[j]) {
-      for (int c = j + 1 + warp; c < k; c += kWarps) {
-        const double lc = n[c + j * ldn];
-        for (int i = c + lane; i < k; i += 32) n[i + c * ldn] = fma(-n[i + j * ldn], lc, n[i + c * ldn]);
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
+    double dmax = 0.0;
+    int b = 0;
+    for (int j = 0; j < k; ++j) dmax = fmax(dmax, n[j + j * ldn]);
     for (int j = 0; j < k; ++j)
-      if (!null_col[j] && n[j + j * ldn] < kCholFlag * dmax) bad = 1;
+      if (status[j] == 2 || (status[j] == 0 && n[j + j * ldn] < kCholFlag * dmax)) b = 1;
+    bad = b;
   }
   __syncthreads();
   return bad == 0;
 }
 
-// y (k x nr, ld ldy) <- N^{-1} y with N = L L^T; null columns give zero rows.
-// One thread per right-hand side; each substitution sum runs as four
-// independent partial sums (a quarter of the dependent FMA chain).
-__device__ void chol_solve(const double* n, int k, int ldn, const int* null_col, double* y, int nr, int ldy) {
-  for (int c = threadIdx.x; c < nr; c += kBsThreads) {
-    double* yc = y + c * ldy;
-    for (int i = 0; i < k; ++i) {
-      if (null_col[i]) {
-        yc[i] = 0.0;
-        continue;
-      }
-      double s0 = yc[i], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int l = 0;
-      for (; l + 4 <= i; l += 4) {
-        s0 = fma(-n[i + l * ldn], yc[l], s0);
-        s1 = fma(-n[i + (l + 1) * ldn], yc[l + 1], s1);
-        s2 = fma(-n[i + (l + 2) * ldn], yc[l + 2], s2);
-        s3 = fma(-n[i + (l + 3) * ldn], yc[l + 3], s3);
-      }
-      for (; l < i; ++l) s0 = fma(-n[i + l * ldn], yc[l], s0);
-      yc[i] = ((s0 + s1) + (s2 + s3)) / n[i + i * ldn];
-    }
-    for (int i = k - 1; i >= 0; --i) {
-      if (null_col[i]) continue;
-      double s0 = yc[i], s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int l = i + 1;
-      for (; l + 4 <= k; l += 4) {
-        s0 = fma(-n[l + i * ldn], yc[l], s0);
-        s1 = fma(-n[l + 1 + i * ldn], yc[l + 1], s1);
-        s2 = fma(-n[l + 2 + i * ldn], yc[l + 2], s2);
-        s3 = fma(-n[l + 3 + i * ldn], yc[l + 3], s3);
-      }
-      for (; l < k; ++l) s0 = fma(-n[l + i * ldn], yc[l], s0);
-      yc[i] = ((s0 + s1) + (s2 + s3)) / n[i + i * ldn];
-    }
-  }
-  __syncthreads();
+// y (k x nr, ld ldy) <- N^{-1} y = X (X^T y) on DMMA tiles.
+__device__ void chol_solve(const double* xinv, int k, int ldx, double* y, int nr, int ldy) {
+  atb_dmma(xinv, 1, ldx, y, 1, ldy, k, k, nr, [&](int c, int d, double v) { y[c + d * ldy] = v; });
+  atb_dmma(xinv, ldx, 1, y, 1, ldy, k, k, nr, [&](int c, int d, double v) { y[c + d * ldy] = v; });
 }
 
 __global__ void __launch_bounds__(kBsThreads)
@@ -191,11 +124,14 @@ bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ m
                    const double* __restrict__ vg, int r, int k, const std::int64_t* __restrict__ boff,
                    double* __restrict__ bout, int* __restrict__ flags) {
   extern __shared__ double sm[];
-  __shared__ int null_col[64];
-  const int lda = r + 1, ldx = r + 1, ldn = k + 1;
-  double* a = sm;                         // r x k (ld r + 1)
-  double* x = a + lda * k;                // r x r (ld r + 1); later k x r / k x k (ld k + 1)
-  double* n = x + ldx * (r > k ? r : k);  // k x k (ld k + 1)
+  __shared__ int status[64];
+  __shared__ CholShared cs;
+  // leading dimensions == 4 (mod 16): conflict-free DMMA fragment reads
+  const int lda = ld4(r), ldx = ld4(r), ldn = ld4(k);
+  double* a = sm;               // r x k (ld lda)
+  double* x = a + lda * k;      // r x r (ld ldx); later k x r / k x k (ld ldn)
+  double* n = x + ldx * r;      // k x k (ld ldn)
+  double* xinv = n + ldn * k;   // k x k (ld ldn)
   const std::int64_t p = blockIdx.x;
   const int t = threadIdx.x;
   // 1) left = pinv(M1) middle, M1 = G'^T U (r x k), middle r x r
@@ -203,8 +139,8 @@ bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ m
   for (int e = t; e < r * r; e += kBsThreads) x[e % r + (e / r) * ldx] = middle[p * r * r + e];
   __syncthreads();
   gram_pair(a, x, n, r, k, r, lda, ldx, ldn);
-  const bool ok1 = cholesky(n, k, ldn, null_col);
-  chol_solve(n, k, ldn, null_col, x, r, k + 1);  // left (k x r, ld k + 1) in x
+  const bool ok1 = cholesky_inv(n, k, ldn, xinv, ldn, status, cs);
+  chol_solve(xinv, k, ldn, x, r, ldn);  // left (k x r, ld ldn) in x
   // 2) out2 = pinv(M2) left^T, M2 = (V^T G)^T (r x k): M2(i, c) = vg(c, i)
   for (int e = t; e < r * k; e += kBsThreads) {
     const int i = e % r, c = e / r;
@@ -213,17 +149,17 @@ bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ m
   __syncthreads();
   // Y2 = M2^T left^T (k x k): Y2(c, d) = sum_i M2(i, c) left(d, i), over x;
   // N2 = M2^T M2 (lower)
-  atb_dmma(a, 1, lda, x, k + 1, 1, r, k, k, [&](int c, int d, double v) { x[c + d * (k + 1)] = v; });
+  atb_dmma(a, 1, lda, x, ldn, 1, r, k, k, [&](int c, int d, double v) { x[c + d * ldn] = v; });
   atb_dmma(a, 1, lda, a, 1, lda, r, k, k, [&](int c, int d, double v) {
     if (c >= d) n[c + d * ldn] = v;
   });
-  const bool ok2 = cholesky(n, k, ldn, null_col);
-  chol_solve(n, k, ldn, null_col, x, k, k + 1);  // out2 (k x k, ld k + 1)
+  const bool ok2 = cholesky_inv(n, k, ldn, xinv, ldn, status, cs);
+  chol_solve(xinv, k, ldn, x, k, ldn);  // out2 (k x k, ld ldn)
   const bool ok = ok1 && ok2;
   if (ok)
     for (int e = t; e < k * k; e += kBsThreads) {
       const int i = e % k, j = e / k;  // B(i, j) = out2(j, i)
-      bout[boff[p] + e] = x[j + i * (k + 1)];
+      bout[boff[p] + e] = x[j + i * ldn];
     }
   if (t == 0) flags[p] = ok ? 0 : 1;
 }
@@ -234,8 +170,7 @@ bool launch_bsolve_reg(int npairs, const double* gpu_, const double* middle, con
                        const std::int64_t* boff, double* b, int* flags, cudaStream_t s) {
   if (k > 64 || k > r || k * r > kBsThreads * 24 || k * k > kBsThreads * 16) return false;
   if (((k + 7) / 8) * ((r + 7) / 8) > (kBsThreads / 32) * kAtbTiles) return false;
-  const int mx = r > k ? r : k;
-  const size_t smem = size_t((r + 1) * k + (r + 1) * mx + (k + 1) * k) * sizeof(double);
+  const size_t smem = size_t(ld4(r) * k + ld4(r) * r + 2 * ld4(k) * k) * sizeof(double);
   if (smem > 220 * 1024) return false;
   HP_CUDA(cudaFuncSetAttribute(bsolve_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   bsolve_chol_kernel<<<npairs, kBsThreads, smem, s>>>(gpu_, middle, vg, r, k, boff, b, flags);

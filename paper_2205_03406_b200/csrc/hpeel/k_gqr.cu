@@ -33,21 +33,22 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "async.cuh"
+#include "chol.cuh"
 #include "kernels.hpp"
 
 namespace hpeel {
 
 namespace {
 
+constexpr double kGqrGap = 3e-13;  // runner-up margin in units of the stage's first pivot (chol.cuh)
 constexpr int kGqrThreads = 256;  // 8 warps: Gram / apply kernels
 constexpr int kSlice = 64;        // rows per shared-memory slice
 constexpr int kLds = 68;          // slice leading dimension: == 4 (mod 16) doubles, conflict-free fragments
 
 __host__ __device__ constexpr int up(int n, int q) { return (n + q - 1) / q * q; }
-// smallest ld >= n with ld == 4 (mod 16)
-__host__ __device__ constexpr int ld4(int n) { return (n + 11) / 16 * 16 + 4; }
 
 // rows [row0, row0 + rows) x cols [0, nc) of a col-major global block into a
 // slice (ld kLds) with cp.async (the caller commits and waits), zero-filled up
@@ -72,8 +73,10 @@ __device__ __forceinline__ void load_slice(double* dst, const double* src, std::
 // MODE 1: HG = Q(:, 0:kq+j)^T Q(:, kq:kq+j)   ((kq + j) x j)
 // MODE 2: Wd = Q(:, kq:kq+j)^T Y          (j x r)
 // One CTA per row task; partial at part + task * psz (col-major, ld = nx).
-template <int MODE>
-__global__ void __launch_bounds__(kGqrThreads, 2)
+// NV / NU: 8 x 8 output tiles per warp along X (half of the tile rows) / Y
+// (every fourth tile column) - sized by the launcher from r
+template <int MODE, int NV, int NU>
+__global__ void __launch_bounds__(kGqrThreads, (NV * NU <= 8 ? 3 : 2))
 gqr_gram_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__ tasks,
                 const GqrState* __restrict__ state, const double* data, const double* q, double* part, int r,
                 std::int64_t psz, int nbuf, int bufsz) {
@@ -120,11 +123,11 @@ gqr_gram_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__
   const int wi = warp & 1, wj = warp >> 1;  // tile-row half, tile-column residue (mod 4)
   const int ntx = nx8 / 8, nty = ny8 / 8;
   const int ti0 = wi * ((ntx + 1) / 2), ti1 = wi ? ntx : (ntx + 1) / 2;
-  double acc[3][6][2];
+  double acc[NU][NV][2];
 #pragma unroll
-  for (int u = 0; u < 3; ++u)
+  for (int u = 0; u < NU; ++u)
 #pragma unroll
-    for (int v = 0; v < 6; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+    for (int v = 0; v < NV; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
 
   // slices stream through one or two buffers (the next slice's cp.async
   // copies overlap this slice's DMMAs when two fit)
@@ -149,16 +152,16 @@ gqr_gram_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__
     const double* xc = xs + cur * bufsz;
     const double* yc = ys + cur * bufsz;
     for (int k0 = 0; k0 < rows4; k0 += 4) {
-      double af[6];
+      double af[NV];
 #pragma unroll
-      for (int v = 0; v < 6; ++v) af[v] = ti0 + v < ti1 ? xc[((ti0 + v) * 8 + g) * kLds + k0 + t4] : 0.0;
+      for (int v = 0; v < NV; ++v) af[v] = ti0 + v < ti1 ? xc[((ti0 + v) * 8 + g) * kLds + k0 + t4] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 3; ++u) {
+      for (int u = 0; u < NU; ++u) {
         const int tj = wj + 4 * u;
         if (tj < nty) {
           const double bf = yc[(tj * 8 + g) * kLds + k0 + t4];
 #pragma unroll
-          for (int v = 0; v < 6; ++v)
+          for (int v = 0; v < NV; ++v)
             if (ti0 + v < ti1) dmma8x8x4(acc[u][v][0], acc[u][v][1], af[v], bf);
         }
       }
@@ -170,11 +173,11 @@ gqr_gram_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__
   }
   double* out = part + std::int64_t(blockIdx.x) * psz;
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
+  for (int u = 0; u < NU; ++u) {
     const int tj = wj + 4 * u;
     if (tj >= nty) continue;
 #pragma unroll
-    for (int v = 0; v < 6; ++v) {
+    for (int v = 0; v < NV; ++v) {
       if (ti0 + v >= ti1) continue;
       const int c = (ti0 + v) * 8 + g, d = tj * 8 + 2 * t4;
       if (c < nx) {
@@ -189,8 +192,9 @@ gqr_gram_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__
 // MODE 0: Q(:, kq:kq+j)  = Y W1                 W1: r x j       (ld r)
 // MODE 1: Q(:, kq:kq+j)  = Q(:, 0:kq+j) W2      W2: (kq+j) x j  (ld kq+j), in place
 // MODE 2: Y             -= Q(:, kq:kq+j) Wd     Wd: j x r = the block's summed MODE-2 Gram matrix
-template <int MODE>
-__global__ void __launch_bounds__(kGqrThreads, 2)
+// NT: 8-column output tiles per warp (every second tile column)
+template <int MODE, int NT>
+__global__ void __launch_bounds__(kGqrThreads, (NT <= 4 ? 3 : 2))
 gqr_apply_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__ tasks,
                  const GqrState* __restrict__ state, double* data, double* q, const double* wbuf,
                  const double* part, int r, std::int64_t wsz, std::int64_t psz, int nbuf, int bufsz) {
@@ -269,17 +273,17 @@ gqr_apply_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict_
     __syncthreads();  // (also orders the W fill before its first use)
     const double* xc = xs + cur * bufsz;
     if (wm * 16 < rows8) {
-      double acc[2][6][2];
+      double acc[2][NT][2];
 #pragma unroll
       for (int u = 0; u < 2; ++u)
 #pragma unroll
-        for (int v = 0; v < 6; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
+        for (int v = 0; v < NT; ++v) acc[u][v][0] = acc[u][v][1] = 0.0;
       const bool two = wm * 16 + 8 < rows8;
       for (int k0 = 0; k0 < nin4; k0 += 4) {
         const double a0 = xc[(k0 + t4) * kLds + wm * 16 + g];
         const double a1 = two ? xc[(k0 + t4) * kLds + wm * 16 + 8 + g] : 0.0;
 #pragma unroll
-        for (int v = 0; v < 6; ++v) {
+        for (int v = 0; v < NT; ++v) {
           const int tn = wn + 2 * v;
           if (tn < ntn) {
             const double bf = ws[(tn * 8 + g) * ldw + k0 + t4];
@@ -293,7 +297,7 @@ gqr_apply_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict_
         const int row = wm * 16 + u * 8 + g;
         if (row >= rows) continue;
 #pragma unroll
-        for (int v = 0; v < 6; ++v) {
+        for (int v = 0; v < NT; ++v) {
           const int tn = wn + 2 * v;
           if (tn >= ntn) continue;
           const int d = tn * 8 + 2 * t4;
@@ -316,143 +320,6 @@ gqr_apply_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict_
 }
 
 // ------------------------------------------------------------------ small factorizations
-// Left-looking (lazy) Cholesky with the triangular inverse built alongside:
-// step j needs only column p_j of G, the rows of L built so far and the
-// downdated diagonal, so a step is one dot product per row (length j) and
-// ONE block barrier. Threads [0, 96) own the rows of L (and the diagonal
-// entry of their column); threads [96, 192) own the rows of
-// X = (L restricted to the pivots)^-T, X(:, j) = (e_j - sum_b L(p_j, b) X(:, b)) / L_jj,
-// the coefficients of Q1's column j over the pivot columns of Y.
-// L and X are column-major in shared memory (a thread walks its row with
-// stride ld: consecutive threads hit consecutive banks; the pivot row is a
-// broadcast). G (column-major, ld ldg) may live in global memory: column p is
-// read once, at its step. With PIVOT = false (natural order) L may alias G.
-constexpr int kCholThreads = 192;
-constexpr int kCholRows = 96;
-
-struct CholShared {
-  double wbest[2][4];
-  int widx[2][4];
-  int piv[96];
-  int pos[96];  // pivot position of a column chosen in this call, else -1
-};
-
-struct CholStops {  // PIVOT only
-  int steps;        // total pivots allowed (kq + j < steps)
-  double theta, tol2;
-};
-
-template <bool PIVOT>
-__device__ __forceinline__ int lazy_chol(const double* G, int ldg, double* L, int ldl, double* X, int ldx,
-                                         int n, int kq, int jmax, const CholStops& stops, double& d00,
-                                         int& last, bool& used, CholShared& cs) {
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const bool is_a = t < kCholRows;
-  const int i = t, bp = t - kCholRows;
-  const bool row = is_a && i < n;
-  double d = row ? G[std::int64_t(i) * ldg + i] : -1.0;
-  int mypos = -1;
-  auto publish = [&](int buf) {
-    double key = (row && !used) ? d : -1.0;
-    int idx = i;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const double ok = __shfl_xor_sync(0xffffffffu, key, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-      if (ok > key || (ok == key && oi < idx)) {
-        key = ok;
-        idx = oi;
-      }
-    }
-    if (lane == 0) {
-      cs.wbest[buf][warp] = key;
-      cs.widx[buf][warp] = idx;
-    }
-  };
-  if (PIVOT && is_a) publish(0);
-  if (is_a && i < 96) cs.pos[i] = -1;
-  __syncthreads();
-  double dstage = 0.0;
-  int j = 0;
-  while (j < jmax) {
-    double dp;
-    int p;
-    if (PIVOT) {
-      dp = cs.wbest[j & 1][0];
-      p = cs.widx[j & 1][0];
-#pragma unroll
-      for (int w = 1; w < kCholRows / 32; ++w)
-        if (cs.wbest[j & 1][w] > dp) {
-          dp = cs.wbest[j & 1][w];
-          p = cs.widx[j & 1][w];
-        }
-      if (kq + j == 0) {
-        if (!(dp > 0.0)) {  // zero block
-          last = 1;
-          break;
-        }
-        d00 = dp;
-      }
-      if (j == 0) dstage = dp;
-      if (!(dp > stops.tol2 * d00)) {  // |R_jj| <= tol |R_00|: numerical rank reached
-        last = 1;
-        break;
-      }
-      if (dp < stops.theta * dstage) break;  // next stage, on the deflated block
-    } else {
-      p = j;
-      dp = fmax(__shfl_sync(0xffffffffu, d, p & 31), 1e-300);  // valid in warp p / 32 only
-      if (lane == 0 && warp == (p >> 5)) cs.wbest[j & 1][0] = dp;
-      __syncthreads();
-      dp = cs.wbest[j & 1][0];
-    }
-    const double rsq = rsqrt(dp);
-    if (is_a) {
-      if (row && !used) {
-        if (i == p) {
-          L[j * ldl + i] = dp * rsq;
-          used = true;
-          mypos = j;
-          cs.piv[j] = p;
-        } else {
-          const double g = G[std::int64_t(p) * ldg + i];
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-          int q = 0;
-          for (; q + 4 <= j; q += 4) {
-            s0 = fma(L[q * ldl + i], L[q * ldl + p], s0);
-            s1 = fma(L[(q + 1) * ldl + i], L[(q + 1) * ldl + p], s1);
-            s2 = fma(L[(q + 2) * ldl + i], L[(q + 2) * ldl + p], s2);
-            s3 = fma(L[(q + 3) * ldl + i], L[(q + 3) * ldl + p], s3);
-          }
-          for (; q < j; ++q) s0 = fma(L[q * ldl + i], L[q * ldl + p], s0);
-          const double l = (g - ((s0 + s1) + (s2 + s3))) * rsq;
-          L[j * ldl + i] = l;
-          d = fma(-l, l, d);
-        }
-      }
-      if (PIVOT) publish((j + 1) & 1);
-    } else if (bp <= j) {
-      if (bp == j) {
-        X[j * ldx + bp] = rsq;
-      } else {
-        double s0 = 0.0, s1 = 0.0;
-        int q = bp;
-        for (; q + 2 <= j; q += 2) {
-          s0 = fma(X[q * ldx + bp], L[q * ldl + p], s0);
-          s1 = fma(X[(q + 1) * ldx + bp], L[(q + 1) * ldl + p], s1);
-        }
-        if (q < j) s0 = fma(X[q * ldx + bp], L[q * ldl + p], s0);
-        X[j * ldx + bp] = -(s0 + s1) * rsq;
-      }
-    }
-    __syncthreads();
-    ++j;
-  }
-  if (row) cs.pos[i] = mypos;
-  __syncthreads();
-  return j;
-}
-
 // Partial Gram matrices of a block's row tasks summed into the first task's
 // slot, in task order (blocks of one task: nothing to do). MODE as in
 // gqr_gram_kernel (the element count).
@@ -480,7 +347,8 @@ __global__ void gqr_sum_kernel(const GqrBlock* __restrict__ blocks, const GqrSta
 // W1 = P X (r x j, ld r) and the block's state.
 __global__ void __launch_bounds__(kCholThreads, 3)
 gqr_pchol_kernel(const GqrBlock* __restrict__ blocks, GqrState* state, const double* part, double* wbuf,
-                 int r, int kmax, double theta, double tol, int stage, std::int64_t psz, std::int64_t wsz) {
+                 int r, int kmax, double theta, double tol, int stage, std::int64_t psz, std::int64_t wsz,
+                 int g_shared) {
   extern __shared__ __align__(16) double sm[];
   __shared__ CholShared cs;
   const GqrBlock b = blocks[blockIdx.x];
@@ -500,11 +368,23 @@ gqr_pchol_kernel(const GqrBlock* __restrict__ blocks, GqrState* state, const dou
   const int t = threadIdx.x;
   const int steps = min(min(b.rows, r), kmax);
   const double* G = part + std::int64_t(b.task0) * psz;
+  int ldg = r;
+  if (g_shared) {  // the Gram matrix staged in shared memory: no L2 round trip per step
+    double* Gs = X + kmax * ldx;
+    for (int e = t; e < r * r; e += kCholThreads) {
+      const int c = e / r;
+      Gs[c * ldl + (e - c * r)] = G[e];
+    }
+    G = Gs;
+    ldg = ldl;
+    __syncthreads();
+  }
   double d00 = stage > 0 ? st->d00 : 0.0;
   int last = 0;
   bool used = (t < r && stage > 0) ? st->used[t] != 0 : false;
-  const CholStops stops{steps, theta, tol * tol};
-  const int j = lazy_chol<true>(G, r, L, ldl, X, ldx, r, kq, steps - kq, stops, d00, last, used, cs);
+  // (the last stage the launcher runs takes every pivot still owed)
+  const CholStops stops{steps, theta, tol * tol, theta > 0.0 ? kGqrGap : 0.0};
+  const int j = lazy_chol<true>(G, ldg, L, ldl, X, ldx, r, kq, steps - kq, stops, d00, last, used, cs);
   if (kq + j >= steps) last = 1;
   // W1(i, bq) = X(pos(i), bq) for the pivots i placed at or before bq
   double* w = wbuf + std::int64_t(blockIdx.x) * wsz;
@@ -563,7 +443,7 @@ gqr_chol2_kernel(const GqrBlock* __restrict__ blocks, const GqrState* __restrict
   double d00 = 0.0;
   int last = 0;
   bool used = false;
-  const CholStops stops{0, 0.0, 0.0};
+  const CholStops stops{0, 0.0, 0.0, 0.0};
   lazy_chol<false>(S, lds, S, lds, X, lds, j, 0, j, stops, d00, last, used, cs);
   double* w = wbuf + std::int64_t(blockIdx.x) * wsz;
   for (int e = t; e < n * j; e += kCholThreads) {
@@ -615,39 +495,43 @@ bool gqr_supported(int r, int kmax) { return r >= 1 && r <= 96 && kmax >= 1 && k
 std::int64_t gqr_part_doubles(int r, int kmax) { return std::int64_t(r) * r; }
 std::int64_t gqr_w_doubles(int r, int kmax) { return std::int64_t(r) * kmax; }
 
-void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
-                double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
-                cudaStream_t s) {
-  if (nb == 0) return;
-  if (!gqr_supported(r, kmax)) throw std::invalid_argument("gqr: unsupported widths");
-  constexpr double kTheta = 1e-12;
-  constexpr int kStages = 3;
+namespace {
+
+// W: width class (tiles sized for r <= 8 W)
+template <int W>
+void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
+                  double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
+                  cudaStream_t s) {
+  static const double kTheta = std::getenv("HP_GQR_THETA") ? std::atof(std::getenv("HP_GQR_THETA")) : 1e-12;
+  static const int kStages = std::getenv("HP_GQR_STAGES") ? std::atoi(std::getenv("HP_GQR_STAGES")) : 5;
+  constexpr int NV = (W + 1) / 2, NU = (W + 3) / 4, NT = (W + 1) / 2;
   const std::int64_t psz = gqr_part_doubles(r, kmax), wsz = gqr_w_doubles(r, kmax);
   const int r8 = up(r, 8), k8 = up(kmax, 8);
   // shared-memory sizes (bytes) at the widest shapes
   const size_t sm_g0 = size_t(r8) * kLds * 8;
   const size_t sm_g1 = size_t(k8 + 8) * kLds * 8;
   const size_t sm_g2 = size_t(k8 + r8) * kLds * 8;
-  const size_t sm_a0 = (size_t(k8) * ld4(up(r, 4)) + size_t(up(r, 4)) * kLds) * 8;
-  const size_t sm_a1 = (size_t(k8) * ld4(up(kmax, 4)) + size_t(up(kmax, 4)) * kLds) * 8;
-  const size_t sm_a2 = (size_t(r8) * ld4(up(kmax, 4)) + size_t(up(kmax, 4)) * kLds) * 8;
-  const size_t sm_pc = (size_t(kmax) * (r | 1) + size_t(kmax) * (kmax | 1)) * 8;
-  const size_t sm_c2 = size_t(3) * kmax * (kmax | 1) * 8;
-  // two slice buffers where two CTAs per SM still fit
-  constexpr size_t kTwo = 104 * 1024;
-  auto two = [&](size_t fixed, size_t slice) { return fixed + 2 * slice <= kTwo ? 2 : 1; };
-  const int nb_g0 = two(0, sm_g0), nb_g1 = two(0, sm_g1), nb_g2 = two(0, sm_g2);
   const size_t w0 = size_t(k8) * ld4(up(r, 4)) * 8, w1 = size_t(k8) * ld4(up(kmax, 4)) * 8,
                w2 = size_t(r8) * ld4(up(kmax, 4)) * 8;
-  const int nb_a0 = two(w0, sm_a0 - w0), nb_a1 = two(w1, sm_a1 - w1), nb_a2 = two(w2, sm_a2 - w2);
+  const size_t sl_a0 = size_t(up(r, 4)) * kLds * 8, sl_a1 = size_t(up(kmax, 4)) * kLds * 8, sl_a2 = sl_a1;
+  const size_t sm_pc0 = (size_t(kmax) * (r | 1) + size_t(kmax) * (kmax | 1)) * 8;
+  // the Gram matrix joins L and X in shared memory while three CTAs per SM fit
+  const int g_shared = (sm_pc0 + size_t(r) * (r | 1) * 8) * 3 <= 216 * 1024 ? 1 : 0;
+  const size_t sm_pc = sm_pc0 + (g_shared ? size_t(r) * (r | 1) * 8 : 0);
+  const size_t sm_c2 = size_t(3) * kmax * (kmax | 1) * 8;
+  // two slice buffers where the CTAs per SM the registers allow still fit
+  auto two = [&](size_t fixed, size_t slice, int ctas) { return (fixed + 2 * slice) * ctas <= 208 * 1024 ? 2 : 1; };
+  constexpr int cg = NV * NU <= 8 ? 3 : 2, ca = NT <= 4 ? 3 : 2;
+  const int nb_g0 = two(0, sm_g0, cg), nb_g1 = two(0, sm_g1, cg), nb_g2 = two(0, sm_g2, cg);
+  const int nb_a0 = two(w0, sl_a0, ca), nb_a1 = two(w1, sl_a1, ca), nb_a2 = two(w2, sl_a2, ca);
   static bool attr = false;
   if (!attr) {
-    set_smem(gqr_gram_kernel<0>, 200 * 1024);
-    set_smem(gqr_gram_kernel<1>, 200 * 1024);
-    set_smem(gqr_gram_kernel<2>, 200 * 1024);
-    set_smem(gqr_apply_kernel<0>, 200 * 1024);
-    set_smem(gqr_apply_kernel<1>, 200 * 1024);
-    set_smem(gqr_apply_kernel<2>, 200 * 1024);
+    set_smem(gqr_gram_kernel<0, NV, NU>, 200 * 1024);
+    set_smem(gqr_gram_kernel<1, NV, NU>, 200 * 1024);
+    set_smem(gqr_gram_kernel<2, NV, NU>, 200 * 1024);
+    set_smem(gqr_apply_kernel<0, NT>, 200 * 1024);
+    set_smem(gqr_apply_kernel<1, NT>, 200 * 1024);
+    set_smem(gqr_apply_kernel<2, NT>, 200 * 1024);
     set_smem(gqr_pchol_kernel, 200 * 1024);
     set_smem(gqr_chol2_kernel, 200 * 1024);
     attr = true;
@@ -655,37 +539,60 @@ void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, Gq
   gqr_init_kernel<<<cdiv(nb, 256), 256, 0, s>>>(state, nb);
   HP_LAUNCHED();
   for (int stage = 0; stage < kStages; ++stage) {
-    gqr_gram_kernel<0><<<nt, kGqrThreads, sm_g0 * nb_g0, s>>>(blocks, tasks, state, data, q, part, r, psz, nb_g0, int(sm_g0 / 8));
+    gqr_gram_kernel<0, NV, NU><<<nt, kGqrThreads, sm_g0 * nb_g0, s>>>(blocks, tasks, state, data, q, part, r, psz,
+                                                                        nb_g0, int(sm_g0 / 8));
     HP_LAUNCHED();
     gqr_sum_kernel<0><<<nb, 256, 0, s>>>(blocks, state, part, r, psz);
     HP_LAUNCHED();
-    gqr_pchol_kernel<<<nb, kCholThreads, sm_pc, s>>>(blocks, state, part, wbuf, r, kmax, kTheta, tol, stage,
-                                                      psz, wsz);
+    gqr_pchol_kernel<<<nb, kCholThreads, sm_pc, s>>>(blocks, state, part, wbuf, r, kmax, stage + 1 < kStages ? kTheta : 0.0, tol, stage,
+                                                      psz, wsz, g_shared);
     HP_LAUNCHED();
-    gqr_apply_kernel<0><<<nt, kGqrThreads, w0 + (sm_a0 - w0) * nb_a0, s>>>(blocks, tasks, state, data, q, wbuf, part, r, wsz, psz,
-                                                       nb_a0, int((sm_a0 - w0) / 8));
+    gqr_apply_kernel<0, NT><<<nt, kGqrThreads, w0 + sl_a0 * nb_a0, s>>>(blocks, tasks, state, data, q, wbuf, part,
+                                                                         r, wsz, psz, nb_a0, int(sl_a0 / 8));
     HP_LAUNCHED();
-    gqr_gram_kernel<1><<<nt, kGqrThreads, sm_g1 * nb_g1, s>>>(blocks, tasks, state, data, q, part, r, psz, nb_g1, int(sm_g1 / 8));
+    gqr_gram_kernel<1, NV, NU><<<nt, kGqrThreads, sm_g1 * nb_g1, s>>>(blocks, tasks, state, data, q, part, r, psz,
+                                                                        nb_g1, int(sm_g1 / 8));
     HP_LAUNCHED();
     gqr_sum_kernel<1><<<nb, 256, 0, s>>>(blocks, state, part, r, psz);
     HP_LAUNCHED();
     gqr_chol2_kernel<<<nb, kCholThreads, sm_c2, s>>>(blocks, state, part, wbuf, kmax, psz, wsz);
     HP_LAUNCHED();
-    gqr_apply_kernel<1><<<nt, kGqrThreads, w1 + (sm_a1 - w1) * nb_a1, s>>>(blocks, tasks, state, data, q, wbuf, part, r, wsz, psz,
-                                                       nb_a1, int((sm_a1 - w1) / 8));
+    gqr_apply_kernel<1, NT><<<nt, kGqrThreads, w1 + sl_a1 * nb_a1, s>>>(blocks, tasks, state, data, q, wbuf, part,
+                                                                         r, wsz, psz, nb_a1, int(sl_a1 / 8));
     HP_LAUNCHED();
     if (stage + 1 < kStages) {
-      gqr_gram_kernel<2><<<nt, kGqrThreads, sm_g2 * nb_g2, s>>>(blocks, tasks, state, data, q, part, r, psz, nb_g2, int(sm_g2 / 8));
+      gqr_gram_kernel<2, NV, NU><<<nt, kGqrThreads, sm_g2 * nb_g2, s>>>(blocks, tasks, state, data, q, part, r,
+                                                                          psz, nb_g2, int(sm_g2 / 8));
       HP_LAUNCHED();
       gqr_sum_kernel<2><<<nb, 256, 0, s>>>(blocks, state, part, r, psz);
       HP_LAUNCHED();
-      gqr_apply_kernel<2><<<nt, kGqrThreads, w2 + (sm_a2 - w2) * nb_a2, s>>>(blocks, tasks, state, data, q, wbuf, part, r, wsz, psz,
-                                                       nb_a2, int((sm_a2 - w2) / 8));
+      gqr_apply_kernel<2, NT><<<nt, kGqrThreads, w2 + sl_a2 * nb_a2, s>>>(blocks, tasks, state, data, q, wbuf,
+                                                                           part, r, wsz, psz, nb_a2, int(sl_a2 / 8));
       HP_LAUNCHED();
     }
   }
   gqr_finish_kernel<<<nt, 128, 0, s>>>(blocks, tasks, state, q, ranks, kmax);
   HP_LAUNCHED();
+}
+
+}  // namespace
+
+void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
+                double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
+                cudaStream_t s) {
+  if (nb == 0) return;
+  if (!gqr_supported(r, kmax)) throw std::invalid_argument("gqr: unsupported widths");
+  const int w = (r + 7) / 8;
+#define HP_GQR(W) launch_gqr_w<W>(blocks, nb, tasks, nt, state, data, q, part, wbuf, ranks, r, kmax, tol, s)
+  if (w <= 6)
+    HP_GQR(6);
+  else if (w <= 8)
+    HP_GQR(8);
+  else if (w <= 10)
+    HP_GQR(10);
+  else
+    HP_GQR(12);
+#undef HP_GQR
 }
 
 }  // namespace hpeel
