@@ -840,12 +840,13 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
     h_ranks = static_cast<int*>(persistent_pinned(size_t(std::max<std::int64_t>(rank_total, 1)) * sizeof(int), 0));
 
     // Host plans of every level and of the leaf phase, built concurrently.
+    // (the leaf plan is the longest -- its DSatur colors the densest graph -- so it starts first)
+    auto leaf_fut = std::async(std::launch::async, build_leaf, std::cref(e), std::cref(*rep), std::cref(config),
+                               std::cref(own));
     std::vector<std::future<LevelWork>> futs(size_t(tree->depth()) + 1);
     for (int l = 2; l <= tree->depth(); ++l)
       futs[size_t(l)] = std::async(std::launch::async, build_level, std::cref(e), std::cref(*rep), l,
                                    std::cref(config), std::cref(own));
-    auto leaf_fut = std::async(std::launch::async, build_leaf, std::cref(e), std::cref(*rep), std::cref(config),
-                               std::cref(own));
 
     const int gld = 2 * r;
     // payload Gaussians of two levels: K1 of level l + 1 (apply stream) runs

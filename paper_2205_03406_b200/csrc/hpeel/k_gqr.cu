@@ -475,6 +475,41 @@ __global__ void gqr_finish_kernel(const GqrBlock* __restrict__ blocks, const Gqr
   }
 }
 
+// The Gram matrix squares the block's scale: blocks whose largest entry lies
+// outside [2^-300, 2^300] are rescaled by an exact power of two first (Q and
+// the kept rank do not depend on the scale; the Householder form has no such
+// limit, so this keeps the same domain). Pass 1: largest |entry| per block.
+__global__ void gqr_absmax_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__ tasks,
+                                  GqrState* state, const double* data, int r) {
+  const GqrTask tk = tasks[blockIdx.x];
+  const GqrBlock b = blocks[tk.block];
+  const double* y = data + b.a + tk.row0;
+  double m = 0.0;
+  for (int c = 0; c < r; ++c)
+    for (int i = threadIdx.x; i < tk.rows; i += blockDim.x) m = fmax(m, fabs(y[std::int64_t(c) * b.lda + i]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(&state[tk.block].amax, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+// Pass 2: out-of-range blocks scaled to a largest entry in [1, 2).
+__global__ void gqr_rescale_kernel(const GqrBlock* __restrict__ blocks, const GqrTask* __restrict__ tasks,
+                                   const GqrState* __restrict__ state, double* data, int r) {
+  const GqrTask tk = tasks[blockIdx.x];
+  const double m = __longlong_as_double(static_cast<long long>(state[tk.block].amax));
+  if (!(m > 0.0) || (m >= 0x1p-300 && m <= 0x1p300) || !isfinite(m)) return;
+  const GqrBlock b = blocks[tk.block];
+  int e;
+  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  double* y = data + b.a + tk.row0;
+  for (int c = 0; c < r; ++c)
+    for (int i = threadIdx.x; i < tk.rows; i += blockDim.x) {
+      double& v = y[std::int64_t(c) * b.lda + i];
+      v = scalbn(v, 1 - e);
+    }
+}
+
 __global__ void gqr_init_kernel(GqrState* state, int nb) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < nb) {
@@ -537,6 +572,10 @@ void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, 
     attr = true;
   }
   gqr_init_kernel<<<cdiv(nb, 256), 256, 0, s>>>(state, nb);
+  HP_LAUNCHED();
+  gqr_absmax_kernel<<<nt, 256, 0, s>>>(blocks, tasks, state, data, r);
+  HP_LAUNCHED();
+  gqr_rescale_kernel<<<nt, 256, 0, s>>>(blocks, tasks, state, data, r);
   HP_LAUNCHED();
   for (int stage = 0; stage < kStages; ++stage) {
     gqr_gram_kernel<0, NV, NU><<<nt, kGqrThreads, sm_g0 * nb_g0, s>>>(blocks, tasks, state, data, q, part, r, psz,

@@ -223,6 +223,7 @@ struct GqrTask {
 struct GqrState {    // per block, device-only
   int done, last, kq, j, keep, pad;
   double d00;
+  unsigned long long amax;  // bit pattern of the block's largest |entry|
   unsigned char used[96];
 };
 constexpr int kGqrTaskRows = 256;
