@@ -682,6 +682,21 @@ def qr_orthonormal(m, max_rank=-1):
     return q[:, :keep]
 
 
+def svd_trunc_fixed(m, k):
+    """svd_trunc for TruncationSpec::fixed_rank (proj/src/linalg.cpp:80-108):
+    the leading min(k, #{sigma > 0}) left singular vectors (LAPACK dgesdd for
+    Eigen's BDCSVD: signs of the vectors are not pinned)."""
+    if m.shape[0] == 0 or m.shape[1] == 0:
+        return np.zeros((m.shape[0], 0))
+    if not np.isfinite(m).all():
+        raise ValueError("non-finite matrix in svd")
+    u, sv, _ = scipy.linalg.svd(m, full_matrices=False, lapack_driver="gesdd")
+    keep = 0
+    while keep < min(len(sv), k) and sv[keep] > 0.0:
+        keep += 1
+    return u[:, :keep]
+
+
 def pinv_apply(c, rhs):
     """proj/src/linalg.cpp:110-127 (SVD cutoff 1e-12 sigma_1)."""
     c = np.asarray(c, dtype=np.float64)
@@ -1127,7 +1142,10 @@ def run_uniform(op, tree, adj, k, p, seed, report, capture=None, times=None, res
     stage 1 samples each box against its whole interaction list and takes the
     row basis U_a from them; stage 2 loads U_a into adjoint probes, reads
     S_ab = A_ab^T U_a at I_b, takes the column basis V_b from sum_a S_ab and
-    the couplings B_ab = S_ab^T V_b."""
+    the couplings B_ab = S_ab^T V_b. The bases are the leading left singular
+    vectors (basis_from_sample with a sigma out-parameter takes the svd_trunc
+    branch, peeling.cpp:63-71, :341, :406), not the pivoted-QR range finder of
+    the H1 driver. No device path exists for this format."""
     times = PhaseTimes() if times is None else times
     rep = UnifH1Rep(tree, adj)
     r = k + p
@@ -1146,7 +1164,7 @@ def run_uniform(op, tree, adj, k, p, seed, report, capture=None, times=None, res
                 continue
             sample = ys[plan1.box_to_matrix[a]][tree.box(a).points]
             with _small_blas():
-                rep.box_u[a] = qr_orthonormal(sample, k)
+                rep.box_u[a] = svd_trunc_fixed(sample, k)
         report.append({"phase": "unif-stage1", "level": l, "colors": len(plan1.matrices),
                        "forward_cols": fcols, "adjoint_cols": 0})
         # stage 2 (adjoint probes carrying the stage-1 bases)
@@ -1169,7 +1187,7 @@ def run_uniform(op, tree, adj, k, p, seed, report, capture=None, times=None, res
                 sab = projected[(a, b)]
                 acc[:, :sab.shape[1]] += sab
             with _small_blas():
-                rep.box_v[b] = qr_orthonormal(acc, k)
+                rep.box_v[b] = svd_trunc_fixed(acc, k)
         for a, b in pairs:
             rep.level_b[l][(a, b)] = projected[(a, b)].T @ rep.box_v[b]
         rep.built_level = l

@@ -13,11 +13,14 @@
 // ~1e2 or worse) is flagged and solved by the Jacobi-SVD kernel instead,
 // which implements pinv_apply itself.
 //
-// One CTA per pair: M and the right-hand side in shared memory (leading
-// dimensions == 4 mod 16: conflict-free DMMA fragments), Gram products on
-// DMMA tiles, a left-looking Cholesky that builds X = L^-T alongside
-// (chol.cuh) and the solves as N^-1 Y = X (X^T Y) on DMMA tiles (were
-// column-per-thread triangular substitutions: a 2 k^2-long dependent chain).
+// With N = M^T M the two solves collapse to k x k work,
+//   B = N1^-1 (M1^T middle M2) N2^-1,
+// done by two kernels per batch of pairs (see bprep_kernel / bfinal_kernel):
+// the r-long contractions on DMMA tiles, then a left-looking Cholesky that
+// builds X = L^-T alongside (chol.cuh) and N^-1 Y = X (X^T Y) on DMMA tiles
+// (the round-1 kernel ran column-per-thread triangular substitutions, a
+// 2 k^2-long dependent chain, in one 126 KB CTA per SM). Shared-memory
+// leading dimensions are == 4 (mod 16): conflict-free DMMA fragments.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -80,16 +83,6 @@ __device__ __forceinline__ void atb_dmma(const double* P, int ps_i, int ps_c, co
   __syncthreads();
 }
 
-// N = A^T A (lower, k x k, ld ldn) and Y = A^T X (k x nr), Y written over X
-// with ld ldn once every thread has read X. A: r x k (ld lda), X: r x nr.
-__device__ void gram_pair(const double* a, double* x, double* n, int r, int k, int nr, int lda, int ldx,
-                          int ldn) {
-  atb_dmma(a, 1, lda, x, 1, ldx, r, k, nr, [&](int c, int d, double v) { x[c + d * ldn] = v; });
-  atb_dmma(a, 1, lda, a, 1, lda, r, k, k, [&](int c, int d, double v) {
-    if (c >= d) n[c + d * ldn] = v;
-  });
-}
-
 // N = L L^T in place (lower, ld ldn) with X = L^-T (upper, k x k, ld ldx)
 // built alongside (chol.cuh: one barrier pair per column, rows on threads).
 // Exactly zero diagonals mark null columns (zero rows in the solution).
@@ -119,48 +112,74 @@ __device__ void chol_solve(const double* xinv, int k, int ldx, double* y, int nr
   atb_dmma(xinv, ldx, 1, y, 1, ldy, k, k, nr, [&](int c, int d, double v) { y[c + d * ldy] = v; });
 }
 
-__global__ void __launch_bounds__(kBsThreads)
-bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle,
-                   const double* __restrict__ vg, int r, int k, const std::int64_t* __restrict__ boff,
-                   double* __restrict__ bout, int* __restrict__ flags) {
+// B = pinv(M1) middle pinv(M2)^T = N1^-1 (M1^T middle M2) N2^-1 with
+// N = M^T M: everything the pair needs beyond this point is k x k.
+//
+// Kernel 1 (bprep): N1 = M1^T M1, N2 = M2^T M2 and C = (middle^T M1)^T M2 on
+// DMMA tiles; middle (r x r) and one M (r x k) in shared memory at a time, so
+// two CTAs fit per SM (the fused kernel held M, middle, N and X: one CTA per
+// SM, two warps per scheduler, bound by latency).
+// Kernel 2 (bfinal): Cholesky of N1 and N2 with X = L^-T alongside, then
+// B = X1 X1^T C X2 X2^T on DMMA tiles; three k x k buffers.
+__global__ void __launch_bounds__(kBsThreads, 2)
+bprep_kernel(const double* __restrict__ gpu_, const double* __restrict__ middle, const double* __restrict__ vg,
+             int r, int k, std::int64_t p0, double* __restrict__ work) {
+  extern __shared__ double sm[];
+  const int ldm = ld4(r);
+  double* m = sm;             // M1, then M2: r x k (ld ldm)
+  double* x = m + ldm * k;    // middle (r x r, ld ldm), then P = middle^T M1 (r x k, ld ldm)
+  const std::int64_t p = p0 + blockIdx.x;
+  double* out = work + std::int64_t(blockIdx.x) * 3 * k * k;  // N1, N2, C (k x k each, ld k)
+  const int t = threadIdx.x;
+  for (int e = t; e < r * k; e += kBsThreads) m[e % r + (e / r) * ldm] = gpu_[p * r * k + e];
+  for (int e = t; e < r * r; e += kBsThreads) x[e % r + (e / r) * ldm] = middle[p * r * r + e];
+  __syncthreads();
+  atb_dmma(m, 1, ldm, m, 1, ldm, r, k, k, [&](int c, int d, double v) {
+    if (c >= d) out[c + d * k] = v;
+  });
+  // P(c, d) = sum_i middle(i, c) M1(i, d), written over middle once every warp has its sums
+  atb_dmma(x, 1, ldm, m, 1, ldm, r, r, k, [&](int c, int d, double v) { x[c + d * ldm] = v; });
+  for (int e = t; e < r * k; e += kBsThreads) {
+    const int i = e % r, c = e / r;  // M2(i, c) = vg(c, i), vg k x r col-major
+    m[i + c * ldm] = vg[p * k * r + c + std::int64_t(i) * k];
+  }
+  __syncthreads();
+  atb_dmma(m, 1, ldm, m, 1, ldm, r, k, k, [&](int c, int d, double v) {
+    if (c >= d) out[k * k + c + d * k] = v;
+  });
+  atb_dmma(x, 1, ldm, m, 1, ldm, r, k, k, [&](int c, int d, double v) { out[2 * k * k + c + d * k] = v; });
+}
+
+__global__ void __launch_bounds__(kBsThreads, 2)
+bfinal_kernel(const double* __restrict__ work, int k, std::int64_t p0, const std::int64_t* __restrict__ boff,
+              double* __restrict__ bout, int* __restrict__ flags) {
   extern __shared__ double sm[];
   __shared__ int status[64];
   __shared__ CholShared cs;
-  // leading dimensions == 4 (mod 16): conflict-free DMMA fragment reads
-  const int lda = ld4(r), ldx = ld4(r), ldn = ld4(k);
-  double* a = sm;               // r x k (ld lda)
-  double* x = a + lda * k;      // r x r (ld ldx); later k x r / k x k (ld ldn)
-  double* n = x + ldx * r;      // k x k (ld ldn)
-  double* xinv = n + ldn * k;   // k x k (ld ldn)
-  const std::int64_t p = blockIdx.x;
+  const int ldn = ld4(k);
+  double* n = sm;              // N1 then N2 (lower), overwritten by L
+  double* xinv = n + ldn * k;  // X = L^-T
+  double* c = xinv + ldn * k;  // C -> B
+  const std::int64_t p = p0 + blockIdx.x;
+  const double* in = work + std::int64_t(blockIdx.x) * 3 * k * k;
   const int t = threadIdx.x;
-  // 1) left = pinv(M1) middle, M1 = G'^T U (r x k), middle r x r
-  for (int e = t; e < r * k; e += kBsThreads) a[e % r + (e / r) * lda] = gpu_[p * r * k + e];
-  for (int e = t; e < r * r; e += kBsThreads) x[e % r + (e / r) * ldx] = middle[p * r * r + e];
-  __syncthreads();
-  gram_pair(a, x, n, r, k, r, lda, ldx, ldn);
-  const bool ok1 = cholesky_inv(n, k, ldn, xinv, ldn, status, cs);
-  chol_solve(xinv, k, ldn, x, r, ldn);  // left (k x r, ld ldn) in x
-  // 2) out2 = pinv(M2) left^T, M2 = (V^T G)^T (r x k): M2(i, c) = vg(c, i)
-  for (int e = t; e < r * k; e += kBsThreads) {
-    const int i = e % r, c = e / r;
-    a[i + c * lda] = vg[p * k * r + c + std::int64_t(i) * k];
+  for (int e = t; e < k * k; e += kBsThreads) {
+    const int i = e % k, j = e / k;
+    n[i + j * ldn] = in[e];
+    c[i + j * ldn] = in[2 * k * k + e];
   }
   __syncthreads();
-  // Y2 = M2^T left^T (k x k): Y2(c, d) = sum_i M2(i, c) left(d, i), over x;
-  // N2 = M2^T M2 (lower)
-  atb_dmma(a, 1, lda, x, ldn, 1, r, k, k, [&](int c, int d, double v) { x[c + d * ldn] = v; });
-  atb_dmma(a, 1, lda, a, 1, lda, r, k, k, [&](int c, int d, double v) {
-    if (c >= d) n[c + d * ldn] = v;
-  });
+  const bool ok1 = cholesky_inv(n, k, ldn, xinv, ldn, status, cs);
+  chol_solve(xinv, k, ldn, c, k, ldn);  // C <- N1^-1 C
+  for (int e = t; e < k * k; e += kBsThreads) n[e % k + (e / k) * ldn] = in[k * k + e];
+  __syncthreads();
   const bool ok2 = cholesky_inv(n, k, ldn, xinv, ldn, status, cs);
-  chol_solve(xinv, k, ldn, x, k, ldn);  // out2 (k x k, ld ldn)
+  // C <- C X2 X2^T: D(c, d) = sum_i C(c, i) X2(i, d), then sum_i D(c, i) X2(d, i)
+  atb_dmma(c, ldn, 1, xinv, 1, ldn, k, k, k, [&](int cc, int d, double v) { c[cc + d * ldn] = v; });
+  atb_dmma(c, ldn, 1, xinv, ldn, 1, k, k, k, [&](int cc, int d, double v) { c[cc + d * ldn] = v; });
   const bool ok = ok1 && ok2;
   if (ok)
-    for (int e = t; e < k * k; e += kBsThreads) {
-      const int i = e % k, j = e / k;  // B(i, j) = out2(j, i)
-      bout[boff[p] + e] = x[j + i * ldn];
-    }
+    for (int e = t; e < k * k; e += kBsThreads) bout[boff[p] + e] = c[e % k + (e / k) * ldn];
   if (t == 0) flags[p] = ok ? 0 : 1;
 }
 
@@ -168,13 +187,26 @@ bsolve_chol_kernel(const double* __restrict__ gpu_, const double* __restrict__ m
 
 bool launch_bsolve_reg(int npairs, const double* gpu_, const double* middle, const double* vg, int r, int k,
                        const std::int64_t* boff, double* b, int* flags, cudaStream_t s) {
-  if (k > 64 || k > r || k * r > kBsThreads * 24 || k * k > kBsThreads * 16) return false;
-  if (((k + 7) / 8) * ((r + 7) / 8) > (kBsThreads / 32) * kAtbTiles) return false;
-  const size_t smem = size_t(ld4(r) * k + ld4(r) * r + 2 * ld4(k) * k) * sizeof(double);
-  if (smem > 220 * 1024) return false;
-  HP_CUDA(cudaFuncSetAttribute(bsolve_chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  bsolve_chol_kernel<<<npairs, kBsThreads, smem, s>>>(gpu_, middle, vg, r, k, boff, b, flags);
-  HP_LAUNCHED();
+  if (k > 64 || k > r || r > 96) return false;
+  if (((r + 7) / 8) * ((k + 7) / 8) > (kBsThreads / 32) * kAtbTiles) return false;
+  const size_t sm1 = size_t(ld4(r)) * (k + r) * sizeof(double);
+  const size_t sm2 = size_t(3) * ld4(k) * k * sizeof(double);
+  if (sm1 > 220 * 1024 || sm2 > 220 * 1024) return false;
+  HP_CUDA(cudaFuncSetAttribute(bprep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm1)));
+  HP_CUDA(cudaFuncSetAttribute(bfinal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2)));
+  // pairs in batches: N1, N2, C of a batch live in a workspace of <= 1.5 GB
+  const std::int64_t per = std::int64_t(3) * k * k;
+  const int batch = int(std::max<std::int64_t>(1, std::min<std::int64_t>(npairs, (std::int64_t(3) << 26) / per)));
+  double* work = nullptr;
+  HP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work), size_t(batch) * size_t(per) * sizeof(double), s));
+  for (std::int64_t p0 = 0; p0 < npairs; p0 += batch) {
+    const int nb = int(std::min<std::int64_t>(batch, npairs - p0));
+    bprep_kernel<<<nb, kBsThreads, sm1, s>>>(gpu_, middle, vg, r, k, p0, work);
+    HP_LAUNCHED();
+    bfinal_kernel<<<nb, kBsThreads, sm2, s>>>(work, k, p0, boff, b, flags);
+    HP_LAUNCHED();
+  }
+  HP_CUDA(cudaFreeAsync(work, s));
   return true;
 }
 
