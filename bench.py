@@ -185,9 +185,9 @@ def k2_roofline(report, w):
     # the batched reconstruction kernels, same FP64 peak (spans on the main stream)
     others = {}
     for key, fk, tk, what in (("K3_peel", "peel_flops", "peel_ms", "peel_coeff_dmma + peel_apply (all phases)"),
-                              ("K4_qr", "qr_flops", "qr_ms", "pivoted Householder QR, 2 m r^2 per U / V block"),
+                              ("K4_qr", "qr_flops", "qr_ms", "range finder (staged pivoted Cholesky-QR on DMMA, k_gqr.cu), nominal 2 m r^2 per U / V block"),
                               ("K5_bsolve", "bsolve_flops", "bsolve_ms",
-                               "grams + Cholesky B solve, the reference's flop formulas")):
+                               "grams + two-kernel B solve (N1^-1 C N2^-1), the reference's flop formulas")):
         f = sum(ph.get(fk, 0.0) for ph in report["phases"])
         t = sum(ph[tk] for ph in report["phases"])
         if t > 0 and f > 0:

@@ -92,7 +92,9 @@ int hp_tree_layout(const hp_tree* tree, int* perm, int64_t* start, int64_t* coun
  *      proj/src/peeling.cpp:98-154; binding level_coloring module.cpp:190-205).
  *      pairwise_graph: 0 inverted-index graph, 1 literal pairwise scan,
  *      2 implicit graph (no edge lists; the path compress() uses for
- *      single-payload sets) */
+ *      single-payload sets), 3 the fallback-pattern strategy
+ *      (fallback_pattern_matrices, proj/src/coloring.cpp:334-407: no sets,
+ *      graph or coloring; matrices + hp_plan_block_map only) */
 int hp_plan_build(const hp_tree* tree, int level, int mode, int width, uint64_t seed, int phase,
                   int pairwise_graph, hp_plan** out);
 void hp_plan_free(hp_plan* plan);
@@ -106,6 +108,9 @@ int hp_plan_graph(const hp_plan* plan, int64_t* off, int* adj);
 int hp_plan_coloring(const hp_plan* plan, int* color, int* dsatur_color, int* dsatur_colors);
 /* per color: payload boxes (CSR) */
 int hp_plan_matrices(const hp_plan* plan, int64_t* off, int* boxes);
+/* fallback-pattern plans: block_to_matrix as (alpha, beta, matrix) triples
+ * (beta = -1 for the uniform stage-1 boxes); triples may be NULL to count */
+int hp_plan_block_map(const hp_plan* plan, int64_t* count, int* triples);
 /* dense realization of one color (BlockTestMatrix::realize), n x width */
 int hp_plan_realize(const hp_plan* plan, int color, double* out);
 /* DSatur on an explicit graph (CSR) */
@@ -133,8 +138,9 @@ void hp_op_free(hp_op* op);
 int hp_op_apply(const hp_op* op, int adjoint, const double* x, int64_t w, double* y);
 
 /* ---- compress (proj/include/hpeel/peeling.hpp:66-68, binding compress_py
- *      module.cpp:65-93). format must be HP_FORMAT_H1 and strategy
- *      HP_STRATEGY_GRAPH (the hot path); capture != 0 keeps the post-peel
+ *      module.cpp:65-93). format must be HP_FORMAT_H1; strategy
+ *      HP_STRATEGY_GRAPH or HP_STRATEGY_FALLBACK_PATTERN (fully populated
+ *      trees only, as in the reference); capture != 0 keeps the post-peel
  *      sample blocks for parity tests. ---- */
 int hp_compress(const hp_op* op, const hp_tree* tree, int rank, int oversample, uint64_t seed,
                 int format, int strategy, int capture, hp_rep** out);

@@ -637,8 +637,68 @@ class Plan:
     box_to_matrix: dict = field(default_factory=dict)
 
 
-def make_plan(tree, adj, level, mode, width, seed, phase, basis_table=None):
-    """proj/src/peeling.cpp:98-154 (graph strategy)."""
+def pattern_index(box, mod):
+    """proj/src/peeling.cpp:88-96."""
+    idx, mul = 0, 1
+    for c in box.coord:
+        idx += (c % mod) * mul
+        mul *= mod
+    return idx
+
+
+def fallback_pattern_matrices(tree, adj, level, mode, width, seed, phase):
+    """proj/src/coloring.cpp:334-407: the 6^d / 5^d / 3^d shifted grid
+    patterns of a fully populated uniform tree (no graph, no coloring)."""
+    if not tree.is_fully_populated():
+        raise ValueError("pattern test matrices require a fully populated uniform tree")
+    if mode == UNIF2:
+        raise ValueError("no pattern construction for basis probes")
+    d = tree.dim
+    mod = 6 if mode == H1 else 5 if mode == UNIF1 else 3
+    if mode == LEAF:
+        level = tree.depth
+    if level < 2 or level > tree.depth:
+        raise ValueError("sampling level out of range")
+    mats = []
+    for idx in range(mod ** d):
+        shift, rem = [], idx
+        for _ in range(d):
+            shift.append(rem % mod)
+            rem //= mod
+        m = BlockTestMatrix(tree.num_points, width, seed, level, phase, [], [], [])
+        for b in tree.level_boxes(level):
+            coord = tree.box(b).coord
+            if mode == UNIF1:
+                # zero on the 3^d cluster around each aligned center, payload elsewhere
+                active = not all((coord[j] - shift[j]) % mod in (0, 1, mod - 1) for j in range(d))
+            else:
+                active = all(coord[j] % mod == shift[j] for j in range(d))
+            if active:
+                m.payload.append((b, IDENTITY if mode == LEAF else GAUSSIAN))
+            else:
+                m.zero.append(b)
+        mats.append(m)
+    return mats
+
+
+def make_plan(tree, adj, level, mode, width, seed, phase, basis_table=None, strategy="graph"):
+    """proj/src/peeling.cpp:98-154 (graph strategy; the fallback-pattern
+    strategy for every mode but the basis probes, :131-153)."""
+    if strategy != "graph" and mode != UNIF2:
+        mats = fallback_pattern_matrices(tree, adj, level, mode, width, seed, phase)
+        mod = 6 if mode == H1 else 5 if mode == UNIF1 else 3
+        b2m, box2m = {}, {}
+        if mode == H1:
+            for a, b in admissible_pairs(tree, adj, level):
+                b2m[(a, b)] = pattern_index(tree.box(b), mod)
+        elif mode == UNIF1:
+            for a in tree.level_boxes(level):
+                if adj.interaction[a]:
+                    box2m[a] = pattern_index(tree.box(a), mod)
+        else:
+            for lam, mu in dense_pairs(tree, adj):
+                b2m[(lam, mu)] = pattern_index(tree.box(mu), mod)
+        return Plan([], [], [], mats, b2m, box2m)
     sets = build_constraints(tree, adj, level, mode)
     if not sets:
         return Plan([], [], [], [], {})
@@ -1077,7 +1137,8 @@ def _residual_samples(op, rep, prev_level, plan, adjoint, phase=None, times=None
     return samples, cols
 
 
-def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict=False, raw_capture=None):
+def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict=False, raw_capture=None,
+           strategy="graph"):
     """proj/src/peeling.cpp:211-275 (Alg. 4.1)."""
     times = PhaseTimes() if times is None else times
     rep = H1Rep(tree, adj)
@@ -1090,7 +1151,7 @@ def run_h1(op, tree, adj, k, p, seed, report, capture=None, times=None, restrict
         if any((b, a) not in ps for a, b in pairs):
             raise AssertionError("asymmetric admissibility structure")
         t0 = _now()
-        plan = make_plan(tree, adj, l, H1, r, seed, 0)
+        plan = make_plan(tree, adj, l, H1, r, seed, 0, strategy=strategy)
         times.add("plan", t0)
         yraw, zraw = ([], []) if raw_capture is not None else (None, None)
         ys, fcols = _residual_samples(op, rep, l - 1, plan, False, times=times, restrict=restrict, raw=yraw)
@@ -1197,7 +1258,7 @@ def run_uniform(op, tree, adj, k, p, seed, report, capture=None, times=None, res
     return rep
 
 
-def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False):
+def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False, strategy="graph"):
     """proj/src/peeling.cpp:490-524."""
     times = PhaseTimes() if times is None else times
     tree, adj = rep.tree, rep.adj
@@ -1205,7 +1266,7 @@ def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False
         raise RuntimeError("leaf extraction needs all admissible levels built")
     width = tree.max_leaf_size()
     t0 = _now()
-    plan = make_plan(tree, adj, tree.depth, LEAF, width, seed, 0)
+    plan = make_plan(tree, adj, tree.depth, LEAF, width, seed, 0, strategy=strategy)
     times.add("leaf_plan", t0)
     leaf_times = PhaseTimes()
     ys, fcols = _residual_samples(op, rep, tree.depth, plan, False, times=leaf_times, restrict=restrict)
@@ -1223,7 +1284,7 @@ def extract_leaf(op, rep, seed, report, capture=None, times=None, restrict=False
 
 
 def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, restrict=False, raw_capture=None,
-             fmt="h1"):
+             fmt="h1", strategy="graph"):
     """proj/src/peeling.cpp:576-639 for format h1. Returns (rep, report).
     `times` (a PhaseTimes) collects wall seconds per phase. restrict=True
     evaluates each color's black-box product and peeling only on the rows the
@@ -1243,10 +1304,10 @@ def compress(op, tree, k, p, seed, capture=None, leaf_capture=None, times=None, 
     if fmt == "unif-h1":
         rep = run_uniform(op, tree, adj, k, p, seed, report, capture, times, restrict)
     elif fmt == "h1":
-        rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict, raw_capture)
+        rep = run_h1(op, tree, adj, k, p, seed, report, capture, times, restrict, raw_capture, strategy)
     else:
         raise ValueError("unsupported format: " + fmt)
-    extract_leaf(op, rep, seed, report, leaf_capture, times, restrict)
+    extract_leaf(op, rep, seed, report, leaf_capture, times, restrict, strategy)
     return rep, report
 
 

@@ -201,12 +201,20 @@ class Plan:
     """make_plan output for one level (proj/src/peeling.cpp:98-154)."""
 
     def __init__(self, tree: BoxTree, level: int, mode: str, width: int, seed: int, phase: int,
-                 pairwise: bool = False):
+                 pairwise: bool = False, strategy: str = "graph"):
         self.tree = tree
         self.width = width
         h = C.c_void_p()
-        check(lib().hp_plan_build(tree._h, level, MODES[mode], width, seed, phase, int(pairwise), C.byref(h)))
+        kind = 3 if strategy == "fallback-pattern" else int(pairwise)
+        check(lib().hp_plan_build(tree._h, level, MODES[mode], width, seed, phase, kind, C.byref(h)))
         self._h = h
+        self.pattern_map = None
+        if kind == 3:
+            cnt = C.c_int64(0)
+            check(lib().hp_plan_block_map(h, C.byref(cnt), None))
+            tri = np.zeros(max(3 * cnt.value, 3), dtype=np.int32)
+            check(lib().hp_plan_block_map(h, C.byref(cnt), iptr(tri)))
+            self.pattern_map = {(int(tri[3 * i]), int(tri[3 * i + 1])): int(tri[3 * i + 2]) for i in range(cnt.value)}
         info = np.zeros(8, dtype=np.int64)
         check(lib().hp_plan_info(h, lptr(info)))
         self.n_vertices, self.n_edges, self.n_colors, self.queue_ops = (int(v) for v in info[:4])
@@ -242,7 +250,7 @@ class Plan:
         self.dsatur_colors = dn.value
         moff = np.zeros(self.n_colors + 1, dtype=np.int64)
         mbox = np.zeros(max(nmp, 1), dtype=np.int32)
-        if nv:
+        if nv or self.pattern_map is not None:
             check(lib().hp_plan_matrices(h, lptr(moff), iptr(mbox)))
         self.color_payload = [[int(b) for b in mbox[moff[c]:moff[c + 1]]] for c in range(self.n_colors)]
 
@@ -253,6 +261,8 @@ class Plan:
             pass
 
     def block_to_matrix(self):
+        if self.pattern_map is not None:
+            return dict(self.pattern_map)
         out = {}
         for i, s in enumerate(self.sets):
             for o in s["owners"]:

@@ -48,6 +48,7 @@ _SIGNATURES = {
     "hp_plan_graph": (C.c_int, [P, lp, ip]),
     "hp_plan_coloring": (C.c_int, [P, ip, ip, ip]),
     "hp_plan_matrices": (C.c_int, [P, lp, ip]),
+    "hp_plan_block_map": (C.c_int, [P, C.POINTER(C.c_int64), ip]),
     "hp_plan_realize": (C.c_int, [P, C.c_int, dp]),
     "hp_dsatur": (C.c_int, [C.c_int, lp, ip, ip, ip, lp]),
     "hp_op_dense": (C.c_int, [dp, i64, C.c_int, C.POINTER(P)]),

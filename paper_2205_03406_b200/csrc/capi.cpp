@@ -2,6 +2,7 @@
 #include "../../include/hpeel_b200.h"
 #include "hpeel_probe.h"
 
+#include <array>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -31,6 +32,7 @@ struct hp_plan {
   IncompatibilityGraph graph;
   Coloring coloring, dsatur;
   std::vector<BlockTestMatrix> mats;
+  std::vector<std::array<int, 3>> block_map;  // fallback pattern: (alpha, beta, matrix)
   std::shared_ptr<const BoxTree> tree;
 };
 struct hp_op {
@@ -250,6 +252,15 @@ int hp_plan_build(const hp_tree* t, int level, int mode, int width, uint64_t see
     const SampleMode m = SampleMode(mode);
     auto p = std::make_unique<hp_plan>();
     p->tree = t->tree;
+    if (pairwise_graph == 3) {  // ColoringStrategy::kFallbackPattern: no sets, graph or coloring
+      const SamplingPlan sp = make_plan(*t->tree, *t->adj, level, m, width, seed, phase, true);
+      p->mats = sp.matrices;
+      p->coloring.num_colors = int(sp.matrices.size());
+      p->graph.num_vertices = 0;
+      for (const auto& [key, c] : sp.block_to_matrix) p->block_map.push_back({key.first, key.second, c});
+      *out = p.release();
+      return;
+    }
     p->sets = build_constraints(*t->tree, *t->adj, level, m);
     if (pairwise_graph == 2) {  // implicit graph (the driver's path): no edge lists kept
       if (!ImplicitGraph::applicable(p->sets)) throw std::invalid_argument("implicit graph needs single-payload sets");
@@ -365,6 +376,17 @@ int hp_plan_matrices(const hp_plan* p, int64_t* off, int* boxes) {
       }
     }
     off[p->mats.size()] = o;
+  });
+}
+
+int hp_plan_block_map(const hp_plan* p, int64_t* count, int* triples) {
+  return guard([&] {
+    need(p, "plan");
+    need(count, "count");
+    *count = int64_t(p->block_map.size());
+    if (triples)
+      for (size_t i = 0; i < p->block_map.size(); ++i)
+        for (int j = 0; j < 3; ++j) triples[3 * i + size_t(j)] = p->block_map[i][size_t(j)];
   });
 }
 

@@ -867,9 +867,88 @@ std::vector<BlockTestMatrix> assemble_test_matrices(const std::vector<Constraint
   return mats;
 }
 
+namespace {
+int pattern_modulus(SampleMode mode) {
+  return mode == SampleMode::kH1 ? 6 : mode == SampleMode::kUnifStage1 ? 5 : 3;
+}
+}  // namespace
+
+int pattern_index(const Box& box, int mod) {
+  int idx = 0, weight = 1;
+  for (const std::int64_t c : box.coord) {
+    idx += int(c % mod) * weight;
+    weight *= mod;
+  }
+  return idx;
+}
+
+std::vector<BlockTestMatrix> fallback_pattern_matrices(const BoxTree& tree, const AdjacencyInfo&, int level,
+                                                       SampleMode mode, int width, std::uint64_t seed,
+                                                       int phase) {
+  if (!tree.is_fully_populated())
+    throw std::invalid_argument("pattern test matrices require a fully populated uniform tree");
+  if (mode == SampleMode::kUnifStage2) throw std::invalid_argument("no pattern construction for basis probes");
+  if (mode == SampleMode::kLeaf) level = tree.depth();
+  if (level < 2 || level > tree.depth()) throw std::invalid_argument("sampling level out of range");
+  const int d = tree.dim(), mod = pattern_modulus(mode);
+  int count = 1;
+  for (int j = 0; j < d; ++j) count *= mod;
+  std::vector<BlockTestMatrix> mats(static_cast<size_t>(count));
+  for (BlockTestMatrix& m : mats) {
+    m.rows = tree.num_points();
+    m.width = width;
+    m.seed = seed;
+    m.level = level;
+    m.phase = phase;
+  }
+  const PayloadTag tag = mode == SampleMode::kLeaf ? PayloadTag::kIdentity : PayloadTag::kGaussian;
+  // One pass over the level (ascending ids keep every list sorted): a box
+  // carries payload in the one pattern its coordinates select (pairs, leaf
+  // probes) or in every pattern whose shifted 3^d clusters miss it (stage 1).
+  std::vector<char> active(static_cast<size_t>(count), 0);
+  for (const int id : tree.level_boxes(level)) {
+    const Box& b = tree.box(id);
+    if (mode == SampleMode::kUnifStage1) {
+      for (int idx = 0; idx < count; ++idx) {
+        bool in_cluster = true;
+        for (int j = 0, rem = idx; j < d && in_cluster; ++j, rem /= mod) {
+          const int rel = int(((b.coord[size_t(j)] - rem % mod) % mod + mod) % mod);
+          in_cluster = rel == 0 || rel == 1 || rel == mod - 1;
+        }
+        active[size_t(idx)] = !in_cluster;
+      }
+    } else {
+      std::fill(active.begin(), active.end(), 0);
+      active[size_t(pattern_index(b, mod))] = 1;
+    }
+    for (int idx = 0; idx < count; ++idx) {
+      if (active[size_t(idx)])
+        mats[size_t(idx)].payload.emplace_back(id, tag);
+      else
+        mats[size_t(idx)].zero.push_back(id);
+    }
+  }
+  return mats;
+}
+
 SamplingPlan make_plan(const BoxTree& tree, const AdjacencyInfo& adj, int level, SampleMode mode,
-                       int width, std::uint64_t seed, int phase) {
+                       int width, std::uint64_t seed, int phase, bool pattern) {
   SamplingPlan plan;
+  if (pattern && mode != SampleMode::kUnifStage2) {  // basis probes always go through the graph
+    plan.matrices = fallback_pattern_matrices(tree, adj, level, mode, width, seed, phase);
+    const int mod = pattern_modulus(mode);
+    if (mode == SampleMode::kH1) {
+      for (const auto& [a, b] : admissible_pairs(tree, adj, level))
+        plan.block_to_matrix[{a, b}] = pattern_index(tree.box(b), mod);
+    } else if (mode == SampleMode::kUnifStage1) {
+      for (const int a : tree.level_boxes(level))
+        if (!adj.interaction[size_t(a)].empty()) plan.block_to_matrix[{a, -1}] = pattern_index(tree.box(a), mod);
+    } else {
+      for (const auto& [lam, mu] : dense_pairs(tree, adj))
+        plan.block_to_matrix[{lam, mu}] = pattern_index(tree.box(mu), mod);
+    }
+    return plan;
+  }
   static const bool timing = std::getenv("HP_PLAN_TIMING") != nullptr;
   using Clock = std::chrono::steady_clock;
   auto t0 = Clock::now();

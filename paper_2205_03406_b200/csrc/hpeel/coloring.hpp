@@ -146,7 +146,17 @@ std::vector<BlockTestMatrix> assemble_test_matrices(const std::vector<Constraint
                                                     int level, int width, std::uint64_t seed,
                                                     int phase);
 
-/// Output of make_plan (proj/src/peeling.cpp:98-154), graph strategy.
+/// proj/src/coloring.cpp:334-407: the shifted grid patterns (6^d for H1
+/// pairs, 5^d for the uniform stage-1 clusters, 3^d for the leaf probes) of a
+/// fully populated uniform tree; matrix pattern_index(box, mod) carries the
+/// payload of `box`. No graph is built and nothing is colored.
+std::vector<BlockTestMatrix> fallback_pattern_matrices(const BoxTree& tree, const AdjacencyInfo& adj,
+                                                       int level, SampleMode mode, int width,
+                                                       std::uint64_t seed, int phase);
+/// proj/src/peeling.cpp:88-96.
+int pattern_index(const Box& box, int mod);
+
+/// Output of make_plan (proj/src/peeling.cpp:98-154).
 struct SamplingPlan {
   std::vector<BlockTestMatrix> matrices;
   std::map<std::pair<int, int>, int> block_to_matrix;
@@ -154,7 +164,8 @@ struct SamplingPlan {
   std::size_t n_edges = 0;
   int colors() const { return int(matrices.size()); }
 };
+/// `pattern`: ColoringStrategy::kFallbackPattern (every mode but the basis probes).
 SamplingPlan make_plan(const BoxTree& tree, const AdjacencyInfo& adj, int level, SampleMode mode,
-                       int width, std::uint64_t seed, int phase);
+                       int width, std::uint64_t seed, int phase, bool pattern = false);
 
 }  // namespace hpeel

@@ -276,7 +276,8 @@ LevelWork build_level(const Engine& e, const H1Rep& rep, int l, const PeelConfig
                  std::chrono::duration<double, std::milli>(t1 - t0).count());
     t0 = t1;
   };
-  const SamplingPlan plan = make_plan(e.tree, e.adj, l, SampleMode::kH1, r, cfg.seed, kForwardPhase);
+  const SamplingPlan plan = make_plan(e.tree, e.adj, l, SampleMode::kH1, r, cfg.seed, kForwardPhase,
+                                      cfg.strategy == ColoringStrategy::kFallbackPattern);
   lap("make_plan");
   w.nc = plan.colors();
   std::vector<std::vector<int>> color_boxes(size_t(w.nc));
@@ -499,7 +500,8 @@ LeafWork build_leaf(const Engine& e, const H1Rep& rep, const PeelConfig& cfg, co
     t0 = t1;
   };
   const SamplingPlan plan =
-      make_plan(tree, e.adj, tree.depth(), SampleMode::kLeaf, lw.w, cfg.seed, kForwardPhase);
+      make_plan(tree, e.adj, tree.depth(), SampleMode::kLeaf, lw.w, cfg.seed, kForwardPhase,
+                cfg.strategy == ColoringStrategy::kFallbackPattern);
   lap("make_plan");
   lw.nc = plan.colors();
   std::vector<std::vector<int>> color_boxes(size_t(lw.nc));
@@ -769,8 +771,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
   config.validate();
   if (config.format != PeelFormat::kH1)
     throw std::invalid_argument("only format h1 is on the device hot path");
-  if (config.strategy != ColoringStrategy::kGraph)
-    throw std::invalid_argument("only the graph coloring strategy is on the device hot path");
+  if (config.strategy == ColoringStrategy::kFallbackPattern && !tree->is_fully_populated())
+    throw std::invalid_argument("pattern test matrices require a fully populated uniform tree");
   if (op.kind() != kOpDense && !op.is_callback() && op.dim() != tree->dim())
     throw std::invalid_argument("operator and tree dimensions differ");
   if (config.comm && config.comm->device() != op.device())

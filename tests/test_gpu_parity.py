@@ -75,7 +75,8 @@ def test_exact_recovery_adaptive_2d(hp, gpu_available):
 
 
 def _compare_with_oracle(hp, pts, leaf, op_dev, op_ref, k, p, seed, sample_tol=1e-12,
-                         exact_ranks=False, restrict=False, post_relative=True, peeled_tol=None, block_tol=1e-8):
+                         exact_ranks=False, restrict=False, post_relative=True, peeled_tol=None, block_tol=1e-8,
+                         strategy="graph"):
     """Samples: the black-box products A Omega of every block (1e-12), the
     post-peel blocks relative to A Omega (1e-12, or `peeled_tol` where the
     peeled part inherits rank choices made at the 1e-14 noise floor) and --
@@ -84,9 +85,10 @@ def _compare_with_oracle(hp, pts, leaf, op_dev, op_ref, k, p, seed, sample_tol=1
     1e-4 x the level's largest block for blocks at the noise floor). Dense
     blocks 1e-9. Report counts equal."""
     t, ot = both_trees(hp, pts, leaf)
-    rep = hp.compress(op_dev, t, rank=k, oversample=p, seed=seed, capture=True)
+    rep = hp.compress(op_dev, t, rank=k, oversample=p, seed=seed, capture=True, strategy=strategy)
     cap, leaf_cap, raw_cap = {}, {}, {}
-    orep, oreport = O.compress(op_ref, ot, k, p, seed, cap, leaf_cap, restrict=restrict, raw_capture=raw_cap)
+    orep, oreport = O.compress(op_ref, ot, k, p, seed, cap, leaf_cap, restrict=restrict, raw_capture=raw_cap,
+                               strategy=strategy)
     # report counts (proj/src/peeling.cpp:478-488)
     got_phases = [(ph["phase"], ph["level"], ph["colors"], ph["forward_cols"], ph["adjoint_cols"])
                   for ph in rep.report["phases"]]
@@ -207,3 +209,19 @@ def test_matvec_counts_worked_example(hp, gpu_available):
     truth2 = O.synth_rank_structured(ot2, O.adjacency(ot2), 4, 21)
     rep2 = hp.compress(hp.dense_operator(truth2), t2, rank=4, oversample=6, seed=20240601)
     assert rep2.report["forward_cols"] - rep.report["forward_cols"] == 6 * r
+
+
+@pytest.mark.parametrize("d,per,leaf", [(1, 256, 8), (2, 32, 4)])
+def test_fallback_pattern_strategy_matches_oracle(hp, gpu_available, d, per, leaf):
+    """compress with ColoringStrategy::kFallbackPattern on fully populated
+    trees (proj/src/peeling.cpp:131-153): the report's colors (6^d per level,
+    3^d for the leaf probes) and column counts, every sample block, the
+    factors and the dense leaves against the oracle run with the same
+    strategy."""
+    pts = O.uniform_grid_points(per, d) + 1e-3 * (O.random_cloud(per ** d, d, 5) - 0.5) / per
+    t = hp.build_tree(pts, leaf)
+    assert t.fully_populated
+    rep, _, _ = _compare_with_oracle(hp, pts, leaf, hp.kernel_operator("log", pts), O.KernelOperator("log", pts),
+                                     6, 6, 99, strategy="fallback-pattern", post_relative=False)
+    colors = {(ph["phase"], ph["colors"]) for ph in rep.report["phases"]}
+    assert colors == {("h1", 6 ** d), ("leaf", 3 ** d)}

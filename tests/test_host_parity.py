@@ -310,3 +310,38 @@ def test_threaded_dsatur_equals_serial():
     env = dict(os.environ, HP_DSATUR_THREADS="4", HP_DSATUR_SWEEP_MIN="0")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("d,per", [(1, 32), (2, 16), (3, 8)])
+def test_fallback_pattern_plans_match_oracle(hp, d, per):
+    """ColoringStrategy::kFallbackPattern (proj/src/coloring.cpp:334-407,
+    proj/src/peeling.cpp:131-153): per pattern matrix the payload boxes, and
+    the block -> matrix map, for the H1 pairs of every level, the uniform
+    stage-1 boxes and the leaf probes; dense realizations agree (same nonzero
+    pattern, values to the last bits of the numpy vs libm Box-Muller)."""
+    pts = O.uniform_grid_points(per, d)
+    t = hp.build_tree(pts, 1)
+    ot = O.BoxTree(O.PointCloud(pts), 1)
+    oadj = O.adjacency(ot)
+    assert t.fully_populated
+    for mode, omode, levels in (("h1", O.H1, range(2, t.depth + 1)), ("unif-stage1", O.UNIF1, range(2, t.depth + 1)),
+                                ("leaf", O.LEAF, [t.depth])):
+        for l in levels:
+            got = hp.Plan(t, l, mode, 3, 7, 0, strategy="fallback-pattern")
+            want = O.make_plan(ot, oadj, l, omode, 3, 7, 0, strategy="fallback-pattern")
+            assert got.n_colors == len(want.matrices) == {"h1": 6, "unif-stage1": 5, "leaf": 3}[mode] ** d
+            assert got.color_payload == [[b for b, _ in m.payload] for m in want.matrices]
+            wmap = dict(want.block_to_matrix)
+            wmap.update({(a, -1): c for a, c in want.box_to_matrix.items()})
+            assert got.block_to_matrix() == wmap
+            for c in (0, got.n_colors // 2, got.n_colors - 1):
+                a, b = got.realize(c), want.matrices[c].realize(ot)
+                assert np.array_equal(a != 0, b != 0)
+                assert np.max(np.abs(a - b)) <= 4e-16 * max(1.0, np.max(np.abs(b)))  # numpy vs libm log / sincos
+
+
+def test_fallback_pattern_needs_a_full_tree(hp):
+    t = hp.build_tree(O.random_cloud(300, 2, 3), 16)
+    assert not t.fully_populated
+    with pytest.raises(ValueError):
+        hp.Plan(t, 2, "h1", 3, 7, 0, strategy="fallback-pattern")
