@@ -50,8 +50,20 @@ __host__ __device__ constexpr int k2_plan(int nt, int rows, bool log_kind) {
 }
 
 /// Rows per K2 CTA: 128 (8 DMMA + 8 evaluation warps, one CTA per SM) when the
-/// accumulators fit 128 registers (2r <= 88), else 64 (4 + 4 warps).
+/// accumulators fit 128 registers (2r <= 88), else 64.
 __host__ __device__ constexpr int k2_rows_for(int nt) { return nt <= 11 ? 128 : 64; }
+/// 8-row tiles per DMMA warp: 2 at 128 rows, 1 at 64 rows (8 DMMA warps either
+/// way, half the accumulators per thread at 64 rows).
+__host__ __device__ constexpr int k2_mt_for(int rows) { return rows == 128 ? 2 : 1; }
+/// Evaluation threads: 8 warps either way. At 64 rows four column groups share
+/// a row (8 kernel values per thread and chunk): with 4 + 4 warps the probe
+/// (tools/k2_modes.py, config 4 scaled) showed 0.48 s of the 1.71 s apply
+/// exposed in the evaluation (one evaluation warp per scheduler, bound by its
+/// own latency) on top of a 0.67 s streaming skeleton.
+__host__ __device__ constexpr int k2_eval_for(int rows) { return 256; }
+__host__ __device__ constexpr int k2_threads_for(int rows) {
+  return rows / (8 * k2_mt_for(rows)) * 32 + k2_eval_for(rows);
+}
 
 // Warp-specialized colored apply. The payload rows of each color are stored
 // contiguously in color order (gc, xc, pc: payload values, coordinates and
@@ -63,7 +75,7 @@ __host__ __device__ constexpr int k2_rows_for(int nt) { return nt <= 11 ? 128 : 
 // per k-step from K[b] / G[b]. Double-buffered; full/empty hand-off through
 // named barriers, so evaluation of chunk c+1 overlaps the DMMA of chunk c.
 template <int NT, int KIND, int DIM, bool TRANS, int ROWS>
-__global__ void __launch_bounds__(ROWS * 4, 1)
+__global__ void __launch_bounds__(k2_threads_for(ROWS), 1)
 sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __restrict__ rowtab,
                     const std::int64_t* __restrict__ pay_off, const int* __restrict__ pc,
                     const double* __restrict__ gc, int gld, int gcol0, int ncols,
@@ -71,8 +83,11 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
                     int ocol0, int mode) {
   constexpr int S = smem_stride(NT);
   constexpr int D = DIM > 0 ? DIM : 1;
-  constexpr int kThreads = ROWS * 4;   // ROWS/16 DMMA warps + ROWS/16 evaluation warps
-  constexpr int kEval = ROWS * 2;      // evaluation threads
+  constexpr int MT = k2_mt_for(ROWS);            // 8-row tiles per DMMA warp
+  constexpr int kDmmaWarps = ROWS / (8 * MT);
+  constexpr int kEval = k2_eval_for(ROWS);       // evaluation threads
+  constexpr int NG = kEval / ROWS;               // column groups sharing a row (2 or 4)
+  constexpr int kThreads = kDmmaWarps * 32 + kEval;
   constexpr int kKR = ROWS + 4;        // kernel tile column stride (== 4 mod 16)
   constexpr int kBM = ROWS;
   constexpr int kPlan = k2_plan(NT, ROWS, KIND == kOpLog);
@@ -111,9 +126,9 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
   const bool rev = (mode & 16) != 0;
   auto chunk_base = [&](int c) { return p0 + std::int64_t(rev ? nchunks - 1 - c : c) * kBK; };
 
-  if (warp >= ROWS / 16) {
+  if (warp >= kDmmaWarps) {
     // ------------------------------------------------ evaluation warps
-    const int et = tid - kEval;
+    const int et = tid - kDmmaWarps * 32;
     const int row = et & (kBM - 1), cgrp = et / kBM;
     const int ipos = k2_row(task, rowtab, row < task.rows ? row : task.rows - 1).pos;
     double xi[D];
@@ -185,21 +200,22 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
       // (shared-memory stores would otherwise order them). Unchecked tiles
       // (mode bit 3 clear) skip the i == j / coincident-point tests.
       constexpr int kGrp = 8;
+      static_assert((kBK / NG) % kGrp == 0, "kernel values per thread and chunk in groups of kGrp");
       if (skip) {
-        for (int u = 0; u < kBK / 2; ++u) kb[(cgrp + 2 * u) * kKR + row] = 0.0;
+        for (int u = 0; u < kBK / NG; ++u) kb[(cgrp + NG * u) * kKR + row] = 0.0;
         bar_arrive(kBarFull + b, kThreads);
         continue;
       }
       auto eval_tile = [&](auto check) {
         constexpr bool C = decltype(check)::value;
 #pragma unroll
-        for (int h = 0; h < kBK / 2; h += kGrp) {
+        for (int h = 0; h < kBK / NG; h += kGrp) {
           int jp[kGrp];
           double xj[kGrp][DP];
           double v[kGrp];
 #pragma unroll
           for (int u = 0; u < kGrp; ++u) {
-            const int col = cgrp + 2 * (h + u);
+            const int col = cgrp + NG * (h + u);
             if (KIND == kOpDense || C) jp[u] = js[st][col];
             if constexpr (KIND != kOpDense) {
 #pragma unroll
@@ -216,7 +232,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
           }
 #pragma unroll
           for (int u = 0; u < kGrp; ++u) {
-            const int col = cgrp + 2 * (h + u);
+            const int col = cgrp + NG * (h + u);
             if constexpr (KIND == kOpDense) {
               const int jj = col < cnt ? jp[u] : ipos;
               v[u] = TRANS ? op.a[std::int64_t(jj) + std::int64_t(ipos) * n]
@@ -227,7 +243,7 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
           }
 #pragma unroll
           for (int u = 0; u < kGrp; ++u) {
-            const int col = cgrp + 2 * (h + u);
+            const int col = cgrp + NG * (h + u);
             kb[col * kKR + row] = (KIND != kOpDense || col < cnt) ? v[u] : 0.0;
           }
         }
@@ -243,9 +259,9 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
   }
 
   // -------------------------------------------------- DMMA warps
-  double acc[2][NT][2];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int m = 0; m < 2; ++m)
+  for (int m = 0; m < MT; ++m)
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[m][t][0] = acc[m][t][1] = 0.0;
 
@@ -256,24 +272,26 @@ sample_apply_kernel(DevOp op, const K2Task* __restrict__ tasks, const K2Row* __r
       if (c + NK < nchunks) bar_arrive(kBarEmpty + b, kThreads);
       continue;
     }
-    const double* arow = ksm + b * kBK * kKR + (lane & 3) * kKR + warp * 16 + (lane >> 2);
+    const double* arow = ksm + b * kBK * kKR + (lane & 3) * kKR + warp * 8 * MT + (lane >> 2);
     const double* brow = gsm + (c % kStages) * kBK * S + (lane & 3) * S + (lane >> 2);
 #pragma unroll
     for (int kk = 0; kk < kBK / 4; ++kk) {
-      const double a0 = arow[kk * 4 * kKR], a1 = arow[kk * 4 * kKR + 8];
+      double a[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) a[m] = arow[kk * 4 * kKR + 8 * m];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const double bb = brow[kk * 4 * S + nt * 8];
-        dmma8x8x4(acc[0][nt][0], acc[0][nt][1], a0, bb);
-        dmma8x8x4(acc[1][nt][0], acc[1][nt][1], a1, bb);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) dmma8x8x4(acc[m][nt][0], acc[m][nt][1], a[m], bb);
       }
     }
     if (c + NK < nchunks) bar_arrive(kBarEmpty + b, kThreads);
   }
 
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    const int rr = warp * 16 + m * 8 + (lane >> 2);
+  for (int m = 0; m < MT; ++m) {
+    const int rr = warp * 8 * MT + m * 8 + (lane >> 2);
     if (rr >= task.rows) continue;
     const K2Row dst = k2_row(task, rowtab, rr);
 #pragma unroll
@@ -296,11 +314,11 @@ void launch_rows(const DevOp& op, bool trans, const K2Task* tasks, const K2Row* 
   if (KIND == kOpDense && trans) {
     auto* fn = sample_apply_kernel<NT, KIND, DIM, KIND == kOpDense, R>;
     HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    fn<<<ntasks, R * 4, smem, s>>>(op, tasks, rowtab, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode() | flags);
+    fn<<<ntasks, k2_threads_for(R), smem, s>>>(op, tasks, rowtab, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode() | flags);
   } else {
     auto* fn = sample_apply_kernel<NT, KIND, DIM, false, R>;
     HP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    fn<<<ntasks, R * 4, smem, s>>>(op, tasks, rowtab, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode() | flags);
+    fn<<<ntasks, k2_threads_for(R), smem, s>>>(op, tasks, rowtab, pay_off, pc, gc, gld, gcol0, ncols, xc, nnz, out, ocol0, k2_mode() | flags);
   }
 }
 
