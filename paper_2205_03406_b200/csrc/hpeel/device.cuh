@@ -63,6 +63,20 @@ __device__ __forceinline__ double fast_rcp(double d) {
   return fma(r, e, r);
 }
 
+/// 1/sqrt(x) for positive normal x to ~1 ulp: MUFU.RSQ64H seed (2^-22) and
+/// two Newton steps on the FP64 pipe (9 instructions; rsqrt() adds the
+/// special-case paths the unchecked K2 tiles never take).
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double t = x * y;
+  double e = fma(-t, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  t = x * y;
+  e = fma(-t, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
 /// Table for half_log (built on the host in extended precision, see
 /// log_table_device): kLogTab pairs {1/(2 T_k), 0.5 log(T_k')}, 16-byte aligned.
 constexpr int kLogBits = 10;                      // T_k = 1 + k / 1024
@@ -121,8 +135,10 @@ __device__ __forceinline__ double kernel_value(const double* xi, const double* x
     return zero ? (same ? 0.0 : -INFINITY) : v;
   } else if (KIND == kOpInvDist4Pi) {
     if (CHECK && same) return 0.0;
-    return rsqrt(r2) * 0.07957747154594767;  // 1 / (4 pi)
+    // unchecked tiles: r2 > 0 (no coincident points, i != j)
+    return (CHECK ? rsqrt(r2) : fast_rsqrt(r2)) * 0.07957747154594767;  // 1 / (4 pi)
   } else {
+    if (!CHECK) return exp(-(r2 * fast_rsqrt(r2)) / param);  // sqrt(r2) = r2 / sqrt(r2), r2 > 0
     return exp(-sqrt(r2) / param);
   }
 }

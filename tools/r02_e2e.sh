@@ -1,0 +1,9 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+O=gpurun_out/${1:-r03e}
+mkdir -p $O
+timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > $O/bench_c3_gram.json 2> $O/bench_c3_gram.err
+HP_QR=householder timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu > $O/bench_c3_hh.json 2> $O/bench_c3_hh.err
+timeout 900 python bench.py --config c4 --n 262144 --steps 3 --warmup 2 --no-cpu --no-e2e > $O/bench_c4s.json 2> $O/bench_c4s.err
+timeout 900 python bench.py --config c5 --n 131072 --steps 3 --warmup 2 --no-cpu --no-e2e > $O/bench_c5s.json 2> $O/bench_c5s.err
+timeout 900 python -m pytest tests/test_gpu_k2.py tests/test_gpu_configs.py tests/test_gpu_parity.py tests/test_gpu_k2_int8.py -m gpu -q -x -p no:cacheprovider > $O/pytest.txt 2>&1; echo "rc $?" >> $O/pytest.txt
