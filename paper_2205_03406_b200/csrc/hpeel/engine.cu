@@ -201,12 +201,35 @@ static bool qr_use_gram(int r, int kmax) {
   return gqr_supported(r, kmax);
 }
 
+// Blocks the register-resident Householder kernel still factors faster than
+// the Gram path: short blocks of narrow samples (<= 128 rows at r <= 48, where
+// a Gram stage is dominated by per-kernel set-up; profiles/r02_qr_bench.txt:
+// 128 x 42, 8000 blocks, 2.9 ms vs 3.9 ms). Depends on the block's shape only,
+// so sharded runs route every block as the unsharded run does.
+static bool qr_small_block(int rows, int r, int kmax) {
+  return rows <= 128 && r <= 48 && qr_reg_cols(r) != 0 && qr_reg_cols(kmax) != 0 &&
+         std::min(qr_reg_rows_max(r), qr_reg_rows_max(kmax)) >= 128;
+}
+
 QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
   QrPlan pl;
+  std::vector<QrRequest> house;  // requests left to the Householder kernels
   if (qr_use_gram(r, kmax)) {
     pl.gram = true;
     pl.gblocks.reserve(reqs.size());
     for (const QrRequest& q : reqs) {
+      if (qr_small_block(q.rows, r, kmax)) {
+        house.push_back(q);
+        GqrBlock hb{};
+        hb.a = q.a;
+        hb.lda = q.rows;
+        hb.rows = q.rows;
+        hb.task0 = int(pl.htasks.size());
+        hb.ntasks = 1;
+        pl.htasks.push_back(GqrTask{int(pl.hblocks.size()), 0, q.rows});
+        pl.hblocks.push_back(hb);
+        continue;
+      }
       GqrBlock b{};
       b.a = q.a;
       b.out = q.out;
@@ -227,15 +250,16 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
       b.ntasks = nt;
       pl.gblocks.push_back(b);
     }
-    return pl;
+    if (house.empty()) return pl;
   }
+  const std::vector<QrRequest>& todo = pl.gram ? house : reqs;
   // register-resident kernels when the widths allow, else shared-memory ones
   // (chunks must hold more than r rows or TSQR cannot shrink the stack)
   pl.reg = qr_reg_cols(r) != 0 && qr_reg_cols(kmax) != 0 &&
            std::min(qr_reg_rows_max(r), qr_reg_rows_max(kmax)) >= 2 * r;
   const int rm = pl.reg ? std::min(qr_reg_rows_max(r), qr_reg_rows_max(kmax)) : qr_rows_max(r);
   const int rc = pl.reg ? rm : qr_chunk_rows(r, kmax);  // TSQR chunk
-  for (const QrRequest& q : reqs) {
+  for (const QrRequest& q : todo) {
     if (q.rows <= rm) {
       pl.direct.push_back(QrBlock{q.a, q.out, 0, 0, q.rows, q.rows, q.ldo, 0, q.rank_slot, 0});
       continue;
@@ -327,7 +351,16 @@ static void run_gqr(const QrPlan& pl, double* data, double* out, int* d_ranks, i
 
 void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, int kmax,
             cudaStream_t s) {
-  if (pl.gram) return run_gqr(pl, data, out, d_ranks, r, kmax, s);
+  if (pl.gram) {
+    if (!pl.gblocks.empty()) run_gqr(pl, data, out, d_ranks, r, kmax, s);
+    if (pl.direct.empty()) return;  // (the blocks left to the Householder kernels are all direct)
+    DevBuf<GqrBlock> d_hb;
+    d_hb.upload(pl.hblocks, s);
+    DevBuf<GqrTask> d_ht;
+    d_ht.upload(pl.htasks, s);
+    DevBuf<GqrState> d_hs(pl.hblocks.size(), s);
+    launch_qr_rescale(d_hb.get(), int(pl.hblocks.size()), d_ht.get(), int(pl.htasks.size()), d_hs.get(), data, r, s);
+  }
   auto max_rows = [](const std::vector<QrBlock>& v) {
     int m = 1;
     for (const QrBlock& b : v) m = std::max(m, b.rows);

@@ -202,10 +202,13 @@ struct QrPlan {
   std::vector<std::vector<QrBlock>> chunk_rounds, back_rounds;
   std::int64_t wsize = 0, tausize = 0;
   bool reg = false;  // register-resident kernels (k_qr2.cu)
-  // Gram-based range finder (k_gqr.cu): when set, the lists above stay empty
+  // Gram-based range finder (k_gqr.cu) for gblocks; the lists above then hold only the short
+  // narrow blocks left to the Householder kernels (plan_qr)
   bool gram = false;
   std::vector<GqrBlock> gblocks;
   std::vector<GqrTask> gtasks;
+  std::vector<GqrBlock> hblocks;  // the Householder-routed blocks, for the range rescale
+  std::vector<GqrTask> htasks;
 };
 QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax);
 void run_qr(const QrPlan& plan, double* data, double* out, int* d_ranks, int r, int kmax,

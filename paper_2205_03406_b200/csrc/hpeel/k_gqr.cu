@@ -616,6 +616,17 @@ void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, 
 
 }  // namespace
 
+void launch_qr_rescale(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state,
+                       double* data, int r, cudaStream_t s) {
+  if (nb == 0) return;
+  gqr_init_kernel<<<cdiv(nb, 256), 256, 0, s>>>(state, nb);
+  HP_LAUNCHED();
+  gqr_absmax_kernel<<<nt, 256, 0, s>>>(blocks, tasks, state, data, r);
+  HP_LAUNCHED();
+  gqr_rescale_kernel<<<nt, 256, 0, s>>>(blocks, tasks, state, data, r);
+  HP_LAUNCHED();
+}
+
 void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
                 double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
                 cudaStream_t s) {

@@ -230,6 +230,11 @@ constexpr int kGqrTaskRows = 256;
 bool gqr_supported(int r, int kmax);
 std::int64_t gqr_part_doubles(int r, int kmax);  // Gram workspace per row task
 std::int64_t gqr_w_doubles(int r, int kmax);     // transform workspace per block
+/// The power-of-two rescale of out-of-range blocks alone (launch_gqr runs it
+/// itself): for the short blocks left to the Householder kernels, whose sums
+/// of squares have the same [2^-300, 2^300] domain.
+void launch_qr_rescale(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state,
+                       double* data, int r, cudaStream_t s);
 void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
                 double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
                 cudaStream_t s);
