@@ -97,6 +97,15 @@ __device__ __forceinline__ int lazy_chol(const double* G, int ldg, double* L, in
     }
   };
   if (PIVOT && is_a) publish(0);
+  // natural order: the owner of the next pivot row publishes its downdated
+  // diagonal before the step's barrier (a zero pivot marks a null column --
+  // zero row and column of X, as the pseudo-inverse gives -- a negative one a
+  // failed factorization)
+  auto publish_next = [&](int jn) {
+    cs.wbest[jn & 1][0] = d;
+    if (status) status[jn] = d == 0.0 ? 1 : (d < 0.0 ? 2 : 0);
+  };
+  if (!PIVOT && row && i == 0) publish_next(0);
   if (is_a && i < 96) cs.pos[i] = -1;
   __syncthreads();
   double dstage = 0.0;
@@ -135,14 +144,6 @@ __device__ __forceinline__ int lazy_chol(const double* G, int ldg, double* L, in
       if (j > 0 && dp - d2 < stops.gap * dstage) break;  // too close to call on this Gram matrix
     } else {
       p = j;
-      dp = __shfl_sync(0xffffffffu, d, p & 31);  // valid in warp p / 32 only
-      if (lane == 0 && warp == (p >> 5)) {
-        cs.wbest[j & 1][0] = dp;
-        // natural order: a zero pivot marks a null column (zero row and column
-        // of X, as the pseudo-inverse gives), a negative one a failed factorization
-        if (status) status[j] = dp == 0.0 ? 1 : (dp < 0.0 ? 2 : 0);
-      }
-      __syncthreads();
       dp = cs.wbest[j & 1][0];
     }
     const double rsq = dp > 0.0 ? rsqrt(dp) : 0.0;
@@ -167,6 +168,7 @@ __device__ __forceinline__ int lazy_chol(const double* G, int ldg, double* L, in
           const double l = (g - ((s0 + s1) + (s2 + s3))) * rsq;
           L[j * ldl + i] = l;
           d = fma(-l, l, d);
+          if (!PIVOT && i == j + 1) publish_next(j + 1);
         }
       }
       if (PIVOT) publish((j + 1) & 1);
