@@ -553,7 +553,8 @@ void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, 
   // the Gram matrix joins L and X in shared memory while three CTAs per SM fit
   const int g_shared = (sm_pc0 + size_t(r) * (r | 1) * 8) * 3 <= 216 * 1024 ? 1 : 0;
   const size_t sm_pc = sm_pc0 + (g_shared ? size_t(r) * (r | 1) * 8 : 0);
-  const size_t sm_c2 = size_t(3) * kmax * (kmax | 1) * 8;
+  // S and X (j x j each) + H ((kq + j <= kmax) : kq x j): j (j|1) 2 + j (kq|1) <= 2 kmax (kmax|1) + 2 kmax
+  const size_t sm_c2 = (size_t(2) * kmax * (kmax | 1) + size_t(2) * kmax) * 8;
   // two slice buffers where the CTAs per SM the registers allow still fit
   auto two = [&](size_t fixed, size_t slice, int ctas) { return (fixed + 2 * slice) * ctas <= 208 * 1024 ? 2 : 1; };
   constexpr int cg = NV * NU <= 8 ? 3 : 2, ca = NT <= 4 ? 3 : 2;

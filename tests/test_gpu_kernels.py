@@ -32,7 +32,7 @@ def _spectrum_block(rng, rows, r, decay):
     return (u * 10.0 ** (-np.arange(q) / decay)) @ v.T
 
 
-@pytest.mark.parametrize("r,kmax", [(42, 32), (64, 48), (80, 64), (14, 6)])
+@pytest.mark.parametrize("r,kmax", [(42, 32), (64, 48), (80, 64), (14, 6), (96, 96), (96, 64), (33, 33), (8, 3)])
 def test_range_finder_matches_pivoted_qr(hp, gpu_available, r, kmax):
     """K4 (k_gqr.cu: staged pivoted Cholesky-QR) against LAPACK's dgeqp3 on
     ragged batches: kept rank (|R_jj| > 1e-14 |R_00|, capped at kmax,
@@ -48,6 +48,7 @@ def test_range_finder_matches_pivoted_qr(hp, gpu_available, r, kmax):
     for rows, decay in [(256, 10.0), (128, 3.0), (100, 1.5), (33, 4.0), (7, 2.0), (1500, 5.0), (600, 2.0)]:
         for _ in range(3):
             blocks.append(_spectrum_block(rng, rows, r, decay))
+    blocks += [_spectrum_block(rng, 1, r, 3.0), _spectrum_block(rng, 2, r, 3.0), _spectrum_block(rng, 257, r, 6.0)]
     low = rng.standard_normal((90, 5)) @ rng.standard_normal((5, r))  # exact rank 5
     blocks += [low, np.zeros((40, r)), 1e-200 * _spectrum_block(rng, 64, r, 3.0)]
     qs, ranks, _ = hp.debug_qr(blocks, kmax)
