@@ -20,10 +20,11 @@ namespace {
 constexpr int kGramThreads = 256;
 constexpr int kGramRows = 32;
 
-// Row stride of a staged operand: >= the 8-padded width and == 8 mod 16
-// doubles, so a DMMA fragment read (4 rows x 8 columns) hits each bank pair
-// at most twice.
-__host__ __device__ constexpr int gram_stride(int n) { return ((n + 7) / 16) * 16 + 8; }
+// Row stride of a staged operand: >= the 8-padded width and == 4 mod 16
+// doubles: a DMMA fragment read is served per half warp (4 rows x 4 columns),
+// which then hits 16 distinct bank pairs (== 8 mod 16 gave two-way conflicts
+// on half of the shared loads, profiles/r02_ncu_kernels.txt).
+__host__ __device__ constexpr int gram_stride(int n) { return ((((n + 7) / 8) * 8 + 11) / 16) * 16 + 4; }
 
 // out (nx x ny, col-major) = X^T Y over t.rows rows, on FP64 DMMA (m8n8k4):
 // 32-row chunks of X and Y staged row-major in shared memory (rows past the
