@@ -43,7 +43,8 @@ namespace hpeel {
 
 namespace {
 
-constexpr double kGqrGap = 3e-13;  // runner-up margin in units of the stage's first pivot (chol.cuh)
+// runner-up margin in units of the stage's first pivot (chol.cuh); HP_GQR_GAP overrides (probe)
+static const double kGqrGapHost = std::getenv("HP_GQR_GAP") ? std::atof(std::getenv("HP_GQR_GAP")) : 3e-13;
 constexpr int kGqrThreads = 256;  // 8 warps: Gram / apply kernels
 constexpr int kSlice = 64;        // rows per shared-memory slice
 constexpr int kLds = 68;          // slice leading dimension: == 4 (mod 16) doubles, conflict-free fragments
@@ -348,7 +349,7 @@ __global__ void gqr_sum_kernel(const GqrBlock* __restrict__ blocks, const GqrSta
 __global__ void __launch_bounds__(kCholThreads, 3)
 gqr_pchol_kernel(const GqrBlock* __restrict__ blocks, GqrState* state, const double* part, double* wbuf,
                  int r, int kmax, double theta, double tol, int stage, std::int64_t psz, std::int64_t wsz,
-                 int g_shared) {
+                 int g_shared, double gap) {
   extern __shared__ __align__(16) double sm[];
   __shared__ CholShared cs;
   const GqrBlock b = blocks[blockIdx.x];
@@ -383,7 +384,7 @@ gqr_pchol_kernel(const GqrBlock* __restrict__ blocks, GqrState* state, const dou
   int last = 0;
   bool used = (t < r && stage > 0) ? st->used[t] != 0 : false;
   // (the last stage the launcher runs takes every pivot still owed)
-  const CholStops stops{steps, theta, tol * tol, theta > 0.0 ? kGqrGap : 0.0};
+  const CholStops stops{steps, theta, tol * tol, theta > 0.0 ? gap : 0.0};
   const int j = lazy_chol<true>(G, ldg, L, ldl, X, ldx, r, kq, steps - kq, stops, d00, last, used, cs);
   if (kq + j >= steps) last = 1;
   // W1(i, bq) = X(pos(i), bq) for the pivots i placed at or before bq
@@ -585,7 +586,7 @@ void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, 
     gqr_sum_kernel<0><<<nb, 256, 0, s>>>(blocks, state, part, r, psz);
     HP_LAUNCHED();
     gqr_pchol_kernel<<<nb, kCholThreads, sm_pc, s>>>(blocks, state, part, wbuf, r, kmax, stage + 1 < kStages ? kTheta : 0.0, tol, stage,
-                                                      psz, wsz, g_shared);
+                                                      psz, wsz, g_shared, kGqrGapHost);
     HP_LAUNCHED();
     gqr_apply_kernel<0, NT><<<nt, kGqrThreads, w0 + sl_a0 * nb_a0, s>>>(blocks, tasks, state, data, q, wbuf, part,
                                                                          r, wsz, psz, nb_a0, int(sl_a0 / 8));
