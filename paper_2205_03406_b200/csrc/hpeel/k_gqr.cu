@@ -561,7 +561,11 @@ void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, 
   constexpr int cg = NV * NU <= 8 ? 3 : 2, ca = NT <= 4 ? 3 : 2;
   const int nb_g0 = two(0, sm_g0, cg), nb_g1 = two(0, sm_g1, cg), nb_g2 = two(0, sm_g2, cg);
   const int nb_a0 = two(w0, sl_a0, ca), nb_a1 = two(w1, sl_a1, ca), nb_a2 = two(w2, sl_a2, ca);
-  static bool attr = false;
+  // (function attributes are per device: a process may drive several)
+  static bool attr_set[64] = {};
+  int dev = 0;
+  HP_CUDA(cudaGetDevice(&dev));
+  bool& attr = attr_set[dev & 63];
   if (!attr) {
     set_smem(gqr_gram_kernel<0, NV, NU>, 200 * 1024);
     set_smem(gqr_gram_kernel<1, NV, NU>, 200 * 1024);
