@@ -362,7 +362,8 @@ def run_ours(args, ws, rank, local):
         host_pts_src = hp.pinned_empty(pts.size).reshape(pts.shape)
         host_pts_src[...] = pts
         etimes, parts = [], []
-        for i in range(max(1, min(args.steps, 2))):
+        n_e2e = max(1, min(args.steps, 3))
+        for i in range(1 + n_e2e):  # one untimed warm-up pass (first use of the export path), then n_e2e timed
             barrier(ws)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -376,8 +377,9 @@ def run_ours(args, ws, rank, local):
             r2 = hp.compress(o2, t_tree, **kw, export_to=(hf, hd))
             hp.device_synchronize()
             t3 = time.perf_counter()
-            etimes.append(t3 - t0)
-            parts.append((t1 - t0, t2 - t1, t3 - t2))
+            if i > 0:
+                etimes.append(t3 - t0)
+                parts.append((t1 - t0, t2 - t1, t3 - t2))
             del r2, o2
         d2h = (nf + nd) * 8
         e2e = {"value": dist_max(float(np.mean(etimes)), ws, "ours"), "unit": "s",
@@ -385,6 +387,7 @@ def run_ours(args, ws, rank, local):
                "breakdown_s": {"tree_build": round(float(np.mean([p[0] for p in parts])), 4),
                                "operator_h2d": round(float(np.mean([p[1] for p in parts])), 4),
                                "compress_with_export": round(float(np.mean([p[2] for p in parts])), 4)},
+               "steps": n_e2e, "warmup": 1,
                "includes": "points from pinned host memory: tree build, operator H2D, compress with every "
                            "factor and dense block streamed D2H into pinned host arrays as levels finish"}
     cpu = None
