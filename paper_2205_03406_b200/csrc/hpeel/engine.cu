@@ -238,8 +238,10 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
       b.rows = q.rows;
       b.rank_slot = q.rank_slot;
       b.task0 = int(pl.gtasks.size());
-      // row tasks of equal size (<= kGqrTaskRows)
-      const int nt = std::max(1, (q.rows + kGqrTaskRows - 1) / kGqrTaskRows);
+      // row tasks of equal size: <= kGqrTaskRows rows, 4x that for very tall blocks (their
+      // partial Gram matrices would otherwise add a quarter of the block's own volume)
+      const int cap = q.rows >= 8 * kGqrTaskRows ? 4 * kGqrTaskRows : kGqrTaskRows;
+      const int nt = std::max(1, (q.rows + cap - 1) / cap);
       const int base = q.rows / nt, extra = q.rows % nt;
       int row = 0;
       for (int i = 0; i < nt; ++i) {
