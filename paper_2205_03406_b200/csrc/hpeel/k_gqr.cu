@@ -552,7 +552,8 @@ void launch_gqr_w(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, 
   const size_t sl_a0 = size_t(up(r, 4)) * kLds * 8, sl_a1 = size_t(up(kmax, 4)) * kLds * 8, sl_a2 = sl_a1;
   const size_t sm_pc0 = (size_t(kmax) * (r | 1) + size_t(kmax) * (kmax | 1)) * 8;
   // the Gram matrix joins L and X in shared memory while three CTAs per SM fit
-  const int g_shared = (sm_pc0 + size_t(r) * (r | 1) * 8) * 3 <= 216 * 1024 ? 1 : 0;
+  static const int g_force = std::getenv("HP_GQR_GSHARED") ? std::atoi(std::getenv("HP_GQR_GSHARED")) : -1;
+  const int g_shared = g_force >= 0 ? g_force : ((sm_pc0 + size_t(r) * (r | 1) * 8) * 3 <= 216 * 1024 ? 1 : 0);
   const size_t sm_pc = sm_pc0 + (g_shared ? size_t(r) * (r | 1) * 8 : 0);
   // S and X (j x j each) + H ((kq + j <= kmax) : kq x j): j (j|1) 2 + j (kq|1) <= 2 kmax (kmax|1) + 2 kmax
   const size_t sm_c2 = (size_t(2) * kmax * (kmax | 1) + size_t(2) * kmax) * 8;
