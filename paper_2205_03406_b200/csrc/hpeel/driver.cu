@@ -1157,6 +1157,8 @@ PeelResult compress(const DeviceOperator& op, std::shared_ptr<const BoxTree> tre
         if (ld.uoff[p] < 0) continue;
         ld.ku[p] = h_ranks[rank_off[size_t(l)] + std::int64_t(p)];
         ld.kv[p] = h_ranks[rank_off[size_t(l)] + std::int64_t(np + p)];
+        // qr_orthonormal's check (proj/src/linalg.cpp:59), reported by K4 as rank -1
+        if (ld.ku[p] < 0 || ld.kv[p] < 0) throw std::invalid_argument("non-finite matrix in qr");
       }
     }
     for (int l = 2; l <= tree->depth(); ++l) {

@@ -224,6 +224,7 @@ QrPlan plan_qr(const std::vector<QrRequest>& reqs, int r, int kmax) {
         hb.a = q.a;
         hb.lda = q.rows;
         hb.rows = q.rows;
+        hb.rank_slot = q.rank_slot;
         hb.task0 = int(pl.htasks.size());
         hb.ntasks = 1;
         pl.htasks.push_back(GqrTask{int(pl.hblocks.size()), 0, q.rows});
@@ -353,14 +354,15 @@ static void run_gqr(const QrPlan& pl, double* data, double* out, int* d_ranks, i
 
 void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, int kmax,
             cudaStream_t s) {
+  DevBuf<GqrBlock> d_hb;
+  DevBuf<GqrState> d_hs;
   if (pl.gram) {
     if (!pl.gblocks.empty()) run_gqr(pl, data, out, d_ranks, r, kmax, s);
     if (pl.direct.empty()) return;  // (the blocks left to the Householder kernels are all direct)
-    DevBuf<GqrBlock> d_hb;
     d_hb.upload(pl.hblocks, s);
     DevBuf<GqrTask> d_ht;
     d_ht.upload(pl.htasks, s);
-    DevBuf<GqrState> d_hs(pl.hblocks.size(), s);
+    d_hs.alloc(pl.hblocks.size(), s);
     launch_qr_rescale(d_hb.get(), int(pl.hblocks.size()), d_ht.get(), int(pl.htasks.size()), d_hs.get(), data, r, s);
   }
   auto max_rows = [](const std::vector<QrBlock>& v) {
@@ -395,6 +397,8 @@ void run_qr(const QrPlan& pl, double* data, double* out, int* d_ranks, int r, in
     else
       launch_qr_top(d, nb, data, out, d_ranks, r, kmax, kQrRankDropTol, mr, s);
   });
+  if (pl.gram && d_ranks)  // non-finite blocks among the Householder-routed ones report rank -1
+    launch_qr_flag(d_hb.get(), int(pl.hblocks.size()), d_hs.get(), d_ranks, s);
   for (size_t rd = 0; rd < pl.chunk_rounds.size(); ++rd) {
     by_class(pl.chunk_rounds[rd], r, [&](const QrBlock* d, int nb, int mr) {
       if (pl.reg)

@@ -45,6 +45,7 @@ namespace {
 
 // runner-up margin in units of the stage's first pivot (chol.cuh); HP_GQR_GAP overrides (probe)
 static const double kGqrGapHost = std::getenv("HP_GQR_GAP") ? std::atof(std::getenv("HP_GQR_GAP")) : 3e-13;
+constexpr unsigned long long kGqrNonFinite = 0x7ff8000000000000ull;  // amax of a block holding NaN / Inf
 constexpr int kGqrThreads = 256;  // 8 warps: Gram / apply kernels
 constexpr int kSlice = 64;        // rows per shared-memory slice
 constexpr int kLds = 68;          // slice leading dimension: == 4 (mod 16) doubles, conflict-free fragments
@@ -466,8 +467,10 @@ __global__ void gqr_finish_kernel(const GqrBlock* __restrict__ blocks, const Gqr
   const GqrTask tk = tasks[blockIdx.x];
   const GqrBlock b = blocks[tk.block];
   const GqrState* st = state + tk.block;
-  const int keep = st->last ? st->keep : st->kq + st->j;
-  if (tk.row0 == 0 && threadIdx.x == 0 && b.rank_slot >= 0) ranks[b.rank_slot] = keep;
+  const bool nonfinite = st->amax >= kGqrNonFinite;
+  const int keep = nonfinite ? 0 : (st->last ? st->keep : st->kq + st->j);
+  if (nonfinite && tk.row0 == 0 && threadIdx.x == 0 && b.rank_slot >= 0) ranks[b.rank_slot] = -1;
+  if (!nonfinite && tk.row0 == 0 && threadIdx.x == 0 && b.rank_slot >= 0) ranks[b.rank_slot] = keep;
   double* o = q + b.out + tk.row0;
   const int ncol = kmax - keep;
   for (int e = threadIdx.x; e < ncol * tk.rows; e += blockDim.x) {
@@ -486,12 +489,30 @@ __global__ void gqr_absmax_kernel(const GqrBlock* __restrict__ blocks, const Gqr
   const GqrBlock b = blocks[tk.block];
   const double* y = data + b.a + tk.row0;
   double m = 0.0;
+  bool bad = false;  // NaN / Inf: qr_orthonormal throws "non-finite matrix in qr" (linalg.cpp:59)
   for (int c = 0; c < r; ++c)
-    for (int i = threadIdx.x; i < tk.rows; i += blockDim.x) m = fmax(m, fabs(y[std::int64_t(c) * b.lda + i]));
+    for (int i = threadIdx.x; i < tk.rows; i += blockDim.x) {
+      const double v = y[std::int64_t(c) * b.lda + i];
+      bad |= !isfinite(v);
+      m = fmax(m, fabs(v));
+    }
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0.0)
-    atomicMax(&state[tk.block].amax, static_cast<unsigned long long>(__double_as_longlong(m)));
+  bad = __any_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad)
+      atomicMax(&state[tk.block].amax, kGqrNonFinite);
+    else if (m > 0.0)
+      atomicMax(&state[tk.block].amax, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+// Blocks with a non-finite entry report rank -1 (the driver raises the
+// reference's exception): for the blocks the Householder kernels factor.
+__global__ void gqr_flag_kernel(const GqrBlock* __restrict__ blocks, const GqrState* __restrict__ state, int* ranks,
+                                int nb) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < nb && state[i].amax >= kGqrNonFinite && blocks[i].rank_slot >= 0) ranks[blocks[i].rank_slot] = -1;
 }
 
 // Pass 2: out-of-range blocks scaled to a largest entry in [1, 2).
@@ -631,6 +652,12 @@ void launch_qr_rescale(const GqrBlock* blocks, int nb, const GqrTask* tasks, int
   gqr_absmax_kernel<<<nt, 256, 0, s>>>(blocks, tasks, state, data, r);
   HP_LAUNCHED();
   gqr_rescale_kernel<<<nt, 256, 0, s>>>(blocks, tasks, state, data, r);
+  HP_LAUNCHED();
+}
+
+void launch_qr_flag(const GqrBlock* blocks, int nb, const GqrState* state, int* ranks, cudaStream_t s) {
+  if (nb == 0) return;
+  gqr_flag_kernel<<<cdiv(nb, 256), 256, 0, s>>>(blocks, state, ranks, nb);
   HP_LAUNCHED();
 }
 

@@ -235,6 +235,9 @@ std::int64_t gqr_w_doubles(int r, int kmax);     // transform workspace per bloc
 /// of squares have the same [2^-300, 2^300] domain.
 void launch_qr_rescale(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state,
                        double* data, int r, cudaStream_t s);
+/// ranks[rank_slot] = -1 for the blocks launch_qr_rescale found non-finite
+/// (launch_gqr reports its own): qr_orthonormal's "non-finite matrix in qr".
+void launch_qr_flag(const GqrBlock* blocks, int nb, const GqrState* state, int* ranks, cudaStream_t s);
 void launch_gqr(const GqrBlock* blocks, int nb, const GqrTask* tasks, int nt, GqrState* state, double* data,
                 double* q, double* part, double* wbuf, int* ranks, int r, int kmax, double tol,
                 cudaStream_t s);

@@ -100,3 +100,33 @@ def test_callback_errors_propagate(hp, gpu_available):
         hp.compress(hp.callback_operator(256, bad), t, rank=4, oversample=4, seed=1)
     with pytest.raises(ValueError):  # wrong output shape, reported by the binding
         hp.compress(hp.callback_operator(256, lambda x, adj: np.zeros((3, 3))), t, rank=4, oversample=4, seed=1)
+
+
+@pytest.mark.parametrize("n,leaf", [(512, 64), (4096, 64)])
+def test_non_finite_samples_raise_like_reference(hp, gpu_available, n, leaf):
+    """A black box that returns NaN: the reference's qr_orthonormal throws
+    std::invalid_argument("non-finite matrix in qr") (proj/src/linalg.cpp:59),
+    which leaves compress(); K4 reports such blocks and the driver raises the
+    same exception (both K4 routes: short blocks at n = 512, tall ones too at
+    n = 4096). The oracle raises alike."""
+    pts = O.equispaced_1d(n)
+    ot = O.BoxTree(O.PointCloud(pts), leaf)
+    a = O.synth_rank_structured(ot, O.adjacency(ot), 4, 21)
+
+    def bad(x, adj):
+        y = a @ x
+        y[n // 3, 0] = np.nan
+        return y
+
+    t = hp.build_tree(pts, leaf)
+    with pytest.raises(ValueError, match="non-finite matrix in qr"):
+        hp.compress(hp.callback_operator(n, bad, symmetric=True), t, rank=4, oversample=6, seed=5)
+
+    class Bad(O.DenseOperator):
+        def apply(self, x):
+            y = super().apply(x)
+            y[n // 3, 0] = np.nan
+            return y
+
+    with pytest.raises(ValueError, match="non-finite matrix in qr"):
+        O.compress(Bad(a), ot, 4, 6, 5)
